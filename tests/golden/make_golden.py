@@ -1,0 +1,196 @@
+"""Generate golden fixtures by running the REAL reference package.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports ``sketchals`` from /root/reference/pkg/src (read-only; nothing is
+copied), runs small cases of every hot-path operator and driver, and writes
+``tests/golden/golden.npz``.  The fixtures travel with the repo; nothing on
+the GPU box reads /root/reference.  Inputs are regenerated in the tests from
+the same seeds (numpy 2.3.5), so only outputs plus small inputs are stored.
+"""
+import os
+import sys
+
+import numpy as np
+import scipy.sparse as sp
+
+sys.dont_write_bytecode = True
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REF)
+sys.path.insert(0, ROOT)
+
+import sketchals as ref  # noqa: E402
+from sketchals.rng import make_rng  # noqa: E402
+
+from paper_2104_01101_b200.synth import planted_cp_coo_host, planted_tucker_dense  # noqa: E402
+
+OUT = {}
+
+
+def put(name, arr):
+    OUT[name] = np.asarray(arr)
+
+
+def orthonormal(s, r, gen):
+    return np.linalg.qr(gen.standard_normal((s, r)))[0]
+
+
+def tables():
+    for seed in (0, 7):
+        op = ref.TensorSketchOp.build((100, 120, 90), 400, make_rng(seed))
+        for k, md in enumerate(op.modes):
+            put(f"ts_tab_s{seed}_h{k}", md.hash.astype(np.int32))
+            put(f"ts_tab_s{seed}_s{k}", md.signs.astype(np.int8))
+    op = ref.TensorSketchOp.build((3, 4, 2), 5, make_rng(7))
+    for k, md in enumerate(op.modes):
+        put(f"ts_small_h{k}", md.hash)
+        put(f"ts_small_s{k}", md.signs)
+    c = ref.CompositeSketchOp.build(1000, 20, 45, make_rng(3))
+    put("rrf_hash", c.stage.hash.astype(np.int32))
+    put("rrf_signs", c.stage.signs.astype(np.int8))
+    put("rrf_gauss", c.gauss)
+    gen = np.random.default_rng(5)
+    f = [orthonormal(40, 3, gen), orthonormal(30, 3, gen)]
+    put("lev_f0", f[0])
+    put("lev_f1", f[1])
+    s = ref.lev_build(f, 200, "random", make_rng(9))
+    put("lev_idx", s.indices)
+    put("lev_w", s.weights)
+
+
+def operators():
+    gen = np.random.default_rng(101)
+    # ts_apply_rhs dense + sparse
+    op = ref.TensorSketchOp.build((6, 5), 16, make_rng(1))
+    b = gen.standard_normal((30, 4))
+    put("rhs_b", b)
+    put("rhs_dense", ref.ts_apply_rhs(op, b))
+    bs = sp.random(30, 4, density=0.3, random_state=3, format="csr")
+    put("rhs_bs", bs.toarray())
+    put("rhs_sparse", ref.ts_apply_rhs(op, bs))
+    # ts_apply_kron over several m (direct for m<64, fft otherwise)
+    for m, ext in ((3, (4, 4)), (8, (4, 4)), (16, (5, 3, 4)), (64, (5, 3, 4)), (400, (30, 20))):
+        opk = ref.TensorSketchOp.build(ext, m, make_rng(200 + m))
+        fs = [gen.standard_normal((s, 2)) for s in ext]
+        for k, fk in enumerate(fs):
+            put(f"kron_m{m}_f{k}", fk)
+        put(f"kron_m{m}", ref.ts_apply_kron(opk, fs))
+    # composite sketch dense + sparse
+    c = ref.CompositeSketchOp.build(50, 4, 20, make_rng(4))
+    mat = gen.standard_normal((7, 50))
+    put("comp_mat", mat)
+    put("comp_dense", ref.composite_apply(mat, c))
+    ms = sp.csr_matrix(mat * (np.abs(mat) > 0.8))
+    put("comp_sparse", ref.composite_apply(ms, c))
+    # lev_apply dense + sparse
+    f = [orthonormal(8, 2, gen), orthonormal(6, 3, gen)]
+    bt = gen.standard_normal((48, 5))
+    put("levapp_f0", f[0])
+    put("levapp_f1", f[1])
+    put("levapp_bt", bt)
+    s = ref.lev_build(f, 30, "random", make_rng(12))
+    z, y = ref.lev_apply(s, f, bt)
+    put("levapp_idx", s.indices)
+    put("levapp_w", s.weights)
+    put("levapp_z", z)
+    put("levapp_y", y)
+    bts = sp.csr_matrix(bt * (np.abs(bt) > 1.0))
+    _, ys = ref.lev_apply(s, f, bts)
+    put("levapp_ys", ys)
+    # rsvd_lrls
+    z = gen.standard_normal((40, 6))
+    y = gen.standard_normal((40, 30))
+    ct, v = ref.rsvd_lrls(z, y, 2, make_rng(2))
+    put("rsvd_z", z)
+    put("rsvd_y", y)
+    put("rsvd_core_t", ct)
+    put("rsvd_v", v)
+    # init_rrf
+    tn = gen.standard_normal((25, 120))
+    put("rrf_tn", tn)
+    put("rrf_u", ref.init_rrf(tn, 4, 8, make_rng(6)))
+    # fitness
+    t = gen.standard_normal((6, 5, 4))
+    core = gen.standard_normal((2, 2, 2))
+    fs = [orthonormal(s, 2, gen) for s in t.shape]
+    put("fit_t", t)
+    put("fit_core", core)
+    for k, fk in enumerate(fs):
+        put(f"fit_a{k}", fk)
+    put("fit_dense", ref.fitness(t, ref.TuckerModel(core, fs)))
+    st = ref.SparseTensor.from_dense(t * (np.abs(t) > 0.7))
+    put("fit_sparse", ref.fitness(st, ref.TuckerModel(core, fs)))
+    cpf = [gen.standard_normal((s, 3)) for s in t.shape]
+    for k, fk in enumerate(cpf):
+        put(f"fitcp_a{k}", fk)
+    put("fitcp_w", np.array([1.5, -0.5, 0.25]))
+    put("fitcp_dense", ref.fitness(t, ref.CPModel(cpf, np.array([1.5, -0.5, 0.25]))))
+    put("fitcp_sparse", ref.fitness(st, ref.CPModel(cpf, np.array([1.5, -0.5, 0.25]))))
+
+
+def store_run(tag, model, trace):
+    put(f"{tag}_core", model.core)
+    for k, a in enumerate(model.factors):
+        put(f"{tag}_a{k}", a)
+    put(f"{tag}_fitness", np.array(trace.fitness))
+    put(f"{tag}_residuals", np.array(trace.residuals))
+
+
+DRIVER_CASES = {
+    # tag: (input spec, config kwargs)
+    "cfg1": (("dense", (100, 100, 100), 5, 1e-2, 0),
+             dict(ranks=(5, 5, 5), max_sweeps=5, sketch="tensorsketch", sketch_factor=16, seed=0)),
+    "dlev": (("dense", (30, 30, 30), 3, 1e-2, 1),
+             dict(ranks=(3, 3, 3), max_sweeps=3, sketch="leverage-random", sketch_size=144, seed=0)),
+    "d4ts": (("dense", (12, 12, 12, 12), 2, 1e-3, 2),
+             dict(ranks=(2, 2, 2, 2), max_sweeps=3, sketch="tensorsketch", sketch_size=64, seed=0)),
+    "sts": (("sparse", (40, 40, 40), 3000, 3),
+            dict(ranks=(4, 4, 4), max_sweeps=3, sketch="tensorsketch", sketch_size=256, seed=0)),
+    "slev": (("sparse", (40, 40, 40), 3000, 4),
+             dict(ranks=(4, 4, 4), max_sweeps=3, sketch="leverage-random", sketch_size=256, seed=0)),
+}
+
+
+def make_input(spec):
+    if spec[0] == "dense":
+        _, shape, r, noise, seed = spec
+        return planted_tucker_dense(shape, r, noise, seed)
+    _, shape, nnz, seed = spec
+    c, v = planted_cp_coo_host(shape, nnz, rank=3, seed=seed)
+    return ref.SparseTensor(shape, c, v)
+
+
+def drivers():
+    for tag, (spec, cfg) in DRIVER_CASES.items():
+        t = make_input(spec)
+        model, trace = ref.sketched_tucker_als(t, ref.TuckerConfig(**cfg))
+        store_run(tag, model, trace)
+    # CP via Tucker compression (reference ties Tucker ranks to the CP rank)
+    c, v = planted_cp_coo_host((30, 30, 30), 4000, rank=3, seed=5)
+    st = ref.SparseTensor((30, 30, 30), c, v)
+    cfg = ref.CPConfig(rank=3, sketch="leverage-random", sketch_factor=16,
+                       tucker_sweeps=3, max_sweeps=10, seed=11)
+    model, trace = ref.cp_via_sketched_tucker(st, cfg)
+    for k, a in enumerate(model.factors):
+        put(f"cpt_a{k}", a)
+    put("cpt_w", model.weights)
+    put("cpt_fitness", np.array(trace.fitness))
+    put("cpt_residuals", np.array(trace.residuals))
+    put("cpt_split", np.array(trace.stage_split))
+
+
+def main():
+    tables()
+    operators()
+    drivers()
+    path = os.path.join(HERE, "golden.npz")
+    np.savez_compressed(path, **OUT)
+    print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")
+
+
+if __name__ == "__main__":
+    main()
