@@ -1,0 +1,213 @@
+/*
+ * skx.h -- C ABI of libskx, the B200 (sm_100a) implementation of the hot path
+ * of the sketched Tucker-ALS algorithm (arXiv 2104.01101) whose reference is
+ * the pure-Python package `sketchals` (/root/reference/pkg/src/sketchals,
+ * cited as src/<file>:<line>).
+ *
+ * The reference has no FFI: its boundary is the Python function API re-exported
+ * by src/__init__.py:3-69.  The Python package paper_2104_01101_b200 keeps that
+ * API verbatim and binds these entry points with ctypes (INTEGRATION.md shows
+ * the binding).  Each entry cites the reference function it replaces.
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless its name ends in _h;
+ *  - every call takes the cudaStream_t `stream` (as void*) and is asynchronous;
+ *  - no hidden allocations: calls that need scratch take (ws, ws_bytes); pass
+ *    ws = NULL to query the required size, returned in *ws_bytes;
+ *  - return codes: 0 ok, 1 invalid argument (-> ValueError), 2 rank deficient
+ *    (-> RankDeficientError), 3 CUDA error; skx_last_error() has the message;
+ *  - matrices are row-major float64; index arrays int32 unless stated;
+ *  - "packed table": uint32 per index, low 31 bits = bucket, bit 31 = sign -1.
+ *
+ * Random streams follow numpy 2.3.5 Generator(Philox) exactly: raw u64 number p
+ * of a stream with key (k0,k1) is word p%4 of Philox4x64-10 at counter
+ * (p/4+1,0,0,0).  The host keeps numpy's Generator state and hands the device
+ * (key, raw position, buffered-uint32 flag and value).
+ */
+#ifndef SKX_H_
+#define SKX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKX_OK 0
+#define SKX_EINVAL 1
+#define SKX_ERANK 2
+#define SKX_ECUDA 3
+
+const char* skx_last_error(void);
+/* number of kernels libskx has launched since load (all threads) */
+long long skx_launch_count(void);
+int skx_version(void);
+
+/* ---------------------------------------------------------------- K0: RNG */
+
+/* Generator.random(n) from raw position p0 (numpy next_double).
+ * Replaces the draws inside rng.choice at src/sketching.py:211. */
+int skx_philox_uniform(uint64_t k0, uint64_t k1, uint64_t p0, int64_t n, double* out,
+                       void* stream);
+
+/* Generator.standard_normal(n) (numpy 256-level ziggurat, bit-exact) starting
+ * at the raw position *p0 (device u64); writes the position after the last
+ * consumed draw to *p_end (device u64; may alias p0).
+ * Replaces rng.standard_normal at src/linalg.py:107 and src/sketching.py:323. */
+int skx_philox_normal(uint64_t k0, uint64_t k1, const uint64_t* p0, int64_t n, double* out,
+                      uint64_t* p_end, void* ws, size_t* ws_bytes, void* stream);
+
+/* Lemire rejection scan for Generator.integers(0, k, .): lists (unordered)
+ * every draw index q in [0, n_u32) of the u32 run (raw start p0, optional
+ * buffered high half) that numpy would reject.  Count written to *count
+ * (device int64); positions beyond cap are counted but not stored.
+ * Used to place RRF CountSketch tables (src/sketching.py:54-56). */
+int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
+                    uint32_t pending, uint64_t n_u32, uint32_t k, uint64_t* rej, int64_t cap,
+                    unsigned long long* count, void* stream);
+
+/* ------------------------------------------------- K1/K2: TensorSketch */
+
+/* Packed per-mode tables from the polynomial-hash coefficients drawn on the
+ * host (4 hash then 5 sign coefficients per mode, coeffs_h = nmodes x 9).
+ * Replaces _poly_hash/_hash_family/_sign_family, src/sketching.py:25-43,80-86.
+ * tab receives sum(extents) entries, mode after mode. */
+int skx_ts_tables(int nmodes, const int64_t* extents_h, const int64_t* coeffs_h, int64_t m,
+                  uint32_t* tab, void* stream);
+
+/* Y^T = (S . T_(n)^T)^T for a COO tensor in "fibre-major" layout for mode n:
+ * nonzeros sorted by (i_n, other modes ascending); colptr (int64, s_n+1);
+ * oth = (N-1) x nnz SoA int32 coordinates of the other modes (ascending);
+ * tab = packed tables of the other modes concatenated, tab_off_h offsets.
+ * yt is s_n x m (row i_n = column i_n of the reference's m x s_n output).
+ * Replaces ts_apply_rhs sparse branch, src/sketching.py:150-167. */
+int skx_ts_rhs_coo(int n_other, int64_t nnz, int64_t s_n, const int64_t* colptr,
+                   const int32_t* oth, const double* vals, const uint32_t* tab,
+                   const int64_t* tab_off_h, int64_t m, double* yt, void* stream);
+
+/* Same for a dense C-order tensor (ndim, shape_h) and target mode.
+ * Replaces ts_apply_rhs dense branch, src/sketching.py:168-175. */
+int skx_ts_rhs_dense(const double* t, int ndim, const int64_t* shape_h, int mode,
+                     const uint32_t* tab, const int64_t* tab_off_h, int64_t m, double* yt,
+                     void* ws, size_t* ws_bytes, void* stream);
+
+/* Composed packed table over all P = prod(ext) rows of the chain (first mode
+ * slowest): bucket = sum of per-mode buckets mod m, sign = product
+ * (src/sketching.py:92-102).  Lets a dense (P x c) right-hand side be
+ * sketched by skx_rrf_stage1_dense. */
+int skx_ts_combine(int n, const int64_t* ext_h, const uint32_t* tab, const int64_t* tab_off_h,
+                   int64_t m, int64_t P, uint32_t* out, void* stream);
+
+/* Z = S . kron(A_1, ..., A_k) (first factor slowest), m x prod(R), written
+ * COLUMN-major (z[col*m + row]) -- the layout cuSOLVER's QR consumes.
+ * factors_h: host array of device pointers to s_k x R_k row-major factors.
+ * Replaces ts_apply_kron, src/sketching.py:113-147 (exact circular convolution
+ * instead of FFT; equal up to rounding). */
+int skx_ts_kron(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
+                const double* const* factors_h, const uint32_t* tab, const int64_t* tab_off_h,
+                int64_t m, double* z, void* ws, size_t* ws_bytes, void* stream);
+
+/* ------------------------------------------------------ K3: leverage */
+
+/* p = max(scores,0)/sum, cdf = cumsum(p)/cdf[-1] (src/sketching.py:207-210 and
+ * numpy Generator.choice).  */
+int skx_lev_prepare(const double* scores, int64_t s, double* p, double* cdf, void* ws,
+                    size_t* ws_bytes, void* stream);
+
+/* Draw m samples per mode: for mode k, uniforms at raw positions
+ * p0 + k*m + j; idx[j*n_other+k] = searchsorted(cdf_k, u, 'right');
+ * w[j] = 1/sqrt(m * prod_k p_k[idx]).  src/sketching.py:211-216. */
+int skx_lev_sample(int n_other, const int64_t* ext_h, const double* const* p_h,
+                   const double* const* cdf_h, int64_t m, uint64_t k0, uint64_t k1, uint64_t p0,
+                   int64_t* idx, double* w, void* stream);
+
+/* Z[j,:] = w_j kron_k A_k[idx_jk,:], column-major m x prod(R)
+ * (src/sketching.py:280-285). */
+int skx_kron_rows(int n_other, const int64_t* ranks_h, const double* const* factors_h,
+                  const int64_t* idx, const double* w, int64_t m, double* z, void* stream);
+
+/* Y[j,:] = w_j * T_(n)^T[flat_j,:] for a dense tensor (src/sketching.py:262-266). */
+int skx_gather_fibers_dense(const double* t, int ndim, const int64_t* shape_h, int mode,
+                            const int64_t* idx, const double* w, int64_t m, double* y,
+                            void* stream);
+
+/* Sparse fibre gather.  keys: per-mode "other-major" layout sorted by
+ * key = flat_other * s_n + i_n (int64), vals matching.  Sample j's hits are
+ * hit_col/hit_val[hit_off[j] .. hit_off[j+1]) (i_n ascending, value w_j*v);
+ * hit_off has m+1 entries, hit_off[m] = total (entries past cap dropped).
+ * Deterministic (count, scan, write).  src/sketching.py:262-264. */
+int skx_gather_fibers_coo(int n_other, const int64_t* ext_h, int64_t s_n, int64_t nnz,
+                          const int64_t* keys, const double* vals, const int64_t* idx,
+                          const double* w, int64_t m, int64_t* hit_off, int64_t* hit_col,
+                          double* hit_val, int64_t cap, void* ws, size_t* ws_bytes, void* stream);
+
+/* ------------------------------------------------- K4: range finder */
+
+/* stage1[i_n, c] = sum_j T_(n)[i_n, j] sign_j [hash_j == c] where hash/sign are
+ * the numpy draws integers(0,k2,P) then integers(0,2,P) of the u32 run
+ * (p0, has_pending, pending), hash draws shifted past the sorted rejection
+ * list rej (nrej entries).  COO input in fibre-major layout (as ts_rhs_coo).
+ * Replaces CountSketchOp.build + composite_apply stage 1, src/sketching.py:
+ * 54-56, 327-340. */
+int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t nnz, int64_t s_n,
+                       const int64_t* colptr, const int32_t* oth, const double* vals,
+                       uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
+                       uint32_t pending, uint64_t sign_q0, const uint64_t* rej, int64_t nrej,
+                       int64_t k2, double* stage1, void* stream);
+
+/* Fill n u64 with UINT64_MAX (pre-fill of a rejection buffer). */
+int skx_fill_u64max(uint64_t* a, int64_t n, void* stream);
+
+/* Sort the rejection list of skx_lemire_scan (cap entries, pre-filled with
+ * UINT64_MAX) into the d-array d_i = r_i - i (padded with UINT64_MAX) and
+ * write #{d_i <= P-1} -- the rejections among the first P accepted draws --
+ * to *n_le (device u64).  The sign run then starts at u32 index P + *n_le. */
+int skx_lemire_finish(uint64_t* rej, const unsigned long long* count, int64_t cap, uint64_t P,
+                      uint64_t* d, unsigned long long* n_le, void* ws, size_t* ws_bytes,
+                      void* stream);
+
+/* Materialise the packed (hash|sign) table for columns [0, P) (dense inputs). */
+int skx_rrf_table(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
+                  uint32_t pending, uint64_t sign_q0, const uint64_t* rej, int64_t nrej,
+                  int64_t P, int64_t k2, uint32_t* tab, void* stream);
+
+/* Dense stage 1 given a full packed table over the P_n columns (s_n x k2 out). */
+int skx_rrf_stage1_dense(const double* t, int ndim, const int64_t* shape_h, int mode,
+                         const uint32_t* tab, int64_t k2, double* stage1, void* ws,
+                         size_t* ws_bytes, void* stream);
+
+/* --------------------------------------- K5/K7: residual and fitness */
+
+/* out[0] = || P a^T - Y ||_F^2 with P (m x R), a (s x R), Y addressed as
+ * Y[j,i] = y[j*ys_j + i*ys_i] (covers Y and Y^T storage).  src/tucker.py:274. */
+int skx_resid_sq(const double* p, const double* a, int64_t m, int64_t s, int64_t R,
+                 const double* y, int64_t ys_j, int64_t ys_i, double* out, void* ws,
+                 size_t* ws_bytes, void* stream);
+
+/* out[0] = sum(x^2) with a fixed-order reduction. */
+int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,
+              void* stream);
+
+/* Tucker cross term <ttmc(T,{A}), C> over a lexsorted COO tensor (coords =
+ * ndim x nnz SoA int32), factors_h device pointers (s_k x R_k), core C
+ * (C-order R_0 x ... x R_{N-1}); colptr0 (s_0+1 offsets of the mode-0 slices,
+ * may be NULL) enables the order-3 sliced kernel.  out[0] = cross.
+ * Replaces the sparse ttmc + vdot at src/tensors.py:249-258, 351-352. */
+int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h,
+                         int64_t nnz, const int32_t* coords, const double* vals,
+                         const double* const* factors_h, const double* core,
+                         const int64_t* colptr0, double* out, void* ws, size_t* ws_bytes,
+                         void* stream);
+
+/* CP cross term sum(weights * A_0 .* mttkrp(T, A, 0)) over lexsorted COO.
+ * Replaces src/tensors.py:354-357 (+ mttkrp :322-323). */
+int skx_cp_cross_coo(int ndim, const int64_t* shape_h, int64_t R, int64_t nnz,
+                     const int32_t* coords, const double* vals, const double* const* factors_h,
+                     const double* weights, double* out, void* ws, size_t* ws_bytes,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKX_H_ */

@@ -1,0 +1,191 @@
+"""CP via sketched Tucker compression (drop-in for the path of src/cp.py).
+
+``cp_via_sketched_tucker`` = Algorithm 6: sketched Tucker-ALS (leverage
+sampling) to compress, exact CP-ALS on the small core (hosvd-of-core init),
+then the factor chains multiplied back and renormalised, with the final
+fitness measured against the full tensor (src/cp.py:177-224).  ``cp_als`` is
+the exact normal-equations CP-ALS (src/cp.py:119-174) on a dense tensor held
+on the GPU -- used on the core.  ``sketched_cp_als`` (leverage-sampled CP on
+the full tensor) is a different algorithm outside this build's path.
+
+Extension: ``CPConfig.tucker_rank`` (default None = the reference's tie of the
+Tucker ranks to the CP rank) lets config 5 of BASELINE.json request Tucker
+rank 20 with CP rank 10.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import rng as rngmod
+from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, shape_of)
+from .tucker import SweepTrace, TuckerConfig, hosvd_init_dev, sketched_tucker_als_dev
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class CPConfig:
+    rank: int
+    max_sweeps: int | None = None
+    sketch: str | None = None
+    sketch_size: int | None = None
+    sketch_factor: float | None = None
+    init: str | None = None
+    seed: int = 0
+    tucker_sweeps: int = 5
+    tucker_rank: int | None = None
+
+    def __post_init__(self):
+        if self.sketch not in (None, "leverage-random"):
+            raise ValueError(f"unknown sketch kind {self.sketch!r} for CP")
+
+    def resolved_sweeps(self, on_core=False):
+        if self.max_sweeps is not None:
+            return self.max_sweeps
+        return 25 if on_core else 30
+
+    def resolved_sketch_size(self):
+        if self.sketch_size is not None:
+            return int(self.sketch_size)
+        if self.sketch_factor is not None:
+            return int(math.ceil(self.sketch_factor * self.rank ** 2))
+        raise ValueError("sketched CP needs sketch_size or sketch_factor")
+
+
+def _normalize_columns_dev(a):
+    torch = _torch()
+    nrm = torch.linalg.vector_norm(a, dim=0)
+    safe = torch.where(nrm > 0, nrm, torch.ones_like(nrm))
+    return a / safe, nrm
+
+
+def _mttkrp_dense_dev(t, factors, n):
+    nd = t.dim()
+    others = [k for k in range(nd) if k != n]
+    R = factors[others[0]].shape[1]
+    kr = factors[others[0]]
+    for k in others[1:]:
+        kr = (kr[:, None, :] * factors[k][None, :, :]).reshape(-1, R)
+    return t.movedim(n, 0).reshape(t.shape[n], -1) @ kr
+
+
+def cp_als_dev(t, config, on_core=False):
+    """Exact CP-ALS on a dense CUDA tensor (src/cp.py:119-174, unsketched)."""
+    torch = _torch()
+    shape = tuple(t.shape)
+    ndim = len(shape)
+    rank = config.rank
+    if rank < 1:
+        raise ValueError("rank must be positive")
+    norm_t2 = (t * t).sum()
+    nt2 = float(norm_t2.item())
+    if nt2 == 0.0:
+        raise ValueError("CP decomposition of a zero-norm tensor is undefined")
+    rng_init, _ = rngmod.split_rng(config.seed, 2)
+    init = config.init or ("hosvd-of-core" if on_core else "rrf")
+    if init == "hosvd-of-core":
+        factors = hosvd_init_dev(t, [min(rank, s) for s in shape])
+    elif init == "random":
+        factors = [torch.from_numpy(rng_init.uniform(size=(shape[n], rank))).cuda() for n in range(ndim)]
+    elif init == "rrf":
+        # src/cp.py:72-87 with the rrf width of src/cp.py:559-564
+        from .tucker import init_rrf_dev
+        width = None
+        if config.sketch_factor is not None:
+            width = max(rank, int(math.ceil(math.sqrt(config.sketch_factor) * rank)))
+        elif config.sketch_size is not None:
+            width = max(rank, int(math.ceil(math.sqrt(config.sketch_size / rank ** 2) * rank)))
+        width = width or max(rank + 8, 2 * rank)
+        factors = []
+        for n in range(ndim):
+            if shape[n] > rank:
+                factors.append(init_rrf_dev(t, n, rank, min(width, shape[n]), rng_init))
+            else:
+                g = torch.from_numpy(rng_init.standard_normal((shape[n], rank))).cuda()
+                factors.append(torch.linalg.qr(g, mode="reduced")[0].contiguous())
+    else:
+        raise ValueError(f"unknown init {init!r} for CP")
+    weights = torch.ones(rank, dtype=torch.float64, device="cuda")
+    grams = [a.t() @ a for a in factors]
+    res_dev, fit_dev, walls = [], [], []
+    for _ in range(config.resolved_sweeps(on_core)):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for n in range(ndim):
+            go = torch.ones((rank, rank), dtype=torch.float64, device="cuda")
+            for k in range(ndim):
+                if k != n:
+                    go = go * grams[k]
+            mm = _mttkrp_dense_dev(t, factors, n)
+            sc = mm @ torch.linalg.pinv(go, rtol=1e-12)
+            cross = (sc * mm).sum()
+            mod = ((sc.t() @ sc) * go).sum()
+            res_dev.append(torch.sqrt(torch.clamp(norm_t2 - 2.0 * cross + mod, min=0.0)))
+            factors[n], weights = _normalize_columns_dev(sc)
+            grams[n] = factors[n].t() @ factors[n]
+        fit_dev.append(fitness_cp_dev(t, factors, weights, norm_t2))
+        e1.record()
+        walls.append((e0, e1))
+    torch.cuda.synchronize()
+    trace = SweepTrace(fitness=torch.stack(fit_dev).cpu().tolist(),
+                       residuals=torch.stack(res_dev).cpu().tolist(),
+                       wall_s=[a.elapsed_time(b) / 1e3 for a, b in walls])
+    return factors, weights, trace
+
+
+def cp_als(t, config, on_core=False):
+    """Exact CP-ALS (src/cp.py:102-107) for dense tensors on the GPU."""
+    if config.sketch is not None:
+        raise ValueError("cp_als is the unsketched driver; got a sketch config")
+    d = device_of(t)
+    if is_sparse_dev(d):
+        raise NotImplementedError("direct CP-ALS on a sparse tensor is outside this build's hot path")
+    factors, weights, trace = cp_als_dev(d, config, on_core=on_core)
+    return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
+
+
+def sketched_cp_als(t, config):
+    raise NotImplementedError("sketched_cp_als (leverage-sampled CP on the full tensor) is outside "
+                              "this build's hot path (SURVEY 2.1 / 8f)")
+
+
+def cp_via_sketched_tucker(t, config):
+    """CP through sketched Tucker compression (Alg. 6, src/cp.py:177-224)."""
+    torch = _torch()
+    shape = tuple(int(s) for s in t.shape)
+    ndim = len(shape)
+    rank = config.rank
+    if any(rank > s for s in shape):
+        raise ValueError("rank exceeds a tensor extent")
+    if not config.sketch:
+        raise NotImplementedError("the exact-HOOI compression stage is outside this build's hot path")
+    seed_tucker, seed_cp = (s.generate_state(1)[0] for s in np.random.SeedSequence(config.seed).spawn(2))
+    tr_rank = rank if config.tucker_rank is None else int(config.tucker_rank)
+    tucker_cfg = TuckerConfig(ranks=(tr_rank,) * ndim, max_sweeps=config.tucker_sweeps,
+                              sketch="leverage-random", sketch_size=config.sketch_size,
+                              sketch_factor=config.sketch_factor, init="rrf", seed=int(seed_tucker))
+    d = device_of(t)
+    core, tfac, ttrace = sketched_tucker_als_dev(d, tucker_cfg)
+    core_cfg = replace(config, sketch=None, sketch_size=None, sketch_factor=None,
+                       init="hosvd-of-core", seed=int(seed_cp))
+    cfac, cw, ctrace = cp_als_dev(core, core_cfg, on_core=True)
+    weights = cw.clone()
+    out = []
+    for b, a in zip(tfac, cfac):
+        unit, nrm = _normalize_columns_dev(b @ a)
+        out.append(unit)
+        weights = weights * nrm
+    norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
+    fin = float(fitness_cp_dev(d, out, weights, norm2).item())
+    trace = SweepTrace(fitness=list(ttrace.fitness) + [fin], residuals=list(ctrace.residuals),
+                       wall_s=list(ttrace.wall_s) + [sum(ctrace.wall_s)],
+                       stage_split=len(ttrace.fitness))
+    return CPModel([a.cpu().numpy() for a in out], weights.cpu().numpy()), trace

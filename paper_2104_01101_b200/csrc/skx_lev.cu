@@ -1,0 +1,268 @@
+// K3: leverage-score row sampling of a Kronecker chain and the matching fibre
+// gather (src/sketching.py:193-217, 262-287; src/linalg.py:73-84).
+#include <cub/cub.cuh>
+
+#include "skx_common.cuh"
+
+namespace skx {
+
+// Single-CTA: p = max(s,0)/sum; cdf = cumsum(p); cdf /= cdf[-1].
+// Fixed-order chunked scan (deterministic; rounding differs from numpy's
+// sequential cumsum only in the last bits).
+__global__ void __launch_bounds__(1024) k_lev_prepare(const double* __restrict__ sc, int64_t s,
+                                                      double* __restrict__ p, double* __restrict__ cdf) {
+  __shared__ double part[1024];
+  __shared__ double total;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t per = (s + nt - 1) / nt;
+  const int64_t lo = imin(tid * per, s), hi = imin(lo + per, s);
+  double acc = 0.0;
+  for (int64_t i = lo; i < hi; ++i) acc += fmax(sc[i], 0.0);
+  part[tid] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < nt; ++i) t += part[i];
+    total = t;
+  }
+  __syncthreads();
+  const double tot = total;
+  double run = 0.0;
+  for (int64_t i = lo; i < hi; ++i) {
+    const double pi = fmax(sc[i], 0.0) / tot;
+    p[i] = pi;
+    run += pi;
+    cdf[i] = run;
+  }
+  __syncthreads();
+  part[tid] = run;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < nt; ++i) {
+      const double v = part[i];
+      part[i] = t;
+      t += v;
+    }
+  }
+  __syncthreads();
+  const double offs = part[tid];
+  for (int64_t i = lo; i < hi; ++i) cdf[i] += offs;
+  __syncthreads();
+  __shared__ double last;
+  if (tid == 0) last = cdf[s - 1];
+  __syncthreads();
+  const double L = last;
+  for (int64_t i = lo; i < hi; ++i) cdf[i] /= L;
+}
+
+struct PtrPack {
+  const double* p[15];
+  const double* c[15];
+  int64_t ext[15];
+};
+
+__global__ void k_lev_sample(int n_other, PtrPack pk, int64_t m, uint64_t k0, uint64_t k1,
+                             uint64_t p0, int64_t* __restrict__ idx, double* __restrict__ w) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double pp = 1.0;
+  for (int k = 0; k < n_other; ++k) {
+    const double u = u64_to_unit(philox_raw(k0, k1, p0 + (uint64_t)(k * m + j)));
+    // searchsorted(cdf, u, side='right'): first i with cdf[i] > u
+    const double* c = pk.c[k];
+    int64_t lo = 0, hi = pk.ext[k];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (c[mid] <= u) lo = mid + 1; else hi = mid;
+    }
+    if (lo >= pk.ext[k]) lo = pk.ext[k] - 1;  // unreachable: cdf[-1] == 1 > u
+    idx[j * n_other + k] = lo;
+    pp *= pk.p[k][lo];
+  }
+  w[j] = 1.0 / sqrt((double)m * pp);
+}
+
+struct FacPack {
+  const double* a[15];
+  int64_t R[15];
+};
+
+// z column-major (ld = m): z[col*m + j], col = (p_1, ..., p_k) first slowest.
+__global__ void k_kron_rows(int n_other, FacPack fp, int64_t r, const int64_t* __restrict__ idx,
+                            const double* __restrict__ w, int64_t m, double* __restrict__ z) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * r) return;
+  const int64_t j = e % m, col = e / m;
+  // decode col into per-mode column indices (last mode fastest)
+  int64_t rem = col;
+  int64_t pc[15];
+  for (int k = n_other - 1; k >= 0; --k) {
+    pc[k] = rem % fp.R[k];
+    rem /= fp.R[k];
+  }
+  double prod = fp.a[0][idx[j * n_other] * fp.R[0] + pc[0]];
+  for (int k = 1; k < n_other; ++k) prod *= fp.a[k][idx[j * n_other + k] * fp.R[k] + pc[k]];
+  z[e] = w[j] * prod;
+}
+
+// Y[j, i_n] = w_j * T[multi(flat_j) with i_n inserted], row-major m x s_n.
+struct ShapePack {
+  int ndim, mode;
+  int64_t shape[16];
+  int64_t stride[16];
+};
+
+__global__ void k_gather_dense(const double* __restrict__ t, ShapePack sp, int n_other,
+                               const int64_t* __restrict__ idx, const double* __restrict__ w,
+                               int64_t m, double* __restrict__ y) {
+  const int64_t s_n = sp.shape[sp.mode];
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * s_n) return;
+  const int64_t j = e / s_n, in = e - j * s_n;
+  int64_t off = in * sp.stride[sp.mode];
+  int kk = 0;
+  for (int k = 0; k < sp.ndim; ++k) {
+    if (k == sp.mode) continue;
+    off += idx[j * n_other + kk] * sp.stride[k];
+    ++kk;
+  }
+  y[e] = w[j] * t[off];
+}
+
+// ---- sparse gather: keys = flat_other * s_n + i_n, sorted ascending.
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t n, int64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_gather_coo_count(int n_other, PtrPack pk, int64_t s_n, int64_t nnz,
+                                   const int64_t* __restrict__ keys, const int64_t* __restrict__ idx,
+                                   int64_t m, int64_t* __restrict__ lo_out, int64_t* __restrict__ cnt) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  int64_t flat = 0;
+  for (int k = 0; k < n_other; ++k) flat = flat * pk.ext[k] + idx[j * n_other + k];
+  const int64_t a = lower_bound_i64(keys, nnz, flat * s_n);
+  const int64_t b = lower_bound_i64(keys, nnz, (flat + 1) * s_n);
+  lo_out[j] = a;
+  cnt[j] = b - a;
+}
+
+__global__ void k_gather_coo_write(const int64_t* __restrict__ keys, const double* __restrict__ vals,
+                                   int64_t s_n, const int64_t* __restrict__ lo_in,
+                                   const int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                                   const double* __restrict__ w, int64_t m, int64_t cap,
+                                   int64_t* __restrict__ hit_col, double* __restrict__ hit_val) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int64_t a = lo_in[j], c = cnt[j], o = off[j];
+  for (int64_t t = 0; t < c; ++t) {
+    if (o + t >= cap) break;
+    hit_col[o + t] = keys[a + t] % s_n;
+    hit_val[o + t] = w[j] * vals[a + t];
+  }
+}
+
+}  // namespace skx
+
+using namespace skx;
+
+extern "C" int skx_lev_prepare(const double* scores, int64_t s, double* p, double* cdf, void* ws,
+                               size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(s >= 1, "skx_lev_prepare: empty score vector");
+  if (ws_bytes && ws == nullptr) {
+    *ws_bytes = 0;
+    return SKX_OK;
+  }
+  k_lev_prepare<<<1, 1024, 0, (cudaStream_t)stream>>>(scores, s, p, cdf);
+  return check_launch("k_lev_prepare");
+}
+
+extern "C" int skx_lev_sample(int n_other, const int64_t* ext_h, const double* const* p_h,
+                              const double* const* cdf_h, int64_t m, uint64_t k0, uint64_t k1,
+                              uint64_t p0, int64_t* idx, double* w, void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_lev_sample: 1..15 modes");
+  SKX_REQUIRE(m >= 1, "skx_lev_sample: sample count must be positive");
+  PtrPack pk{};
+  for (int k = 0; k < n_other; ++k) {
+    pk.p[k] = p_h[k];
+    pk.c[k] = cdf_h[k];
+    pk.ext[k] = ext_h[k];
+  }
+  k_lev_sample<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_other, pk, m, k0, k1,
+                                                                              p0, idx, w);
+  return check_launch("k_lev_sample");
+}
+
+extern "C" int skx_kron_rows(int n_other, const int64_t* ranks_h, const double* const* factors_h,
+                             const int64_t* idx, const double* w, int64_t m, double* z,
+                             void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_kron_rows: 1..15 modes");
+  FacPack fp{};
+  int64_t r = 1;
+  for (int k = 0; k < n_other; ++k) {
+    fp.a[k] = factors_h[k];
+    fp.R[k] = ranks_h[k];
+    r *= ranks_h[k];
+  }
+  const int64_t n = m * r;
+  if (n == 0) return SKX_OK;
+  k_kron_rows<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_other, fp, r, idx, w,
+                                                                              m, z);
+  return check_launch("k_kron_rows");
+}
+
+extern "C" int skx_gather_fibers_dense(const double* t, int ndim, const int64_t* shape_h, int mode,
+                                       const int64_t* idx, const double* w, int64_t m, double* y,
+                                       void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 16 && mode >= 0 && mode < ndim, "skx_gather_fibers_dense: bad mode");
+  ShapePack sp{};
+  sp.ndim = ndim;
+  sp.mode = mode;
+  int64_t st = 1;
+  for (int k = ndim - 1; k >= 0; --k) {
+    sp.shape[k] = shape_h[k];
+    sp.stride[k] = st;
+    st *= shape_h[k];
+  }
+  const int64_t n = m * shape_h[mode];
+  if (n == 0) return SKX_OK;
+  k_gather_dense<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(t, sp, ndim - 1, idx,
+                                                                                 w, m, y);
+  return check_launch("k_gather_dense");
+}
+
+extern "C" int skx_gather_fibers_coo(int n_other, const int64_t* ext_h, int64_t s_n, int64_t nnz,
+                                     const int64_t* keys, const double* vals, const int64_t* idx,
+                                     const double* w, int64_t m, int64_t* hit_off, int64_t* hit_col,
+                                     double* hit_val, int64_t cap, void* ws, size_t* ws_bytes,
+                                     void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_gather_fibers_coo: 1..15 modes");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_gather_fibers_coo: ws_bytes is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  Arena ar(ws, *ws_bytes);
+  int64_t* lo = ar.take<int64_t>(m);
+  int64_t* cnt = ar.take<int64_t>(m + 1);
+  size_t cb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cb, cnt, hit_off, (int)(m + 1), s);
+  void* tmp = ar.take<char>(cb);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_gather_fibers_coo: workspace too small");
+  PtrPack pk{};
+  for (int k = 0; k < n_other; ++k) pk.ext[k] = ext_h[k];
+  const unsigned g = (unsigned)((m + 255) / 256);
+  cudaMemsetAsync(cnt + m, 0, sizeof(int64_t), s);
+  k_gather_coo_count<<<g, 256, 0, s>>>(n_other, pk, s_n, nnz, keys, idx, m, lo, cnt);
+  cub::DeviceScan::ExclusiveSum(tmp, cb, cnt, hit_off, (int)(m + 1), s);
+  k_gather_coo_write<<<g, 256, 0, s>>>(keys, vals, s_n, lo, cnt, hit_off, w, m, cap, hit_col,
+                                       hit_val);
+  return check_launch("gather_fibers_coo", 3);
+}

@@ -1,0 +1,202 @@
+// K4: randomized range finder, CountSketch stage (src/sketching.py:54-56,
+// 305-341; src/tucker.py:129-144).
+//
+// numpy draws hash = integers(0, k2, P) then sign = integers(0, 2, P) from
+// rng_init.  Column j's hash is the j-th *accepted* Lemire draw: with the
+// sorted rejection positions r_0 < r_1 < ... (skx_lemire_scan) and
+// d_i = r_i - i, its u32 index is q(j) = j + #{i : d_i <= j}.  k = 2 never
+// rejects, so sign j sits at u32 index sign_q0 + j.  The P_n-long tables of
+// the reference (160-640 GB at configs 4-5) are never materialised for COO
+// inputs: each nonzero evaluates its two Philox blocks on the fly.
+#include <cub/cub.cuh>
+
+#include "skx_common.cuh"
+
+namespace skx {
+
+__global__ void k_rej_to_d(const uint64_t* __restrict__ sorted, const unsigned long long* count,
+                           int64_t cap, uint64_t* __restrict__ d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= cap) return;
+  const int64_t n = (int64_t)umin64(*count, (unsigned long long)cap);
+  d[i] = i < n ? sorted[i] - (uint64_t)i : ~0ULL;
+}
+
+__global__ void k_fill_max(uint64_t* a, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = ~0ULL;
+}
+
+__device__ __forceinline__ uint64_t count_le(const uint64_t* d, int64_t n, uint64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (d[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return (uint64_t)lo;
+}
+
+__global__ void k_count_le(const uint64_t* __restrict__ d, int64_t n, uint64_t v,
+                           unsigned long long* out) {
+  *out = count_le(d, n, v);
+}
+
+struct RrfRng {
+  U32Stream st;
+  uint64_t sign_q0;
+  const uint64_t* d;
+  int64_t nd;
+  uint32_t k2;
+};
+
+__device__ __forceinline__ uint32_t rrf_entry(const RrfRng& r, uint64_t j) {
+  const uint64_t q = j + count_le(r.d, r.nd, j);
+  const uint32_t hu = r.st.at(q);
+  const uint32_t h = (uint32_t)(((uint64_t)hu * r.k2) >> 32);
+  const uint32_t su = r.st.at(r.sign_q0 + j);
+  return h | (su & 0x80000000u);  // integers(0,2) = u >> 31; sign = 1 - 2g
+}
+
+__global__ void k_rrf_table(RrfRng r, int64_t P, uint32_t* __restrict__ tab) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; j < P; j += stride) tab[j] = rrf_entry(r, (uint64_t)j);
+}
+
+// Fibre-major COO: warp per column i_n, warp-private k2 accumulator; ordered.
+struct OthExt {
+  int n;
+  int64_t ext[15];
+};
+
+template <int U>
+__global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t nnz, int64_t s_n,
+                                                 const int64_t* __restrict__ colptr,
+                                                 const int32_t* __restrict__ oth,
+                                                 const double* __restrict__ vals,
+                                                 double* __restrict__ st1) {
+  extern __shared__ double smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int64_t k2 = r.k2;
+  double* acc = smem + (size_t)wid * (k2 + 32);
+  double* stage = acc + k2;
+  const int64_t gw = blockIdx.x * (int64_t)nw + wid;
+  const int64_t tw = (int64_t)gridDim.x * nw;
+  for (int64_t col = gw; col < s_n; col += tw) {
+    for (int64_t h = lane; h < k2; h += 32) acc[h] = 0.0;
+    __syncwarp();
+    const int64_t e0 = colptr[col], e1 = colptr[col + 1];
+    for (int64_t base = e0; base < e1; base += 32 * U) {
+      uint32_t bk[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = base + u * 32 + lane;
+        bk[u] = kNoBucket;
+        v[u] = 0.0;
+        if (e < e1) {
+          uint64_t j = 0;
+          for (int k = 0; k < oe.n; ++k) j = j * (uint64_t)oe.ext[k] + (uint64_t)oth[(int64_t)k * nnz + e];
+          const uint32_t t = rrf_entry(r, j);
+          bk[u] = pk_bucket(t);
+          const double x = vals[e];
+          v[u] = pk_neg(t) ? -x : x;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], v[u], stage);
+    }
+    double* dst = st1 + col * k2;
+    for (int64_t h = lane; h < k2; h += 32) dst[h] = acc[h];
+    __syncwarp();
+  }
+}
+
+}  // namespace skx
+
+using namespace skx;
+
+// Sort the scan output and turn it into the d-array (length cap, padded with
+// UINT64_MAX); *n_le receives #{d_i <= P-1} = rejections among the P hash
+// draws, i.e. the sign run starts at u32 index P + *n_le.
+extern "C" int skx_lemire_finish(uint64_t* rej, const unsigned long long* count, int64_t cap,
+                                 uint64_t P, uint64_t* d, unsigned long long* n_le, void* ws,
+                                 size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_lemire_finish: ws_bytes is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  Arena ar(ws, *ws_bytes);
+  uint64_t* sorted = ar.take<uint64_t>(cap);
+  size_t cb = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, cb, rej, sorted, (int)cap, 0, 64, s);
+  void* tmp = ar.take<char>(cb);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_lemire_finish: workspace too small");
+  // entries beyond count were never written: neutralise them before sorting
+  // (the caller pre-fills rej with UINT64_MAX via skx_fill_u64max).
+  cub::DeviceRadixSort::SortKeys(tmp, cb, rej, sorted, (int)cap, 0, 64, s);
+  k_rej_to_d<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(sorted, count, cap, d);
+  k_count_le<<<1, 1, 0, s>>>(d, cap, P - 1, n_le);
+  return check_launch("skx_lemire_finish", 3);
+}
+
+extern "C" int skx_fill_u64max(uint64_t* a, int64_t n, void* stream) {
+  if (n <= 0) return SKX_OK;
+  k_fill_max<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(a, n);
+  return check_launch("k_fill_max");
+}
+
+static RrfRng make_rng(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending, uint32_t pending,
+                       uint64_t sign_q0, const uint64_t* d, int64_t nd, int64_t k2) {
+  RrfRng r;
+  r.st.k0 = k0;
+  r.st.k1 = k1;
+  r.st.p0 = p0;
+  r.st.has_pending = has_pending;
+  r.st.pending = pending;
+  r.sign_q0 = sign_q0;
+  r.d = d;
+  r.nd = nd;
+  r.k2 = (uint32_t)k2;
+  return r;
+}
+
+extern "C" int skx_rrf_table(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
+                             uint32_t pending, uint64_t sign_q0, const uint64_t* rej, int64_t nrej,
+                             int64_t P, int64_t k2, uint32_t* tab, void* stream) {
+  SKX_REQUIRE(k2 >= 1 && k2 < (int64_t(1) << 31), "skx_rrf_table: k2 out of range");
+  if (P == 0) return SKX_OK;
+  RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
+  int blocks = (int)imin((P + 255) / 256, (int64_t)num_sms() * 16);
+  k_rrf_table<<<blocks, 256, 0, (cudaStream_t)stream>>>(r, P, tab);
+  return check_launch("k_rrf_table");
+}
+
+extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t nnz, int64_t s_n,
+                                  const int64_t* colptr, const int32_t* oth, const double* vals,
+                                  uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
+                                  uint32_t pending, uint64_t sign_q0, const uint64_t* rej,
+                                  int64_t nrej, int64_t k2, double* stage1, void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_rrf_stage1_coo: 1..15 other modes");
+  const int64_t per = (k2 + 32) * 8;
+  int nw = (int)imin(8, (int64_t)(max_smem_optin() - 1024) / per);
+  SKX_REQUIRE(nw >= 1, "skx_rrf_stage1_coo: k2 too large for shared memory");
+  if (s_n == 0) return SKX_OK;
+  RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
+  OthExt oe{};
+  oe.n = n_other;
+  for (int k = 0; k < n_other; ++k) oe.ext[k] = ext_h[k];
+  const size_t smem = (size_t)nw * per;
+  auto kern = k_rrf_coo<2>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t blocks = imin((int64_t)num_sms() * per_sm, (s_n + nw - 1) / nw);
+  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(r, oe, nnz, s_n, colptr, oth, vals,
+                                                                  stage1);
+  return check_launch("k_rrf_coo");
+}

@@ -1,0 +1,655 @@
+// K1/K2: TensorSketch (src/sketching.py:25-43, 67-175) and the shared
+// "sketch a tensor unfolding" machinery also used by the range finder (K4).
+//
+// Layout of every sketch output: Y^T, s_n x m row-major (row i_n holds the
+// reference's column i_n of the m x s_n sketch), so one i_n owns one
+// contiguous m-vector.
+//
+// Determinism: no floating-point atomics anywhere.  Each output vector is
+// owned by one warp (sparse, gather) or built from per-warp shared-memory
+// accumulators reduced in a fixed order (dense rows), so results are bitwise
+// reproducible run to run (pkg/tests/test_tucker.py:200-209 demands that).
+#include <cub/cub.cuh>
+
+#include "skx_common.cuh"
+
+namespace skx {
+
+// =========================================================== table building
+struct Coeffs {
+  int nmodes;
+  int64_t ext[16];
+  int64_t off[16];
+  int64_t c[16][9];
+};
+
+__device__ __forceinline__ uint64_t horner(const int64_t* c, int nc, uint64_t x) {
+  const uint64_t P = 2147483647ULL;
+  uint64_t acc = (uint64_t)c[0];
+  for (int i = 1; i < nc; ++i) acc = (acc * x + (uint64_t)c[i]) % P;
+  return acc;
+}
+
+__global__ void k_ts_tables(Coeffs cf, int64_t m, uint32_t* tab) {
+  const int k = blockIdx.y;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= cf.ext[k]) return;
+  uint64_t h = horner(cf.c[k], 4, (uint64_t)i) % (uint64_t)m;
+  uint64_t g = horner(cf.c[k] + 4, 5, (uint64_t)i) % 2ULL;  // sign = 1 - 2g
+  tab[cf.off[k] + i] = (uint32_t)h | (g ? 0x80000000u : 0u);
+}
+
+// ======================================================= sparse RHS sketch
+// One warp per column i_n (fibre-major layout).  Warp-private accumulator of
+// m doubles in shared memory; contributions enter in ascending-j order, so
+// each Y cell is the same sequential sum numpy's add.at forms.
+struct OtherTabs {
+  int n;
+  const uint32_t* t[15];
+};
+
+template <int U>
+__global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t nnz, int64_t s_n,
+                                                    const int64_t* __restrict__ colptr,
+                                                    const int32_t* __restrict__ oth,
+                                                    const double* __restrict__ vals, int64_t m,
+                                                    double* __restrict__ yt) {
+  extern __shared__ double smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  double* acc = smem + (size_t)wid * (m + 32);
+  double* stage = acc + m;
+  const int64_t gw = blockIdx.x * (int64_t)nw + wid;
+  const int64_t tw = (int64_t)gridDim.x * nw;
+  for (int64_t col = gw; col < s_n; col += tw) {
+    for (int64_t h = lane; h < m; h += 32) acc[h] = 0.0;
+    __syncwarp();
+    const int64_t e0 = colptr[col], e1 = colptr[col + 1];
+    for (int64_t base = e0; base < e1; base += 32 * U) {
+      uint32_t bk[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = base + u * 32 + lane;
+        bk[u] = kNoBucket;
+        v[u] = 0.0;
+        if (e < e1) {
+          uint64_t hs = 0;
+          uint32_t neg = 0;
+          for (int k = 0; k < ot.n; ++k) {
+            const uint32_t t = __ldg(ot.t[k] + oth[(int64_t)k * nnz + e]);
+            hs += pk_bucket(t);
+            neg ^= pk_neg(t);
+          }
+          bk[u] = (uint32_t)(hs % (uint64_t)m);
+          const double x = vals[e];
+          v[u] = neg ? -x : x;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], v[u], stage);
+    }
+    double* dst = yt + col * m;
+    for (int64_t h = lane; h < m; h += 32) dst[h] = acc[h];
+    __syncwarp();
+  }
+}
+
+// ======================================================== dense RHS sketch
+// View the C-order tensor as [A, s_n, B] around the target mode.  Element
+// (a, i_n, b) belongs to other-index j = a*B + b.  Its bucket/sign come from
+// either two partial packed tables (TensorSketch: tabA over a, tabB over b,
+// buckets add mod m) or one full table over j (range finder).
+struct DenseView {
+  int64_t A, s_n, B;
+};
+
+template <bool FULL>
+__device__ __forceinline__ uint32_t dense_bucket(const uint32_t* tA, const uint32_t* tB,
+                                                 int64_t a, int64_t b, int64_t B, int64_t m,
+                                                 uint32_t& neg) {
+  if (FULL) {
+    uint32_t t = __ldg(tA + a * B + b);
+    neg = pk_neg(t);
+    return pk_bucket(t);
+  }
+  uint32_t ta = __ldg(tA + a), tb = __ldg(tB + b);
+  neg = pk_neg(ta) ^ pk_neg(tb);
+  uint32_t h = pk_bucket(ta) + pk_bucket(tb);
+  return h >= (uint32_t)m ? h - (uint32_t)m : h;
+}
+
+// Work item = (i_n, chunk) where chunk is a contiguous range of j of length
+// `chunk`; the CTA's warps split it into contiguous pieces, accumulate in
+// order, and the CTA writes acc_0 + acc_1 + ... (warp order) to part[item].
+template <bool FULL, int U>
+__global__ void __launch_bounds__(256) k_dense_rows(const double* __restrict__ t, DenseView v,
+                                                    const uint32_t* __restrict__ tA,
+                                                    const uint32_t* __restrict__ tB, int64_t m,
+                                                    int64_t chunk, int64_t nch,
+                                                    double* __restrict__ part) {
+  extern __shared__ double smem[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  double* acc = smem + (size_t)wid * (m + 32);
+  double* stage = acc + m;
+  const int64_t P = v.A * v.B;
+  const int64_t items = v.s_n * nch;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t in = item / nch, ch = item % nch;
+    const int64_t j0 = ch * chunk, j1 = imin(j0 + chunk, P);
+    const int64_t per = (j1 - j0 + nw - 1) / nw;
+    const int64_t g0 = imin(j0 + wid * per, j1), g1 = imin(g0 + per, j1);
+    for (int64_t h = lane; h < m; h += 32) acc[h] = 0.0;
+    __syncwarp();
+    int64_t g = g0;
+    while (g < g1) {
+      const int64_t a = g / v.B, b0 = g - a * v.B;
+      const int64_t len = imin(v.B - b0, g1 - g);
+      const double* row = t + (a * v.s_n + in) * v.B + b0;
+      for (int64_t o = 0; o < len; o += 32 * U) {
+        uint32_t bk[U];
+        double x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t e = o + u * 32 + lane;
+          bk[u] = kNoBucket;
+          x[u] = 0.0;
+          if (e < len) {
+            uint32_t neg;
+            bk[u] = dense_bucket<FULL>(tA, tB, a, b0 + e, v.B, m, neg);
+            const double xv = __ldcs(row + e);
+            x[u] = neg ? -xv : xv;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], x[u], stage);
+      }
+      g += len;
+    }
+    __syncthreads();
+    double* dst = part + item * m;
+    for (int64_t h = threadIdx.x; h < m; h += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += smem[(size_t)w * (m + 32) + h];
+      dst[h] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// yt[i_n, :] = sum over chunks (in order) of part[(i_n, ch), :]
+__global__ void k_sum_chunks(const double* __restrict__ part, int64_t s_n, int64_t nch, int64_t m,
+                             double* __restrict__ yt) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= s_n * m) return;
+  const int64_t in = idx / m, h = idx - in * m;
+  double s = 0.0;
+  for (int64_t c = 0; c < nch; ++c) s += part[(in * nch + c) * m + h];
+  yt[idx] = s;
+}
+
+// ---- gather form for B == 1 (target mode is the fastest-varying one): rows
+// of s_n contiguous values share one bucket; a warp owns a bucket and adds the
+// rows of its (ascending) list -- exactly numpy's add.at order.
+template <bool FULL>
+__global__ void k_bucket_keys(const uint32_t* __restrict__ tA, int64_t A, uint32_t* keys,
+                              uint32_t* idx, uint32_t* neg) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  uint32_t t = __ldg(tA + a);
+  keys[a] = pk_bucket(t);
+  idx[a] = (uint32_t)a;
+  neg[a] = pk_neg(t);
+}
+
+__global__ void k_run_bounds(const uint32_t* __restrict__ keys, int64_t n, int64_t m,
+                             int64_t* __restrict__ start) {
+  // start[c] = first position with key >= c, for c in [0, m]; keys sorted
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > m) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)keys[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  start[c] = lo;
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(256) k_gather_rows(const double* __restrict__ t, int64_t s_n,
+                                                     const int64_t* __restrict__ start,
+                                                     const uint32_t* __restrict__ list,
+                                                     const uint32_t* __restrict__ neg_of,
+                                                     int64_t m, double* __restrict__ yt) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ncb = (s_n + 32 * CPL - 1) / (32 * CPL);
+  const int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + wid;
+  if (task >= m * ncb) return;
+  const int64_t c = task / ncb, cb = task - c * ncb;
+  const int64_t col0 = cb * 32 * CPL;
+  double acc[CPL];
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
+  const int64_t r0 = start[c], r1 = start[c + 1];
+  for (int64_t r = r0; r < r1; ++r) {
+    const uint32_t a = list[r];
+    const bool ng = neg_of[a] != 0;
+    const double* row = t + (int64_t)a * s_n;
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+      const int64_t col = col0 + u * 32 + lane;
+      if (col < s_n) {
+        const double x = __ldcs(row + col);
+        acc[u] += ng ? -x : x;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) {
+    const int64_t col = col0 + u * 32 + lane;
+    if (col < s_n) yt[col * m + c] = acc[u];
+  }
+}
+
+// =========================================================== Kronecker sketch
+// Bucket-sorted row lists of one mode: run r covers rows list[rs[r]..rs[r+1])
+// all hashing to bucket rb[r]; *nrun runs.  CountSketch values per run.
+__global__ void k_cs_runs(const double* __restrict__ A, int64_t R, const uint32_t* __restrict__ rows,
+                          const uint32_t* __restrict__ negs, const int64_t* __restrict__ rs,
+                          const int* __restrict__ nrun, double* __restrict__ cs) {
+  // cs[r*R + p] = sum_{i in run r, ascending} sign_i A[i,p]
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nr = *nrun;
+  if (idx >= nr * R) return;
+  const int64_t r = idx / R, p = idx - r * R;
+  double s = 0.0;
+  for (int64_t e = rs[r]; e < rs[r + 1]; ++e) {
+    const uint32_t i = rows[e];
+    const double x = A[(int64_t)i * R + p];
+    s += negs[i] ? -x : x;
+  }
+  cs[idx] = s;
+}
+
+// First mode: dense column-major m x R CountSketch from the runs.
+__global__ void k_cs_dense(const double* __restrict__ cs, const uint32_t* __restrict__ rb,
+                           const int* __restrict__ nrun, int64_t R, int64_t m,
+                           double* __restrict__ zt) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nr = *nrun;
+  if (idx >= nr * R) return;
+  const int64_t r = idx / R, p = idx - r * R;
+  zt[p * m + rb[r]] = cs[idx];
+}
+
+// z_new[:, q*R + p] = z_cur[:, q] (circular-conv) y_p, y_p sparse over runs.
+// Grid: (h-blocks, q, p-chunks of 8); z stored column-major (ld = m).
+__global__ void __launch_bounds__(256) k_cconv(const double* __restrict__ zc, int64_t m,
+                                               const double* __restrict__ cs,
+                                               const uint32_t* __restrict__ rb,
+                                               const int* __restrict__ nrun, int64_t R,
+                                               double* __restrict__ zn) {
+  extern __shared__ double zs[];
+  const int64_t q = blockIdx.y;
+  const int64_t p0 = blockIdx.z * 8;
+  const int np = (int)imin(8, R - p0);
+  for (int64_t h = threadIdx.x; h < m; h += blockDim.x) zs[h] = zc[q * m + h];
+  __syncthreads();
+  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (h >= m) return;
+  const int nr = *nrun;
+  double acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+  for (int r = 0; r < nr; ++r) {
+    int64_t src = h - (int64_t)rb[r];
+    if (src < 0) src += m;
+    const double zv = zs[src];
+    const double* y = cs + (int64_t)r * R + p0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < np) acc[u] = fma(y[u], zv, acc[u]);
+  }
+  const int64_t rn = R;  // columns of this mode
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (u < np) zn[(q * rn + p0 + u) * m + h] = acc[u];
+}
+
+// ------------------------------------------------------------------ helpers
+struct SortBufs {
+  uint32_t *k_in, *k_out, *v_in, *v_out, *neg;
+  int64_t* rs;
+  uint32_t* rb;
+  int* nrun;
+  int64_t* counts;
+  void* cub_tmp;
+  size_t cub_bytes;
+};
+
+}  // namespace skx
+
+using namespace skx;
+
+extern "C" int skx_ts_tables(int nmodes, const int64_t* extents_h, const int64_t* coeffs_h,
+                             int64_t m, uint32_t* tab, void* stream) {
+  SKX_REQUIRE(nmodes >= 1 && nmodes <= 16, "skx_ts_tables: 1..16 modes supported");
+  SKX_REQUIRE(m >= 1 && m < (int64_t(1) << 31), "skx_ts_tables: m out of range");
+  Coeffs cf{};
+  cf.nmodes = nmodes;
+  int64_t off = 0, mx = 0;
+  for (int k = 0; k < nmodes; ++k) {
+    cf.ext[k] = extents_h[k];
+    cf.off[k] = off;
+    off += extents_h[k];
+    mx = extents_h[k] > mx ? extents_h[k] : mx;
+    for (int i = 0; i < 9; ++i) cf.c[k][i] = coeffs_h[k * 9 + i];
+  }
+  if (mx == 0) return SKX_OK;
+  dim3 grid((unsigned)((mx + 255) / 256), nmodes);
+  k_ts_tables<<<grid, 256, 0, (cudaStream_t)stream>>>(cf, m, tab);
+  return check_launch("k_ts_tables");
+}
+
+namespace {
+int warps_for(int64_t m) {
+  const int64_t per = (m + 32) * 8;
+  int64_t w = (int64_t)(max_smem_optin() - 1024) / per;
+  if (w > 8) w = 8;
+  return (int)w;
+}
+}  // namespace
+
+extern "C" int skx_ts_rhs_coo(int n_other, int64_t nnz, int64_t s_n, const int64_t* colptr,
+                              const int32_t* oth, const double* vals, const uint32_t* tab,
+                              const int64_t* tab_off_h, int64_t m, double* yt, void* stream) {
+  SKX_REQUIRE(n_other >= 0 && n_other <= 15, "skx_ts_rhs_coo: up to 15 other modes");
+  const int nw = warps_for(m);
+  SKX_REQUIRE(nw >= 1, "skx_ts_rhs_coo: sketch size %lld exceeds shared-memory capacity",
+              (long long)m);
+  if (s_n == 0) return SKX_OK;
+  OtherTabs ot{};
+  ot.n = n_other;
+  for (int k = 0; k < n_other; ++k) ot.t[k] = tab + tab_off_h[k];
+  const size_t smem = (size_t)nw * (m + 32) * 8;
+  auto kern = k_ts_rhs_coo<4>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = imin((int64_t)num_sms() * per_sm, (s_n + nw - 1) / nw);
+  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(ot, nnz, s_n, colptr, oth, vals,
+                                                                  m, yt);
+  return check_launch("k_ts_rhs_coo");
+}
+
+// Shared by TS (two partial tables) and the range finder (one full table).
+static int dense_sketch(bool full, const double* t, int ndim, const int64_t* shape_h, int mode,
+                        const uint32_t* tA, const uint32_t* tB, int64_t m, double* yt, void* ws,
+                        size_t* ws_bytes, cudaStream_t s) {
+  SKX_REQUIRE(ws_bytes != nullptr, "dense sketch: ws_bytes is NULL");
+  SKX_REQUIRE(mode >= 0 && mode < ndim, "dense sketch: mode out of range");
+  DenseView v{1, shape_h[mode], 1};
+  for (int k = 0; k < mode; ++k) v.A *= shape_h[k];
+  for (int k = mode + 1; k < ndim; ++k) v.B *= shape_h[k];
+  const int64_t P = v.A * v.B;
+  Arena ar(ws, *ws_bytes);
+  if (v.B == 1) {
+    // gather form over buckets of a (= j)
+    uint32_t* k_in = ar.take<uint32_t>(P);
+    uint32_t* k_out = ar.take<uint32_t>(P);
+    uint32_t* v_in = ar.take<uint32_t>(P);
+    uint32_t* v_out = ar.take<uint32_t>(P);
+    uint32_t* neg = ar.take<uint32_t>(P);
+    int64_t* start = ar.take<int64_t>(m + 1);
+    size_t cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, k_in, k_out, v_in, v_out, (int)P, 0, 32, s);
+    void* cub_tmp = ar.take<char>(cub_bytes);
+    if (ws == nullptr) {
+      *ws_bytes = ar.used + 256;
+      return SKX_OK;
+    }
+    SKX_REQUIRE(ar.ok(), "dense sketch: workspace too small");
+    SKX_REQUIRE(P < (int64_t(1) << 31), "dense sketch: too many columns for the gather form");
+    if (full) {
+      k_bucket_keys<true><<<(unsigned)((P + 255) / 256), 256, 0, s>>>(tA, P, k_in, v_in, neg);
+    } else {
+      k_bucket_keys<false><<<(unsigned)((P + 255) / 256), 256, 0, s>>>(tA, P, k_in, v_in, neg);
+    }
+    int bits = 1;
+    while ((int64_t(1) << bits) < m) ++bits;
+    cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k_in, k_out, v_in, v_out, (int)P, 0, bits,
+                                    s);
+    k_run_bounds<<<(unsigned)((m + 1 + 255) / 256), 256, 0, s>>>(k_out, P, m, start);
+    const int64_t s_n = v.s_n;
+    if (s_n <= 32 * 4) {
+      const int64_t tasks = m * ((s_n + 127) / 128);
+      k_gather_rows<4><<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(t, s_n, start, v_out, neg, m, yt);
+    } else {
+      const int64_t tasks = m * ((s_n + 255) / 256);
+      k_gather_rows<8><<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(t, s_n, start, v_out, neg, m, yt);
+    }
+    return check_launch("dense sketch (gather form)", 4);
+  }
+  const int nw = warps_for(m);
+  SKX_REQUIRE(nw >= 1, "dense sketch: sketch size %lld exceeds shared-memory capacity",
+              (long long)m);
+  // chunk so that there are >= ~4 items per SM but each chunk is >= 64K values
+  int64_t chunk = imax(int64_t(1) << 16, (v.s_n * P) / ((int64_t)num_sms() * 4));
+  chunk = imin(chunk, int64_t(1) << 22);
+  if (chunk > P) chunk = P;
+  if (chunk < 1) chunk = 1;
+  const int64_t nch = (P + chunk - 1) / chunk;
+  double* part = ar.take<double>((size_t)v.s_n * nch * m);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "dense sketch: workspace too small");
+  const size_t smem = (size_t)nw * (m + 32) * 8;
+  auto kern = full ? k_dense_rows<true, 8> : k_dense_rows<false, 8>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t items = v.s_n * nch;
+  const int64_t blocks = imin((int64_t)num_sms() * per_sm, items);
+  kern<<<(unsigned)blocks, nw * 32, smem, s>>>(t, v, tA, tB, m, chunk, nch, part);
+  k_sum_chunks<<<(unsigned)((v.s_n * m + 255) / 256), 256, 0, s>>>(part, v.s_n, nch, m, yt);
+  return check_launch("dense sketch (row form)", 2);
+}
+
+// Partial TS tables for the [A, s_n, B] split of a dense tensor: combine the
+// per-mode tables of modes before / after the target mode.
+namespace skx {
+__global__ void k_combine_tabs(OtherTabs ot, int nmodes_part, const int64_t* __restrict__ dummy,
+                               int64_t n, int64_t m, uint32_t* out, int first, int64_t ext0,
+                               int64_t ext1, int64_t ext2, int64_t ext3, int64_t ext4,
+                               int64_t ext5, int64_t ext6, int64_t ext7) {
+  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int64_t ext[8] = {ext0, ext1, ext2, ext3, ext4, ext5, ext6, ext7};
+  uint64_t hs = 0;
+  uint32_t neg = 0;
+  int64_t rem = x;
+  for (int k = nmodes_part - 1; k >= 0; --k) {
+    const int64_t i = rem % ext[k];
+    rem /= ext[k];
+    const uint32_t t = __ldg(ot.t[first + k] + i);
+    hs += pk_bucket(t);
+    neg ^= pk_neg(t);
+  }
+  out[x] = (uint32_t)(hs % (uint64_t)m) | (neg ? 0x80000000u : 0u);
+}
+}  // namespace skx
+
+extern "C" int skx_ts_rhs_dense(const double* t, int ndim, const int64_t* shape_h, int mode,
+                                const uint32_t* tab, const int64_t* tab_off_h, int64_t m,
+                                double* yt, void* ws, size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 9, "skx_ts_rhs_dense: 2..9 modes supported");
+  SKX_REQUIRE(mode >= 0 && mode < ndim, "skx_ts_rhs_dense: mode out of range");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_ts_rhs_dense: ws_bytes is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t A = 1, B = 1;
+  for (int k = 0; k < mode; ++k) A *= shape_h[k];
+  for (int k = mode + 1; k < ndim; ++k) B *= shape_h[k];
+  // partial tables live at the front of the workspace
+  Arena ar(ws, *ws_bytes);
+  uint32_t* tA = ar.take<uint32_t>(A);
+  uint32_t* tB = ar.take<uint32_t>(B);
+  size_t inner = 0;
+  int rc = dense_sketch(false, t, ndim, shape_h, mode, nullptr, nullptr, m, yt, nullptr, &inner, s);
+  if (rc) return rc;
+  char* inner_ws = ar.take<char>(inner);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_ts_rhs_dense: workspace too small");
+  OtherTabs ot{};
+  ot.n = ndim - 1;
+  for (int k = 0; k < ndim - 1; ++k) ot.t[k] = tab + tab_off_h[k];
+  int64_t ex[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+  // modes before the target: others 0..mode-1
+  for (int k = 0; k < mode; ++k) ex[k] = shape_h[k];
+  if (mode == 0) {
+    // A == 1: bucket 0 / sign + for the empty prefix
+    cudaMemsetAsync(tA, 0, sizeof(uint32_t), s);
+  } else {
+    k_combine_tabs<<<(unsigned)((A + 255) / 256), 256, 0, s>>>(
+        ot, mode, nullptr, A, m, tA, 0, ex[0], ex[1], ex[2], ex[3], ex[4], ex[5], ex[6], ex[7]);
+  }
+  int64_t ey[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+  for (int k = mode + 1; k < ndim; ++k) ey[k - mode - 1] = shape_h[k];
+  if (mode == ndim - 1) {
+    cudaMemsetAsync(tB, 0, sizeof(uint32_t), s);
+  } else {
+    k_combine_tabs<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(ot, ndim - 1 - mode, nullptr, B, m,
+                                                               tB, mode, ey[0], ey[1], ey[2], ey[3],
+                                                               ey[4], ey[5], ey[6], ey[7]);
+  }
+  SKX_TRY(check_launch("k_combine_tabs", 2));
+  return dense_sketch(false, t, ndim, shape_h, mode, tA, tB, m, yt, inner_ws, &inner, s);
+}
+
+namespace skx {
+struct CombPack {
+  int n;
+  int64_t ext[15];
+  const uint32_t* t[15];
+};
+__global__ void k_ts_combine(CombPack cp, int64_t P, int64_t m, uint32_t* __restrict__ out) {
+  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; x < P; x += stride) {
+    uint64_t hs = 0;
+    uint32_t neg = 0;
+    int64_t rem = x;
+    for (int k = cp.n - 1; k >= 0; --k) {
+      const int64_t i = rem % cp.ext[k];
+      rem /= cp.ext[k];
+      const uint32_t t = __ldg(cp.t[k] + i);
+      hs += pk_bucket(t);
+      neg ^= pk_neg(t);
+    }
+    out[x] = (uint32_t)(hs % (uint64_t)m) | (neg ? 0x80000000u : 0u);
+  }
+}
+}  // namespace skx
+
+extern "C" int skx_ts_combine(int n, const int64_t* ext_h, const uint32_t* tab,
+                              const int64_t* tab_off_h, int64_t m, int64_t P, uint32_t* out,
+                              void* stream) {
+  SKX_REQUIRE(n >= 1 && n <= 15, "skx_ts_combine: 1..15 modes");
+  CombPack cp{};
+  cp.n = n;
+  for (int k = 0; k < n; ++k) {
+    cp.ext[k] = ext_h[k];
+    cp.t[k] = tab + tab_off_h[k];
+  }
+  if (P == 0) return SKX_OK;
+  const int blocks = (int)imin((P + 255) / 256, (int64_t)num_sms() * 16);
+  k_ts_combine<<<blocks, 256, 0, (cudaStream_t)stream>>>(cp, P, m, out);
+  return check_launch("k_ts_combine");
+}
+
+extern "C" int skx_rrf_stage1_dense(const double* t, int ndim, const int64_t* shape_h, int mode,
+                                    const uint32_t* tab, int64_t k2, double* stage1, void* ws,
+                                    size_t* ws_bytes, void* stream) {
+  return dense_sketch(true, t, ndim, shape_h, mode, tab, nullptr, k2, stage1, ws, ws_bytes,
+                      (cudaStream_t)stream);
+}
+
+extern "C" int skx_ts_kron(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
+                           const double* const* factors_h, const uint32_t* tab,
+                           const int64_t* tab_off_h, int64_t m, double* z, void* ws,
+                           size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_ts_kron: 1..15 factors supported");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_ts_kron: ws_bytes is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t smax = 0, rtot = 1, rmid = 1;
+  for (int k = 0; k < n_other; ++k) {
+    smax = imax(smax, ext_h[k]);
+    rtot *= ranks_h[k];
+  }
+  for (int k = 0; k + 1 < n_other; ++k) rmid *= ranks_h[k];
+  Arena ar(ws, *ws_bytes);
+  uint32_t* k_in = ar.take<uint32_t>(smax);
+  uint32_t* k_out = ar.take<uint32_t>(smax);
+  uint32_t* v_in = ar.take<uint32_t>(smax);
+  uint32_t* v_out = ar.take<uint32_t>(smax);
+  uint32_t* neg = ar.take<uint32_t>(smax);
+  uint32_t* rb = ar.take<uint32_t>(smax);
+  int64_t* cnt = ar.take<int64_t>(smax + 1);
+  int64_t* rs = ar.take<int64_t>(smax + 1);
+  int* nrun = ar.take<int>(1);
+  int64_t rmax = 1;
+  for (int k = 0; k < n_other; ++k) rmax = imax(rmax, ranks_h[k]);
+  double* cs = ar.take<double>(smax * rmax);
+  double* zbuf = ar.take<double>(n_other > 2 ? rmid * m : 1);
+  size_t b1 = 0, b2 = 0, b3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b1, k_in, k_out, v_in, v_out, (int)smax, 0, 32, s);
+  cub::DeviceRunLengthEncode::Encode(nullptr, b2, k_out, rb, cnt, nrun, (int)smax, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, b3, cnt, rs, (int)smax + 1, s);
+  size_t cb = std::max(b1, std::max(b2, b3));
+  void* cub_tmp = ar.take<char>(cb);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_ts_kron: workspace too small");
+  int bits = 1;
+  while ((int64_t(1) << bits) < m) ++bits;
+  int launches = 0;
+  int64_t rcur = 1;
+  for (int k = 0; k < n_other; ++k) {
+    const int64_t sk = ext_h[k], R = ranks_h[k];
+    const uint32_t* tk = tab + tab_off_h[k];
+    k_bucket_keys<true><<<(unsigned)((sk + 255) / 256), 256, 0, s>>>(tk, sk, k_in, v_in, neg);
+    size_t c1 = cb;
+    cub::DeviceRadixSort::SortPairs(cub_tmp, c1, k_in, k_out, v_in, v_out, (int)sk, 0, bits, s);
+    cudaMemsetAsync(cnt, 0, (smax + 1) * sizeof(int64_t), s);
+    c1 = cb;
+    cub::DeviceRunLengthEncode::Encode(cub_tmp, c1, k_out, rb, cnt, nrun, (int)sk, s);
+    c1 = cb;
+    cub::DeviceScan::ExclusiveSum(cub_tmp, c1, cnt, rs, (int)sk + 1, s);
+    k_cs_runs<<<(unsigned)((sk * R + 255) / 256), 256, 0, s>>>(factors_h[k], R, v_out, neg, rs,
+                                                              nrun, cs);
+    launches += 5;
+    // destination of this step: final z for the last mode, else ping-pong
+    double* dst = (k == n_other - 1) ? z : ((k % 2 == 0) == (n_other % 2 == 0) ? zbuf : z);
+    if (k == 0) {
+      cudaMemsetAsync(dst, 0, (size_t)R * m * sizeof(double), s);
+      k_cs_dense<<<(unsigned)((sk * R + 255) / 256), 256, 0, s>>>(cs, rb, nrun, R, m, dst);
+      launches += 1;
+    } else {
+      const double* src = (dst == z) ? zbuf : z;
+      dim3 grid((unsigned)((m + 255) / 256), (unsigned)rcur, (unsigned)((R + 7) / 8));
+      k_cconv<<<grid, 256, (size_t)m * 8, s>>>(src, m, cs, rb, nrun, R, dst);
+      launches += 1;
+    }
+    rcur *= R;
+  }
+  return check_launch("skx_ts_kron", launches);
+}

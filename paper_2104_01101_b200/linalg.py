@@ -1,0 +1,206 @@
+"""Dense factorisations, leverage scores and the randomized rank-constrained
+least-squares solver (drop-in for src/linalg.py), computed on the GPU.
+
+QR/SVD/TRSM/GEMM run on-device through cuSOLVER/cuBLAS (torch.linalg with the
+cuSOLVER backend); the Gaussian test matrix of rsvd_lrls is drawn on-device by
+libskx's bit-exact numpy ziggurat; the sub-problem residual is a fused libskx
+pass over Y.  numpy in / numpy out at the API boundary, torch CUDA tensors in
+the drivers (the *_dev functions).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from . import rng as rngmod
+
+
+class RankDeficientError(ValueError):
+    """A matrix that must have full column rank numerically does not."""
+
+
+@dataclass
+class SvdResult:
+    u: np.ndarray
+    singular_values: np.ndarray
+    v: np.ndarray
+
+    def reconstruct(self):
+        return (self.u * self.singular_values) @ self.v.T
+
+
+@dataclass
+class LeverageProfile:
+    """Squared row norms of an orthonormal column basis; they sum to the rank."""
+
+    scores: np.ndarray
+    rank: int
+
+
+_BACKEND_SET = False
+
+
+def _torch():
+    global _BACKEND_SET
+    import torch
+    if not _BACKEND_SET:
+        # cuSOLVER for every factorisation (MAGMA's hybrid paths would run on the host)
+        torch.backends.cuda.preferred_linalg_library("cusolver")
+        _BACKEND_SET = True
+    return torch
+
+
+def _dev(a):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).cuda()
+
+
+def _np(t):
+    return t.detach().contiguous().cpu().numpy()
+
+
+# ------------------------------------------------------------------ QR
+def qr_flag_dev(mat):
+    """Reduced QR on device plus the reference's rank test as a device bool:
+    any |R_ii| < 1e-12 * ||mat||_F (src/linalg.py:38-52)."""
+    torch = _torch()
+    q, r = torch.linalg.qr(mat, mode="reduced")
+    tol = 1e-12 * torch.linalg.vector_norm(mat)
+    bad = (torch.diagonal(r).abs() < tol).any()
+    return q, r, bad
+
+
+def reduced_qr_dev(mat):
+    q, r, bad = qr_flag_dev(mat)
+    if bool(bad.item()):
+        d = _torch().diagonal(r).abs()
+        raise RankDeficientError(
+            f"rank-deficient input: min |R_ii| = {float(d.min()):.3e} < "
+            f"{1e-12 * float(_torch().linalg.vector_norm(mat)):.3e}")
+    return q, r
+
+
+def reduced_qr(mat):
+    q, r = reduced_qr_dev(_dev(mat))
+    return _np(q), _np(r)
+
+
+# ------------------------------------------------------------------ SVD
+def thin_svd_dev(mat):
+    """Thin SVD (k = min(m, n)), singular values non-increasing.  Wide or tall
+    inputs are first reduced by a QR so cuSOLVER only sees a k x k problem."""
+    torch = _torch()
+    m, n = mat.shape
+    if m >= n:
+        q, r = torch.linalg.qr(mat, mode="reduced")
+        u, s, vh = torch.linalg.svd(r, full_matrices=False)
+        return q @ u, s, vh.transpose(0, 1)
+    q, r = torch.linalg.qr(mat.transpose(0, 1), mode="reduced")  # mat^T = q r
+    u, s, vh = torch.linalg.svd(r.transpose(0, 1), full_matrices=False)  # r^T = u s vh
+    return u, s, q @ vh.transpose(0, 1)
+
+
+def thin_svd(mat):
+    u, s, v = thin_svd_dev(_dev(mat))
+    return SvdResult(_np(u), _np(s), _np(v))
+
+
+def truncated_svd(mat, rank):
+    res = thin_svd(mat)
+    return SvdResult(res.u[:, :rank], res.singular_values[:rank], res.v[:, :rank])
+
+
+# ------------------------------------------------------------------ leverage
+def leverage_scores_dev(a, check=True):
+    torch = _torch()
+    if a.shape[0] <= a.shape[1]:
+        raise ValueError("leverage scores need a strictly tall matrix")
+    q, r, bad = qr_flag_dev(a)
+    if check and bool(bad.item()):
+        raise RankDeficientError("rank-deficient factor in leverage_scores")
+    return (q * q).sum(dim=1), bad
+
+
+def leverage_scores(a):
+    a = _dev(a)
+    sc, _ = leverage_scores_dev(a)
+    return LeverageProfile(_np(sc), a.shape[1])
+
+
+# ------------------------------------------------------------------ normals
+class NormalSource:
+    """Device-resident cursor over a Generator's raw stream for
+    standard_normal draws (the position lives in HBM, so consecutive draws
+    need no host round trip)."""
+
+    def __init__(self, gen):
+        torch = _torch()
+        self.gen = gen
+        c = rngmod.cursor(gen)
+        self.k0, self.k1 = c.k0, c.k1
+        self.pos = torch.tensor([c.p], dtype=torch.int64, device="cuda")
+
+    def normal(self, shape):
+        torch = _torch()
+        n = int(np.prod(shape))
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        nat.call_ws("skx_philox_normal",
+                    (ctypes.c_uint64(self.k0), ctypes.c_uint64(self.k1), nat.ptr(self.pos), n,
+                     nat.ptr(out), nat.ptr(self.pos)), slot=1)
+        return out.view(*shape)
+
+    def sync_host(self):
+        """Move the numpy Generator to where numpy would be (one D2H)."""
+        rngmod.set_cursor(self.gen, int(self.pos.item()))
+
+
+# ------------------------------------------------------------------ rsvd_lrls
+def resid_dev(z, core_t, a, y):
+    """|| Z core_t a^T - Y ||_F as a device scalar (src/tucker.py:274)."""
+    torch = _torch()
+    p = (z @ core_t).contiguous()
+    a = a.contiguous()
+    m, s = y.shape
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_resid_sq", (nat.ptr(p), nat.ptr(a), m, s, int(p.shape[1]), nat.ptr(y),
+                                 int(y.stride(0)), int(y.stride(1)), nat.ptr(out)))
+    return torch.sqrt(out[0])
+
+
+def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
+    """Algorithm 5 (src/linalg.py:87-113) on device.
+    z: (m, r) CUDA tensor (any strides), y: (m, s) CUDA tensor view.
+    Returns (core_t (r, rank), a (s, rank), rank_bad flag)."""
+    torch = _torch()
+    m, r = z.shape
+    s = y.shape[1]
+    if m < r:
+        raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
+    if rank > min(r, s):
+        raise ValueError(f"rank {rank} exceeds min({r}, {s})")
+    qz, rz, bad = qr_flag_dev(z)
+    if check and bool(bad.item()):
+        raise RankDeficientError("rank-deficient sketched system")
+    x = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ y, upper=True)
+    width = min(rank + oversample, s)
+    g = normals.normal((s, width))
+    q, _ = torch.linalg.qr(x @ g, mode="reduced")
+    d = q.transpose(0, 1) @ x
+    u, sv, v = thin_svd_dev(d)
+    core_t = q @ (u[:, :rank] * sv[:rank])
+    return core_t, v[:, :rank].contiguous(), bad
+
+
+def rsvd_lrls(z, y, rank, rng, oversample=10):
+    """Rank-constrained least squares min ||z x - y|| via randomized SVD."""
+    z = _dev(z)
+    y = _dev(y)
+    src = NormalSource(rngmod.make_rng(rng))
+    core_t, v, _ = rsvd_lrls_dev(z, y, rank, src, oversample)
+    src.sync_host()
+    return _np(core_t), _np(v)

@@ -1,0 +1,516 @@
+"""Sketch operators (drop-in for src/sketching.py), executed by libskx.
+
+Operators keep the reference's dataclass names and fields.  Table data lives
+on the GPU; the numpy ``hash`` / ``signs`` arrays the reference exposes are
+materialised lazily on attribute access.  Randomness follows the reference's
+draw order exactly: TensorSketch coefficients are drawn on the host from the
+numpy Generator (9 values per mode), while bulk draws (CountSketch tables,
+leverage uniforms) are produced on the GPU from the Generator's Philox state
+and the host Generator is advanced to where numpy would be.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from . import rng as rngmod
+from .linalg import LeverageProfile, leverage_scores_dev, RankDeficientError
+
+_MERSENNE = (1 << 31) - 1
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(a):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).cuda()
+
+
+def _unpack(tab):
+    t = tab.cpu().numpy().astype(np.uint32)
+    return (t & 0x7FFFFFFF).astype(np.int64), np.where(t >> 31, -1, 1).astype(np.int64)
+
+
+def _pack(hash_, signs):
+    torch = _torch()
+    h = np.asarray(hash_, dtype=np.int64)
+    s = np.asarray(signs)
+    t = (h.astype(np.uint64) | np.where(s < 0, np.uint64(1 << 31), np.uint64(0))).astype(np.uint32)
+    return torch.from_numpy(t.view(np.int32)).cuda()
+
+
+# ============================================================ CountSketch
+@dataclass
+class CountSketchOp:
+    """Bucket-and-sign projection: row i lands in bucket hash[i] (src/sketching.py:46-63)."""
+
+    m: int
+    hash: np.ndarray
+    signs: np.ndarray
+
+    @classmethod
+    def build(cls, n, m, rng):
+        rng = rngmod.make_rng(rng)
+        h = rng.integers(0, m, size=n)
+        s = 1 - 2 * rng.integers(0, 2, size=n)
+        return cls(m, h, s)
+
+    def apply(self, mat):
+        """S @ mat for a dense (n, c) matrix -> (m, c), on the GPU."""
+        torch = _torch()
+        mat = _dev(mat)
+        n, c = mat.shape
+        tab = _pack(self.hash, self.signs)
+        out = torch.empty((c, self.m), dtype=torch.float64, device="cuda")
+        shp, sp_ = nat.host_i64([n, c])
+        nat.call_ws("skx_rrf_stage1_dense", (nat.ptr(mat.contiguous()), 2, sp_, 1, nat.ptr(tab),
+                                             self.m, nat.ptr(out)))
+        return out.t().cpu().numpy()
+
+
+# ============================================================ TensorSketch
+class TensorSketchOp:
+    """TensorSketch over a chain of modes (src/sketching.py:66-110): per-mode
+    degree-3 polynomial bucket hash and degree-4 sign hash over GF(2^31-1),
+    composed bucket = sum mod m, composed sign = product."""
+
+    def __init__(self, m, extents, coeffs, tab=None):
+        self.m = int(m)
+        self.extents = tuple(int(s) for s in extents)
+        self.coeffs = np.asarray(coeffs, dtype=np.int64).reshape(len(self.extents), 9)
+        self.tab_off = np.concatenate([[0], np.cumsum(self.extents)[:-1]]).astype(np.int64)
+        self._tab = tab
+        self._modes = None
+
+    @classmethod
+    def build(cls, extents, m, rng):
+        rng = rngmod.make_rng(rng)
+        coeffs = []
+        for _ in extents:
+            ch = rng.integers(0, _MERSENNE, size=4, dtype=np.int64)
+            cs = rng.integers(0, _MERSENNE, size=5, dtype=np.int64)
+            coeffs.append(np.concatenate([ch, cs]))
+        return cls(m, extents, np.array(coeffs).reshape(len(extents), 9))
+
+    # device packed tables (sum(extents) uint32)
+    @property
+    def tab(self):
+        torch = _torch()
+        if self._tab is None:
+            total = int(sum(self.extents))
+            self._tab = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+            ext, ep = nat.host_i64(self.extents)
+            cf, cp = nat.host_i64(self.coeffs.ravel())
+            nat.call("skx_ts_tables", len(self.extents), ep, cp, self.m, nat.ptr(self._tab),
+                     nat.stream())
+        return self._tab
+
+    @property
+    def modes(self):
+        if self._modes is None:
+            mods = []
+            t = self.tab
+            for k, s in enumerate(self.extents):
+                h, g = _unpack(t[self.tab_off[k]:self.tab_off[k] + s])
+                mods.append(CountSketchOp(self.m, h, g))
+            self._modes = mods
+        return self._modes
+
+    @property
+    def n_rows(self):
+        return int(np.prod(self.extents))
+
+    def combined_hash(self, multi_idx):
+        h = np.zeros(len(multi_idx[0]), dtype=np.int64)
+        for k, idx in enumerate(multi_idx):
+            h += self.modes[k].hash[idx]
+        return h % self.m
+
+    def combined_sign(self, multi_idx):
+        s = np.ones(len(multi_idx[0]), dtype=np.int64)
+        for k, idx in enumerate(multi_idx):
+            s *= self.modes[k].signs[idx]
+        return s
+
+    def materialize(self):
+        flat = np.arange(self.n_rows)
+        multi = np.unravel_index(flat, self.extents)
+        out = np.zeros((self.m, self.n_rows))
+        out[self.combined_hash(multi), flat] = self.combined_sign(multi)
+        return out
+
+    def full_table(self):
+        """Packed composed (bucket|sign) table over all prod(extents) rows."""
+        torch = _torch()
+        P = self.n_rows
+        out = torch.empty(P, dtype=torch.int32, device="cuda")
+        ext, ep = nat.host_i64(self.extents)
+        off, op = nat.host_i64(self.tab_off)
+        nat.call("skx_ts_combine", len(self.extents), ep, nat.ptr(self.tab), op, self.m, P,
+                 nat.ptr(out), nat.stream())
+        return out
+
+
+def ts_kron_dev(ts, factors):
+    """Z = S kron(factors) on device, returned as an (m, r) column-major view."""
+    torch = _torch()
+    fs = [f.contiguous() for f in factors]
+    r = int(np.prod([f.shape[1] for f in fs]))
+    zt = torch.empty((r, ts.m), dtype=torch.float64, device="cuda")
+    ext, ep = nat.host_i64(ts.extents)
+    rk, rp = nat.host_i64([f.shape[1] for f in fs])
+    arr, fp = nat.host_ptrs(fs)
+    off, op = nat.host_i64(ts.tab_off)
+    nat.call_ws("skx_ts_kron", (len(fs), ep, rp, fp, nat.ptr(ts.tab), op, ts.m, nat.ptr(zt)))
+    return zt.t()
+
+
+def ts_apply_kron(ts, factors, method="auto"):
+    """Apply a TensorSketch to the Kronecker chain of the factors
+    (src/sketching.py:113-147).  `method` is accepted for interface parity: the
+    device computes the circular convolutions exactly (no FFT), which agrees
+    with both reference methods to rounding."""
+    if len(factors) != len(ts.extents):
+        raise ValueError("factor count does not match sketch mode count")
+    for k, f in enumerate(factors):
+        if np.shape(f)[0] != ts.extents[k]:
+            raise ValueError(f"factor {k} has {np.shape(f)[0]} rows, sketch extent is {ts.extents[k]}")
+    if method not in ("auto", "fft", "direct"):
+        raise ValueError(f"unknown method {method!r}")
+    z = ts_kron_dev(ts, [_dev(f) for f in factors])
+    return z.cpu().numpy()
+
+
+def ts_rhs_coo_dev(ts, colptr, oth, vals, s_n):
+    """Y^T (s_n x m) from a fibre-major COO layout."""
+    torch = _torch()
+    yt = torch.empty((s_n, ts.m), dtype=torch.float64, device="cuda")
+    off, op = nat.host_i64(ts.tab_off)
+    nat.call("skx_ts_rhs_coo", len(ts.extents), int(vals.numel()), s_n, nat.ptr(colptr),
+             nat.ptr(oth), nat.ptr(vals), nat.ptr(ts.tab), op, ts.m, nat.ptr(yt), nat.stream())
+    return yt
+
+
+def ts_rhs_dense_dev(ts, t, mode):
+    """Y^T (s_n x m) for mode `mode` of a dense CUDA tensor."""
+    torch = _torch()
+    shape = tuple(t.shape)
+    yt = torch.empty((shape[mode], ts.m), dtype=torch.float64, device="cuda")
+    shp, sp_ = nat.host_i64(shape)
+    off, op = nat.host_i64(ts.tab_off)
+    nat.call_ws("skx_ts_rhs_dense", (nat.ptr(t), len(shape), sp_, mode, nat.ptr(ts.tab), op, ts.m,
+                                     nat.ptr(yt)))
+    return yt
+
+
+def ts_apply_rhs(ts, b, chunk=1 << 20):
+    """Apply a TensorSketch to a tall right-hand side (src/sketching.py:150-175).
+    b: (prod(extents), c) dense array or scipy sparse matrix."""
+    import scipy.sparse as sp
+    torch = _torch()
+    n_rows = ts.n_rows
+    if b.shape[0] != n_rows:
+        raise ValueError(f"rhs has {b.shape[0]} rows, sketch expects {n_rows}")
+    c = int(b.shape[1])
+    if sp.issparse(b):
+        coo = b.tocoo()
+        if coo.nnz == 0:
+            return np.zeros((ts.m, c))
+        order = np.lexsort((coo.row, coo.col))
+        rows, cols, data = coo.row[order], coo.col[order], coo.data[order]
+        multi = np.stack(np.unravel_index(rows, ts.extents)).astype(np.int32)
+        colptr = np.zeros(c + 1, dtype=np.int64)
+        np.cumsum(np.bincount(cols, minlength=c), out=colptr[1:])
+        yt = ts_rhs_coo_dev(ts, torch.from_numpy(colptr).cuda(),
+                            torch.from_numpy(np.ascontiguousarray(multi)).cuda(),
+                            torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).cuda(), c)
+        return yt.t().cpu().numpy()
+    bd = _dev(b).contiguous()
+    full = ts.full_table()
+    out = torch.empty((c, ts.m), dtype=torch.float64, device="cuda")
+    shp, sp_ = nat.host_i64([n_rows, c])
+    nat.call_ws("skx_rrf_stage1_dense", (nat.ptr(bd), 2, sp_, 1, nat.ptr(full), ts.m, nat.ptr(out)))
+    return out.t().cpu().numpy()
+
+
+# ============================================================ leverage sampling
+@dataclass
+class LevSamplerOp:
+    """Row sampler over a Kronecker/Khatri-Rao chain (src/sketching.py:178-190)."""
+
+    m: int
+    extents: tuple
+    profiles: list
+    variant: str
+    indices: np.ndarray
+    weights: np.ndarray
+    _dev: tuple = field(default=None, repr=False)
+
+    def flat_indices(self):
+        return np.ravel_multi_index(self.indices.T, self.extents)
+
+
+def lev_sample_dev(factors, m, gen, check=True):
+    """Random leverage sampler on device.  Computes every factor's scores
+    first (QR rank check before any draw, as src/sketching.py:204-211), then
+    m uniforms per factor from `gen`'s stream.  Returns (idx (m, k) int64,
+    weights (m,), scores list, bad flag)."""
+    torch = _torch()
+    if m < 1:
+        raise ValueError("sample count must be positive")
+    scores, bads = [], []
+    for f in factors:
+        sc, bad = leverage_scores_dev(f, check=check)
+        scores.append(sc)
+        bads.append(bad)
+    ps, cdfs = [], []
+    for sc in scores:
+        p = torch.empty_like(sc)
+        cdf = torch.empty_like(sc)
+        nat.call("skx_lev_prepare", nat.ptr(sc), int(sc.numel()), nat.ptr(p), nat.ptr(cdf), None,
+                 None, nat.stream())
+        ps.append(p)
+        cdfs.append(cdf)
+    k = len(factors)
+    idx = torch.empty((m, k), dtype=torch.int64, device="cuda")
+    w = torch.empty(m, dtype=torch.float64, device="cuda")
+    c = rngmod.cursor(gen)
+    ext, ep = nat.host_i64([f.shape[0] for f in factors])
+    pa, pp = nat.host_ptrs(ps)
+    ca, cp = nat.host_ptrs(cdfs)
+    nat.call("skx_lev_sample", k, ep, pp, cp, m, ctypes.c_uint64(c.k0), ctypes.c_uint64(c.k1),
+             ctypes.c_uint64(c.p), nat.ptr(idx), nat.ptr(w), nat.stream())
+    rngmod.set_cursor(gen, c.p + k * m)
+    bad = bads[0]
+    for b in bads[1:]:
+        bad = bad | b
+    return idx, w, scores, bad
+
+
+def lev_build(factors, m, variant, rng):
+    """Build a leverage-score row sampler (src/sketching.py:193-221)."""
+    if m < 1:
+        raise ValueError("sample count must be positive")
+    if variant == "deterministic":
+        raise NotImplementedError(
+            "leverage-deterministic (top-m products) is outside this build's hot path (SURVEY 8f)")
+    if variant != "random":
+        raise ValueError(f"unknown variant {variant!r}")
+    fs = [_dev(f) for f in factors]
+    idx, w, scores, _ = lev_sample_dev(fs, m, rngmod.make_rng(rng))
+    extents = tuple(f.shape[0] for f in fs)
+    profiles = [LeverageProfile(s.cpu().numpy(), f.shape[1]) for s, f in zip(scores, fs)]
+    return LevSamplerOp(m, extents, profiles, variant, idx.cpu().numpy(), w.cpu().numpy(),
+                        _dev=(idx, w))
+
+
+def kron_rows_dev(factors, idx, w):
+    """Z (m, r) column-major view: weighted Kronecker rows."""
+    torch = _torch()
+    m = idx.shape[0]
+    fs = [f.contiguous() for f in factors]
+    r = int(np.prod([f.shape[1] for f in fs]))
+    zt = torch.empty((r, m), dtype=torch.float64, device="cuda")
+    rk, rp = nat.host_i64([f.shape[1] for f in fs])
+    arr, fp = nat.host_ptrs(fs)
+    nat.call("skx_kron_rows", len(fs), rp, fp, nat.ptr(idx), nat.ptr(w), m, nat.ptr(zt), nat.stream())
+    return zt.t()
+
+
+def gather_dense_dev(t, mode, idx, w):
+    """Y (m, s_n) row-major: weighted mode-`mode` fibres of a dense tensor."""
+    torch = _torch()
+    shape = tuple(t.shape)
+    m = idx.shape[0]
+    y = torch.empty((m, shape[mode]), dtype=torch.float64, device="cuda")
+    shp, sp_ = nat.host_i64(shape)
+    nat.call("skx_gather_fibers_dense", nat.ptr(t), len(shape), sp_, mode, nat.ptr(idx), nat.ptr(w), m,
+             nat.ptr(y), nat.stream())
+    return y
+
+
+def gather_coo_dev(keys, vals, ext_others, s_n, idx, w):
+    """Sparse fibre gather -> (hit_off (m+1), hit_col, hit_val) on device."""
+    torch = _torch()
+    m = idx.shape[0]
+    nnz = int(vals.numel())
+    # count first to size the outputs exactly (one small D2H)
+    hit_off = torch.empty(m + 1, dtype=torch.int64, device="cuda")
+    cap = 0
+    dummy_c = torch.empty(1, dtype=torch.int64, device="cuda")
+    dummy_v = torch.empty(1, dtype=torch.float64, device="cuda")
+    ext, ep = nat.host_i64(ext_others)
+    nat.call_ws("skx_gather_fibers_coo", (len(ext_others), ep, s_n, nnz, nat.ptr(keys), nat.ptr(vals),
+                                          nat.ptr(idx), nat.ptr(w), m, nat.ptr(hit_off),
+                                          nat.ptr(dummy_c), nat.ptr(dummy_v), cap))
+    total = int(hit_off[m].item())
+    hit_col = torch.empty(max(total, 1), dtype=torch.int64, device="cuda")
+    hit_val = torch.empty(max(total, 1), dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_gather_fibers_coo", (len(ext_others), ep, s_n, nnz, nat.ptr(keys), nat.ptr(vals),
+                                          nat.ptr(idx), nat.ptr(w), m, nat.ptr(hit_off),
+                                          nat.ptr(hit_col), nat.ptr(hit_val), total))
+    return hit_off, hit_col[:total], hit_val[:total]
+
+
+def hits_to_dense(hit_off, hit_col, hit_val, m, s_n):
+    torch = _torch()
+    y = torch.zeros((m, s_n), dtype=torch.float64, device="cuda")
+    counts = hit_off[1:] - hit_off[:-1]
+    rows = torch.repeat_interleave(torch.arange(m, device="cuda"), counts)
+    y[rows, hit_col] = hit_val
+    return y
+
+
+def lev_apply(sampler, factors, bt):
+    """Sampled-and-rescaled (Z, Y) for a Kronecker chain (src/sketching.py:270-287)."""
+    import scipy.sparse as sp
+    torch = _torch()
+    if tuple(np.shape(f)[0] for f in factors) != sampler.extents:
+        raise ValueError("factors do not match the sampler's extents")
+    if bt.shape[0] != int(np.prod(sampler.extents)):
+        raise ValueError("rhs row count does not match the sampled chain")
+    idx, w = sampler._dev if sampler._dev is not None else (
+        torch.from_numpy(sampler.indices).cuda(), torch.from_numpy(sampler.weights).cuda())
+    fs = [_dev(f) for f in factors]
+    z = kron_rows_dev(fs, idx, w)
+    flat = torch.zeros(idx.shape[0], dtype=torch.int64, device="cuda")
+    for k, e in enumerate(sampler.extents):
+        flat = flat * e + idx[:, k]
+    P, s = bt.shape
+    if sp.issparse(bt):
+        c = bt.tocsr()
+        c.sort_indices()
+        rows = np.repeat(np.arange(P, dtype=np.int64), np.diff(c.indptr))
+        keys = torch.from_numpy(rows * s + c.indices.astype(np.int64)).cuda()
+        vals = torch.from_numpy(np.ascontiguousarray(c.data, dtype=np.float64)).cuda()
+        off, col, val = gather_coo_dev(keys, vals, [P], s, flat.view(-1, 1).contiguous(), w)
+        y = hits_to_dense(off, col, val, idx.shape[0], s)
+    else:
+        y = gather_dense_dev(_dev(bt).contiguous(), 1, flat.view(-1, 1).contiguous(), w)
+    return z.cpu().numpy(), y.cpu().numpy()
+
+
+def lev_apply_krp(sampler, factors, bt):
+    """Khatri-Rao variant (src/sketching.py:290-301): Hadamard rows."""
+    torch = _torch()
+    if tuple(np.shape(f)[0] for f in factors) != sampler.extents:
+        raise ValueError("factors do not match the sampler's extents")
+    idx, w = sampler._dev if sampler._dev is not None else (
+        torch.from_numpy(sampler.indices).cuda(), torch.from_numpy(sampler.weights).cuda())
+    fs = [_dev(f) for f in factors]
+    z = fs[0][idx[:, 0]].clone()
+    for k in range(1, len(fs)):
+        z *= fs[k][idx[:, k]]
+    z = w[:, None] * z
+    _, y = lev_apply(sampler, [np.zeros((e, 1)) for e in sampler.extents], bt)
+    return z.cpu().numpy(), y
+
+
+# ============================================================ composite (RRF)
+class RrfTables:
+    """Device description of CountSketch tables drawn as numpy's
+    integers(0,k2,P) then integers(0,2,P) from a Philox stream: the start
+    cursor, the sorted rejection offsets d_i and the sign run start."""
+
+    def __init__(self, k0, k1, p0, has, pending, d, nd, sign_q0, k2, P):
+        self.k0, self.k1, self.p0, self.has, self.pending = k0, k1, p0, has, pending
+        self.d, self.nd, self.sign_q0, self.k2, self.P = d, nd, sign_q0, k2, P
+
+    def args(self):
+        return (ctypes.c_uint64(self.k0), ctypes.c_uint64(self.k1), ctypes.c_uint64(self.p0),
+                ctypes.c_uint32(self.has), ctypes.c_uint32(self.pending),
+                ctypes.c_uint64(self.sign_q0), nat.ptr(self.d), self.nd)
+
+
+def draw_rrf_tables(gen, P, k2):
+    """Reproduce rng.integers(0,k2,P); rng.integers(0,2,P) on device without
+    materialising them; advances `gen` exactly as numpy would."""
+    torch = _torch()
+    c = rngmod.cursor(gen)
+    thresh = (2 ** 32 - k2) % k2
+    expect = P * thresh / 2 ** 32
+    cap = int(max(1024, 4 * expect + 64 * np.sqrt(expect + 1) + 64))
+    while True:
+        rej = torch.empty(cap, dtype=torch.int64, device="cuda")
+        nat.call("skx_fill_u64max", nat.ptr(rej), cap, nat.stream())
+        count = torch.zeros(1, dtype=torch.int64, device="cuda")
+        n_u32 = P + cap  # enough as long as fewer than cap rejections occur
+        nat.call("skx_lemire_scan", ctypes.c_uint64(c.k0), ctypes.c_uint64(c.k1), ctypes.c_uint64(c.p),
+                 ctypes.c_uint32(c.has), ctypes.c_uint32(c.pending), ctypes.c_uint64(n_u32),
+                 ctypes.c_uint32(k2), nat.ptr(rej), cap, nat.ptr(count), nat.stream())
+        d = torch.empty(cap, dtype=torch.int64, device="cuda")
+        n_le = torch.zeros(1, dtype=torch.int64, device="cuda")
+        nat.call_ws("skx_lemire_finish", (nat.ptr(rej), nat.ptr(count), cap, ctypes.c_uint64(P),
+                                          nat.ptr(d), nat.ptr(n_le)))
+        both = torch.stack([count[0], n_le[0]]).cpu().numpy()
+        if int(both[0]) < cap:
+            break
+        cap *= 4
+    nrej = int(both[1])
+    sign_q0 = P + nrej
+    tabs = RrfTables(c.k0, c.k1, c.p, c.has, c.pending, d, cap, sign_q0, k2, P)
+    rngmod.advance_u32(gen, 2 * P + nrej)
+    return tabs
+
+
+@dataclass
+class CompositeSketchOp:
+    """CountSketch stage followed by a Gaussian stage (src/sketching.py:304-324)."""
+
+    k1: int
+    k2: int
+    stage: CountSketchOp
+    gauss: np.ndarray
+
+    @classmethod
+    def build(cls, n_cols, k1, k2, rng):
+        if k2 < k1:
+            raise ValueError(f"intermediate width {k2} below target width {k1}")
+        rng = rngmod.make_rng(rng)
+        tabs = draw_rrf_tables(rng, n_cols, k2)
+        tab = rrf_table_dev(tabs)
+        h, s = _unpack(tab)
+        gauss = rng.standard_normal((k2, k1)) / np.sqrt(k1)
+        op = cls(k1, k2, CountSketchOp(k2, h, s), gauss)
+        return op
+
+
+def rrf_table_dev(tabs):
+    torch = _torch()
+    tab = torch.empty(max(tabs.P, 1), dtype=torch.int32, device="cuda")
+    nat.call("skx_rrf_table", *tabs.args(), tabs.P, tabs.k2, nat.ptr(tab), nat.stream())
+    return tab[:tabs.P]
+
+
+def composite_apply(mat, op):
+    """mat @ (countsketch stage) @ (gaussian stage) (src/sketching.py:327-341)."""
+    import scipy.sparse as sp
+    torch = _torch()
+    if mat.shape[1] != len(op.stage.hash):
+        raise ValueError(f"matrix has {mat.shape[1]} columns, sketch expects {len(op.stage.hash)}")
+    s, P = mat.shape
+    tab = _pack(op.stage.hash, op.stage.signs)
+    st1 = torch.empty((s, op.k2), dtype=torch.float64, device="cuda")
+    if sp.issparse(mat):
+        c = mat.tocsr()
+        c.sort_indices()
+        colptr = torch.from_numpy(c.indptr.astype(np.int64)).cuda()
+        oth = torch.from_numpy(c.indices.astype(np.int32).reshape(1, -1)).cuda()
+        vals = torch.from_numpy(np.ascontiguousarray(c.data, dtype=np.float64)).cuda()
+        off = np.zeros(1, dtype=np.int64)
+        nat.call("skx_ts_rhs_coo", 1, int(vals.numel()), s, nat.ptr(colptr), nat.ptr(oth),
+                 nat.ptr(vals), nat.ptr(tab), off.ctypes.data_as(ctypes.c_void_p), op.k2,
+                 nat.ptr(st1), nat.stream())
+    else:
+        md = _dev(mat).contiguous()
+        shp, sp_ = nat.host_i64([s, P])
+        nat.call_ws("skx_rrf_stage1_dense", (nat.ptr(md), 2, sp_, 0, nat.ptr(tab), op.k2, nat.ptr(st1)))
+    return (st1 @ _dev(op.gauss)).cpu().numpy()

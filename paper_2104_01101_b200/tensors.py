@@ -1,0 +1,507 @@
+"""Tensor data model (drop-in for src/tensors.py) with device-resident mirrors.
+
+Host-facing types keep the reference's contract (src/tensors.py:26-138):
+``SparseTensor`` is lexsorted, duplicate-free, immutable COO with int64
+coordinates and float64 values; dense tensors are C-order float64 arrays;
+``TuckerModel`` / ``CPModel`` hold numpy arrays.
+
+Device side (HBM layout):
+* ``DeviceCoo``: coordinates as an (N, nnz) int32 SoA in lexicographic order
+  (4 B per coordinate instead of 8; extents < 2^31) + float64 values, plus
+  lazily built, cached per-mode layouts:
+    - fibre-major (mode n): nonzeros sorted by (i_n, other modes ascending)
+      with int64 column offsets -> TS right-hand side, RRF stage 1;
+    - other-major (mode n): int64 keys flat_other * s_n + i_n sorted, values
+      -> leverage fibre gather.
+  The reference caches its scipy unfoldings on the tensor the same way
+  (``SparseTensor._unfoldings``, src/tensors.py:158-176).
+* dense tensors: one contiguous float64 CUDA tensor.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+
+
+# ============================================================ host types
+class SparseTensor:
+    """Order-N COO tensor (src/tensors.py:26-98): coords (nnz, N) int64
+    lexsorted, duplicates rejected, immutable."""
+
+    def __init__(self, shape, coords, values):
+        shape = tuple(int(s) for s in shape)
+        if len(shape) < 1 or any(s < 1 for s in shape):
+            raise ValueError(f"invalid shape {shape}")
+        coords = np.atleast_2d(np.asarray(coords, dtype=np.int64))
+        values = np.asarray(values, dtype=np.float64).ravel()
+        if coords.size == 0:
+            coords = coords.reshape(0, len(shape))
+        if coords.shape[1] != len(shape):
+            raise ValueError("coordinate width does not match tensor order")
+        if coords.shape[0] != values.shape[0]:
+            raise ValueError("number of coordinates does not match number of values")
+        if coords.size and ((coords < 0).any() or (coords >= np.asarray(shape)).any()):
+            raise ValueError("coordinate out of range")
+        order = np.lexsort(coords.T[::-1])
+        coords = coords[order]
+        values = values[order]
+        if coords.shape[0] > 1 and (np.diff(coords, axis=0) == 0).all(axis=1).any():
+            raise ValueError("duplicate coordinates")
+        self._init(shape, coords, values)
+
+    def _init(self, shape, coords, values):
+        self.shape = shape
+        self._coords = coords
+        self._values = values
+        if coords is not None:
+            coords.setflags(write=False)
+            values.setflags(write=False)
+        self._unfoldings = {}
+        self._mode_sort = {}
+        self._device = None
+
+    @classmethod
+    def from_device(cls, shape, coords, values, validate=True):
+        """Wrap device arrays (coords (nnz, N) or (N, nnz) integer CUDA tensor,
+        values float64 CUDA tensor) that are already lexsorted.  Host copies
+        are materialised only on demand (``.coords`` / ``.values``)."""
+        obj = cls.__new__(cls)
+        dev = DeviceCoo.from_torch(shape, coords, values, validate=validate)
+        obj._init(tuple(int(s) for s in shape), None, None)
+        obj._device = dev
+        return obj
+
+    def _materialise(self):
+        dev = self._device
+        self._coords = dev.coords.t().cpu().numpy().astype(np.int64)
+        self._values = dev.vals.cpu().numpy()
+        self._coords.setflags(write=False)
+        self._values.setflags(write=False)
+
+    @property
+    def coords(self):
+        if self._coords is None:
+            self._materialise()
+        return self._coords
+
+    @property
+    def values(self):
+        if self._values is None:
+            self._materialise()
+        return self._values
+
+    @property
+    def ndim(self):
+        return len(self.shape)
+
+    @property
+    def nnz(self):
+        if self._values is None and self._device is not None:
+            return self._device.nnz
+        return self._values.shape[0]
+
+    @property
+    def density(self):
+        return self.nnz / float(np.prod(self.shape))
+
+    def norm(self):
+        return float(np.sqrt(device_of(self).norm2().item()))
+
+    def to_dense(self):
+        out = np.zeros(self.shape)
+        out[tuple(self.coords.T)] = self.values
+        return out
+
+    @classmethod
+    def from_dense(cls, a, tol=0.0):
+        a = np.asarray(a, dtype=np.float64)
+        mask = np.abs(a) > tol
+        return cls(a.shape, np.argwhere(mask), a[mask])
+
+    def mode_sort(self, n):
+        if n not in self._mode_sort:
+            order = np.argsort(self.coords[:, n], kind="stable")
+            order.setflags(write=False)
+            self._mode_sort[n] = order
+        return self._mode_sort[n]
+
+    def __repr__(self):
+        return f"SparseTensor(shape={self.shape}, nnz={self.nnz})"
+
+
+@dataclass
+class TuckerModel:
+    """Core tensor plus per-mode factors with orthonormal columns."""
+
+    core: np.ndarray
+    factors: list
+
+    @property
+    def ranks(self):
+        return tuple(self.core.shape)
+
+    def reconstruct(self):
+        out = np.asarray(self.core)
+        for n, a in enumerate(self.factors):
+            out = np.moveaxis(np.tensordot(a, out, axes=(1, n)), 0, n)
+        return out
+
+
+@dataclass
+class CPModel:
+    """Rank-R CP model: unit-column factors and per-component weights."""
+
+    factors: list
+    weights: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        if self.weights is None:
+            self.weights = np.ones(self.factors[0].shape[1])
+        self.weights = np.asarray(self.weights, dtype=np.float64)
+
+    @property
+    def rank(self):
+        return self.factors[0].shape[1]
+
+    def reconstruct(self):
+        subs = "abcdefgh"[: len(self.factors)]
+        expr = ",".join(f"{c}z" for c in subs) + ",z->" + subs
+        return np.einsum(expr, *self.factors, self.weights, optimize=True)
+
+
+# ============================================================ device types
+def _torch():
+    import torch
+    return torch
+
+
+class DeviceCoo:
+    """HBM-resident COO tensor with cached per-mode layouts."""
+
+    def __init__(self, shape, coords_i32, vals):
+        self.shape = tuple(int(s) for s in shape)
+        self.ndim = len(self.shape)
+        self.coords = coords_i32  # (N, nnz) int32, lexsorted
+        self.vals = vals          # (nnz,) float64
+        self.nnz = int(vals.numel())
+        self._fibre = {}
+        self._keys = {}
+        self._norm2 = None
+
+    @classmethod
+    def from_host(cls, st: SparseTensor):
+        torch = _torch()
+        if max(st.shape) >= 2 ** 31:
+            raise ValueError("extents must be < 2^31 for the device layout")
+        c = torch.from_numpy(np.ascontiguousarray(st.coords.T.astype(np.int32))).cuda()
+        v = torch.from_numpy(np.ascontiguousarray(st.values)).cuda()
+        return cls(st.shape, c, v)
+
+    @classmethod
+    def from_torch(cls, shape, coords, vals, validate=True):
+        torch = _torch()
+        shape = tuple(int(s) for s in shape)
+        nd = len(shape)
+        if coords.dim() != 2:
+            raise ValueError("coords must be 2-D")
+        if coords.shape[0] != nd and coords.shape[1] == nd:
+            coords = coords.t()
+        coords = coords.to(device="cuda", dtype=torch.int32).contiguous()
+        vals = vals.to(device="cuda", dtype=torch.float64).contiguous()
+        if coords.shape[1] != vals.numel():
+            raise ValueError("number of coordinates does not match number of values")
+        obj = cls(shape, coords, vals)
+        if validate and obj.nnz:
+            ext = torch.tensor(shape, device="cuda", dtype=torch.int64).view(-1, 1)
+            if bool(((coords < 0) | (coords.long() >= ext)).any()):
+                raise ValueError("coordinate out of range")
+            if obj.nnz > 1:
+                # lexicographic strictly increasing <=> sorted and unique
+                c = coords.long()
+                lt = torch.zeros(obj.nnz - 1, dtype=torch.bool, device="cuda")
+                eq = torch.ones(obj.nnz - 1, dtype=torch.bool, device="cuda")
+                for k in range(nd):
+                    a, b = c[k, :-1], c[k, 1:]
+                    lt |= eq & (a < b)
+                    eq &= a == b
+                if not bool(lt.all()):
+                    raise ValueError("coordinates must be lexsorted and duplicate-free")
+        return obj
+
+    # ---- norms
+    def norm2(self):
+        torch = _torch()
+        if self._norm2 is None:
+            out = torch.empty(1, dtype=torch.float64, device="cuda")
+            if self.nnz == 0:
+                out.zero_()
+            else:
+                nat.call_ws("skx_sumsq", (nat.ptr(self.vals), self.nnz, nat.ptr(out)))
+            self._norm2 = out
+        return self._norm2
+
+    # ---- fibre-major layout for mode n
+    def fibre(self, n):
+        torch = _torch()
+        if n not in self._fibre:
+            others = [k for k in range(self.ndim) if k != n]
+            s_n = self.shape[n]
+            cnt = torch.bincount(self.coords[n].long(), minlength=s_n) if self.nnz else \
+                torch.zeros(s_n, dtype=torch.int64, device="cuda")
+            colptr = torch.zeros(s_n + 1, dtype=torch.int64, device="cuda")
+            torch.cumsum(cnt, 0, out=colptr[1:])
+            if n == 0:
+                oth = self.coords[1:].contiguous() if self.ndim > 1 else \
+                    torch.empty((0, self.nnz), dtype=torch.int32, device="cuda")
+                vals = self.vals
+            else:
+                perm = torch.argsort(self.coords[n], stable=True)
+                oth = self.coords[others][:, perm].contiguous()
+                vals = self.vals[perm].contiguous()
+                del perm
+            self._fibre[n] = (colptr, oth, vals)
+        return self._fibre[n]
+
+    def colptr0(self):
+        return self.fibre(0)[0]
+
+    # ---- other-major keys for mode n
+    def keys(self, n):
+        torch = _torch()
+        if n not in self._keys:
+            others = [k for k in range(self.ndim) if k != n]
+            s_n = self.shape[n]
+            flat = torch.zeros(self.nnz, dtype=torch.int64, device="cuda")
+            for k in others:
+                flat = flat * self.shape[k] + self.coords[k].long()
+            key = flat * s_n + self.coords[n].long()
+            del flat
+            if n == self.ndim - 1:
+                self._keys[n] = (key, self.vals)
+            else:
+                key, perm = torch.sort(key)
+                self._keys[n] = (key, self.vals[perm].contiguous())
+        return self._keys[n]
+
+    def release_layouts(self):
+        self._fibre.clear()
+        self._keys.clear()
+
+
+def device_of(t):
+    """Device representation of a tensor argument (cached for SparseTensor)."""
+    torch = _torch()
+    if isinstance(t, SparseTensor):
+        if t._device is None:
+            t._device = DeviceCoo.from_host(t)
+        return t._device
+    if isinstance(t, DeviceCoo):
+        return t
+    if isinstance(t, torch.Tensor):
+        if not t.is_cuda:
+            t = t.cuda()
+        return t.to(torch.float64).contiguous()
+    a = np.ascontiguousarray(np.asarray(t, dtype=np.float64))
+    return torch.from_numpy(a).cuda()
+
+
+def is_sparse_dev(d):
+    return isinstance(d, DeviceCoo)
+
+
+def shape_of(t):
+    return tuple(int(s) for s in t.shape)
+
+
+# ============================================================ operations
+def tensor_norm(t):
+    d = device_of(t)
+    if is_sparse_dev(d):
+        return float(np.sqrt(d.norm2().item()))
+    return float(_torch().linalg.vector_norm(d).item())
+
+
+def matricize(t, n):
+    """Mode-n unfolding s_n x prod(others) (host view/copy; src/tensors.py:151-166)."""
+    if isinstance(t, SparseTensor):
+        import scipy.sparse as sp
+        key = ("m", n)
+        if key not in t._unfoldings:
+            others = [k for k in range(t.ndim) if k != n]
+            rest = [t.shape[k] for k in others]
+            cols = (np.ravel_multi_index([t.coords[:, k] for k in others], rest)
+                    if t.nnz else np.zeros(0, dtype=np.int64))
+            t._unfoldings[key] = sp.coo_matrix(
+                (t.values, (t.coords[:, n], cols)), shape=(t.shape[n], int(np.prod(rest)))).tocsr()
+        return t._unfoldings[key]
+    t = np.asarray(t)
+    if not 0 <= n < t.ndim:
+        raise ValueError(f"mode {n} out of range for order-{t.ndim} tensor")
+    return np.moveaxis(t, n, 0).reshape(t.shape[n], -1)
+
+
+def matricize_t(t, n):
+    """Transposed unfolding T_(n)^T (src/tensors.py:169-176)."""
+    if isinstance(t, SparseTensor):
+        return matricize(t, n).T.tocsr()
+    return matricize(t, n).T
+
+
+def fold(mat, n, shape):
+    """Inverse of matricize (src/tensors.py:197-201); numpy or torch."""
+    shape = tuple(shape)
+    rest = [shape[k] for k in range(len(shape)) if k != n]
+    if not isinstance(mat, np.ndarray) and hasattr(mat, "movedim"):
+        return mat.reshape([shape[n]] + rest).movedim(0, n)
+    return np.moveaxis(np.asarray(mat).reshape([shape[n]] + rest), 0, n)
+
+
+def ttm_dev(t, mat, n):
+    """Mode-n product on device: t x_n mat (mat: new x s_n)."""
+    torch = _torch()
+    out = torch.tensordot(mat, t, dims=([1], [n]))
+    return out.movedim(0, n)
+
+
+def ttm(t, mat, n):
+    torch = _torch()
+    mat = np.asarray(mat)
+    t = np.asarray(t)
+    if mat.shape[1] != t.shape[n]:
+        raise ValueError(
+            f"ttm mode {n}: matrix has {mat.shape[1]} columns, tensor extent is {t.shape[n]}")
+    out = ttm_dev(torch.from_numpy(np.ascontiguousarray(t)).cuda(),
+                  torch.from_numpy(np.ascontiguousarray(mat)).cuda(), n)
+    return out.contiguous().cpu().numpy()
+
+
+def khatri_rao(mats):
+    """Column-wise Kronecker product, first matrix slowest (src/tensors.py:288-301)."""
+    torch = _torch()
+    mats = [np.asarray(m) for m in mats]
+    k = mats[0].shape[1]
+    if any(m.shape[1] != k for m in mats):
+        raise ValueError("khatri_rao inputs must share the column count")
+    out = torch.from_numpy(mats[0]).cuda()
+    for m in mats[1:]:
+        out = (out[:, None, :] * torch.from_numpy(m).cuda()[None, :, :]).reshape(-1, k)
+    return out.cpu().numpy()
+
+
+# ---- fitness -------------------------------------------------------------
+def tucker_cross_dev(d, core, factors):
+    """<ttmc(T, {A}), C> on device; returns a 0-d CUDA tensor."""
+    torch = _torch()
+    if is_sparse_dev(d):
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        shp, sp_ = nat.host_i64(d.shape)
+        rk, rp = nat.host_i64([f.shape[1] for f in factors])
+        fa = [f.contiguous() for f in factors]
+        arr, fp = nat.host_ptrs(fa)
+        cpt = d.colptr0() if d.ndim == 3 else None
+        nat.call_ws("skx_tucker_cross_coo",
+                    (d.ndim, sp_, rp, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp,
+                     nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(out)))
+        return out[0]
+    proj = d
+    for k, a in enumerate(factors):
+        proj = ttm_dev(proj, a.t(), k)
+    return (proj * core).sum()
+
+
+def fitness_tucker_dev(d, core, factors, norm2=None):
+    torch = _torch()
+    if norm2 is None:
+        norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
+    cross = tucker_cross_dev(d, core, factors)
+    mod = (core * core).sum()
+    r2 = torch.clamp(norm2 - 2.0 * cross + mod, min=0.0)
+    return 1.0 - torch.sqrt(r2) / torch.sqrt(norm2)
+
+
+def cp_cross_dev(d, factors, weights):
+    torch = _torch()
+    if is_sparse_dev(d):
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        shp, sp_ = nat.host_i64(d.shape)
+        fa = [f.contiguous() for f in factors]
+        arr, fp = nat.host_ptrs(fa)
+        nat.call_ws("skx_cp_cross_coo",
+                    (d.ndim, sp_, int(factors[0].shape[1]), d.nnz, nat.ptr(d.coords),
+                     nat.ptr(d.vals), fp, nat.ptr(weights.contiguous()), nat.ptr(out)))
+        return out[0]
+    # dense: mttkrp mode 0 then dot with scaled A0
+    nd = d.dim()
+    R = factors[0].shape[1]
+    kr = factors[1]
+    for a in factors[2:]:
+        kr = (kr[:, None, :] * a[None, :, :]).reshape(-1, R)
+    m0 = d.reshape(d.shape[0], -1) @ kr
+    return ((factors[0] * weights) * m0).sum()
+
+
+def fitness_cp_dev(d, factors, weights, norm2=None):
+    torch = _torch()
+    if norm2 is None:
+        norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
+    cross = cp_cross_dev(d, factors, weights)
+    scaled = factors[0] * weights
+    g = torch.ones((factors[0].shape[1],) * 2, dtype=torch.float64, device="cuda")
+    for a in factors[1:]:
+        g = g * (a.t() @ a)
+    mod = ((scaled.t() @ scaled) * g).sum()
+    r2 = torch.clamp(norm2 - 2.0 * cross + mod, min=0.0)
+    return 1.0 - torch.sqrt(r2) / torch.sqrt(norm2)
+
+
+def _to_dev_mat(a):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).cuda()
+
+
+def fitness(t, model):
+    """1 - ||T - model|| / ||T|| without densifying (src/tensors.py:339-368)."""
+    d = device_of(t)
+    norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
+    if float(norm2.item()) == 0.0:
+        raise ValueError("fitness undefined for a zero-norm tensor")
+    if isinstance(model, TuckerModel):
+        f = fitness_tucker_dev(d, _to_dev_mat(model.core), [_to_dev_mat(a) for a in model.factors],
+                               norm2)
+    elif isinstance(model, CPModel):
+        f = fitness_cp_dev(d, [_to_dev_mat(a) for a in model.factors], _to_dev_mat(model.weights),
+                           norm2)
+    else:
+        raise TypeError(f"unsupported model type {type(model)!r}")
+    return float(f.item())
+
+
+def mttkrp(t, factors, n):
+    """T_(n) @ khatri_rao(others) on device (src/tensors.py:307-336)."""
+    torch = _torch()
+    d = device_of(t)
+    nd = len(shape_of(d))
+    others = [k for k in range(nd) if k != n]
+    fs = [_to_dev_mat(factors[k]) for k in others]
+    R = fs[0].shape[1]
+    for k, f in zip(others, fs):
+        if f.shape[0] != shape_of(d)[k]:
+            raise ValueError(f"mttkrp mode {k}: factor has {f.shape[0]} rows, extent is {shape_of(d)[k]}")
+        if f.shape[1] != R:
+            raise ValueError("mttkrp factors must share the column count")
+    if is_sparse_dev(d):
+        prod = d.vals[:, None].expand(-1, R).clone()
+        for k, f in zip(others, fs):
+            prod *= f[d.coords[k].long()]
+        out = torch.zeros((d.shape[n], R), dtype=torch.float64, device="cuda")
+        out.index_add_(0, d.coords[n].long(), prod)
+        return out.cpu().numpy()
+    kr = fs[0]
+    for f in fs[1:]:
+        kr = (kr[:, None, :] * f[None, :, :]).reshape(-1, R)
+    return (d.movedim(n, 0).reshape(d.shape[n], -1) @ kr).cpu().numpy()

@@ -1,0 +1,99 @@
+"""GPU: the drivers against fixtures from the real reference and the oracle.
+
+Factors/core compared after sign canonicalisation at 1e-10 relative (f64);
+1 - fitness within max(1e-10, reference floor)."""
+import numpy as np
+import pytest
+
+from tests.conftest import canon, relerr
+from tests.test_oracle_golden import DRIVERS, make_input
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def skx():
+    import paper_2104_01101_b200 as m
+    return m
+
+
+def _as_api_input(skx, oracle, spec):
+    t = make_input(oracle, spec)
+    if isinstance(t, oracle.Coo):
+        return skx.SparseTensor(t.shape, t.coords, t.values)
+    return t
+
+
+def _compare_model(model, trace, golden, tag, tol=1e-10):
+    nd = len(model.factors)
+    got_f, got_c = canon(model.factors, model.core)
+    ref_f, ref_c = canon([golden[f"{tag}_a{k}"] for k in range(nd)], golden[f"{tag}_core"])
+    for a, b in zip(got_f, ref_f):
+        assert relerr(a, b) <= tol, (tag, relerr(a, b))
+    assert relerr(got_c, ref_c) <= tol
+    fr = golden[f"{tag}_fitness"]
+    assert np.allclose(1 - np.array(trace.fitness), 1 - fr, rtol=1e-8, atol=1e-10), tag
+    assert np.allclose(trace.residuals, golden[f"{tag}_residuals"], rtol=1e-9, atol=0), tag
+
+
+@pytest.mark.parametrize("tag", list(DRIVERS))
+def test_driver_vs_reference_golden(golden, oracle, skx, tag):
+    spec, cfg = DRIVERS[tag]
+    t = _as_api_input(skx, oracle, spec)
+    model, trace = skx.sketched_tucker_als(t, skx.TuckerConfig(**cfg))
+    _compare_model(model, trace, golden, tag)
+    assert len(trace.wall_s) == cfg["max_sweeps"]
+
+
+def test_driver_bitwise_deterministic(oracle, skx):
+    for tag in ("dlev", "sts"):
+        spec, cfg = DRIVERS[tag]
+        t = _as_api_input(skx, oracle, spec)
+        m1, t1 = skx.sketched_tucker_als(t, skx.TuckerConfig(**cfg))
+        m2, t2 = skx.sketched_tucker_als(t, skx.TuckerConfig(**cfg))
+        assert t1.fitness == t2.fitness
+        assert t1.residuals == t2.residuals
+        assert np.array_equal(m1.core, m2.core)
+        for a, b in zip(m1.factors, m2.factors):
+            assert np.array_equal(a, b)
+
+
+def test_cp_via_tucker_vs_reference_golden(golden, skx):
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    c, v = planted_cp_coo_host((30, 30, 30), 4000, rank=3, seed=5)
+    st = skx.SparseTensor((30, 30, 30), c, v)
+    cfg = skx.CPConfig(rank=3, sketch="leverage-random", sketch_factor=16, tucker_sweeps=3,
+                       max_sweeps=10, seed=11)
+    model, trace = skx.cp_via_sketched_tucker(st, cfg)
+    assert trace.stage_split == int(golden["cpt_split"])
+    assert np.allclose(trace.fitness, golden["cpt_fitness"], rtol=0, atol=1e-9)
+    assert np.allclose(trace.residuals, golden["cpt_residuals"], rtol=1e-8, atol=0)
+    for k in range(3):
+        assert relerr(np.abs(model.factors[k]), np.abs(golden[f"cpt_a{k}"])) <= 1e-8
+    assert relerr(np.abs(model.weights), np.abs(golden["cpt_w"])) <= 1e-8
+
+
+def test_sketch_size_invariant_and_errors(skx):
+    t = np.random.default_rng(0).standard_normal((10, 10, 10))
+    with pytest.raises(ValueError):
+        skx.sketched_tucker_als(t, skx.TuckerConfig(ranks=(3, 3, 3), sketch="tensorsketch", sketch_size=8))
+    with pytest.raises(ValueError):
+        skx.sketched_tucker_als(t, skx.TuckerConfig(ranks=(11, 3, 3), sketch="tensorsketch", sketch_size=99))
+    with pytest.raises(ValueError):
+        skx.sketched_tucker_als(t, skx.TuckerConfig(ranks=(3, 3, 3)))
+
+
+@pytest.mark.parametrize("kind", ["tensorsketch", "leverage-random"])
+def test_sparse_reduced_config_vs_oracle(oracle, skx, kind):
+    """Reduced-scale configs 4/5: s=2000, 1e5 nonzeros."""
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    shape = (2000, 2000, 2000)
+    c, v = planted_cp_coo_host(shape, 100_000, rank=10, seed=0)
+    st = skx.SparseTensor(shape, c, v)
+    oc = oracle.Coo(shape, c, v)
+    kw = dict(ranks=(10, 10, 10), max_sweeps=2, sketch=kind, sketch_size=1600, seed=0)
+    model, trace = skx.sketched_tucker_als(st, skx.TuckerConfig(**kw))
+    core, fac, tr = oracle.sketched_tucker(oc, **kw)
+    # residuals are sketch-space quantities: compare directly
+    assert np.allclose(trace.residuals, tr.residuals, rtol=1e-8), (trace.residuals, tr.residuals)
+    assert np.allclose(trace.fitness, tr.fitness, rtol=0, atol=1e-9)

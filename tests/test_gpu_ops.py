@@ -1,0 +1,246 @@
+"""GPU parity of the operators against fixtures from the real reference
+(tests/golden) and against the CPU oracle on the same seeded inputs.
+
+Tolerances: integer tables / index sets bit-exact; sketches
+<= 1e-12 Frobenius-relative; factors after sign canonicalisation <= 1e-10."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from tests.conftest import canon, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def skx():
+    import paper_2104_01101_b200 as m
+    return m
+
+
+def test_ts_tables_bit_exact(golden, skx):
+    for seed in (0, 7):
+        op = skx.TensorSketchOp.build((100, 120, 90), 400, skx.make_rng(seed))
+        for k in range(3):
+            assert np.array_equal(op.modes[k].hash, golden[f"ts_tab_s{seed}_h{k}"])
+            assert np.array_equal(op.modes[k].signs, golden[f"ts_tab_s{seed}_s{k}"])
+
+
+def test_ts_apply_rhs(golden, skx):
+    op = skx.TensorSketchOp.build((6, 5), 16, skx.make_rng(1))
+    assert relerr(skx.ts_apply_rhs(op, golden["rhs_b"]), golden["rhs_dense"]) <= 1e-14
+    bs = sp.csr_matrix(golden["rhs_bs"])
+    assert relerr(skx.ts_apply_rhs(op, bs), golden["rhs_sparse"]) <= 1e-14
+
+
+def test_ts_apply_rhs_single_nonzero_exact(skx):
+    # reference pkg/tests/test_sketching.py:109-121 (array_equal)
+    op = skx.TensorSketchOp.build((3, 4), 6, skx.make_rng(23))
+    b = sp.coo_matrix(([2.5], ([7], [0])), shape=(12, 1))
+    out = skx.ts_apply_rhs(op, b)
+    multi = np.unravel_index(np.array([7]), (3, 4))
+    exp = np.zeros((6, 1))
+    exp[op.combined_hash(multi)[0], 0] = op.combined_sign(multi)[0] * 2.5
+    assert np.array_equal(out, exp)
+
+
+def test_ts_apply_rhs_empty_sparse(skx):
+    op = skx.TensorSketchOp.build((3, 4), 6, skx.make_rng(31))
+    assert np.array_equal(skx.ts_apply_rhs(op, sp.coo_matrix((12, 3))), np.zeros((6, 3)))
+
+
+@pytest.mark.parametrize("m,ext", [(3, (4, 4)), (8, (4, 4)), (16, (5, 3, 4)), (64, (5, 3, 4)),
+                                   (400, (30, 20))])
+def test_ts_apply_kron(golden, skx, m, ext):
+    op = skx.TensorSketchOp.build(ext, m, skx.make_rng(200 + m))
+    fs = [golden[f"kron_m{m}_f{k}"] for k in range(len(ext))]
+    assert relerr(skx.ts_apply_kron(op, fs), golden[f"kron_m{m}"]) <= 1e-13
+
+
+def test_ts_apply_kron_materialized(skx):
+    rng = np.random.default_rng(3)
+    for m in (3, 8, 16, 97, 256):
+        op = skx.TensorSketchOp.build((4, 5, 3), m, skx.make_rng(m))
+        fs = [rng.standard_normal((s, 2)) for s in (4, 5, 3)]
+        exp = op.materialize() @ np.kron(np.kron(fs[0], fs[1]), fs[2])
+        assert relerr(skx.ts_apply_kron(op, fs), exp) <= 1e-13
+
+
+def test_composite(golden, skx):
+    op = skx.CompositeSketchOp.build(1000, 20, 45, skx.make_rng(3))
+    assert np.array_equal(op.stage.hash, golden["rrf_hash"])
+    assert np.array_equal(op.stage.signs, golden["rrf_signs"])
+    assert np.array_equal(op.gauss, golden["rrf_gauss"])
+    c = skx.CompositeSketchOp.build(50, 4, 20, skx.make_rng(4))
+    mat = golden["comp_mat"]
+    assert relerr(skx.composite_apply(mat, c), golden["comp_dense"]) <= 1e-13
+    ms = sp.csr_matrix(mat * (np.abs(mat) > 0.8))
+    assert relerr(skx.composite_apply(ms, c), golden["comp_sparse"]) <= 1e-13
+
+
+def test_lev_build_bit_exact(golden, skx):
+    f = [golden["lev_f0"], golden["lev_f1"]]
+    s = skx.lev_build(f, 200, "random", skx.make_rng(9))
+    assert np.array_equal(s.indices, golden["lev_idx"])
+    assert np.allclose(s.weights, golden["lev_w"], rtol=1e-12, atol=0)
+
+
+def test_lev_apply(golden, skx):
+    f = [golden["levapp_f0"], golden["levapp_f1"]]
+    s = skx.lev_build(f, 30, "random", skx.make_rng(12))
+    assert np.array_equal(s.indices, golden["levapp_idx"])
+    z, y = skx.lev_apply(s, f, golden["levapp_bt"])
+    assert relerr(z, golden["levapp_z"]) <= 1e-13
+    assert relerr(y, golden["levapp_y"]) <= 1e-13
+    bt = golden["levapp_bt"]
+    _, ys = skx.lev_apply(s, f, sp.csr_matrix(bt * (np.abs(bt) > 1.0)))
+    assert relerr(ys, golden["levapp_ys"]) <= 1e-13
+
+
+def test_lev_errors(skx):
+    with pytest.raises(ValueError):
+        skx.lev_build([np.eye(4)[:, :2]] * 2, 0, "random", skx.make_rng(0))
+    col = np.random.default_rng(1).standard_normal((8, 1))
+    with pytest.raises(skx.RankDeficientError):
+        skx.leverage_scores(np.hstack([col, col]))
+
+
+def test_rsvd_lrls(golden, skx):
+    ct, v = skx.rsvd_lrls(golden["rsvd_z"], golden["rsvd_y"], 2, skx.make_rng(2))
+    assert relerr(ct @ v.T, golden["rsvd_core_t"] @ golden["rsvd_v"].T) <= 1e-12
+    (a,), _ = canon([v])
+    (b,), _ = canon([golden["rsvd_v"]])
+    assert relerr(a, b) <= 1e-11
+
+
+def test_rsvd_rank_deficient(skx):
+    col = np.random.default_rng(15).standard_normal((10, 1))
+    with pytest.raises(skx.RankDeficientError):
+        skx.rsvd_lrls(np.hstack([col, col]), np.ones((10, 4)), 1, skx.make_rng(0))
+    with pytest.raises(ValueError):
+        skx.rsvd_lrls(np.random.default_rng(0).standard_normal((10, 3)), np.ones((10, 4)), 4,
+                      skx.make_rng(0))
+
+
+def test_init_rrf(golden, skx):
+    u = skx.init_rrf(golden["rrf_tn"], 4, 8, skx.make_rng(6))
+    (a,), _ = canon([u])
+    (b,), _ = canon([golden["rrf_u"]])
+    assert relerr(a, b) <= 1e-11
+
+
+def test_fitness(golden, skx):
+    t = golden["fit_t"]
+    fs = [golden[f"fit_a{k}"] for k in range(3)]
+    core = golden["fit_core"]
+    assert skx.fitness(t, skx.TuckerModel(core, fs)) == pytest.approx(float(golden["fit_dense"]), abs=1e-13)
+    st = skx.SparseTensor.from_dense(t * (np.abs(t) > 0.7))
+    assert skx.fitness(st, skx.TuckerModel(core, fs)) == pytest.approx(float(golden["fit_sparse"]), abs=1e-13)
+    cpf = [golden[f"fitcp_a{k}"] for k in range(3)]
+    w = golden["fitcp_w"]
+    assert skx.fitness(t, skx.CPModel(cpf, w)) == pytest.approx(float(golden["fitcp_dense"]), abs=1e-13)
+    assert skx.fitness(st, skx.CPModel(cpf, w)) == pytest.approx(float(golden["fitcp_sparse"]), abs=1e-13)
+
+
+# ---------------------------------------------------------- device kernels vs oracle
+def _coo_rand(shape, nnz, seed):
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    return planted_cp_coo_host(shape, nnz, rank=3, seed=seed)
+
+
+@pytest.mark.parametrize("shape,nnz,m", [((30, 40, 50), 5000, 64), ((200, 150, 100), 60000, 1600),
+                                         ((20, 10, 30, 8), 9000, 100)])
+def test_sparse_ts_rhs_all_modes_vs_oracle(skx, oracle, shape, nnz, m):
+    from paper_2104_01101_b200.sketching import ts_rhs_coo_dev
+    from paper_2104_01101_b200.tensors import device_of
+    c, v = _coo_rand(shape, nnz, 1)
+    st = skx.SparseTensor(shape, c, v)
+    oc = oracle.Coo(shape, c, v)
+    d = device_of(st)
+    gen = skx.make_rng(5)
+    ogen = oracle.generator(5)
+    for n in range(len(shape)):
+        ext = tuple(shape[k] for k in range(len(shape)) if k != n)
+        op = skx.TensorSketchOp.build(ext, m, gen)
+        hs, ss = oracle.ts_tables(ext, m, ogen)
+        colptr, oth, vals = d.fibre(n)
+        yt = ts_rhs_coo_dev(op, colptr, oth, vals, shape[n]).cpu().numpy()
+        ref = oracle.ts_rhs(hs, ss, ext, m, oracle.unfold_t(oc, n))
+        assert relerr(yt.T, ref) <= 1e-14  # same summation order -> (near) bit-exact
+
+
+@pytest.mark.parametrize("shape,m", [((30, 40, 50), 64), ((12, 13, 14, 15), 256), ((100, 100, 100), 400),
+                                     ((3, 200, 5), 4096)])
+def test_dense_ts_rhs_all_modes_vs_oracle(skx, oracle, shape, m):
+    from paper_2104_01101_b200.sketching import ts_rhs_dense_dev
+    from paper_2104_01101_b200.tensors import device_of
+    t = np.random.default_rng(2).standard_normal(shape)
+    d = device_of(t)
+    gen = skx.make_rng(9)
+    ogen = oracle.generator(9)
+    for n in range(len(shape)):
+        ext = tuple(shape[k] for k in range(len(shape)) if k != n)
+        op = skx.TensorSketchOp.build(ext, m, gen)
+        hs, ss = oracle.ts_tables(ext, m, ogen)
+        yt = ts_rhs_dense_dev(op, d, n).cpu().numpy()
+        ref = oracle.ts_rhs(hs, ss, ext, m, oracle.unfold_t(t, n))
+        assert relerr(yt.T, ref) <= 1e-13
+
+
+def test_sparse_rrf_stage1_vs_oracle(skx, oracle):
+    from paper_2104_01101_b200.sketching import draw_rrf_tables
+    from paper_2104_01101_b200.tensors import device_of
+    from paper_2104_01101_b200.tucker import rrf_stage1_dev
+    shape = (300, 200, 100)
+    c, v = _coo_rand(shape, 50000, 2)
+    st = skx.SparseTensor(shape, c, v)
+    oc = oracle.Coo(shape, c, v)
+    d = device_of(st)
+    for n, k2 in ((1, 157), (2, 480), (0, 45)):
+        P = int(np.prod(shape)) // shape[n]
+        g = skx.make_rng(n)
+        og = oracle.generator(n)
+        tabs = draw_rrf_tables(g, P, k2)
+        st1 = rrf_stage1_dev(d, n, tabs).cpu().numpy()
+        h, s, gauss = oracle.rrf_tables(P, 4, k2, og)
+        tm = sp.csr_matrix((s, (np.arange(P), h)), shape=(P, k2))
+        ref = np.asarray((oracle.unfold(oc, n) @ tm).todense())
+        assert relerr(st1, ref) <= 1e-14
+        assert np.array_equal(g.standard_normal((k2, 4)) / 2.0, gauss)
+
+
+def test_dense_gather_and_kron_rows(skx, oracle):
+    from paper_2104_01101_b200.sketching import gather_dense_dev, kron_rows_dev, lev_sample_dev
+    from paper_2104_01101_b200.tensors import device_of
+    import torch
+    shape = (20, 30, 25)
+    t = np.random.default_rng(4).standard_normal(shape)
+    d = device_of(t)
+    rng = np.random.default_rng(8)
+    A = [np.linalg.qr(rng.standard_normal((s, 3)))[0] for s in shape]
+    for n in range(3):
+        others = [k for k in range(3) if k != n]
+        fs = [torch.from_numpy(A[k]).cuda() for k in others]
+        g = skx.make_rng(3 + n)
+        idx, w, _, _ = lev_sample_dev(fs, 77, g)
+        oidx, ow, _ = oracle.lev_sample([A[k] for k in others], 77, oracle.generator(3 + n))
+        assert np.array_equal(idx.cpu().numpy(), oidx)
+        z = kron_rows_dev(fs, idx, w).cpu().numpy()
+        y = gather_dense_dev(d, n, idx, w).cpu().numpy()
+        ext = tuple(shape[k] for k in others)
+        oz, oy = oracle.lev_rows(oidx, ow, ext, [A[k] for k in others], oracle.unfold_t(t, n))
+        assert relerr(z, oz) <= 1e-14
+        assert relerr(y, oy) <= 1e-14
+
+
+def test_sparse_fitness_order3_and_generic(skx, oracle):
+    rng = np.random.default_rng(6)
+    for shape, R in (((50, 40, 30), (3, 4, 5)), ((10, 12, 9, 7), (2, 3, 2, 2)), ((60, 50, 40), (20, 20, 20))):
+        c, v = _coo_rand(shape, 4000, 3)
+        st = skx.SparseTensor(shape, c, v)
+        oc = oracle.Coo(shape, c, v)
+        A = [np.linalg.qr(rng.standard_normal((s, r)))[0] for s, r in zip(shape, R)]
+        core = rng.standard_normal(R)
+        got = skx.fitness(st, skx.TuckerModel(core, A))
+        exp = oracle.fitness_tucker(oc, core, A)
+        assert got == pytest.approx(exp, rel=1e-11, abs=1e-12)
