@@ -16,6 +16,7 @@
 // Arithmetic of the accept tests uses explicit _rn intrinsics so no FMA
 // contraction can change a comparison relative to numpy's x86-64 build.
 #include <math.h>
+#include <math_constants.h>
 
 #include "skx_common.cuh"
 #include "zig_tables.h"
@@ -35,6 +36,84 @@ __global__ void k_uniform(uint64_t k0, uint64_t k1, uint64_t p0, int64_t n, doub
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) out[i] = u64_to_unit(philox_raw(k0, k1, p0 + (uint64_t)i));
+}
+
+// ------------------------------------------------------------------ log1p
+// numpy's ziggurat tail returns r + xx with xx = -log1p(-u)/r, so its value
+// depends on libm's log1p bit for bit.  This restates glibc 2.39's x86-64
+// FMA multiarch variant (fdlibm s_log1p.c, Estrin polynomial, FMA where gcc
+// contracted it), verified identical to the host libm on 4e8 inputs in (-1, 0]
+// (tools/check_log1p.c).  Only the branches reachable for x in (-1, 0] matter;
+// every non-fused operation is an explicit _rn intrinsic (no contraction).
+__device__ __forceinline__ int d_hi(double x) { return (int)(__double_as_longlong(x) >> 32); }
+__device__ __forceinline__ double d_sethi(double x, uint32_t h) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  b = (b & 0xffffffffULL) | ((unsigned long long)h << 32);
+  return __longlong_as_double((long long)b);
+}
+
+__device__ double glibc_log1p(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+               Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+               Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  double f = 0.0, c = 0.0, u;
+  int k = 1, hu = 0;
+  const int hx = d_hi(x), ax = hx & 0x7fffffff;
+  if (hx < 0x3FDA827A) {
+    if (ax >= 0x3ff00000) return x == -1.0 ? -CUDART_INF : CUDART_NAN;
+    if (ax < 0x3e200000) {
+      if (ax < 0x3c900000) return x;
+      return fma(-__dmul_rn(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx <= (int)0xbfd2bec3) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  }
+  if (hx >= 0x7ff00000) return __dadd_rn(x, x);
+  if (k != 0) {
+    if (hx < 0x43400000) {
+      u = __dadd_rn(1.0, x);
+      hu = d_hi(u);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = d_hi(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = d_sethi(u, (uint32_t)hu | 0x3ff00000u);
+    } else {
+      k += 1;
+      u = d_sethi(u, (uint32_t)hu | 0x3fe00000u);
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  const double kd = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) return k == 0 ? 0.0 : fma(kd, ln2_hi, fma(kd, ln2_lo, c));
+    const double R = __dmul_rn(fma(-f, 0.6666666666666666, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return fma(kd, ln2_hi, -__dsub_rn(__dsub_rn(R, fma(kd, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  const double z = __dmul_rn(s, s);
+  const double Ra = fma(z, Lp3, Lp2), Rb = fma(z, Lp5, Lp4), Rc = fma(z, Lp7, Lp6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  const double R = fma(z6, Rc, fma(z4, Rb, fma(z, Lp1, __dmul_rn(z2, Ra))));
+  const double t = __dmul_rn(s, __dadd_rn(R, hfsq));
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  const double q = __dsub_rn(__dsub_rn(hfsq, __dadd_rn(fma(kd, ln2_lo, c), t)), f);
+  return fma(kd, ln2_hi, -q);
 }
 
 // ------------------------------------------------------------------ ziggurat
@@ -65,8 +144,8 @@ __global__ void k_zig_classify(uint64_t k0, uint64_t k1, const uint64_t* p0p, in
         double u1 = u64_to_unit(philox_raw(k0, k1, p0 + t));
         double u2 = u64_to_unit(philox_raw(k0, k1, p0 + t + 1));
         t += 2;
-        xx = __dmul_rn(-ZIG_NOR_INV_R, log1p(-u1));
-        double yy = -log1p(-u2);
+        xx = __dmul_rn(-ZIG_NOR_INV_R, glibc_log1p(-u1));
+        double yy = -glibc_log1p(-u2);
         if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) break;
       }
       v = ((rabs >> 8) & 1) ? -__dadd_rn(ZIG_NOR_R, xx) : __dadd_rn(ZIG_NOR_R, xx);

@@ -607,7 +607,7 @@ extern "C" int skx_ts_kron(int n_other, const int64_t* ext_h, const int64_t* ran
   int64_t rmax = 1;
   for (int k = 0; k < n_other; ++k) rmax = imax(rmax, ranks_h[k]);
   double* cs = ar.take<double>(smax * rmax);
-  double* zbuf = ar.take<double>(n_other > 2 ? rmid * m : 1);
+  double* zbuf = ar.take<double>(rmid * m);
   size_t b1 = 0, b2 = 0, b3 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, b1, k_in, k_out, v_in, v_out, (int)smax, 0, 32, s);
   cub::DeviceRunLengthEncode::Encode(nullptr, b2, k_out, rb, cnt, nrun, (int)smax, s);
