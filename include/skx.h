@@ -99,14 +99,22 @@ int skx_ts_rhs_dense(const double* t, int ndim, const int64_t* shape_h, int mode
 int skx_ts_combine(int n, const int64_t* ext_h, const uint32_t* tab, const int64_t* tab_off_h,
                    int64_t m, int64_t P, uint32_t* out, void* stream);
 
+/* Kronecker-sketch plan of a TensorSketch operator: per-mode bucket-sorted,
+ * run-length-encoded row lists (depends only on the tables, so it is built once
+ * per operator and reused by every sub-problem).  plan = NULL or ws = NULL
+ * queries *plan_bytes / *ws_bytes. */
+int skx_ts_kron_plan(int n_other, const int64_t* ext_h, const uint32_t* tab,
+                     const int64_t* tab_off_h, int64_t m, void* plan, size_t* plan_bytes,
+                     void* ws, size_t* ws_bytes, void* stream);
+
 /* Z = S . kron(A_1, ..., A_k) (first factor slowest), m x prod(R), written
  * COLUMN-major (z[col*m + row]) -- the layout cuSOLVER's QR consumes.
  * factors_h: host array of device pointers to s_k x R_k row-major factors.
  * Replaces ts_apply_kron, src/sketching.py:113-147 (exact circular convolution
  * instead of FFT; equal up to rounding). */
-int skx_ts_kron(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
-                const double* const* factors_h, const uint32_t* tab, const int64_t* tab_off_h,
-                int64_t m, double* z, void* ws, size_t* ws_bytes, void* stream);
+int skx_ts_kron_apply(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
+                      const double* const* factors_h, const void* plan, int64_t m, double* z,
+                      void* ws, size_t* ws_bytes, void* stream);
 
 /* ------------------------------------------------------ K3: leverage */
 
@@ -179,11 +187,21 @@ int skx_rrf_stage1_dense(const double* t, int ndim, const int64_t* shape_h, int 
 
 /* --------------------------------------- K5/K7: residual and fitness */
 
-/* out[0] = || P a^T - Y ||_F^2 with P (m x R), a (s x R), Y addressed as
- * Y[j,i] = y[j*ys_j + i*ys_i] (covers Y and Y^T storage).  src/tucker.py:274. */
-int skx_resid_sq(const double* p, const double* a, int64_t m, int64_t s, int64_t R,
-                 const double* y, int64_t ys_j, int64_t ys_i, double* out, void* ws,
-                 size_t* ws_bytes, void* stream);
+/* out[0] = sum_{o,x} (sum_r U[o,r] Vt[r,x] - Y[o*ld + x])^2: the squared
+ * residual || Z core_t a^T - Y ||_F^2 of a sub-problem (src/tucker.py:274) with
+ * P = Z core_t, in whichever orientation makes Y's unit-stride index inner
+ * (U = a, Vt = P^T for Y^T storage; U = P, Vt = a^T for row-major Y). */
+int skx_resid_sq(const double* u, const double* vt, int64_t n_out, int64_t n_in, int64_t R,
+                 const double* y, int64_t ld, double* out, void* ws, size_t* ws_bytes,
+                 void* stream);
+
+/* R factor (w x w, row-major, upper) of the n x w matrix A[i,j] = a[i*rs + j*cs]
+ * by TSQR with Householder blocks (LAPACK dlarfg signs), w <= 64.  Replaces the
+ * LAPACK QRs of tall-skinny operands: np.linalg.qr in src/linalg.py:45 (factor
+ * leverage scores) and the SVDs of src/linalg.py:59 / src/tucker.py:141, which
+ * are taken as SVD(R). */
+int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t cs, double* r, void* ws,
+               size_t* ws_bytes, void* stream);
 
 /* out[0] = sum(x^2) with a fixed-order reduction. */
 int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,

@@ -33,7 +33,8 @@ _SIGS = {
     "skx_ts_rhs_coo": [c_i32, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
     "skx_ts_rhs_dense": [c_p, c_i32, c_p, c_i32, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_ts_combine": [c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_p],
-    "skx_ts_kron": [c_i32, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
+    "skx_ts_kron_plan": [c_i32, c_p, c_p, c_p, c_i64, c_p, c_sz_p, c_p, c_sz_p, c_p],
+    "skx_ts_kron_apply": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_lev_prepare": [c_p, c_i64, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_lev_sample": [c_i32, c_p, c_p, c_p, c_i64, c_u64, c_u64, c_u64, c_p, c_p, c_p],
     "skx_kron_rows": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
@@ -44,8 +45,9 @@ _SIGS = {
                            c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p],
     "skx_rrf_table": [c_u64, c_u64, c_u64, c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_i64, c_p, c_p],
     "skx_rrf_stage1_dense": [c_p, c_i32, c_p, c_i32, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
-    "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
+    "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_sumsq": [c_p, c_i64, c_p, c_p, c_sz_p, c_p],
+    "skx_tsqr_r": [c_p, c_i64, c_i32, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_cp_cross_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_last_error": [],

@@ -294,20 +294,24 @@ __global__ void k_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t ha
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (; t < nb; t += stride) {
     const uint64_t b = b_first + t;
-    U64x4 blk = philox_block(k0, k1, b + 1);
+    const U64x4 blk = philox_block(k0, k1, b + 1);
+    // branch-free screen of the 8 halves (rejections are ~1e-8 rare); the
+    // range checks only run for a block that has a candidate
+    uint32_t flag = 0;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const uint64_t r = 4 * b + w;
-      if (r < p0 || r >= p0 + nraw) continue;
-      const uint64_t q = off + 2 * (r - p0);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (q + h >= n_u32) continue;
-        uint32_t u = h ? (uint32_t)(blk.v[w] >> 32) : (uint32_t)blk.v[w];
-        if ((uint32_t)((uint64_t)u * k) < thresh) {
-          unsigned long long s = atomicAdd(count, 1ULL);
-          if ((int64_t)s < cap) rej[s] = q + h;
-        }
+      flag |= (uint32_t)((uint32_t)blk.v[w] * k < thresh) << (2 * w);
+      flag |= (uint32_t)((uint32_t)(blk.v[w] >> 32) * k < thresh) << (2 * w + 1);
+    }
+    if (flag) {
+      for (int bit = 0; bit < 8; ++bit) {
+        if (!((flag >> bit) & 1)) continue;
+        const uint64_t r = 4 * b + (bit >> 1);
+        if (r < p0 || r >= p0 + nraw) continue;
+        const uint64_t q = off + 2 * (r - p0) + (bit & 1);
+        if (q >= n_u32) continue;
+        const unsigned long long s = atomicAdd(count, 1ULL);
+        if ((int64_t)s < cap) rej[s] = q;
       }
     }
   }

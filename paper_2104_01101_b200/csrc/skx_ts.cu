@@ -252,82 +252,6 @@ __global__ void __launch_bounds__(256) k_gather_rows(const double* __restrict__ 
   }
 }
 
-// =========================================================== Kronecker sketch
-// Bucket-sorted row lists of one mode: run r covers rows list[rs[r]..rs[r+1])
-// all hashing to bucket rb[r]; *nrun runs.  CountSketch values per run.
-__global__ void k_cs_runs(const double* __restrict__ A, int64_t R, const uint32_t* __restrict__ rows,
-                          const uint32_t* __restrict__ negs, const int64_t* __restrict__ rs,
-                          const int* __restrict__ nrun, double* __restrict__ cs) {
-  // cs[r*R + p] = sum_{i in run r, ascending} sign_i A[i,p]
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nr = *nrun;
-  if (idx >= nr * R) return;
-  const int64_t r = idx / R, p = idx - r * R;
-  double s = 0.0;
-  for (int64_t e = rs[r]; e < rs[r + 1]; ++e) {
-    const uint32_t i = rows[e];
-    const double x = A[(int64_t)i * R + p];
-    s += negs[i] ? -x : x;
-  }
-  cs[idx] = s;
-}
-
-// First mode: dense column-major m x R CountSketch from the runs.
-__global__ void k_cs_dense(const double* __restrict__ cs, const uint32_t* __restrict__ rb,
-                           const int* __restrict__ nrun, int64_t R, int64_t m,
-                           double* __restrict__ zt) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nr = *nrun;
-  if (idx >= nr * R) return;
-  const int64_t r = idx / R, p = idx - r * R;
-  zt[p * m + rb[r]] = cs[idx];
-}
-
-// z_new[:, q*R + p] = z_cur[:, q] (circular-conv) y_p, y_p sparse over runs.
-// Grid: (h-blocks, q, p-chunks of 8); z stored column-major (ld = m).
-__global__ void __launch_bounds__(256) k_cconv(const double* __restrict__ zc, int64_t m,
-                                               const double* __restrict__ cs,
-                                               const uint32_t* __restrict__ rb,
-                                               const int* __restrict__ nrun, int64_t R,
-                                               double* __restrict__ zn) {
-  extern __shared__ double zs[];
-  const int64_t q = blockIdx.y;
-  const int64_t p0 = blockIdx.z * 8;
-  const int np = (int)imin(8, R - p0);
-  for (int64_t h = threadIdx.x; h < m; h += blockDim.x) zs[h] = zc[q * m + h];
-  __syncthreads();
-  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (h >= m) return;
-  const int nr = *nrun;
-  double acc[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-  for (int r = 0; r < nr; ++r) {
-    int64_t src = h - (int64_t)rb[r];
-    if (src < 0) src += m;
-    const double zv = zs[src];
-    const double* y = cs + (int64_t)r * R + p0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u < np) acc[u] = fma(y[u], zv, acc[u]);
-  }
-  const int64_t rn = R;  // columns of this mode
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-    if (u < np) zn[(q * rn + p0 + u) * m + h] = acc[u];
-}
-
-// ------------------------------------------------------------------ helpers
-struct SortBufs {
-  uint32_t *k_in, *k_out, *v_in, *v_out, *neg;
-  int64_t* rs;
-  uint32_t* rb;
-  int* nrun;
-  int64_t* counts;
-  void* cub_tmp;
-  size_t cub_bytes;
-};
-
 }  // namespace skx
 
 using namespace skx;
@@ -579,77 +503,4 @@ extern "C" int skx_rrf_stage1_dense(const double* t, int ndim, const int64_t* sh
                                     size_t* ws_bytes, void* stream) {
   return dense_sketch(true, t, ndim, shape_h, mode, tab, nullptr, k2, stage1, ws, ws_bytes,
                       (cudaStream_t)stream);
-}
-
-extern "C" int skx_ts_kron(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
-                           const double* const* factors_h, const uint32_t* tab,
-                           const int64_t* tab_off_h, int64_t m, double* z, void* ws,
-                           size_t* ws_bytes, void* stream) {
-  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_ts_kron: 1..15 factors supported");
-  SKX_REQUIRE(ws_bytes != nullptr, "skx_ts_kron: ws_bytes is NULL");
-  cudaStream_t s = (cudaStream_t)stream;
-  int64_t smax = 0, rtot = 1, rmid = 1;
-  for (int k = 0; k < n_other; ++k) {
-    smax = imax(smax, ext_h[k]);
-    rtot *= ranks_h[k];
-  }
-  for (int k = 0; k + 1 < n_other; ++k) rmid *= ranks_h[k];
-  Arena ar(ws, *ws_bytes);
-  uint32_t* k_in = ar.take<uint32_t>(smax);
-  uint32_t* k_out = ar.take<uint32_t>(smax);
-  uint32_t* v_in = ar.take<uint32_t>(smax);
-  uint32_t* v_out = ar.take<uint32_t>(smax);
-  uint32_t* neg = ar.take<uint32_t>(smax);
-  uint32_t* rb = ar.take<uint32_t>(smax);
-  int64_t* cnt = ar.take<int64_t>(smax + 1);
-  int64_t* rs = ar.take<int64_t>(smax + 1);
-  int* nrun = ar.take<int>(1);
-  int64_t rmax = 1;
-  for (int k = 0; k < n_other; ++k) rmax = imax(rmax, ranks_h[k]);
-  double* cs = ar.take<double>(smax * rmax);
-  double* zbuf = ar.take<double>(rmid * m);
-  size_t b1 = 0, b2 = 0, b3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b1, k_in, k_out, v_in, v_out, (int)smax, 0, 32, s);
-  cub::DeviceRunLengthEncode::Encode(nullptr, b2, k_out, rb, cnt, nrun, (int)smax, s);
-  cub::DeviceScan::ExclusiveSum(nullptr, b3, cnt, rs, (int)smax + 1, s);
-  size_t cb = std::max(b1, std::max(b2, b3));
-  void* cub_tmp = ar.take<char>(cb);
-  if (ws == nullptr) {
-    *ws_bytes = ar.used + 256;
-    return SKX_OK;
-  }
-  SKX_REQUIRE(ar.ok(), "skx_ts_kron: workspace too small");
-  int bits = 1;
-  while ((int64_t(1) << bits) < m) ++bits;
-  int launches = 0;
-  int64_t rcur = 1;
-  for (int k = 0; k < n_other; ++k) {
-    const int64_t sk = ext_h[k], R = ranks_h[k];
-    const uint32_t* tk = tab + tab_off_h[k];
-    k_bucket_keys<true><<<(unsigned)((sk + 255) / 256), 256, 0, s>>>(tk, sk, k_in, v_in, neg);
-    size_t c1 = cb;
-    cub::DeviceRadixSort::SortPairs(cub_tmp, c1, k_in, k_out, v_in, v_out, (int)sk, 0, bits, s);
-    cudaMemsetAsync(cnt, 0, (smax + 1) * sizeof(int64_t), s);
-    c1 = cb;
-    cub::DeviceRunLengthEncode::Encode(cub_tmp, c1, k_out, rb, cnt, nrun, (int)sk, s);
-    c1 = cb;
-    cub::DeviceScan::ExclusiveSum(cub_tmp, c1, cnt, rs, (int)sk + 1, s);
-    k_cs_runs<<<(unsigned)((sk * R + 255) / 256), 256, 0, s>>>(factors_h[k], R, v_out, neg, rs,
-                                                              nrun, cs);
-    launches += 5;
-    // destination of this step: final z for the last mode, else ping-pong
-    double* dst = (k == n_other - 1) ? z : ((k % 2 == 0) == (n_other % 2 == 0) ? zbuf : z);
-    if (k == 0) {
-      cudaMemsetAsync(dst, 0, (size_t)R * m * sizeof(double), s);
-      k_cs_dense<<<(unsigned)((sk * R + 255) / 256), 256, 0, s>>>(cs, rb, nrun, R, m, dst);
-      launches += 1;
-    } else {
-      const double* src = (dst == z) ? zbuf : z;
-      dim3 grid((unsigned)((m + 255) / 256), (unsigned)rcur, (unsigned)((R + 7) / 8));
-      k_cconv<<<grid, 256, (size_t)m * 8, s>>>(src, m, cs, rb, nrun, R, dst);
-      launches += 1;
-    }
-    rcur *= R;
-  }
-  return check_launch("skx_ts_kron", launches);
 }

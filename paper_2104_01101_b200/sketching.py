@@ -159,17 +159,40 @@ class TensorSketchOp:
         return out
 
 
+def ts_kron_plan_dev(ts):
+    """Per-operator Kronecker-sketch plan (bucket-sorted rows), cached on `ts`."""
+    torch = _torch()
+    plan = getattr(ts, "_kron_plan", None)
+    if plan is None:
+        lib = nat.load()
+        ext, ep = nat.host_i64(ts.extents)
+        off, op = nat.host_i64(ts.tab_off)
+        pb = ctypes.c_size_t(0)
+        wb = ctypes.c_size_t(0)
+        st = nat.stream()
+        nat.call("skx_ts_kron_plan", len(ts.extents), ep, nat.ptr(ts.tab), op, ts.m, None,
+                 ctypes.byref(pb), None, ctypes.byref(wb), st)
+        plan = torch.empty(max(pb.value, 256), dtype=torch.uint8, device="cuda")
+        ws = nat.WS.get(wb.value, 0)
+        pb2 = ctypes.c_size_t(plan.numel())
+        wb2 = ctypes.c_size_t(ws.numel())
+        nat.call("skx_ts_kron_plan", len(ts.extents), ep, nat.ptr(ts.tab), op, ts.m, nat.ptr(plan),
+                 ctypes.byref(pb2), nat.ptr(ws), ctypes.byref(wb2), st)
+        ts._kron_plan = plan
+    return plan
+
+
 def ts_kron_dev(ts, factors):
     """Z = S kron(factors) on device, returned as an (m, r) column-major view."""
     torch = _torch()
+    plan = ts_kron_plan_dev(ts)
     fs = [f.contiguous() for f in factors]
     r = int(np.prod([f.shape[1] for f in fs]))
     zt = torch.empty((r, ts.m), dtype=torch.float64, device="cuda")
     ext, ep = nat.host_i64(ts.extents)
     rk, rp = nat.host_i64([f.shape[1] for f in fs])
     arr, fp = nat.host_ptrs(fs)
-    off, op = nat.host_i64(ts.tab_off)
-    nat.call_ws("skx_ts_kron", (len(fs), ep, rp, fp, nat.ptr(ts.tab), op, ts.m, nat.ptr(zt)))
+    nat.call_ws("skx_ts_kron_apply", (len(fs), ep, rp, fp, nat.ptr(plan), ts.m, nat.ptr(zt)))
     return zt.t()
 
 

@@ -64,6 +64,37 @@ class SparseTensor:
         self._device = None
 
     @classmethod
+    def from_sorted(cls, shape, coords, values):
+        """Trusted-order constructor: same validation as __init__ but O(nnz)
+        (checks that coords are strictly lexicographically increasing instead
+        of re-sorting).  Keeps the caller's arrays (e.g. pinned buffers)."""
+        shape = tuple(int(s) for s in shape)
+        coords = np.asarray(coords)
+        values = np.asarray(values)
+        if coords.dtype != np.int64 or values.dtype != np.float64:
+            raise ValueError("from_sorted needs int64 coords and float64 values")
+        if coords.ndim != 2 or coords.shape[1] != len(shape) or coords.shape[0] != values.shape[0]:
+            raise ValueError("coords must be (nnz, N) matching values")
+        if coords.size and ((coords.min(axis=0) < 0).any() or (coords.max(axis=0) >= np.asarray(shape)).any()):
+            raise ValueError("coordinate out of range")
+        chunk = 1 << 24
+        for lo in range(0, max(coords.shape[0] - 1, 0), chunk):
+            a = coords[lo:lo + chunk]
+            b = coords[lo + 1:lo + chunk + 1]
+            k = min(a.shape[0], b.shape[0])
+            a, b = a[:k], b[:k]
+            lt = np.zeros(k, dtype=bool)
+            eq = np.ones(k, dtype=bool)
+            for n in range(len(shape)):
+                lt |= eq & (a[:, n] < b[:, n])
+                eq &= a[:, n] == b[:, n]
+            if not lt.all():
+                raise ValueError("coordinates must be lexsorted and duplicate-free")
+        obj = cls.__new__(cls)
+        obj._init(shape, coords, values)
+        return obj
+
+    @classmethod
     def from_device(cls, shape, coords, values, validate=True):
         """Wrap device arrays (coords (nnz, N) or (N, nnz) integer CUDA tensor,
         values float64 CUDA tensor) that are already lexsorted.  Host copies
@@ -196,9 +227,15 @@ class DeviceCoo:
         torch = _torch()
         if max(st.shape) >= 2 ** 31:
             raise ValueError("extents must be < 2^31 for the device layout")
-        c = torch.from_numpy(np.ascontiguousarray(st.coords.T.astype(np.int32))).cuda()
-        v = torch.from_numpy(np.ascontiguousarray(st.values)).cuda()
-        return cls(st.shape, c, v)
+        import warnings
+        with warnings.catch_warnings():  # read-only host arrays are only read
+            warnings.simplefilter("ignore", UserWarning)
+            c64 = torch.from_numpy(np.ascontiguousarray(st.coords))
+            v = torch.from_numpy(np.ascontiguousarray(st.values))
+        # one H2D of the caller's arrays, then int64 AoS -> int32 SoA on device
+        cd = c64.to("cuda", non_blocking=True)
+        vd = v.to("cuda", non_blocking=True)
+        return cls(st.shape, cd.t().to(torch.int32).contiguous(), vd)
 
     @classmethod
     def from_torch(cls, shape, coords, vals, validate=True):
@@ -249,19 +286,20 @@ class DeviceCoo:
         if n not in self._fibre:
             others = [k for k in range(self.ndim) if k != n]
             s_n = self.shape[n]
-            cnt = torch.bincount(self.coords[n].long(), minlength=s_n) if self.nnz else \
-                torch.zeros(s_n, dtype=torch.int64, device="cuda")
-            colptr = torch.zeros(s_n + 1, dtype=torch.int64, device="cuda")
-            torch.cumsum(cnt, 0, out=colptr[1:])
+            bounds = torch.arange(s_n + 1, dtype=torch.int32, device="cuda")
             if n == 0:
+                keys = self.coords[0]
                 oth = self.coords[1:].contiguous() if self.ndim > 1 else \
                     torch.empty((0, self.nnz), dtype=torch.int32, device="cuda")
                 vals = self.vals
             else:
-                perm = torch.argsort(self.coords[n], stable=True)
+                # stable sort by i_n of the lexsorted order = (i_n, others ascending)
+                keys, perm = torch.sort(self.coords[n], stable=True)
                 oth = self.coords[others][:, perm].contiguous()
                 vals = self.vals[perm].contiguous()
                 del perm
+            colptr = torch.searchsorted(keys, bounds, out_int32=False)
+            del keys
             self._fibre[n] = (colptr, oth, vals)
         return self._fibre[n]
 
@@ -412,11 +450,13 @@ def tucker_cross_dev(d, core, factors):
     return (proj * core).sum()
 
 
-def fitness_tucker_dev(d, core, factors, norm2=None):
+def fitness_tucker_dev(d, core, factors, norm2=None, comm=None):
     torch = _torch()
     if norm2 is None:
         norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
     cross = tucker_cross_dev(d, core, factors)
+    if comm is not None:
+        cross = comm.allreduce(cross.clone().view(1))[0]
     mod = (core * core).sum()
     r2 = torch.clamp(norm2 - 2.0 * cross + mod, min=0.0)
     return 1.0 - torch.sqrt(r2) / torch.sqrt(norm2)
@@ -443,11 +483,13 @@ def cp_cross_dev(d, factors, weights):
     return ((factors[0] * weights) * m0).sum()
 
 
-def fitness_cp_dev(d, factors, weights, norm2=None):
+def fitness_cp_dev(d, factors, weights, norm2=None, comm=None):
     torch = _torch()
     if norm2 is None:
         norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
     cross = cp_cross_dev(d, factors, weights)
+    if comm is not None:
+        cross = comm.allreduce(cross.clone().view(1))[0]
     scaled = factors[0] * weights
     g = torch.ones((factors[0].shape[1],) * 2, dtype=torch.float64, device="cuda")
     for a in factors[1:]:

@@ -19,7 +19,7 @@ import numpy as np
 from . import _native as nat
 from . import rng as rngmod
 from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev,
-                     thin_svd_dev)
+                     top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, gather_coo_dev, gather_dense_dev,
                         hits_to_dense, kron_rows_dev, lev_sample_dev, rrf_table_dev, ts_kron_dev,
                         ts_rhs_coo_dev, ts_rhs_dense_dev)
@@ -116,7 +116,7 @@ def rrf_stage1_dev(d, n, tabs):
     return st1
 
 
-def init_rrf_dev(d, n, rank, width, gen):
+def init_rrf_dev(d, n, rank, width, gen, comm=None):
     """Range-finder init of factor n (src/tucker.py:129-144) on device."""
     torch = _torch()
     if width < rank:
@@ -127,11 +127,13 @@ def init_rrf_dev(d, n, rank, width, gen):
     tabs = draw_rrf_tables(gen, P, k2)
     gauss = gen.standard_normal((k2, width)) / np.sqrt(width)
     st1 = rrf_stage1_dev(d, n, tabs)
+    if comm is not None:
+        comm.allreduce(st1)
     b = st1 @ torch.from_numpy(gauss).cuda()
-    u, _, _ = thin_svd_dev(b)
-    if u.shape[1] < rank:
+    if min(b.shape) < rank:
         raise ValueError(f"cannot extract {rank} directions from a {tuple(b.shape)} sketch")
-    return u[:, :rank].contiguous()
+    u, _, _ = top_svd_dev(b, rank)
+    return u.contiguous()
 
 
 def init_rrf(tn, rank, width, rng):
@@ -161,7 +163,7 @@ def random_orthonormal_dev(n_rows, n_cols, gen):
 class _Run:
     """Device state of one sketched_tucker_als call."""
 
-    def __init__(self, t, config):
+    def __init__(self, t, config, comm=None):
         torch = _torch()
         if config.sketch is None:
             raise ValueError("sketched_tucker_als needs a sketch kind")
@@ -177,7 +179,11 @@ class _Run:
         self.cfg = config
         self.d = device_of(t)
         self.sparse = is_sparse_dev(self.d)
-        self.norm2 = self.d.norm2()[0] if self.sparse else (self.d * self.d).sum()
+        self.comm = comm
+        n2 = self.d.norm2().clone() if self.sparse else (self.d * self.d).sum().view(1)
+        if comm is not None:
+            comm.allreduce(n2)
+        self.norm2 = n2[0]
         self.rng_init, self.rng_sketch, self.rng_solve = rngmod.split_rng(config.seed, 3)
         self.normals = NormalSource(self.rng_solve)
         self.use_ts = config.sketch == "tensorsketch"
@@ -194,7 +200,8 @@ class _Run:
         for n in range(1, self.ndim):
             if init == "rrf":
                 width = self.cfg.resolved_rrf_width(self.ranks[n])
-                self.factors[n] = init_rrf_dev(self.d, n, self.ranks[n], width, self.rng_init)
+                self.factors[n] = init_rrf_dev(self.d, n, self.ranks[n], width, self.rng_init,
+                                               self.comm)
             elif init == "random":
                 self.factors[n] = random_orthonormal_dev(self.shape[n], self.ranks[n], self.rng_init)
             else:
@@ -208,6 +215,8 @@ class _Run:
             yt = ts_rhs_coo_dev(op, colptr, oth, vals, self.shape[n])
         else:
             yt = ts_rhs_dense_dev(op, self.d, n)
+        if self.comm is not None:
+            self.comm.allreduce(yt)
         self.ts_ops[n], self.ts_rhs[n] = op, yt
 
     def prep(self):
@@ -232,6 +241,8 @@ class _Run:
                 y = hits_to_dense(off, col, val, self.m, self.shape[n])
             else:
                 y = gather_dense_dev(self.d, n, idx, w)
+            if self.comm is not None:
+                self.comm.allreduce(y)
         core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals)
         return core_t, a, resid_dev(z, core_t, a, y)
 
@@ -264,7 +275,7 @@ class _Run:
             core = self.fold_core(core_t)
             e1.record()
             ev.append((e0, e1))
-            f = fitness_tucker_dev(self.d, core, self.factors, self.norm2)
+            f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, self.comm)
             fit_dev.append(f)
             if self.cfg.convergence_tol > 0 and len(fit_dev) > 1:
                 if abs(float(fit_dev[-1].item()) - float(fit_dev[-2].item())) < self.cfg.convergence_tol:
@@ -276,9 +287,9 @@ class _Run:
         return core
 
 
-def sketched_tucker_als_dev(t, config):
+def sketched_tucker_als_dev(t, config, comm=None):
     """Device-resident form: returns (core, factors) as CUDA tensors + trace."""
-    run = _Run(t, config)
+    run = _Run(t, config, comm)
     run.initialise()
     run.prep()
     trace = SweepTrace()

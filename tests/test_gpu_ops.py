@@ -142,6 +142,36 @@ def test_fitness(golden, skx):
     assert skx.fitness(st, skx.CPModel(cpf, w)) == pytest.approx(float(golden["fitcp_sparse"]), abs=1e-13)
 
 
+@pytest.mark.parametrize("n,w", [(1, 1), (7, 5), (256, 20), (257, 20), (100_000, 20), (3000, 33),
+                                 (50_000, 64)])
+def test_tsqr_r_matches_lapack(n, w):
+    import torch
+    from paper_2104_01101_b200.linalg import tsqr_r_dev
+    a = np.random.default_rng(n + w).standard_normal((n, w))
+    if n < w:
+        return
+    r = tsqr_r_dev(torch.from_numpy(a).cuda()).cpu().numpy()
+    ref = np.linalg.qr(a, mode="r")
+    assert relerr(np.abs(r), np.abs(ref)) <= 1e-12
+    # strided (transposed) input
+    rt = tsqr_r_dev(torch.from_numpy(a.T.copy()).cuda().t()).cpu().numpy()
+    assert np.array_equal(rt, r)
+
+
+@pytest.mark.parametrize("shape,k", [((50_000, 20), 10), ((30, 100_000), 20), ((400, 300), 5)])
+def test_top_svd(shape, k):
+    import torch
+    from paper_2104_01101_b200.linalg import top_svd_dev
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal(shape) * np.linspace(1, 3, shape[1])
+    u, s, v = (t.cpu().numpy() for t in top_svd_dev(torch.from_numpy(a).cuda(), k))
+    uu, ss, vvt = np.linalg.svd(a, full_matrices=False)
+    assert np.allclose(s, ss[:k], rtol=1e-12)
+    (cu, cv), _ = canon([u, v])
+    (ru, rv), _ = canon([uu[:, :k], vvt[:k].T])
+    assert relerr(cu, ru) <= 1e-10 and relerr(cv, rv) <= 1e-10
+
+
 # ---------------------------------------------------------- device kernels vs oracle
 def _coo_rand(shape, nnz, seed):
     from paper_2104_01101_b200.synth import planted_cp_coo_host
