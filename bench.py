@@ -156,7 +156,7 @@ def run_ours(args, cfgd):
         trace = step()
     # ---- device-resident timed region
     hook_names = ["skx_ts_rhs_coo", "skx_rrf_stage1_coo", "skx_lemire_scan", "skx_tucker_cross_coo",
-                  "skx_resid_sq", "skx_ts_kron", "skx_philox_normal"]
+                  "skx_resid_sq", "skx_ts_kron_apply", "skx_philox_normal", "skx_tsqr_r"]
     sinks = {nm: [] for nm in hook_names}
     for nm in hook_names:
         nat.set_event_hook(nm, sinks[nm])

@@ -59,13 +59,13 @@ int skx_philox_normal(uint64_t k0, uint64_t k1, const uint64_t* p0, int64_t n, d
                       uint64_t* p_end, void* ws, size_t* ws_bytes, void* stream);
 
 /* Lemire rejection scan for Generator.integers(0, k, .): lists (unordered)
- * every draw index q in [0, n_u32) of the u32 run (raw start p0, optional
- * buffered high half) that numpy would reject.  Count written to *count
- * (device int64); positions beyond cap are counted but not stored.
+ * the absolute 32-bit positions A = 2*raw + half of every draw in raw words
+ * [raw_lo, raw_hi) that numpy would reject (rejection depends only on the
+ * drawn value, so the scan may start before the call's exact start is known).
+ * Count written to *count; positions beyond cap are counted, not stored.
  * Used to place RRF CountSketch tables (src/sketching.py:54-56). */
-int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
-                    uint32_t pending, uint64_t n_u32, uint32_t k, uint64_t* rej, int64_t cap,
-                    unsigned long long* count, void* stream);
+int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t raw_lo, uint64_t raw_hi, uint32_t k,
+                    uint64_t* rej, int64_t cap, unsigned long long* count, void* stream);
 
 /* ------------------------------------------------- K1/K2: TensorSketch */
 
@@ -76,15 +76,28 @@ int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
 int skx_ts_tables(int nmodes, const int64_t* extents_h, const int64_t* coeffs_h, int64_t m,
                   uint32_t* tab, void* stream);
 
-/* Y^T = (S . T_(n)^T)^T for a COO tensor in "fibre-major" layout for mode n:
- * nonzeros sorted by (i_n, other modes ascending); colptr (int64, s_n+1);
- * oth = (N-1) x nnz SoA int32 coordinates of the other modes (ascending);
- * tab = packed tables of the other modes concatenated, tab_off_h offsets.
- * yt is s_n x m (row i_n = column i_n of the reference's m x s_n output).
- * Replaces ts_apply_rhs sparse branch, src/sketching.py:150-167. */
-int skx_ts_rhs_coo(int n_other, int64_t nnz, int64_t s_n, const int64_t* colptr,
-                   const int32_t* oth, const double* vals, const uint32_t* tab,
-                   const int64_t* tab_off_h, int64_t m, double* yt, void* stream);
+/* ------------------------------------------------------ COO layouts */
+
+/* Record stride (8-byte words) of the fibre-major layout for a sparse order
+ * ndim: 2 (16-byte records) for ndim <= 3, 3 for ndim 4..5, -1 otherwise. */
+int skx_coo_rec_words(int ndim);
+
+/* Fibre-major layout of `mode` for a lexsorted COO tensor (coords = ndim x nnz
+ * SoA int32, vals f64): records {int32 other coords (ascending modes),
+ * f64 value} ordered by (i_mode, others) -- a stable radix sort by i_mode --
+ * and colptr (s_mode + 1 offsets).  The device counterpart of the cached
+ * unfoldings matricize_t / mode_sort (src/tensors.py:151-194, 89-95). */
+int skx_coo_fibre(int ndim, const int64_t* shape_h, int mode, int64_t nnz, const int32_t* coords,
+                  const double* vals, void* rec_out, int64_t* colptr, void* ws, size_t* ws_bytes,
+                  void* stream);
+
+/* Y^T = (S . T_(n)^T)^T for a COO tensor in the fibre-major layout of mode n
+ * (skx_coo_fibre); tab = packed tables of the other modes concatenated,
+ * tab_off_h offsets.  yt is s_n x m (row i_n = column i_n of the reference's
+ * m x s_n output).  Replaces ts_apply_rhs sparse branch, src/sketching.py:150-167. */
+int skx_ts_rhs_coo(int n_other, int64_t s_n, const int64_t* colptr, const void* rec,
+                   const uint32_t* tab, const int64_t* tab_off_h, int64_t m, double* yt,
+                   void* stream);
 
 /* Same for a dense C-order tensor (ndim, shape_h) and target mode.
  * Replaces ts_apply_rhs dense branch, src/sketching.py:168-175. */
@@ -155,25 +168,27 @@ int skx_gather_fibers_coo(int n_other, const int64_t* ext_h, int64_t s_n, int64_
 /* stage1[i_n, c] = sum_j T_(n)[i_n, j] sign_j [hash_j == c] where hash/sign are
  * the numpy draws integers(0,k2,P) then integers(0,2,P) of the u32 run
  * (p0, has_pending, pending), hash draws shifted past the sorted rejection
- * list rej (nrej entries).  COO input in fibre-major layout (as ts_rhs_coo).
+ * list rej (nrej entries).  COO input in fibre-major layout (skx_coo_fibre).
  * Replaces CountSketchOp.build + composite_apply stage 1, src/sketching.py:
  * 54-56, 327-340. */
-int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t nnz, int64_t s_n,
-                       const int64_t* colptr, const int32_t* oth, const double* vals,
-                       uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
-                       uint32_t pending, uint64_t sign_q0, const uint64_t* rej, int64_t nrej,
-                       int64_t k2, double* stage1, void* stream);
+int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n, const int64_t* colptr,
+                       const void* rec, uint64_t k0, uint64_t k1, uint64_t p0,
+                       uint32_t has_pending, uint32_t pending, uint64_t sign_q0,
+                       const uint64_t* rej, int64_t nrej, int64_t k2, double* stage1,
+                       void* stream);
 
 /* Fill n u64 with UINT64_MAX (pre-fill of a rejection buffer). */
 int skx_fill_u64max(uint64_t* a, int64_t n, void* stream);
 
 /* Sort the rejection list of skx_lemire_scan (cap entries, pre-filled with
- * UINT64_MAX) into the d-array d_i = r_i - i (padded with UINT64_MAX) and
- * write #{d_i <= P-1} -- the rejections among the first P accepted draws --
- * to *n_le (device u64).  The sign run then starts at u32 index P + *n_le. */
-int skx_lemire_finish(uint64_t* rej, const unsigned long long* count, int64_t cap, uint64_t P,
-                      uint64_t* d, unsigned long long* n_le, void* ws, size_t* ws_bytes,
-                      void* stream);
+ * UINT64_MAX), map it onto the run indices r_i of an integers() call starting
+ * at raw word p0 (preceded by the buffered high half of raw word pend_raw when
+ * has = 1), and write the d-array d_i = r_i - i (padded with UINT64_MAX) and
+ * #{d_i <= P-1} -- the rejections among the first P accepted draws -- to
+ * *n_le.  The sign run then starts at run index P + *n_le. */
+int skx_lemire_finish(uint64_t* rej, const unsigned long long* count, int64_t cap, uint64_t p0,
+                      uint32_t has, uint64_t pend_raw, uint64_t P, uint64_t* d,
+                      unsigned long long* n_le, void* ws, size_t* ws_bytes, void* stream);
 
 /* Materialise the packed (hash|sign) table for columns [0, P) (dense inputs). */
 int skx_rrf_table(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
@@ -209,14 +224,14 @@ int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_byte
 
 /* Tucker cross term <ttmc(T,{A}), C> over a lexsorted COO tensor (coords =
  * ndim x nnz SoA int32), factors_h device pointers (s_k x R_k), core C
- * (C-order R_0 x ... x R_{N-1}); colptr0 (s_0+1 offsets of the mode-0 slices,
- * may be NULL) enables the order-3 sliced kernel.  out[0] = cross.
+ * (C-order R_0 x ... x R_{N-1}); colptr0/rec0 (the mode-0 fibre-major layout,
+ * may be NULL) enable the order-3 sliced kernel.  out[0] = cross.
  * Replaces the sparse ttmc + vdot at src/tensors.py:249-258, 351-352. */
 int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h,
                          int64_t nnz, const int32_t* coords, const double* vals,
                          const double* const* factors_h, const double* core,
-                         const int64_t* colptr0, double* out, void* ws, size_t* ws_bytes,
-                         void* stream);
+                         const int64_t* colptr0, const void* rec0, double* out, void* ws,
+                         size_t* ws_bytes, void* stream);
 
 /* CP cross term sum(weights * A_0 .* mttkrp(T, A, 0)) over lexsorted COO.
  * Replaces src/tensors.py:354-357 (+ mttkrp :322-323). */

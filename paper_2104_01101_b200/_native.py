@@ -26,11 +26,13 @@ c_sz_p = ctypes.POINTER(ctypes.c_size_t)
 _SIGS = {
     "skx_philox_uniform": [c_u64, c_u64, c_u64, c_i64, c_p, c_p],
     "skx_philox_normal": [c_u64, c_u64, c_p, c_i64, c_p, c_p, c_p, c_sz_p, c_p],
-    "skx_lemire_scan": [c_u64, c_u64, c_u64, c_u32, c_u32, c_u64, c_u32, c_p, c_i64, c_p, c_p],
+    "skx_lemire_scan": [c_u64, c_u64, c_u64, c_u64, c_u32, c_p, c_i64, c_p, c_p],
     "skx_fill_u64max": [c_p, c_i64, c_p],
-    "skx_lemire_finish": [c_p, c_p, c_i64, c_u64, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_lemire_finish": [c_p, c_p, c_i64, c_u64, c_u32, c_u64, c_u64, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_ts_tables": [c_i32, c_p, c_p, c_i64, c_p, c_p],
-    "skx_ts_rhs_coo": [c_i32, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
+    "skx_coo_rec_words": [c_i32],
+    "skx_coo_fibre": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_ts_rhs_coo": [c_i32, c_i64, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
     "skx_ts_rhs_dense": [c_p, c_i32, c_p, c_i32, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_ts_combine": [c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_p],
     "skx_ts_kron_plan": [c_i32, c_p, c_p, c_p, c_i64, c_p, c_sz_p, c_p, c_sz_p, c_p],
@@ -41,14 +43,15 @@ _SIGS = {
     "skx_gather_fibers_dense": [c_p, c_i32, c_p, c_i32, c_p, c_p, c_i64, c_p, c_p],
     "skx_gather_fibers_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p,
                               c_i64, c_p, c_sz_p, c_p],
-    "skx_rrf_stage1_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_u64, c_u64, c_u64, c_u32,
-                           c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p],
+    "skx_rrf_stage1_coo": [c_i32, c_p, c_i64, c_p, c_p, c_u64, c_u64, c_u64, c_u32, c_u32, c_u64,
+                           c_p, c_i64, c_i64, c_p, c_p],
     "skx_rrf_table": [c_u64, c_u64, c_u64, c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_i64, c_p, c_p],
     "skx_rrf_stage1_dense": [c_p, c_i32, c_p, c_i32, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_sumsq": [c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_tsqr_r": [c_p, c_i64, c_i32, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
-    "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p,
+                             c_p],
     "skx_cp_cross_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],

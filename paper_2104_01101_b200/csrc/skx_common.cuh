@@ -138,6 +138,27 @@ struct U32Stream {
   }
 };
 
+// Fibre-major COO record (skx_layout.cu): NO other-mode int32 coordinates then
+// the f64 value; stride RW 8-byte words (2 for NO <= 2: one 16-byte load).
+template <int NO>
+__device__ __forceinline__ void load_rec(const double* __restrict__ rec, int64_t e, int32_t* c,
+                                         double& v) {
+  if (NO <= 2) {
+    const int4 q = __ldcs(reinterpret_cast<const int4*>(rec) + e);
+    c[0] = q.x;
+    if (NO > 1) c[1] = q.y;
+    v = __hiloint2double(q.w, q.z);
+  } else {
+    const int2* p = reinterpret_cast<const int2*>(rec + e * 3);
+    const int2 a = __ldcs(p), b = __ldcs(p + 1);
+    c[0] = a.x;
+    c[1] = a.y;
+    c[2] = b.x;
+    if (NO > 3) c[3] = b.y;
+    v = __ldcs(rec + e * 3 + 2);
+  }
+}
+
 // Packed sketch table entry: low 31 bits bucket, bit 31 set for sign -1.
 __device__ __forceinline__ uint32_t pk_bucket(uint32_t e) { return e & 0x7fffffffu; }
 __device__ __forceinline__ uint32_t pk_neg(uint32_t e) { return e >> 31; }

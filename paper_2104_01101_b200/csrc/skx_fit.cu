@@ -46,39 +46,47 @@ __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restr
 // is the inner one.  A CTA takes TO outer rows at a time (their U rows staged in
 // shared memory) and sweeps x: the R values Vt[:, x] are loaded once into
 // registers and reused for the TO rows, Y is streamed once, coalesced.
+// grid = (ceil(n_in / 256), n_split): a thread owns one inner column x for the
+// whole kernel (Vt[:, x] lives in registers), the CTA walks its share of outer
+// rows TO at a time with their U rows staged in shared memory; the TO Y loads
+// per step are independent and coalesced across the warp.
 template <int RT, int TO>
 __global__ void __launch_bounds__(256) k_resid(const double* __restrict__ U,
                                                const double* __restrict__ Vt, int64_t n_out,
                                                int64_t n_in, int R, const double* __restrict__ y,
                                                int64_t ld, double* __restrict__ part) {
   __shared__ double us[TO * RT];
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool xok = x < n_in;
+  const int64_t xc = xok ? x : 0;
+  double v[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) v[r] = (r < R) ? __ldg(Vt + (int64_t)r * n_in + xc) : 0.0;
+  const int64_t per = (n_out + gridDim.y - 1) / gridDim.y;
+  const int64_t oa = imin(blockIdx.y * per, n_out), ob = imin(oa + per, n_out);
   double acc = 0.0;
-  for (int64_t o0 = blockIdx.x * (int64_t)TO; o0 < n_out; o0 += (int64_t)gridDim.x * TO) {
-    const int nk = (int)imin(TO, n_out - o0);
+  for (int64_t o0 = oa; o0 < ob; o0 += TO) {
+    const int nk = (int)imin(TO, ob - o0);
     __syncthreads();
     for (int q = threadIdx.x; q < TO * RT; q += blockDim.x) {
       const int k = q / RT, r = q - k * RT;
       us[q] = (k < nk && r < R) ? U[(o0 + k) * R + r] : 0.0;
     }
     __syncthreads();
-    for (int64_t x = threadIdx.x; x < n_in; x += blockDim.x) {
-      double v[RT];
+    double yv[TO];
 #pragma unroll
-      for (int r = 0; r < RT; ++r) v[r] = r < R ? __ldg(Vt + (int64_t)r * n_in + x) : 0.0;
+    for (int k = 0; k < TO; ++k) yv[k] = (k < nk && xok) ? __ldcs(y + (o0 + k) * ld + x) : 0.0;
 #pragma unroll
-      for (int k = 0; k < TO; ++k) {
-        if (k < nk) {
-          double pred = 0.0;
+    for (int k = 0; k < TO; ++k) {
+      double pred = 0.0;
 #pragma unroll
-          for (int r = 0; r < RT; ++r) pred = fma(us[k * RT + r], v[r], pred);
-          const double d = pred - __ldcs(y + (o0 + k) * ld + x);
-          acc = fma(d, d, acc);
-        }
-      }
+      for (int r = 0; r < RT; ++r) pred = fma(us[k * RT + r], v[r], pred);
+      const double d = (k < nk && xok) ? pred - yv[k] : 0.0;
+      acc = fma(d, d, acc);
     }
   }
   acc = block_sum(acc);
-  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = acc;
 }
 
 // Generic R (no register tile): one (o, x) pair per thread step.
@@ -102,71 +110,103 @@ __global__ void k_resid_gen(const double* __restrict__ U, const double* __restri
 // Warp per slice i0: W = A0[i0,:] x_0 C (R1 x R2) in shared memory, then
 // each nonzero adds v * A1[i1,:] W A2[i2,:]^T.  Per-slice sums are written to
 // slice_out and reduced in slice order.
-// v[r2] = sum_r1 A1[i1,r1] W[r1,r2] runs R2 independent FMA chains (ILP), then
-// t = v . A2[i2,:]; two nonzeros per lane share every W load.
-template <int R2T>
-__global__ void __launch_bounds__(256) k_tucker3(const int64_t* __restrict__ colptr, int64_t s0,
-                                                 const int32_t* __restrict__ c1,
-                                                 const int32_t* __restrict__ c2,
-                                                 const double* __restrict__ vals,
+// Per lane NP nonzeros at a time: their coordinates, values and full factor
+// rows are loaded up front (one latency, many loads in flight), then
+// v[r2] = sum_r1 A1[i1,r1] W[r1,r2] runs RT independent FMA chains and
+// t = v . A2[i2,:].  W is shared by the NP nonzeros (one LDS per NP FMAs).
+// Factor rows are gathered warp-cooperatively into shared memory (consecutive
+// lanes read consecutive elements of one row, so a row costs ~3 sectors instead
+// of one sector per element per lane), then each lane contracts its own NP
+// nonzeros: v[r2] = sum_r1 A1[i1,r1] W[r1,r2] (RT independent FMA chains, W
+// read as 16-byte broadcasts shared by the NP nonzeros), t = v . A2[i2,:].
+template <int RT, int NP>
+__global__ void __launch_bounds__(128) k_tucker3(const int64_t* __restrict__ colptr, int64_t s0,
+                                                 const double* __restrict__ rec,
                                                  const double* __restrict__ A0,
                                                  const double* __restrict__ A1,
                                                  const double* __restrict__ A2,
                                                  const double* __restrict__ C, int R0, int R1,
                                                  int R2, double* __restrict__ slice_out) {
+  static_assert(RT % 2 == 0, "RT must be even");
+  constexpr int LD = RT + 1;
+  constexpr int PER_WARP = RT * RT + 2 * 32 * NP * LD + 1;
   extern __shared__ double smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  double* W = smem + (size_t)wid * R1 * R2T;  // rows padded to R2T
+  double* W = smem + (size_t)wid * (PER_WARP + 1);  // 16-byte aligned (PER_WARP + 1 even)
+  double* S1 = W + RT * RT;
+  double* S2 = S1 + 32 * NP * LD;
   for (int64_t i0 = blockIdx.x * (int64_t)nw + wid; i0 < s0; i0 += (int64_t)gridDim.x * nw) {
     const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
     if (e0 == e1) {
       if (lane == 0) slice_out[i0] = 0.0;
       continue;
     }
-    for (int q = lane; q < R1 * R2T; q += 32) {
-      const int r1 = q / R2T, r2 = q - r1 * R2T;
+    for (int q = lane; q < RT * RT; q += 32) {
+      const int r1 = q / RT, r2 = q - r1 * RT;
       double s = 0.0;
-      if (r2 < R2)
+      if (r1 < R1 && r2 < R2)
         for (int r0 = 0; r0 < R0; ++r0)
           s = fma(A0[i0 * R0 + r0], C[((int64_t)r0 * R1 + r1) * R2 + r2], s);
       W[q] = s;
     }
     __syncwarp();
     double acc = 0.0;
-    for (int64_t e = e0 + lane; e < e1; e += 64) {
-      const int64_t f = e + 32;
-      const bool has2 = f < e1;
-      const double* a1 = A1 + (int64_t)c1[e] * R1;
-      const double* a2 = A2 + (int64_t)c2[e] * R2;
-      const double* a1b = A1 + (int64_t)c1[has2 ? f : e] * R1;
-      const double* a2b = A2 + (int64_t)c2[has2 ? f : e] * R2;
-      double v[R2T], w[R2T];
+    for (int64_t base = e0; base < e1; base += 32 * NP) {
+      int i1[NP], i2[NP];
+      double x[NP];
 #pragma unroll
-      for (int r = 0; r < R2T; ++r) {
-        v[r] = 0.0;
-        w[r] = 0.0;
+      for (int u = 0; u < NP; ++u) {
+        const int64_t e = base + 32 * u + lane;
+        const bool ok = e < e1;
+        int32_t c[4];
+        double xv;
+        load_rec<2>(rec, ok ? e : e0, c, xv);
+        i1[u] = c[0];
+        i2[u] = c[1];
+        x[u] = ok ? xv : 0.0;
       }
-      for (int r1 = 0; r1 < R1; ++r1) {
-        const double x = a1[r1], xb = a1b[r1];
-        const double* wr = W + r1 * R2T;
 #pragma unroll
-        for (int r2 = 0; r2 < R2T; ++r2) {
-          const double wv = wr[r2];
-          v[r2] = fma(x, wv, v[r2]);
-          w[r2] = fma(xb, wv, w[r2]);
+      for (int u = 0; u < NP; ++u) {
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+          const int q = t * 32 + lane, j = q / RT, c = q - j * RT;
+          const int r1 = __shfl_sync(0xffffffffu, i1[u], j);
+          const int r2 = __shfl_sync(0xffffffffu, i2[u], j);
+          S1[(u * 32 + j) * LD + c] = c < R1 ? __ldg(A1 + (int64_t)r1 * R1 + c) : 0.0;
+          S2[(u * 32 + j) * LD + c] = c < R2 ? __ldg(A2 + (int64_t)r2 * R2 + c) : 0.0;
         }
       }
-      double t = 0.0, tb = 0.0;
+      __syncwarp();
+      double v[NP][RT];
 #pragma unroll
-      for (int r2 = 0; r2 < R2T; ++r2) {
-        if (r2 < R2) {
-          t = fma(v[r2], a2[r2], t);
-          tb = fma(w[r2], a2b[r2], tb);
+      for (int u = 0; u < NP; ++u)
+#pragma unroll
+        for (int r = 0; r < RT; ++r) v[u][r] = 0.0;
+#pragma unroll
+      for (int r1 = 0; r1 < RT; ++r1) {
+        double a[NP];
+#pragma unroll
+        for (int u = 0; u < NP; ++u) a[u] = S1[(u * 32 + lane) * LD + r1];
+        const double2* wr = reinterpret_cast<const double2*>(W + r1 * RT);
+#pragma unroll
+        for (int r2 = 0; r2 < RT; r2 += 2) {
+          const double2 wv = wr[r2 / 2];
+#pragma unroll
+          for (int u = 0; u < NP; ++u) {
+            v[u][r2] = fma(a[u], wv.x, v[u][r2]);
+            v[u][r2 + 1] = fma(a[u], wv.y, v[u][r2 + 1]);
+          }
         }
       }
-      acc = fma(vals[e], t, acc);
-      if (has2) acc = fma(vals[f], tb, acc);
+#pragma unroll
+      for (int u = 0; u < NP; ++u) {
+        double t = 0.0;
+#pragma unroll
+        for (int r2 = 0; r2 < RT; ++r2) t = fma(v[u][r2], S2[(u * 32 + lane) * LD + r2], t);
+        acc = fma(x[u], t, acc);
+      }
+      __syncwarp();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -251,34 +291,44 @@ extern "C" int skx_resid_sq(const double* u, const double* vt, int64_t n_out, in
   cudaStream_t st = (cudaStream_t)stream;
   double* part = (double*)ws;
   const int r = (int)R;
-  if (R <= 4)
-    k_resid<4, 16><<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 8)
-    k_resid<8, 8><<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 10)
-    k_resid<10, 8><<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 16)
-    k_resid<16, 8><<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 20)
-    k_resid<20, 8><<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 32)
-    k_resid<32, 4><<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else
+  // (x-blocks) x (row splits) <= kRedBlocks CTAs, fixed for given shapes
+  const int64_t xb = (n_in + kRedThreads - 1) / kRedThreads;
+  const int64_t ys = imax(1, imin(kRedBlocks / imax(xb, 1), (n_out + 15) / 16));
+  dim3 grid((unsigned)xb, (unsigned)ys);
+  int nparts = (int)(xb * ys);
+  if (xb > kRedBlocks) {
     k_resid_gen<<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  k_final_sum<<<1, 1024, 0, st>>>(part, kRedBlocks, out);
+    nparts = kRedBlocks;
+  } else if (R <= 4)
+    k_resid<4, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+  else if (R <= 8)
+    k_resid<8, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+  else if (R <= 10)
+    k_resid<10, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+  else if (R <= 16)
+    k_resid<16, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+  else if (R <= 20)
+    k_resid<20, 12><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+  else if (R <= 32)
+    k_resid<32, 8><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+  else {
+    k_resid_gen<<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+    nparts = kRedBlocks;
+  }
+  k_final_sum<<<1, 1024, 0, st>>>(part, nparts, out);
   return check_launch("skx_resid_sq", 2);
 }
 
 extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h,
                                     int64_t nnz, const int32_t* coords, const double* vals,
                                     const double* const* factors_h, const double* core,
-                                    const int64_t* colptr0, double* out, void* ws,
+                                    const int64_t* colptr0, const void* rec0, double* out, void* ws,
                                     size_t* ws_bytes, void* stream) {
   SKX_REQUIRE(ndim >= 1 && ndim <= 8, "skx_tucker_cross_coo: order 1..8");
   SKX_REQUIRE(ws_bytes != nullptr, "skx_tucker_cross_coo: ws_bytes is NULL");
   cudaStream_t s = (cudaStream_t)stream;
-  const bool fast3 = (ndim == 3 && ranks_h[2] <= 32 && colptr0 != nullptr &&
-                      ranks_h[1] * 32 * 8 * 8 <= 200 * 1024);
+  const bool fast3 = (ndim == 3 && ranks_h[1] <= 32 && ranks_h[2] <= 32 && colptr0 != nullptr &&
+                      rec0 != nullptr);
   const size_t need = fast3 ? (size_t)shape_h[0] * 8 + 256 : kRedBlocks * sizeof(double) + 256;
   if (ws == nullptr) {
     *ws_bytes = need;
@@ -293,21 +343,26 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
   if (fast3) {
     const int R0 = (int)ranks_h[0], R1 = (int)ranks_h[1], R2 = (int)ranks_h[2];
     const int64_t s0 = shape_h[0];
-    const unsigned blocks = (unsigned)imin((s0 + 7) / 8, (int64_t)num_sms() * 8);
-    const int32_t* c1 = coords + nnz;
-    const int32_t* c2 = coords + 2 * nnz;
+    const unsigned blocks = (unsigned)imin((s0 + 3) / 4, (int64_t)num_sms() * 16);
+    const double* rec = (const double*)rec0;
     const double* A0 = factors_h[0];
     const double* A1 = factors_h[1];
     const double* A2 = factors_h[2];
-#define SKX_T3(RT)                                                                         \
-  k_tucker3<RT><<<blocks, 256, (size_t)8 * R1 * RT * 8, s>>>(colptr0, s0, c1, c2, vals, A0, A1, \
-                                                              A2, core, R0, R1, R2, part)
-    if (R2 <= 4) SKX_T3(4);
-    else if (R2 <= 8) SKX_T3(8);
-    else if (R2 <= 10) SKX_T3(10);
-    else if (R2 <= 16) SKX_T3(16);
-    else if (R2 <= 20) SKX_T3(20);
-    else SKX_T3(32);
+    const int RM = R1 > R2 ? R1 : R2;
+#define SKX_T3(RT, NP)                                                                    \
+  do {                                                                                    \
+    const size_t sm = (size_t)4 * (RT * RT + 2 * 32 * NP * (RT + 1) + 2) * 8;             \
+    cudaFuncSetAttribute(k_tucker3<RT, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                         (int)sm);                                                        \
+    k_tucker3<RT, NP><<<blocks, 128, sm, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0, R1,  \
+                                              R2, part);                                  \
+  } while (0)
+    if (RM <= 4) SKX_T3(4, 4);
+    else if (RM <= 8) SKX_T3(8, 2);
+    else if (RM <= 10) SKX_T3(10, 2);
+    else if (RM <= 16) SKX_T3(16, 1);
+    else if (RM <= 20) SKX_T3(20, 1);
+    else SKX_T3(32, 1);
 #undef SKX_T3
     k_final_sum<<<1, 1024, 0, s>>>(part, (int)s0, out);
     return check_launch("k_tucker3", 2);

@@ -1,0 +1,128 @@
+// Device layouts of a COO tensor (the B200 counterpart of the reference's
+// cached unfoldings, src/tensors.py:151-194 / mode_sort :89-95).
+//
+// Fibre-major layout of mode n: nonzeros ordered by (i_n, other modes
+// ascending) -- a stable sort by i_n of the lexsorted input -- stored as
+// AoS records {int32 other coords..., double value} so a sketch kernel reads
+// one 16-byte record per nonzero (order 3), plus int64 column offsets colptr.
+// Built by one packing pass and a cub onesweep radix sort over only the
+// ceil(log2 s_n) key bits (skipped for mode 0, already in order).
+#include <cub/cub.cuh>
+
+#include "skx_common.cuh"
+
+namespace skx {
+
+struct __align__(16) Rec16 {
+  int32_t c[2];
+  double v;
+};
+struct __align__(8) Rec24 {
+  int32_t c[4];
+  double v;
+};
+
+// Slot j of a record holds mode j + (j >= mode): compile-time slot indices keep
+// the record in registers (a runtime-indexed array would live in local memory).
+template <class Rec>
+__global__ void k_pack(int ndim, int mode, int64_t nnz, const int32_t* __restrict__ coords,
+                       const double* __restrict__ vals, uint32_t* __restrict__ keys,
+                       Rec* __restrict__ rec) {
+  constexpr int NS = (int)(sizeof(Rec::c) / sizeof(int32_t));
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  Rec r;
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    const int src = j + (j >= mode ? 1 : 0);
+    r.c[j] = (j < ndim - 1) ? __ldcs(coords + (int64_t)src * nnz + e) : 0;
+  }
+  r.v = __ldcs(vals + e);
+  rec[e] = r;
+  if (keys) keys[e] = (uint32_t)__ldcs(coords + (int64_t)mode * nnz + e);
+}
+
+// colptr[c] = first position whose key >= c (keys sorted), c in [0, s]
+__global__ void k_bounds_u32(const uint32_t* __restrict__ keys, int64_t n, int64_t s,
+                             int64_t* __restrict__ colptr) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > s) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)keys[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  colptr[c] = lo;
+}
+
+__global__ void k_bounds_i32(const int32_t* __restrict__ keys, int64_t n, int64_t s,
+                             int64_t* __restrict__ colptr) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > s) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)keys[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  colptr[c] = lo;
+}
+
+template <class Rec>
+static int build(int ndim, const int64_t* shape_h, int mode, int64_t nnz, const int32_t* coords,
+                 const double* vals, void* rec_out, int64_t* colptr, void* ws, size_t* ws_bytes,
+                 cudaStream_t s) {
+  const int64_t sn = shape_h[mode];
+  Arena ar(ws, *ws_bytes);
+  uint32_t* k_in = nullptr;
+  uint32_t* k_out = nullptr;
+  Rec* r_in = nullptr;
+  void* tmp = nullptr;
+  size_t cb = 0;
+  if (mode != 0) {
+    k_in = ar.take<uint32_t>(nnz);
+    k_out = ar.take<uint32_t>(nnz);
+    r_in = ar.take<Rec>(nnz);
+    cub::DeviceRadixSort::SortPairs(nullptr, cb, k_in, k_out, r_in, (Rec*)rec_out, (int64_t)nnz, 0,
+                                    32, s);
+    tmp = ar.take<char>(cb);
+  }
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_coo_fibre: workspace too small");
+  const unsigned g = (unsigned)((nnz + 255) / 256);
+  const unsigned gb = (unsigned)((sn + 1 + 255) / 256);
+  if (mode == 0) {
+    if (nnz) k_pack<Rec><<<g, 256, 0, s>>>(ndim, 0, nnz, coords, vals, nullptr, (Rec*)rec_out);
+    k_bounds_i32<<<gb, 256, 0, s>>>(coords, nnz, sn, colptr);
+    return check_launch("skx_coo_fibre(mode 0)", 2);
+  }
+  if (nnz) k_pack<Rec><<<g, 256, 0, s>>>(ndim, mode, nnz, coords, vals, k_in, r_in);
+  int bits = 1;
+  while ((int64_t(1) << bits) < sn) ++bits;
+  cub::DeviceRadixSort::SortPairs(tmp, cb, k_in, k_out, r_in, (Rec*)rec_out, (int64_t)nnz, 0, bits,
+                                  s);
+  k_bounds_u32<<<gb, 256, 0, s>>>(k_out, nnz, sn, colptr);
+  return check_launch("skx_coo_fibre", 3);
+}
+
+}  // namespace skx
+
+using namespace skx;
+
+extern "C" int skx_coo_rec_words(int ndim) { return ndim - 1 <= 2 ? 2 : (ndim - 1 <= 4 ? 3 : -1); }
+
+extern "C" int skx_coo_fibre(int ndim, const int64_t* shape_h, int mode, int64_t nnz,
+                             const int32_t* coords, const double* vals, void* rec_out,
+                             int64_t* colptr, void* ws, size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 5, "skx_coo_fibre: sparse order 2..5 supported");
+  SKX_REQUIRE(mode >= 0 && mode < ndim, "skx_coo_fibre: mode out of range");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_coo_fibre: ws_bytes is NULL");
+  for (int k = 0; k < ndim; ++k)
+    SKX_REQUIRE(shape_h[k] >= 1 && shape_h[k] < (int64_t(1) << 31), "skx_coo_fibre: extent range");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ndim - 1 <= 2)
+    return build<Rec16>(ndim, shape_h, mode, nnz, coords, vals, rec_out, colptr, ws, ws_bytes, s);
+  return build<Rec24>(ndim, shape_h, mode, nnz, coords, vals, rec_out, colptr, ws, ws_bytes, s);
+}

@@ -275,20 +275,14 @@ __global__ void k_zig_emit(const uint16_t* info, const double* val, int64_t L, L
 }
 
 // ------------------------------------------------------------------ lemire
-__global__ void k_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
-                              uint32_t pending, uint64_t n_u32, uint32_t k, uint32_t thresh,
-                              uint64_t* rej, int64_t cap, unsigned long long* count) {
-  // u32 index of raw r (r >= p0): off + 2(r - p0) (+1 for the high half)
-  const uint64_t off = has_pending ? 1 : 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && has_pending && n_u32 > 0) {
-    if ((uint32_t)((uint64_t)pending * k) < thresh) {
-      unsigned long long s = atomicAdd(count, 1ULL);
-      if ((int64_t)s < cap) rej[s] = 0;
-    }
-  }
-  if (n_u32 <= off) return;
-  const uint64_t nraw = (n_u32 - off + 1) / 2;  // raw draws touched
-  const uint64_t b_first = p0 >> 2, b_last = (p0 + nraw - 1) >> 2;
+// Lists the absolute 32-bit positions A = 2*raw + half (half 0 = low word) of
+// every draw in raw words [raw_lo, raw_hi) that Lemire's method would reject
+// for bound k.  Rejection depends only on the drawn value, so the scan can run
+// before the caller knows exactly where its integers() call starts.
+__global__ void k_lemire_scan(uint64_t k0, uint64_t k1, uint64_t raw_lo, uint64_t raw_hi,
+                              uint32_t k, uint32_t thresh, uint64_t* rej, int64_t cap,
+                              unsigned long long* count) {
+  const uint64_t b_first = raw_lo >> 2, b_last = (raw_hi - 1) >> 2;
   const uint64_t nb = b_last - b_first + 1;
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -307,11 +301,9 @@ __global__ void k_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t ha
       for (int bit = 0; bit < 8; ++bit) {
         if (!((flag >> bit) & 1)) continue;
         const uint64_t r = 4 * b + (bit >> 1);
-        if (r < p0 || r >= p0 + nraw) continue;
-        const uint64_t q = off + 2 * (r - p0) + (bit & 1);
-        if (q >= n_u32) continue;
+        if (r < raw_lo || r >= raw_hi) continue;
         const unsigned long long s = atomicAdd(count, 1ULL);
-        if ((int64_t)s < cap) rej[s] = q;
+        if ((int64_t)s < cap) rej[s] = 2 * r + (bit & 1);
       }
     }
   }
@@ -402,18 +394,18 @@ extern "C" int skx_philox_normal(uint64_t k0, uint64_t k1, const uint64_t* p0, i
   return check_launch("ziggurat", 4 + 2 * (int)(pl.nlev - 1));
 }
 
-extern "C" int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
-                               uint32_t pending, uint64_t n_u32, uint32_t k, uint64_t* rej,
-                               int64_t cap, unsigned long long* count, void* stream) {
+extern "C" int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t raw_lo, uint64_t raw_hi,
+                               uint32_t k, uint64_t* rej, int64_t cap, unsigned long long* count,
+                               void* stream) {
   SKX_REQUIRE(k >= 1, "skx_lemire_scan: k must be >= 1");
   cudaStream_t s = (cudaStream_t)stream;
   cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
   uint32_t thresh = (uint32_t)((0x100000000ULL - (uint64_t)k) % (uint64_t)k);
-  if (thresh == 0 || n_u32 == 0) return check_launch("lemire(no rejections possible)", 0);
-  uint64_t nraw = (n_u32 + 1) / 2 + 1;
-  uint64_t nb = nraw / 4 + 2;
-  int blocks = (int)umin64((nb + 255) / 256, (uint64_t)num_sms() * 16);
-  k_lemire_scan<<<blocks, 256, 0, s>>>(k0, k1, p0, has_pending, pending, n_u32, k, thresh, rej,
-                                       cap, count);
+  if (thresh == 0 || raw_hi <= raw_lo) return check_launch("lemire(no rejections possible)", 0);
+  const uint64_t nb = ((raw_hi - 1) >> 2) - (raw_lo >> 2) + 1;
+  // 4 CTAs (32 warps) per SM saturate the IMAD pipe and leave half of every SM
+  // to memory-bound kernels running concurrently on other streams
+  int blocks = (int)umin64((nb + 255) / 256, (uint64_t)num_sms() * 4);
+  k_lemire_scan<<<blocks, 256, 0, s>>>(k0, k1, raw_lo, raw_hi, k, thresh, rej, cap, count);
   return check_launch("k_lemire_scan");
 }

@@ -14,12 +14,30 @@
 
 namespace skx {
 
+// Map the sorted absolute rejection positions onto run indices of an
+// integers() call that starts at raw word p0 (optionally preceded by the
+// buffered high half of raw word pend_raw): q = 0 for that half, else
+// q = has + (A - 2 p0); positions outside the run are dropped.  Then
+// d_j = q_j - j and n_le = #{d_j <= P-1}.  Single thread: there are O(cap)
+// (~1e3) entries and the order must be preserved.
 __global__ void k_rej_to_d(const uint64_t* __restrict__ sorted, const unsigned long long* count,
-                           int64_t cap, uint64_t* __restrict__ d) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= cap) return;
+                           int64_t cap, uint64_t p0, uint32_t has, uint64_t pend_raw, uint64_t P,
+                           uint64_t* __restrict__ d, unsigned long long* n_le) {
   const int64_t n = (int64_t)umin64(*count, (unsigned long long)cap);
-  d[i] = i < n ? sorted[i] - (uint64_t)i : ~0ULL;
+  int64_t j = 0;
+  unsigned long long le = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t A = sorted[i];
+    uint64_t q;
+    if (has && A == 2 * pend_raw + 1) q = 0;
+    else if (A >= 2 * p0) q = (uint64_t)has + (A - 2 * p0);
+    else continue;
+    const uint64_t dj = q - (uint64_t)j;
+    d[j++] = dj;
+    if (dj <= P - 1) ++le;
+  }
+  for (; j < cap; ++j) d[j] = ~0ULL;
+  *n_le = le;
 }
 
 __global__ void k_fill_max(uint64_t* a, int64_t n) {
@@ -36,10 +54,6 @@ __device__ __forceinline__ uint64_t count_le(const uint64_t* d, int64_t n, uint6
   return (uint64_t)lo;
 }
 
-__global__ void k_count_le(const uint64_t* __restrict__ d, int64_t n, uint64_t v,
-                           unsigned long long* out) {
-  *out = count_le(d, n, v);
-}
 
 struct RrfRng {
   U32Stream st;
@@ -69,11 +83,10 @@ struct OthExt {
   int64_t ext[15];
 };
 
-template <int U>
-__global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t nnz, int64_t s_n,
+template <int U, int NO>
+__global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t s_n,
                                                  const int64_t* __restrict__ colptr,
-                                                 const int32_t* __restrict__ oth,
-                                                 const double* __restrict__ vals,
+                                                 const double* __restrict__ rec,
                                                  double* __restrict__ st1) {
   extern __shared__ double smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -90,19 +103,21 @@ __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t nn
     for (int64_t base = e0; base < e1; base += 32 * U) {
       uint32_t bk[U];
       double v[U];
+      int32_t c[U][4];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t e = base + u * 32 + lane;
-        bk[u] = kNoBucket;
-        v[u] = 0.0;
-        if (e < e1) {
-          uint64_t j = 0;
-          for (int k = 0; k < oe.n; ++k) j = j * (uint64_t)oe.ext[k] + (uint64_t)oth[(int64_t)k * nnz + e];
-          const uint32_t t = rrf_entry(r, j);
-          bk[u] = pk_bucket(t);
-          const double x = vals[e];
-          v[u] = pk_neg(t) ? -x : x;
-        }
+        load_rec<NO>(rec, e < e1 ? e : e0, c[u], v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = base + u * 32 + lane < e1;
+        uint64_t j = 0;
+#pragma unroll
+        for (int k = 0; k < NO; ++k) j = j * (uint64_t)oe.ext[k] + (uint64_t)c[u][k];
+        const uint32_t t = rrf_entry(r, j);
+        bk[u] = ok ? pk_bucket(t) : kNoBucket;
+        v[u] = pk_neg(t) ? -v[u] : v[u];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], v[u], stage);
@@ -117,12 +132,14 @@ __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t nn
 
 using namespace skx;
 
-// Sort the scan output and turn it into the d-array (length cap, padded with
-// UINT64_MAX); *n_le receives #{d_i <= P-1} = rejections among the P hash
-// draws, i.e. the sign run starts at u32 index P + *n_le.
+// Sort the scan output and turn it into the d-array of a run (p0, has,
+// pend_raw) (length cap, padded with UINT64_MAX); *n_le receives
+// #{d_i <= P-1} = rejections among the P hash draws, i.e. the sign run starts
+// at u32 index P + *n_le.
 extern "C" int skx_lemire_finish(uint64_t* rej, const unsigned long long* count, int64_t cap,
-                                 uint64_t P, uint64_t* d, unsigned long long* n_le, void* ws,
-                                 size_t* ws_bytes, void* stream) {
+                                 uint64_t p0, uint32_t has, uint64_t pend_raw, uint64_t P,
+                                 uint64_t* d, unsigned long long* n_le, void* ws, size_t* ws_bytes,
+                                 void* stream) {
   SKX_REQUIRE(ws_bytes != nullptr, "skx_lemire_finish: ws_bytes is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   Arena ar(ws, *ws_bytes);
@@ -138,9 +155,8 @@ extern "C" int skx_lemire_finish(uint64_t* rej, const unsigned long long* count,
   // entries beyond count were never written: neutralise them before sorting
   // (the caller pre-fills rej with UINT64_MAX via skx_fill_u64max).
   cub::DeviceRadixSort::SortKeys(tmp, cb, rej, sorted, (int)cap, 0, 64, s);
-  k_rej_to_d<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(sorted, count, cap, d);
-  k_count_le<<<1, 1, 0, s>>>(d, cap, P - 1, n_le);
-  return check_launch("skx_lemire_finish", 3);
+  k_rej_to_d<<<1, 1, 0, s>>>(sorted, count, cap, p0, has, pend_raw, P, d, n_le);
+  return check_launch("skx_lemire_finish", 2);
 }
 
 extern "C" int skx_fill_u64max(uint64_t* a, int64_t n, void* stream) {
@@ -175,12 +191,12 @@ extern "C" int skx_rrf_table(uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has
   return check_launch("k_rrf_table");
 }
 
-extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t nnz, int64_t s_n,
-                                  const int64_t* colptr, const int32_t* oth, const double* vals,
-                                  uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
-                                  uint32_t pending, uint64_t sign_q0, const uint64_t* rej,
-                                  int64_t nrej, int64_t k2, double* stage1, void* stream) {
-  SKX_REQUIRE(n_other >= 1 && n_other <= 15, "skx_rrf_stage1_coo: 1..15 other modes");
+extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n,
+                                  const int64_t* colptr, const void* rec, uint64_t k0, uint64_t k1,
+                                  uint64_t p0, uint32_t has_pending, uint32_t pending,
+                                  uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
+                                  double* stage1, void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 4, "skx_rrf_stage1_coo: 1..4 other modes");
   const int64_t per = (k2 + 32) * 8;
   int nw = (int)imin(8, (int64_t)(max_smem_optin() - 1024) / per);
   SKX_REQUIRE(nw >= 1, "skx_rrf_stage1_coo: k2 too large for shared memory");
@@ -190,13 +206,16 @@ extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t nnz
   oe.n = n_other;
   for (int k = 0; k < n_other; ++k) oe.ext[k] = ext_h[k];
   const size_t smem = (size_t)nw * per;
-  auto kern = k_rrf_coo<2>;
+  auto kern = n_other == 1 ? k_rrf_coo<4, 1>
+            : n_other == 2 ? k_rrf_coo<4, 2>
+            : n_other == 3 ? k_rrf_coo<4, 3>
+                           : k_rrf_coo<4, 4>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t blocks = imin((int64_t)num_sms() * per_sm, (s_n + nw - 1) / nw);
-  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(r, oe, nnz, s_n, colptr, oth, vals,
-                                                                  stage1);
+  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(r, oe, s_n, colptr,
+                                                                  (const double*)rec, stage1);
   return check_launch("k_rrf_coo");
 }

@@ -48,17 +48,22 @@ struct OtherTabs {
   const uint32_t* t[15];
 };
 
-template <int U>
-__global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t nnz, int64_t s_n,
+// NO = number of other modes (1..4), records from skx_coo_fibre.
+// Three explicit phases per 32*U nonzeros -- (1) the 16/24-byte records,
+// (2) table lookups, (3) ordered accumulation -- so all HBM loads of a chunk
+// are in flight together; bucket sums are reduced mod m by conditional
+// subtraction (each table entry < m), no integer division.
+template <int U, int NO>
+__global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
                                                     const int64_t* __restrict__ colptr,
-                                                    const int32_t* __restrict__ oth,
-                                                    const double* __restrict__ vals, int64_t m,
+                                                    const double* __restrict__ rec, int64_t m,
                                                     double* __restrict__ yt) {
   extern __shared__ double smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
   double* acc = smem + (size_t)wid * (m + 32);
   double* stage = acc + m;
+  const uint32_t mm = (uint32_t)m;
   const int64_t gw = blockIdx.x * (int64_t)nw + wid;
   const int64_t tw = (int64_t)gridDim.x * nw;
   for (int64_t col = gw; col < s_n; col += tw) {
@@ -66,31 +71,33 @@ __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t nnz, i
     __syncwarp();
     const int64_t e0 = colptr[col], e1 = colptr[col + 1];
     for (int64_t base = e0; base < e1; base += 32 * U) {
-      uint32_t bk[U];
+      int32_t c[U][4];
       double v[U];
+      uint32_t bk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t e = base + u * 32 + lane;
-        bk[u] = kNoBucket;
-        v[u] = 0.0;
-        if (e < e1) {
-          uint64_t hs = 0;
-          uint32_t neg = 0;
-          for (int k = 0; k < ot.n; ++k) {
-            const uint32_t t = __ldg(ot.t[k] + oth[(int64_t)k * nnz + e]);
-            hs += pk_bucket(t);
-            neg ^= pk_neg(t);
-          }
-          bk[u] = (uint32_t)(hs % (uint64_t)m);
-          const double x = vals[e];
-          v[u] = neg ? -x : x;
+        load_rec<NO>(rec, e < e1 ? e : e0, c[u], v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t h = 0, neg = 0;
+#pragma unroll
+        for (int k = 0; k < NO; ++k) {
+          const uint32_t t = __ldg(ot.t[k] + c[u][k]);
+          h += pk_bucket(t);
+          if (h >= mm) h -= mm;
+          neg ^= pk_neg(t);
         }
+        const bool ok = base + u * 32 + lane < e1;
+        bk[u] = ok ? h : kNoBucket;
+        v[u] = neg ? -v[u] : v[u];
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], v[u], stage);
     }
     double* dst = yt + col * m;
-    for (int64_t h = lane; h < m; h += 32) dst[h] = acc[h];
+    for (int64_t h = lane; h < m; h += 32) __stcs(dst + h, acc[h]);
     __syncwarp();
   }
 }
@@ -285,10 +292,10 @@ int warps_for(int64_t m) {
 }
 }  // namespace
 
-extern "C" int skx_ts_rhs_coo(int n_other, int64_t nnz, int64_t s_n, const int64_t* colptr,
-                              const int32_t* oth, const double* vals, const uint32_t* tab,
-                              const int64_t* tab_off_h, int64_t m, double* yt, void* stream) {
-  SKX_REQUIRE(n_other >= 0 && n_other <= 15, "skx_ts_rhs_coo: up to 15 other modes");
+extern "C" int skx_ts_rhs_coo(int n_other, int64_t s_n, const int64_t* colptr, const void* rec,
+                              const uint32_t* tab, const int64_t* tab_off_h, int64_t m, double* yt,
+                              void* stream) {
+  SKX_REQUIRE(n_other >= 1 && n_other <= 4, "skx_ts_rhs_coo: 1..4 other modes (sparse order <= 5)");
   const int nw = warps_for(m);
   SKX_REQUIRE(nw >= 1, "skx_ts_rhs_coo: sketch size %lld exceeds shared-memory capacity",
               (long long)m);
@@ -297,14 +304,17 @@ extern "C" int skx_ts_rhs_coo(int n_other, int64_t nnz, int64_t s_n, const int64
   ot.n = n_other;
   for (int k = 0; k < n_other; ++k) ot.t[k] = tab + tab_off_h[k];
   const size_t smem = (size_t)nw * (m + 32) * 8;
-  auto kern = k_ts_rhs_coo<4>;
+  auto kern = n_other == 1 ? k_ts_rhs_coo<8, 1>
+            : n_other == 2 ? k_ts_rhs_coo<8, 2>
+            : n_other == 3 ? k_ts_rhs_coo<6, 3>
+                           : k_ts_rhs_coo<6, 4>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = imin((int64_t)num_sms() * per_sm, (s_n + nw - 1) / nw);
-  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(ot, nnz, s_n, colptr, oth, vals,
-                                                                  m, yt);
+  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(ot, s_n, colptr,
+                                                                  (const double*)rec, m, yt);
   return check_launch("k_ts_rhs_coo");
 }
 

@@ -212,14 +212,25 @@ def ts_apply_kron(ts, factors, method="auto"):
     return z.cpu().numpy()
 
 
-def ts_rhs_coo_dev(ts, colptr, oth, vals, s_n):
-    """Y^T (s_n x m) from a fibre-major COO layout."""
+def ts_rhs_coo_dev(ts, colptr, rec, s_n):
+    """Y^T (s_n x m) from a fibre-major COO layout (DeviceCoo.fibre)."""
     torch = _torch()
     yt = torch.empty((s_n, ts.m), dtype=torch.float64, device="cuda")
     off, op = nat.host_i64(ts.tab_off)
-    nat.call("skx_ts_rhs_coo", len(ts.extents), int(vals.numel()), s_n, nat.ptr(colptr),
-             nat.ptr(oth), nat.ptr(vals), nat.ptr(ts.tab), op, ts.m, nat.ptr(yt), nat.stream())
+    nat.call("skx_ts_rhs_coo", len(ts.extents), s_n, nat.ptr(colptr), nat.ptr(rec), nat.ptr(ts.tab),
+             op, ts.m, nat.ptr(yt), nat.stream())
     return yt
+
+
+def _coo_from_pairs(rows, cols, data, shape):
+    """DeviceCoo of a 2-D scipy-style (rows, cols, data) triple (lexsorted)."""
+    from .tensors import DeviceCoo
+    torch = _torch()
+    order = np.lexsort((cols, rows))
+    c = np.stack([np.asarray(rows)[order], np.asarray(cols)[order]]).astype(np.int32)
+    return DeviceCoo(shape, torch.from_numpy(c).cuda(),
+                     torch.from_numpy(np.ascontiguousarray(np.asarray(data)[order],
+                                                           dtype=np.float64)).cuda())
 
 
 def ts_rhs_dense_dev(ts, t, mode):
@@ -247,15 +258,16 @@ def ts_apply_rhs(ts, b, chunk=1 << 20):
         coo = b.tocoo()
         if coo.nnz == 0:
             return np.zeros((ts.m, c))
-        order = np.lexsort((coo.row, coo.col))
-        rows, cols, data = coo.row[order], coo.col[order], coo.data[order]
-        multi = np.stack(np.unravel_index(rows, ts.extents)).astype(np.int32)
-        colptr = np.zeros(c + 1, dtype=np.int64)
-        np.cumsum(np.bincount(cols, minlength=c), out=colptr[1:])
-        yt = ts_rhs_coo_dev(ts, torch.from_numpy(colptr).cuda(),
-                            torch.from_numpy(np.ascontiguousarray(multi)).cuda(),
-                            torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).cuda(), c)
-        return yt.t().cpu().numpy()
+        # as a (c, *extents) tensor: its mode-0 fibre layout is b's column-major order
+        from .tensors import DeviceCoo
+        multi = np.unravel_index(coo.row, ts.extents)
+        cols = np.stack([coo.col] + list(multi)).astype(np.int64)
+        order = np.lexsort(cols[::-1])
+        d = DeviceCoo((c,) + tuple(ts.extents),
+                      torch.from_numpy(np.ascontiguousarray(cols[:, order].astype(np.int32))).cuda(),
+                      torch.from_numpy(np.ascontiguousarray(coo.data[order], dtype=np.float64)).cuda())
+        colptr, rec = d.fibre(0)
+        return ts_rhs_coo_dev(ts, colptr, rec, c).t().cpu().numpy()
     bd = _dev(b).contiguous()
     full = ts.full_table()
     out = torch.empty((c, ts.m), dtype=torch.float64, device="cuda")
@@ -453,35 +465,105 @@ class RrfTables:
                 ctypes.c_uint64(self.sign_q0), nat.ptr(self.d), self.nd)
 
 
-def draw_rrf_tables(gen, P, k2):
-    """Reproduce rng.integers(0,k2,P); rng.integers(0,2,P) on device without
-    materialising them; advances `gen` exactly as numpy would."""
-    torch = _torch()
-    c = rngmod.cursor(gen)
+def _rej_cap(P, k2):
     thresh = (2 ** 32 - k2) % k2
     expect = P * thresh / 2 ** 32
-    cap = int(max(1024, 4 * expect + 64 * np.sqrt(expect + 1) + 64))
-    while True:
+    return int(max(1024, 4 * expect + 64 * np.sqrt(expect + 1) + 64))
+
+
+class RrfScan:
+    """A Lemire rejection scan over raw words [raw_lo, raw_hi) in flight."""
+
+    def __init__(self, key, raw_lo, raw_hi, k2, cap, rej, count, stream):
+        self.key, self.raw_lo, self.raw_hi, self.k2, self.cap = key, raw_lo, raw_hi, k2, cap
+        self.rej, self.count, self.stream = rej, count, stream
+
+
+def launch_rrf_scan(key, raw_lo, raw_hi, k2, cap, stream=None):
+    """Enqueue the rejection scan of raw words [raw_lo, raw_hi) for bound k2.
+    Compute-bound (one Philox block per 4 raw words); meant to run on a side
+    stream, overlapping memory-bound work, before the exact start of the
+    integers() call it serves is known."""
+    torch = _torch()
+    st = stream or torch.cuda.current_stream()
+    with torch.cuda.stream(st):
         rej = torch.empty(cap, dtype=torch.int64, device="cuda")
         nat.call("skx_fill_u64max", nat.ptr(rej), cap, nat.stream())
         count = torch.zeros(1, dtype=torch.int64, device="cuda")
-        n_u32 = P + cap  # enough as long as fewer than cap rejections occur
-        nat.call("skx_lemire_scan", ctypes.c_uint64(c.k0), ctypes.c_uint64(c.k1), ctypes.c_uint64(c.p),
-                 ctypes.c_uint32(c.has), ctypes.c_uint32(c.pending), ctypes.c_uint64(n_u32),
-                 ctypes.c_uint32(k2), nat.ptr(rej), cap, nat.ptr(count), nat.stream())
-        d = torch.empty(cap, dtype=torch.int64, device="cuda")
+        nat.call("skx_lemire_scan", ctypes.c_uint64(key[0]), ctypes.c_uint64(key[1]),
+                 ctypes.c_uint64(raw_lo), ctypes.c_uint64(raw_hi), ctypes.c_uint32(k2), nat.ptr(rej),
+                 cap, nat.ptr(count), nat.stream())
+    return RrfScan(key, raw_lo, raw_hi, k2, cap, rej, count, st)
+
+
+def finish_rrf_scan(scan, gen, P):
+    """Resolve `scan` for the integers(0,k2,P); integers(0,2,P) call that `gen`
+    makes next: build its d-array, read the rejection count (host waits on the
+    scan's stream only), check the scanned range covered the call (else scan
+    again exactly), and advance `gen` as numpy would."""
+    torch = _torch()
+    c = rngmod.cursor(gen)
+    pend_raw = c.p - 1 if c.has else 0
+    with torch.cuda.stream(scan.stream):
+        d = torch.empty(scan.cap, dtype=torch.int64, device="cuda")
         n_le = torch.zeros(1, dtype=torch.int64, device="cuda")
-        nat.call_ws("skx_lemire_finish", (nat.ptr(rej), nat.ptr(count), cap, ctypes.c_uint64(P),
-                                          nat.ptr(d), nat.ptr(n_le)))
-        both = torch.stack([count[0], n_le[0]]).cpu().numpy()
-        if int(both[0]) < cap:
-            break
-        cap *= 4
-    nrej = int(both[1])
-    sign_q0 = P + nrej
-    tabs = RrfTables(c.k0, c.k1, c.p, c.has, c.pending, d, cap, sign_q0, k2, P)
+        nat.call_ws("skx_lemire_finish", (nat.ptr(scan.rej), nat.ptr(scan.count), scan.cap,
+                                          ctypes.c_uint64(c.p), ctypes.c_uint32(c.has),
+                                          ctypes.c_uint64(pend_raw), ctypes.c_uint64(P),
+                                          nat.ptr(d), nat.ptr(n_le)), slot=3)
+        host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        host[0:1].copy_(scan.count, non_blocking=True)
+        host[1:2].copy_(n_le, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(scan.stream)
+    ev.synchronize()
+    count, nrej = int(host[0]), int(host[1])
+    need_hi = c.p + (P + nrej - c.has + 1) // 2  # raw words the hash run reads
+    covered = (count < scan.cap and c.p >= scan.raw_lo and need_hi <= scan.raw_hi
+               and (not c.has or pend_raw >= scan.raw_lo))
+    if not covered:  # prediction missed or too many rejections: exact rescan
+        cap = max(scan.cap * 4, _rej_cap(P, scan.k2))
+        lo = pend_raw if c.has else c.p
+        exact = launch_rrf_scan(scan.key, lo, c.p + (P + cap) // 2 + 2, scan.k2, cap, scan.stream)
+        return finish_rrf_scan(exact, gen, P)
+    cur = torch.cuda.current_stream()
+    cur.wait_event(ev)
+    d.record_stream(cur)
+    tabs = RrfTables(c.k0, c.k1, c.p, c.has, c.pending, d, scan.cap, P + nrej, scan.k2, P)
     rngmod.advance_u32(gen, 2 * P + nrej)
     return tabs
+
+
+def draw_rrf_tables(gen, P, k2, stream=None):
+    """Reproduce rng.integers(0,k2,P); rng.integers(0,2,P) on device without
+    materialising them; advances `gen` exactly as numpy would."""
+    c = rngmod.cursor(gen)
+    cap = _rej_cap(P, k2)
+    lo = c.p - 1 if c.has else c.p
+    scan = launch_rrf_scan((c.k0, c.k1), lo, c.p + (P + cap) // 2 + 2, k2, cap, stream)
+    return finish_rrf_scan(scan, gen, P)
+
+
+def plan_rrf_scans(gen, jobs, stream=None):
+    """Launch the scans of consecutive RRF table draws at once.  jobs =
+    [(P, k2, n_gauss)] in draw order, where n_gauss normals follow each pair of
+    integers() calls.  Later starts are bracketed (rejections < cap, ziggurat
+    consumption in [n, 1.1 n + 256]); finish_rrf_scan verifies and rescans
+    exactly if a bracket was missed."""
+    c = rngmod.cursor(gen)
+    key = (c.k0, c.k1)
+    lo = c.p - 1 if c.has else c.p
+    hi_start = c.p
+    scans = []
+    for P, k2, n_gauss in jobs:
+        cap = _rej_cap(P, k2)
+        scans.append(launch_rrf_scan(key, lo, hi_start + (P + cap) // 2 + 2, k2, cap, stream))
+        # the next call starts after the hash + sign draws and the normals; a
+        # buffered high half left by the integers() pair sits *before* the
+        # normals, so the next scan starts there (>= lo + P - 2)
+        lo = lo + P - 2
+        hi_start = hi_start + (2 * P + cap) // 2 + 2 + int(1.1 * n_gauss) + 256
+    return scans
 
 
 @dataclass
@@ -523,15 +605,11 @@ def composite_apply(mat, op):
     tab = _pack(op.stage.hash, op.stage.signs)
     st1 = torch.empty((s, op.k2), dtype=torch.float64, device="cuda")
     if sp.issparse(mat):
-        c = mat.tocsr()
-        c.sort_indices()
-        colptr = torch.from_numpy(c.indptr.astype(np.int64)).cuda()
-        oth = torch.from_numpy(c.indices.astype(np.int32).reshape(1, -1)).cuda()
-        vals = torch.from_numpy(np.ascontiguousarray(c.data, dtype=np.float64)).cuda()
+        c = mat.tocoo()
+        colptr, rec = _coo_from_pairs(c.row, c.col, c.data, (s, P)).fibre(0)
         off = np.zeros(1, dtype=np.int64)
-        nat.call("skx_ts_rhs_coo", 1, int(vals.numel()), s, nat.ptr(colptr), nat.ptr(oth),
-                 nat.ptr(vals), nat.ptr(tab), off.ctypes.data_as(ctypes.c_void_p), op.k2,
-                 nat.ptr(st1), nat.stream())
+        nat.call("skx_ts_rhs_coo", 1, s, nat.ptr(colptr), nat.ptr(rec), nat.ptr(tab),
+                 off.ctypes.data_as(ctypes.c_void_p), op.k2, nat.ptr(st1), nat.stream())
     else:
         md = _dev(mat).contiguous()
         shp, sp_ = nat.host_i64([s, P])

@@ -280,27 +280,22 @@ class DeviceCoo:
             self._norm2 = out
         return self._norm2
 
-    # ---- fibre-major layout for mode n
+    # ---- fibre-major layout for mode n (libskx skx_coo_fibre)
     def fibre(self, n):
+        """(colptr, records) of mode n: nonzeros ordered by (i_n, other modes
+        ascending) as AoS records {int32 others..., f64 value}, built by one
+        packing pass + a radix sort over ceil(log2 s_n) key bits."""
         torch = _torch()
         if n not in self._fibre:
-            others = [k for k in range(self.ndim) if k != n]
-            s_n = self.shape[n]
-            bounds = torch.arange(s_n + 1, dtype=torch.int32, device="cuda")
-            if n == 0:
-                keys = self.coords[0]
-                oth = self.coords[1:].contiguous() if self.ndim > 1 else \
-                    torch.empty((0, self.nnz), dtype=torch.int32, device="cuda")
-                vals = self.vals
-            else:
-                # stable sort by i_n of the lexsorted order = (i_n, others ascending)
-                keys, perm = torch.sort(self.coords[n], stable=True)
-                oth = self.coords[others][:, perm].contiguous()
-                vals = self.vals[perm].contiguous()
-                del perm
-            colptr = torch.searchsorted(keys, bounds, out_int32=False)
-            del keys
-            self._fibre[n] = (colptr, oth, vals)
+            rw = int(nat.load().skx_coo_rec_words(self.ndim))
+            if rw < 0 or self.ndim < 2:
+                raise ValueError(f"sparse order {self.ndim} unsupported by the device layout (2..5)")
+            rec = torch.empty(max(self.nnz, 1) * rw, dtype=torch.float64, device="cuda")
+            colptr = torch.empty(self.shape[n] + 1, dtype=torch.int64, device="cuda")
+            shp, sp_ = nat.host_i64(self.shape)
+            nat.call_ws("skx_coo_fibre", (self.ndim, sp_, n, self.nnz, nat.ptr(self.coords),
+                                          nat.ptr(self.vals), nat.ptr(rec), nat.ptr(colptr)), slot=4)
+            self._fibre[n] = (colptr, rec)
         return self._fibre[n]
 
     def colptr0(self):
@@ -439,10 +434,10 @@ def tucker_cross_dev(d, core, factors):
         rk, rp = nat.host_i64([f.shape[1] for f in factors])
         fa = [f.contiguous() for f in factors]
         arr, fp = nat.host_ptrs(fa)
-        cpt = d.colptr0() if d.ndim == 3 else None
+        cpt, rec0 = d.fibre(0) if d.ndim == 3 else (None, None)
         nat.call_ws("skx_tucker_cross_coo",
                     (d.ndim, sp_, rp, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp,
-                     nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(out)))
+                     nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(rec0), nat.ptr(out)))
         return out[0]
     proj = d
     for k, a in enumerate(factors):

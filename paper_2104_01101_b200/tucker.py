@@ -20,9 +20,10 @@ from . import _native as nat
 from . import rng as rngmod
 from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev,
                      top_svd_dev)
-from .sketching import (TensorSketchOp, draw_rrf_tables, gather_coo_dev, gather_dense_dev,
-                        hits_to_dense, kron_rows_dev, lev_sample_dev, rrf_table_dev, ts_kron_dev,
-                        ts_rhs_coo_dev, ts_rhs_dense_dev)
+from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather_coo_dev,
+                        gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
+                        plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_rhs_coo_dev,
+                        ts_rhs_dense_dev)
 from .tensors import (DeviceCoo, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
                       matricize, shape_of)
 
@@ -103,11 +104,11 @@ def rrf_stage1_dev(d, n, tabs):
     s_n = shape[n]
     st1 = torch.empty((s_n, tabs.k2), dtype=torch.float64, device="cuda")
     if is_sparse_dev(d):
-        colptr, oth, vals = d.fibre(n)
+        colptr, rec = d.fibre(n)
         others = [k for k in range(d.ndim) if k != n]
         ext, ep = nat.host_i64([shape[k] for k in others])
-        nat.call("skx_rrf_stage1_coo", len(others), ep, d.nnz, s_n, nat.ptr(colptr), nat.ptr(oth),
-                 nat.ptr(vals), *tabs.args(), tabs.k2, nat.ptr(st1), nat.stream())
+        nat.call("skx_rrf_stage1_coo", len(others), ep, s_n, nat.ptr(colptr), nat.ptr(rec),
+                 *tabs.args(), tabs.k2, nat.ptr(st1), nat.stream())
     else:
         tab = rrf_table_dev(tabs)
         shp, sp_ = nat.host_i64(shape)
@@ -116,16 +117,9 @@ def rrf_stage1_dev(d, n, tabs):
     return st1
 
 
-def init_rrf_dev(d, n, rank, width, gen, comm=None):
-    """Range-finder init of factor n (src/tucker.py:129-144) on device."""
+def _rrf_finish(d, n, rank, tabs, gauss, comm=None):
+    """Composite sketch B = (T_(n) T_cs) G and its leading left singular vectors."""
     torch = _torch()
-    if width < rank:
-        raise ValueError(f"sketch width {width} below target rank {rank}")
-    shape = shape_of(d)
-    k2 = rank * rank + width
-    P = int(np.prod([shape[k] for k in range(len(shape)) if k != n]))
-    tabs = draw_rrf_tables(gen, P, k2)
-    gauss = gen.standard_normal((k2, width)) / np.sqrt(width)
     st1 = rrf_stage1_dev(d, n, tabs)
     if comm is not None:
         comm.allreduce(st1)
@@ -134,6 +128,23 @@ def init_rrf_dev(d, n, rank, width, gen, comm=None):
         raise ValueError(f"cannot extract {rank} directions from a {tuple(b.shape)} sketch")
     u, _, _ = top_svd_dev(b, rank)
     return u.contiguous()
+
+
+def _rrf_dims(shape, n, rank, width):
+    if width < rank:
+        raise ValueError(f"sketch width {width} below target rank {rank}")
+    P = int(np.prod([shape[k] for k in range(len(shape)) if k != n]))
+    return P, rank * rank + width
+
+
+def init_rrf_dev(d, n, rank, width, gen, comm=None):
+    """Range-finder init of factor n (src/tucker.py:129-144) on device: the
+    rng draws integers(0,k2,P), integers(0,2,P), standard_normal((k2,k1)) in
+    the reference's order (src/sketching.py:54-56, 323)."""
+    P, k2 = _rrf_dims(shape_of(d), n, rank, width)
+    tabs = draw_rrf_tables(gen, P, k2)
+    gauss = gen.standard_normal((k2, width)) / np.sqrt(width)
+    return _rrf_finish(d, n, rank, tabs, gauss, comm)
 
 
 def init_rrf(tn, rank, width, rng):
@@ -195,24 +206,47 @@ class _Run:
     def others(self, n):
         return [k for k in range(self.ndim) if k != n]
 
-    def initialise(self):
+    def initialise_and_prep(self):
+        """RRF init of modes 1..N-1 plus the TensorSketch prep, scheduled so the
+        compute-bound rejection scans (side stream) overlap the memory-bound
+        layout builds and right-hand-side sketches (main stream).  Host draws
+        keep the reference order: per mode hash, signs, then Gaussian."""
+        torch = _torch()
         init = self.cfg.init or "rrf"
-        for n in range(1, self.ndim):
-            if init == "rrf":
-                width = self.cfg.resolved_rrf_width(self.ranks[n])
-                self.factors[n] = init_rrf_dev(self.d, n, self.ranks[n], width, self.rng_init,
-                                               self.comm)
-            elif init == "random":
+        if init not in ("rrf", "random"):
+            raise ValueError(f"unknown init {init!r} for sketched_tucker_als")
+        if init == "random" or self.ndim == 1:
+            for n in range(1, self.ndim):
                 self.factors[n] = random_orthonormal_dev(self.shape[n], self.ranks[n], self.rng_init)
-            else:
-                raise ValueError(f"unknown init {init!r} for sketched_tucker_als")
+            self.prep()
+            return
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        modes = list(range(1, self.ndim))
+        dims = []
+        for n in modes:
+            width = self.cfg.resolved_rrf_width(self.ranks[n])
+            P, k2 = _rrf_dims(self.shape, n, self.ranks[n], width)
+            dims.append((P, k2, width))
+        # every mode's rejection scan is enqueued now (their starts are
+        # bracketed); they run on the side stream while the main stream builds
+        # layouts and TensorSketch right-hand sides
+        scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side)
+        if self.sparse:  # layouts first: RRF stage 1 and the TS sketches read them
+            for n in range(self.ndim):
+                self.d.fibre(n)
+        self.prep()
+        for n, scan, (P, k2, width) in zip(modes, scans, dims):
+            tabs = finish_rrf_scan(scan, self.rng_init, P)
+            gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
+            self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm)
 
     def build_ts(self, n):
         ext = tuple(self.shape[k] for k in self.others(n))
         op = TensorSketchOp.build(ext, self.m, self.rng_sketch)
         if self.sparse:
-            colptr, oth, vals = self.d.fibre(n)
-            yt = ts_rhs_coo_dev(op, colptr, oth, vals, self.shape[n])
+            colptr, rec = self.d.fibre(n)
+            yt = ts_rhs_coo_dev(op, colptr, rec, self.shape[n])
         else:
             yt = ts_rhs_dense_dev(op, self.d, n)
         if self.comm is not None:
@@ -290,8 +324,7 @@ class _Run:
 def sketched_tucker_als_dev(t, config, comm=None):
     """Device-resident form: returns (core, factors) as CUDA tensors + trace."""
     run = _Run(t, config, comm)
-    run.initialise()
-    run.prep()
+    run.initialise_and_prep()
     trace = SweepTrace()
     core = run.sweeps(trace)
     return core, list(run.factors), trace

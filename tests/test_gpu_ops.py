@@ -193,10 +193,30 @@ def test_sparse_ts_rhs_all_modes_vs_oracle(skx, oracle, shape, nnz, m):
         ext = tuple(shape[k] for k in range(len(shape)) if k != n)
         op = skx.TensorSketchOp.build(ext, m, gen)
         hs, ss = oracle.ts_tables(ext, m, ogen)
-        colptr, oth, vals = d.fibre(n)
-        yt = ts_rhs_coo_dev(op, colptr, oth, vals, shape[n]).cpu().numpy()
+        colptr, rec = d.fibre(n)
+        yt = ts_rhs_coo_dev(op, colptr, rec, shape[n]).cpu().numpy()
         ref = oracle.ts_rhs(hs, ss, ext, m, oracle.unfold_t(oc, n))
-        assert relerr(yt.T, ref) <= 1e-14  # same summation order -> (near) bit-exact
+        # same per-cell summation order as numpy's add.at -> bit-exact
+        assert np.array_equal(yt.T, ref)
+
+
+def test_fibre_layout_matches_stable_sort(skx):
+    """The radix-sorted fibre-major records equal a stable numpy sort by i_n."""
+    import torch
+    from paper_2104_01101_b200.tensors import device_of
+    shape = (50, 3000, 7)
+    c, v = _coo_rand(shape, 20000, 9)
+    d = device_of(skx.SparseTensor(shape, c, v))
+    for n in range(3):
+        colptr, rec = d.fibre(n)
+        order = np.argsort(c[:, n], kind="stable")
+        others = [k for k in range(3) if k != n]
+        raw = rec.cpu().numpy().view(np.int32).reshape(-1, 4)
+        assert np.array_equal(raw[:, 0], c[order, others[0]])
+        assert np.array_equal(raw[:, 1], c[order, others[1]])
+        assert np.array_equal(rec.cpu().numpy().reshape(-1, 2)[:, 1], v[order])
+        assert np.array_equal(colptr.cpu().numpy(),
+                              np.searchsorted(c[order, n], np.arange(shape[n] + 1)))
 
 
 @pytest.mark.parametrize("shape,m", [((30, 40, 50), 64), ((12, 13, 14, 15), 256), ((100, 100, 100), 400),

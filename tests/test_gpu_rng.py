@@ -66,6 +66,29 @@ def test_rrf_tables_bit_exact(P, k2):
         assert np.array_equal(g.integers(0, 99, size=5), ref.integers(0, 99, size=5))
 
 
+@pytest.mark.parametrize("pre", [0, 1])
+def test_planned_chain_of_rrf_draws_bit_exact(pre):
+    """Scans launched up front for three consecutive (hash, sign, Gaussian)
+    draw groups -- the RRF init of an order-4 tensor -- resolve to numpy's
+    exact tables, including the buffered-half carry across the normals."""
+    import torch
+    from paper_2104_01101_b200.sketching import _unpack, finish_rrf_scan, plan_rrf_scans, rrf_table_dev
+    jobs = [(300_001, 157, 157 * 57), (1_000_003, 480, 480 * 80), (77_777, 45, 45 * 20)]
+    g = _gen(21, 0)
+    ref = _gen(21, 0)
+    if pre:
+        g.integers(0, 2, size=1)
+        ref.integers(0, 2, size=1)
+    side = torch.cuda.Stream()
+    scans = plan_rrf_scans(g, [(P, k2, n) for P, k2, n in jobs], side)
+    for scan, (P, k2, n) in zip(scans, jobs):
+        tabs = finish_rrf_scan(scan, g, P)
+        h, s = _unpack(rrf_table_dev(tabs))
+        assert np.array_equal(h, ref.integers(0, k2, size=P))
+        assert np.array_equal(s, 1 - 2 * ref.integers(0, 2, size=P))
+        assert np.array_equal(g.standard_normal(n), ref.standard_normal(n))
+
+
 def test_lemire_large_offset_spot_check():
     """Full-scale style check: a 2e8-column table, compared at random columns
     against numpy positioned with the cursor."""

@@ -1,0 +1,79 @@
+"""GPU timeline of one sketched_tucker_als run (torch.profiler / CUPTI).
+
+    python tools/timeline.py [--config 4] [--out gpurun_out/trace.json]
+
+Prints per-kernel totals, GPU busy time per stream and the idle gaps of the
+main stream, so host stalls (syncs, Python overhead) are visible next to
+kernel time.  Development tool; not part of the product path.
+"""
+import argparse
+import collections
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
+    args = ap.parse_args()
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    import bench
+    import paper_2104_01101_b200 as skx
+    from paper_2104_01101_b200.synth import planted_cp_coo_device
+    from paper_2104_01101_b200.tucker import sketched_tucker_als_dev
+
+    cfgd = bench.CONFIGS[args.config]
+    coords, vals = planted_cp_coo_device(cfgd["shape"], cfgd["nnz"], rank=10, noise_sd=0.1, seed=0)
+    st = skx.SparseTensor.from_device(cfgd["shape"], coords.t().contiguous(), vals)
+    cfg = skx.TuckerConfig(ranks=cfgd["ranks"], max_sweeps=cfgd["sweeps"], sketch=cfgd["sketch"],
+                           sketch_size=cfgd["sketch_size"], seed=0)
+    for _ in range(2):
+        st._device.release_layouts()
+        sketched_tucker_als_dev(st, cfg)
+    torch.cuda.synchronize()
+    st._device.release_layouts()
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        t0 = time.perf_counter()
+        sketched_tucker_als_dev(st, cfg)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    prof.export_chrome_trace(args.out)
+    ev = json.load(open(args.out))["traceEvents"]
+    kern = [e for e in ev if e.get("cat") == "kernel"]
+    per = collections.defaultdict(lambda: [0, 0.0])
+    streams = collections.defaultdict(float)
+    for e in kern:
+        nm = e["name"][:70]
+        per[nm][0] += 1
+        per[nm][1] += e["dur"]
+        streams[e["args"].get("stream")] += e["dur"]
+    t_lo = min(e["ts"] for e in kern)
+    t_hi = max(e["ts"] + e["dur"] for e in kern)
+    print(f"wall {wall * 1e3:.1f} ms; kernel span {(t_hi - t_lo) / 1e3:.1f} ms; "
+          f"kernel sum {sum(v[1] for v in per.values()) / 1e3:.1f} ms")
+    for s, d in streams.items():
+        print(f"  stream {s}: {d / 1e3:.1f} ms busy")
+    # idle gaps on the union of streams
+    iv = sorted((e["ts"], e["ts"] + e["dur"]) for e in kern)
+    gaps, cur = [], iv[0][1]
+    for a, b in iv[1:]:
+        if a > cur:
+            gaps.append(a - cur)
+        cur = max(cur, b)
+    print(f"  idle (no kernel on any stream): {sum(gaps) / 1e3:.1f} ms in {len(gaps)} gaps; "
+          f"largest {sorted(gaps)[-5:] if gaps else []} us")
+    for nm, (c, d) in sorted(per.items(), key=lambda kv: -kv[1][1])[:30]:
+        print(f"{d / 1e3:9.3f} ms {c:5d}  {nm}")
+
+
+if __name__ == "__main__":
+    main()
