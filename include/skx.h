@@ -218,6 +218,17 @@ int skx_resid_sq(const double* u, const double* vt, int64_t n_out, int64_t n_in,
 int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t cs, double* r, void* ws,
                size_t* ws_bytes, void* stream);
 
+/* Upper Cholesky factor (R^T R = g, row-major n x n, n <= 128) in one CTA;
+ * *info = 0, or k+1 when pivot k is not positive.  Used by the CholeskyQR2
+ * factorisation of the sketched system (src/linalg.py:103). */
+int skx_chol_upper(const double* g, int n, double* r, int* info, void* stream);
+
+/* One-sided Jacobi SVD of the n x n matrix A[i,j] = a[i*rs + j*cs] (n <= 64):
+ * A = U diag(s) V^T with s descending, U and V row-major.  Replaces the LAPACK
+ * SVD of small R factors (src/linalg.py:59, src/tucker.py:141). */
+int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u, double* s,
+                   double* v, void* stream);
+
 /* out[0] = sum(x^2) with a fixed-order reduction. */
 int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,
               void* stream);

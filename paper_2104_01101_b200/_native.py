@@ -50,6 +50,8 @@ _SIGS = {
     "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_sumsq": [c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_tsqr_r": [c_p, c_i64, c_i32, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
+    "skx_chol_upper": [c_p, c_i32, c_p, c_p, c_p],
+    "skx_jacobi_svd": [c_p, c_i32, c_i64, c_i64, c_p, c_p, c_p, c_p],
     "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p,
                              c_p],
     "skx_cp_cross_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],

@@ -1,0 +1,188 @@
+// K5 small dense algebra in one CTA each (launch-latency scale problems):
+//
+//  skx_chol_upper  -- R^T R = G for an SPD n x n Gram (n <= 128); used by the
+//                     CholeskyQR2 factorisation of the sketched system Z
+//                     (src/linalg.py:103 reduced_qr(z); Householder QR is kept
+//                     as the fallback whenever CholeskyQR2 is not safe).
+//  skx_jacobi_svd  -- one-sided (Hestenes) Jacobi SVD of an n x n matrix
+//                     (n <= 64): A W = U diag(s), singular values descending;
+//                     replaces the LAPACK SVD of the small R factors
+//                     (src/linalg.py:59 via thin_svd, src/tucker.py:141).
+// Fixed iteration order everywhere: deterministic.
+#include <math.h>
+
+#include "skx_common.cuh"
+
+namespace skx {
+
+// Right-looking Cholesky in shared memory; row-major upper R output (zero
+// lower part).  info = 0 on success, k+1 if the k-th pivot is not positive.
+__global__ void __launch_bounds__(512) k_chol(const double* __restrict__ G, int n,
+                                              double* __restrict__ R, int* __restrict__ info) {
+  extern __shared__ double A[];  // n x ld, row-major, lower part used
+  __shared__ int bad;
+  const int ld = n | 1;  // odd row stride: column reads A[j*ld + k] hit distinct banks
+  for (int q = threadIdx.x; q < n * n; q += blockDim.x) A[(q / n) * ld + q % n] = G[q];
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = 0; k < n; ++k) {
+    // every thread reads the pivot after the previous step's barrier; thread 0
+    // alone rewrites it, after its own column scaling, so no barrier is needed
+    // between the read and the scaling
+    const double piv = A[k * ld + k];
+    if (!(piv > 0.0)) {  // also catches NaN
+      if (threadIdx.x == 0 && !bad) bad = k + 1;
+      __syncthreads();
+      break;
+    }
+    const double d = sqrt(piv), inv = 1.0 / d;
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[i * ld + k] *= inv;
+    __syncthreads();
+    if (threadIdx.x == 0) A[k * ld + k] = d;
+    // trailing update of the lower triangle: A[i][j] -= A[i][k] A[j][k], k < j <= i
+    // (warp per row, lanes along the row: no integer division)
+    for (int i = k + 1 + wid; i < n; i += nw) {
+      const double lik = A[i * ld + k];
+      for (int j = k + 1 + lane; j <= i; j += 32)
+        A[i * ld + j] = fma(-lik, A[j * ld + k], A[i * ld + j]);
+    }
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
+    const int i = q / n, j = q % n;
+    R[q] = (j >= i && !bad) ? A[j * ld + i] : 0.0;  // R = L^T
+  }
+  if (threadIdx.x == 0) *info = bad;
+}
+
+// One-sided Jacobi: columns of A (n x n, shared, column-major) are rotated
+// pairwise (round-robin tournament, n/2 disjoint pairs per step, one warp per
+// pair) until every pair is orthogonal to eps relative; W accumulates the
+// rotations.  s_j = ||a_j||, u_j = a_j / s_j, sorted descending.
+__global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Ain, int n, int rs,
+                                                int cs, double* __restrict__ U,
+                                                double* __restrict__ S,
+                                                double* __restrict__ V) {
+  extern __shared__ double sm[];
+  const int np = n + (n & 1);  // even number of slots (a zero column when n is odd)
+  double* A = sm;             // np columns of length n (column-major, ld = n)
+  double* W = A + np * n;     // np x np rotations (column-major, ld = np)
+  __shared__ int changed;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = threadIdx.x; q < np * n; q += blockDim.x) {
+    const int j = q / n, i = q % n;
+    A[q] = j < n ? Ain[i * rs + j * cs] : 0.0;
+  }
+  for (int q = threadIdx.x; q < np * np; q += blockDim.x) W[q] = (q / np == q % np) ? 1.0 : 0.0;
+  __syncthreads();
+  // round-robin (circle method): slot 0 holds column 0, slot j >= 1 holds
+  // column 1 + (j - 1 + step) mod (np - 1); pairs are (slot k, slot np-1-k)
+  auto player = [np](int slot, int step) {
+    return slot == 0 ? 0 : 1 + (slot - 1 + step) % (np - 1);
+  };
+  const double eps = 2.220446049250313e-16;
+  const double tol = 4.0 * sqrt((double)n) * eps;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) changed = 0;
+    __syncthreads();
+    for (int step = 0; step < np - 1; ++step) {
+      for (int pr = wid; pr < np / 2; pr += nw) {
+        int p = player(pr, step), q = player(np - 1 - pr, step);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double* ap = A + p * n;
+        double* aq = A + q * n;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          al = fma(ap[i], ap[i], al);
+          be = fma(aq[i], aq[i], be);
+          ga = fma(ap[i], aq[i], ga);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        // dgesvj-style threshold: rotations below sqrt(n) * eps relative are
+        // rounding noise of the dot product itself and would never settle
+        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+          for (int i = lane; i < n; i += 32) {
+            const double x = ap[i], y = aq[i];
+            ap[i] = c * x - s * y;
+            aq[i] = s * x + c * y;
+          }
+          double* wp = W + p * np;
+          double* wq = W + q * np;
+          for (int i = lane; i < np; i += 32) {
+            const double x = wp[i], y = wq[i];
+            wp[i] = c * x - s * y;
+            wq[i] = s * x + c * y;
+          }
+          if (lane == 0) changed = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int any = changed;
+    __syncthreads();  // everyone has read `changed` before thread 0 resets it
+    if (!any) break;
+  }
+  // singular values and descending order (n <= 64: one thread sorts)
+  __shared__ double sv[64];
+  __shared__ int ord[64];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double s2 = 0.0;
+    for (int i = 0; i < n; ++i) s2 = fma(A[j * n + i], A[j * n + i], s2);
+    sv[j] = sqrt(s2);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < n; ++j) ord[j] = j;
+    for (int a = 0; a < n; ++a)
+      for (int b = a + 1; b < n; ++b)
+        if (sv[ord[b]] > sv[ord[a]]) {
+          const int t = ord[a];
+          ord[a] = ord[b];
+          ord[b] = t;
+        }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < n * n; q += blockDim.x) {
+    const int i = q / n, k = q % n;  // row i, output column k (row-major outputs)
+    const int j = ord[k];
+    const double s = sv[j];
+    U[q] = s > 0.0 ? A[j * n + i] / s : (i == k ? 1.0 : 0.0);
+    V[q] = W[j * np + i];
+  }
+  for (int k = threadIdx.x; k < n; k += blockDim.x) S[k] = sv[ord[k]];
+}
+
+}  // namespace skx
+
+using namespace skx;
+
+extern "C" int skx_chol_upper(const double* g, int n, double* r, int* info, void* stream) {
+  SKX_REQUIRE(n >= 1 && n <= 128, "skx_chol_upper: 1 <= n <= 128");
+  const size_t smem = (size_t)n * (n | 1) * 8;
+  cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_chol<<<1, 512, smem, (cudaStream_t)stream>>>(g, n, r, info);
+  return check_launch("k_chol");
+}
+
+extern "C" int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u,
+                              double* s, double* v, void* stream) {
+  SKX_REQUIRE(n >= 1 && n <= 64, "skx_jacobi_svd: 1 <= n <= 64");
+  const int np = n + (n & 1);
+  const size_t smem = (size_t)(np * n + np * np) * 8 + (size_t)np * 4 + 16;
+  cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_jacobi<<<1, 1024, smem, (cudaStream_t)stream>>>(a, n, (int)rs, (int)cs, u, s, v);
+  return check_launch("k_jacobi");
+}

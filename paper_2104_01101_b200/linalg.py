@@ -115,6 +115,39 @@ def tsqr_r_dev(a):
     return r
 
 
+def chol_upper_dev(g):
+    """Upper Cholesky factor R (R^T R = g) of a small SPD matrix (n <= 128), one
+    CTA; returns (R, info) with info a device int (0 = success)."""
+    torch = _torch()
+    n = g.shape[0]
+    r = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    nat.call("skx_chol_upper", nat.ptr(g.contiguous()), n, nat.ptr(r), nat.ptr(info), nat.stream())
+    return r, info
+
+
+def jacobi_svd_dev(a):
+    """SVD of a small square matrix (n <= 64) by one-sided Jacobi in one CTA:
+    a = U diag(s) V^T, s descending."""
+    torch = _torch()
+    n = a.shape[0]
+    u = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    v = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    s = torch.empty(n, dtype=torch.float64, device="cuda")
+    nat.call("skx_jacobi_svd", nat.ptr(a), n, int(a.stride(0)), int(a.stride(1)), nat.ptr(u),
+             nat.ptr(s), nat.ptr(v), nat.stream())
+    return u, s, v
+
+
+def _small_svd(r):
+    """(u, s, vh) of a small square R: libskx Jacobi when n <= 64."""
+    torch = _torch()
+    if r.shape[0] <= 64:
+        u, s, v = jacobi_svd_dev(r)
+        return u, s, v.transpose(0, 1)
+    return torch.linalg.svd(r, full_matrices=False)
+
+
 def top_svd_dev(mat, k):
     """Leading k singular triplets of a matrix with one small dimension.
 
@@ -128,13 +161,13 @@ def top_svd_dev(mat, k):
         return u[:, :k], s[:k], v[:, :k]
     if m >= n:
         r = tsqr_r_dev(mat)
-        _, s, vh = torch.linalg.svd(r, full_matrices=False)
+        _, s, vh = _small_svd(r)
         v = vh[:k].transpose(0, 1)
         sk = s[:k]
         u = (mat @ v) / torch.where(sk > 0, sk, torch.ones_like(sk))
         return u, sk, v.contiguous()
     r = tsqr_r_dev(mat.transpose(0, 1))  # mat^T = Q r  ->  mat = r^T Q^T
-    u, s, _ = torch.linalg.svd(r.transpose(0, 1), full_matrices=False)
+    u, s, _ = _small_svd(r.transpose(0, 1))
     u = u[:, :k]
     sk = s[:k]
     v = (mat.transpose(0, 1) @ u) / torch.where(sk > 0, sk, torch.ones_like(sk))
@@ -225,6 +258,32 @@ def resid_dev(z, core_t, a, y):
     return torch.sqrt(out[0])
 
 
+def sketch_qr_dev(z):
+    """Reduced QR of the sketched system Z (m x r) with the reference's rank
+    test.  r <= 128: CholeskyQR2 (two small Grams, two one-CTA Choleskys, two
+    TRSMs -- no LAPACK panel); it is used only when safe (both Choleskys
+    succeed and diag(R) spans < 1e6, i.e. cond(Z) far below eps^-1/2),
+    otherwise the Householder QR of cuSOLVER runs, giving the same rank
+    decision as src/linalg.py:44-52.  One host sync decides."""
+    torch = _torch()
+    m, r = z.shape
+    if r > 128 or m < r:
+        return qr_flag_dev(z)
+    r1, i1 = chol_upper_dev(z.transpose(0, 1) @ z)
+    z1 = torch.linalg.solve_triangular(r1, z, upper=True, left=False)
+    r2, i2 = chol_upper_dev(z1.transpose(0, 1) @ z1)
+    q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
+    rz = r2 @ r1
+    d1 = torch.diagonal(r1)
+    unsafe = (i1[0] != 0) | (i2[0] != 0) | ~(d1.max() < 1e6 * d1.min())
+    tol = 1e-12 * torch.linalg.vector_norm(z)
+    bad = (torch.diagonal(rz).abs() < tol).any()
+    flags = torch.stack([unsafe, bad]).cpu()
+    if bool(flags[0]):
+        return qr_flag_dev(z)
+    return q, rz, flags[1]
+
+
 def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
     """Algorithm 5 (src/linalg.py:87-113) on device.
     z: (m, r) CUDA tensor (any strides), y: (m, s) CUDA tensor view.
@@ -236,7 +295,7 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
         raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
     if rank > min(r, s):
         raise ValueError(f"rank {rank} exceeds min({r}, {s})")
-    qz, rz, bad = qr_flag_dev(z)
+    qz, rz, bad = sketch_qr_dev(z)
     if check and bool(bad.item()):
         raise RankDeficientError("rank-deficient sketched system")
     width = min(rank + oversample, s)

@@ -158,6 +158,37 @@ def test_tsqr_r_matches_lapack(n, w):
     assert np.array_equal(rt, r)
 
 
+@pytest.mark.parametrize("n", [1, 2, 7, 20, 64, 100, 128])
+def test_small_cholesky(n):
+    import torch
+    from paper_2104_01101_b200.linalg import chol_upper_dev
+    a = np.random.default_rng(n).standard_normal((3 * n, n))
+    g = a.T @ a
+    r, info = chol_upper_dev(torch.from_numpy(g).cuda())
+    assert int(info.item()) == 0
+    ref = np.linalg.cholesky(g).T
+    assert relerr(r.cpu().numpy(), ref) <= 1e-13
+    bad = g.copy()
+    bad[n // 2, n // 2] = -1.0
+    _, info = chol_upper_dev(torch.from_numpy(bad).cuda())
+    assert int(info.item()) >= 1
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 15, 20, 30, 31, 64])
+def test_small_jacobi_svd(n):
+    import torch
+    from paper_2104_01101_b200.linalg import jacobi_svd_dev
+    a = np.random.default_rng(n).standard_normal((n, n)) @ np.diag(np.logspace(0, 3, n))
+    u, s, v = (t.cpu().numpy() for t in jacobi_svd_dev(torch.from_numpy(a).cuda()))
+    ss = np.linalg.svd(a, compute_uv=False)
+    assert np.allclose(s, ss, rtol=1e-12)
+    assert relerr((u * s) @ v.T, a) <= 1e-13
+    assert np.allclose(u.T @ u, np.eye(n), atol=1e-12) and np.allclose(v.T @ v, np.eye(n), atol=1e-12)
+    # transposed (strided) input
+    ut, st, vt = (t.cpu().numpy() for t in jacobi_svd_dev(torch.from_numpy(a.T.copy()).cuda().t()))
+    assert np.allclose(st, s, rtol=1e-13)
+
+
 @pytest.mark.parametrize("shape,k", [((50_000, 20), 10), ((30, 100_000), 20), ((400, 300), 5)])
 def test_top_svd(shape, k):
     import torch
