@@ -234,11 +234,20 @@ def run_ours(args, cfgd):
     dom = max(kern.items(), key=lambda kv: kv[1]["ms_total"])[0] if kern else None
     roof_k = "skx_ts_rhs_coo" if "skx_ts_rhs_coo" in kern else dom
     roof = None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            t = json.load(fh).get(roof_k)
+        if t and world == 1 and args.config == 4:
+            traffic = int(t["dram_read_bytes"] + t["dram_write_bytes"])
+    except Exception:
+        traffic = None
     if roof_k in kern and roof_k in alg_bytes:
         ach = alg_bytes[roof_k] / (kern[roof_k]["ms_avg"] / 1e3) / 1e9
         roof = {"kernel": roof_k, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": None, "alg_bytes_per_launch": int(alg_bytes[roof_k]),
+                "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full)",
+                "alg_bytes_per_launch": int(alg_bytes[roof_k]),
                 "layout": "fibre-major COO: int32 x2 other coords + f64 value = 16 B/nnz; "
                           "canonical int64 COO would be 32 B/nnz"}
 

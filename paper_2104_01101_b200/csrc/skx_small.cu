@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(512) k_chol(const double* __restrict__ G, int 
 // pairwise (round-robin tournament, n/2 disjoint pairs per step, one warp per
 // pair) until every pair is orthogonal to eps relative; W accumulates the
 // rotations.  s_j = ||a_j||, u_j = a_j / s_j, sorted descending.
-__global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Ain, int n, int rs,
+__global__ void __launch_bounds__(512) k_jacobi(const double* __restrict__ Ain, int n, int rs,
                                                 int cs, double* __restrict__ U,
                                                 double* __restrict__ S,
                                                 double* __restrict__ V) {
@@ -78,9 +78,7 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Ain,
   __syncthreads();
   // round-robin (circle method): slot 0 holds column 0, slot j >= 1 holds
   // column 1 + (j - 1 + step) mod (np - 1); pairs are (slot k, slot np-1-k)
-  auto player = [np](int slot, int step) {
-    return slot == 0 ? 0 : 1 + (slot - 1 + step) % (np - 1);
-  };
+  const int nm1 = np - 1;
   const double eps = 2.220446049250313e-16;
   const double tol = 4.0 * sqrt((double)n) * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
@@ -88,7 +86,8 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* __restrict__ Ain,
     __syncthreads();
     for (int step = 0; step < np - 1; ++step) {
       for (int pr = wid; pr < np / 2; pr += nw) {
-        int p = player(pr, step), q = player(np - 1 - pr, step);
+        int p = pr == 0 ? 0 : 1 + (pr - 1 + step) % nm1;
+        int q = 1 + (np - 2 - pr + step) % nm1;  // slot np-1-pr >= 1
         if (p > q) {
           const int t = p;
           p = q;
@@ -183,6 +182,6 @@ extern "C" int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, do
   const int np = n + (n & 1);
   const size_t smem = (size_t)(np * n + np * np) * 8 + (size_t)np * 4 + 16;
   cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_jacobi<<<1, 1024, smem, (cudaStream_t)stream>>>(a, n, (int)rs, (int)cs, u, s, v);
+  k_jacobi<<<1, 512, smem, (cudaStream_t)stream>>>(a, n, (int)rs, (int)cs, u, s, v);
   return check_launch("k_jacobi");
 }
