@@ -178,7 +178,7 @@ __device__ __forceinline__ void warp_ordered_add(double* acc, uint32_t bucket, d
   const unsigned lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   unsigned peers = __match_any_sync(full, bucket);
-  bool solo = (__popc(peers) == 1);
+  const bool solo = peers == (1u << lane) || bucket == kNoBucket;
   if (__all_sync(full, solo)) {
     if (bucket != kNoBucket) acc[bucket] += val;
   } else {

@@ -40,66 +40,173 @@ __global__ void k_ts_tables(Coeffs cf, int64_t m, uint32_t* tab) {
 }
 
 // ======================================================= sparse RHS sketch
-// One warp per column i_n (fibre-major layout).  Warp-private accumulator of
-// m doubles in shared memory; contributions enter in ascending-j order, so
-// each Y cell is the same sequential sum numpy's add.at forms.
+// Fibre-major records (skx_coo_fibre): the nonzeros of column i_n are
+// contiguous and ordered by the other-mode index j.  Each warp owns an
+// nnz-balanced contiguous range of columns (so its records, output rows and
+// TLB entries are walked in address order) and a private accumulator of m
+// doubles in shared memory.  Contributions enter in ascending-j order, so each
+// Y cell is the same sequential sum numpy's add.at forms; a finished column is
+// streamed out and the accumulator re-zeroed (empty columns write zeros).
+//
+// Per chunk of 32*U nonzeros: the records (16 or 24 bytes) were loaded one
+// chunk earlier (two register buffers that swap by name: the loop body is
+// written twice) and prefetched into L2 PF chunks before that; table lookups
+// give bucket/sign; when the chunk lies inside one column, the match_any of
+// all U slices issue back to back before the ordered read-modify-writes.
 struct OtherTabs {
   int n;
   const uint32_t* t[15];
 };
 
-// NO = number of other modes (1..4), records from skx_coo_fibre.
-// Three explicit phases per 32*U nonzeros -- (1) the 16/24-byte records,
-// (2) table lookups, (3) ordered accumulation -- so all HBM loads of a chunk
-// are in flight together; bucket sums are reduced mod m by conditional
-// subtraction (each table entry < m), no integer division.
 template <int U, int NO>
+struct RhsRecs {
+  int32_t c[U][4];
+  double v[U];
+};
+
+template <int U, int NO>
+__device__ __forceinline__ void rhs_load(const double* __restrict__ rec, int64_t base, int64_t e_end,
+                                         int lane, RhsRecs<U, NO>& r) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t e = base + u * 32 + lane;
+    if (e < e_end) {
+      load_rec<NO>(rec, e, r.c[u], r.v[u]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r.c[u][k] = 0;
+      r.v[u] = 0.0;
+    }
+  }
+}
+
+template <int U, int NO, int PF>
 __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
                                                     const int64_t* __restrict__ colptr,
                                                     const double* __restrict__ rec, int64_t m,
                                                     double* __restrict__ yt) {
   extern __shared__ double smem[];
+  constexpr int RW = NO <= 2 ? 2 : 3;  // record words
+  constexpr int CH = 32 * U;
+  constexpr int LINES = CH * RW * 8 / 128;  // 128-byte lines per chunk, one per lane
+  static_assert(LINES <= 32, "chunk too large for one prefetch instruction");
+  const int64_t nnz = colptr[s_n];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
   double* acc = smem + (size_t)wid * (m + 32);
   double* stage = acc + m;
   const uint32_t mm = (uint32_t)m;
-  const int64_t gw = blockIdx.x * (int64_t)nw + wid;
-  const int64_t tw = (int64_t)gridDim.x * nw;
-  for (int64_t col = gw; col < s_n; col += tw) {
-    for (int64_t h = lane; h < m; h += 32) acc[h] = 0.0;
-    __syncwarp();
-    const int64_t e0 = colptr[col], e1 = colptr[col + 1];
-    for (int64_t base = e0; base < e1; base += 32 * U) {
-      int32_t c[U][4];
-      double v[U];
-      uint32_t bk[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t e = base + u * 32 + lane;
-        load_rec<NO>(rec, e < e1 ? e : e0, c[u], v[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        uint32_t h = 0, neg = 0;
-#pragma unroll
-        for (int k = 0; k < NO; ++k) {
-          const uint32_t t = __ldg(ot.t[k] + c[u][k]);
-          h += pk_bucket(t);
-          if (h >= mm) h -= mm;
-          neg ^= pk_neg(t);
-        }
-        const bool ok = base + u * 32 + lane < e1;
-        bk[u] = ok ? h : kNoBucket;
-        v[u] = neg ? -v[u] : v[u];
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], v[u], stage);
+  const int64_t W = (int64_t)gridDim.x * nw, gw = blockIdx.x * (int64_t)nw + wid;
+  auto col_at = [&](int64_t w) -> int64_t {  // first column starting at/after w's share
+    if (w >= W) return s_n;
+    const int64_t target = (nnz * w) / W;
+    int64_t lo = 0, hi = s_n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (colptr[mid] < target) lo = mid + 1; else hi = mid;
     }
+    return lo;
+  };
+  const int64_t c0 = gw == 0 ? 0 : col_at(gw), c1 = col_at(gw + 1);
+  if (c0 >= c1) return;
+  for (int64_t h = lane; h < m; h += 32) acc[h] = 0.0;
+  __syncwarp();
+  const int64_t ebeg = colptr[c0], eend = colptr[c1];
+  int64_t col = c0, cbeg = ebeg, cend = colptr[c0 + 1];
+  auto flush = [&]() {  // write the finished column, re-zero, advance
     double* dst = yt + col * m;
-    for (int64_t h = lane; h < m; h += 32) __stcs(dst + h, acc[h]);
+    if ((m & 1) == 0) {  // 16-byte aligned rows
+      const double2 z = make_double2(0.0, 0.0);
+      for (int64_t h = lane; h < (m >> 1); h += 32) {
+        __stcs(reinterpret_cast<double2*>(dst) + h, reinterpret_cast<const double2*>(acc)[h]);
+        reinterpret_cast<double2*>(acc)[h] = z;
+      }
+    } else {
+      for (int64_t h = lane; h < m; h += 32) {
+        __stcs(dst + h, acc[h]);
+        acc[h] = 0.0;
+      }
+    }
     __syncwarp();
+    ++col;
+    cbeg = cend;
+    cend = col < s_n ? colptr[col + 1] : INT64_MAX;
+  };
+  auto prefetch = [&](int64_t from) {
+    const char* p = reinterpret_cast<const char*>(rec + from * RW) + lane * 128;
+    if (lane < LINES && from + lane * (128 / (RW * 8)) < eend)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  };
+  auto process = [&](int64_t base, const RhsRecs<U, NO>& r) {
+    uint32_t t[U][NO];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < NO; ++k) t[u][k] = __ldg(ot.t[k] + r.c[u][k]);
+    uint32_t hb[U];
+    double xs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // bucket sums reduced mod m by conditional subtraction
+      uint32_t h = 0, neg = 0;
+#pragma unroll
+      for (int k = 0; k < NO; ++k) {
+        h += pk_bucket(t[u][k]);
+        if (h >= mm) h -= mm;
+        neg ^= pk_neg(t[u][k]);
+      }
+      hb[u] = h;
+      xs[u] = neg ? -r.v[u] : r.v[u];
+    }
+    const int64_t nvalid = imin((int64_t)CH, eend - base);
+    if (base >= cbeg && base + nvalid <= cend) {
+      uint32_t b[U];
+      unsigned peers[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) b[u] = u * 32 + lane < nvalid ? hb[u] : kNoBucket;
+#pragma unroll
+      for (int u = 0; u < U; ++u) peers[u] = __match_any_sync(0xffffffffu, b[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (__all_sync(0xffffffffu, peers[u] == (1u << lane) || b[u] == kNoBucket)) {
+          if (b[u] != kNoBucket) acc[b[u]] += xs[u];
+          __syncwarp();
+        } else {
+          warp_ordered_add(acc, b[u], xs[u], stage);
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t sub = base + u * 32;
+      if (sub >= eend) break;
+      const int hi = (int)imin(eend - sub, (int64_t)32);
+      while (true) {
+        // lanes of this slice inside the current column: [lo, min(cend - sub, hi))
+        const int lo = (int)imax(cbeg - sub, (int64_t)0);
+        const int64_t ce = cend - sub;
+        const int top = ce < hi ? (int)ce : hi;
+        warp_ordered_add(acc, lane >= lo && lane < top ? hb[u] : kNoBucket, xs[u], stage);
+        if (ce >= hi) break;
+        flush();
+      }
+    }
+  };
+#pragma unroll 1
+  for (int p = 1; p <= PF; ++p) prefetch(ebeg + p * CH);
+  RhsRecs<U, NO> ra, rb;
+  rhs_load<U, NO>(rec, ebeg, eend, lane, ra);
+#pragma unroll 1
+  for (int64_t base = ebeg; base < eend; base += 2 * CH) {
+    prefetch(base + (PF + 1) * CH);
+    rhs_load<U, NO>(rec, base + CH, eend, lane, rb);
+    process(base, ra);
+    if (base + CH >= eend) break;
+    prefetch(base + (PF + 2) * CH);
+    rhs_load<U, NO>(rec, base + 2 * CH, eend, lane, ra);
+    process(base + CH, rb);
   }
+  while (col < c1) flush();  // trailing (possibly empty) columns of the range
 }
 
 // ======================================================== dense RHS sketch
@@ -304,10 +411,10 @@ extern "C" int skx_ts_rhs_coo(int n_other, int64_t s_n, const int64_t* colptr, c
   ot.n = n_other;
   for (int k = 0; k < n_other; ++k) ot.t[k] = tab + tab_off_h[k];
   const size_t smem = (size_t)nw * (m + 32) * 8;
-  auto kern = n_other == 1 ? k_ts_rhs_coo<8, 1>
-            : n_other == 2 ? k_ts_rhs_coo<8, 2>
-            : n_other == 3 ? k_ts_rhs_coo<6, 3>
-                           : k_ts_rhs_coo<6, 4>;
+  auto kern = n_other == 1 ? k_ts_rhs_coo<4, 1, 8>
+            : n_other == 2 ? k_ts_rhs_coo<4, 2, 8>
+            : n_other == 3 ? k_ts_rhs_coo<4, 3, 8>
+                           : k_ts_rhs_coo<4, 4, 8>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);

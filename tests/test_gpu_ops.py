@@ -231,6 +231,37 @@ def test_sparse_ts_rhs_all_modes_vs_oracle(skx, oracle, shape, nnz, m):
         assert np.array_equal(yt.T, ref)
 
 
+@pytest.mark.parametrize("case", ["skewed", "tiny_columns", "single_nnz"])
+def test_sparse_ts_rhs_column_edge_cases(skx, oracle, case):
+    """Warp column ranges, columns straddling chunk boundaries, long runs of
+    empty columns and a single giant column: still bit-identical to add.at."""
+    from paper_2104_01101_b200.sketching import ts_rhs_coo_dev
+    from paper_2104_01101_b200.tensors import device_of
+    rng = np.random.default_rng(3)
+    shape = (4000, 60, 50)
+    if case == "skewed":  # 90% of nonzeros in 3 mode-0 slices, most slices empty
+        i0 = np.where(rng.uniform(size=30000) < 0.9, rng.choice([5, 1999, 3998], 30000),
+                      rng.integers(0, 4000, 30000))
+    elif case == "tiny_columns":
+        i0 = rng.integers(0, 4000, 3000)
+    else:
+        i0 = np.array([1234])
+    n = i0.size
+    c = np.stack([i0, rng.integers(0, 60, n), rng.integers(0, 50, n)], axis=1)
+    c = np.unique(c, axis=0)
+    v = rng.standard_normal(c.shape[0])
+    st = skx.SparseTensor(shape, c, v)
+    oc = oracle.Coo(shape, c, v)
+    d = device_of(st)
+    for n_mode in range(3):
+        ext = tuple(shape[k] for k in range(3) if k != n_mode)
+        op = skx.TensorSketchOp.build(ext, 300, skx.make_rng(n_mode))
+        hs, ss = oracle.ts_tables(ext, 300, oracle.generator(n_mode))
+        colptr, rec = d.fibre(n_mode)
+        yt = ts_rhs_coo_dev(op, colptr, rec, shape[n_mode]).cpu().numpy()
+        assert np.array_equal(yt.T, oracle.ts_rhs(hs, ss, ext, 300, oracle.unfold_t(oc, n_mode)))
+
+
 def test_fibre_layout_matches_stable_sort(skx):
     """The radix-sorted fibre-major records equal a stable numpy sort by i_n."""
     import torch
