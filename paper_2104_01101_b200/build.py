@@ -56,7 +56,9 @@ def build(verbose=False, force=False):
         obj = os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + deps):
-            cmd = [nvcc()] + ARCH + FLAGS + ["-c", src, "-o", obj]
+            # SKX_NVCC_EXTRA: extra nvcc flags for A/B experiments (e.g. -DNAME=value)
+            extra = os.environ.get("SKX_NVCC_EXTRA", "").split()
+            cmd = [nvcc()] + ARCH + FLAGS + extra + ["-c", src, "-o", obj]
             jobs.append(cmd)
 
     def run(cmd):

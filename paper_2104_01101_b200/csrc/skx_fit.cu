@@ -215,6 +215,151 @@ __global__ void __launch_bounds__(128) k_tucker3(const int64_t* __restrict__ col
   }
 }
 
+// ---- same contraction on the FP64 tensor cores (mma.sync m8n8k4 f64).
+// Warp per slice i0.  W = A0[i0,:] x_0 C (R1 x R2) lives in registers as the
+// B fragments (KS k-steps of 4 x NT n-tiles of 8, zero padded).  Nonzeros go
+// 8 at a time: row q of the A fragment is nonzero e = base + q (lanes 4q..4q+3
+// load the same 16-byte record, a broadcast), so V = A1[i1_e,:] W is one
+// 8 x 8*NT tile after KS*NT DMMAs, and each lane folds its two columns per
+// n-tile with A2[i2_e, cols] and v_e into a private sum.  No shared memory:
+// factor rows come straight from L2 in 32-byte pieces.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+#ifndef SKX_T3_MINB
+#define SKX_T3_MINB 1
+#endif
+template <int G>
+struct T3Rec {
+  int32_t i1[G], i2[G];
+  double v[G];
+};
+template <int KS, int NT, int G>
+struct T3Rows {
+  double a[G][KS], y[G][NT][2], v[G];
+};
+
+// Three-stage software pipeline per warp: records of step s+2 (L2, after the
+// slice prefetch), factor rows of step s+1, DMMAs of step s.  The buffers
+// rotate by static index (body unrolled lcm(3, 2) = 6 times) so nothing is
+// copied while its load is in flight.  R1T/R2T > 0 fix the ranks at compile
+// time (predicates fold away); 0 reads them at run time.
+template <int KS, int NT, int G, int R1T, int R2T>
+__global__ void __launch_bounds__(256, SKX_T3_MINB) k_tucker3_mma(const int64_t* __restrict__ colptr, int64_t s0,
+                                                     const double* __restrict__ rec,
+                                                     const double* __restrict__ A0,
+                                                     const double* __restrict__ A1,
+                                                     const double* __restrict__ A2,
+                                                     const double* __restrict__ C, int R0, int R1_,
+                                                     int R2_, double* __restrict__ slice_out) {
+  const int R1 = R1T > 0 ? R1T : R1_, R2 = R2T > 0 ? R2T : R2_;
+  const int lane = threadIdx.x & 31, q = lane >> 2, c = lane & 3;
+  const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
+  const bool vec2 = (R2 & 1) == 0;  // A2 rows 16-byte aligned: pairs load as one LDG.128
+  constexpr int STEP = 8 * G;
+  auto prefetch_slice = [&](int64_t j) {  // the records of slice j into L2
+    if (j >= s0) return;
+    const int64_t l0 = colptr[j] * 16 / 128, l1 = (colptr[j + 1] * 16 + 127) / 128;
+    for (int64_t l = l0 + lane; l < l1; l += 32)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(rec) + l * 128));
+  };
+  int64_t i0 = blockIdx.x * nw + (threadIdx.x >> 5);
+  prefetch_slice(i0);
+  for (; i0 < s0; i0 += stride) {
+    prefetch_slice(i0 + stride);
+    const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
+    if (e0 == e1) {
+      if (lane == 0) slice_out[i0] = 0.0;
+      continue;
+    }
+    double b[KS][NT];  // B[k][n] = W[ks*4 + c][nt*8 + q]
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int k = ks * 4 + c, n = nt * 8 + q;
+        double w = 0.0;
+        if (k < R1 && n < R2)
+          for (int r0 = 0; r0 < R0; ++r0)
+            w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R1 + k) * R2 + n), w);
+        b[ks][nt] = w;
+      }
+    auto load_recs = [&](int64_t base, T3Rec<G>& r) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int64_t e = base + g * 8 + q;
+        const bool ok = e < e1;
+        int32_t cc[4];
+        double xv;
+        load_rec<2>(rec, ok ? e : e0, cc, xv);
+        r.i1[g] = cc[0];
+        r.i2[g] = cc[1];
+        r.v[g] = ok ? xv : 0.0;
+      }
+    };
+    auto load_rows = [&](const T3Rec<G>& r, T3Rows<KS, NT, G>& w) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double* r1 = A1 + (int64_t)r.i1[g] * R1;
+        const double* r2 = A2 + (int64_t)r.i2[g] * R2;
+        w.v[g] = r.v[g];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) w.a[g][ks] = ks * 4 + c < R1 ? __ldg(r1 + ks * 4 + c) : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int n = nt * 8 + 2 * c;
+          if (vec2) {
+            const double2 p = n < R2 ? __ldg(reinterpret_cast<const double2*>(r2 + n))
+                                     : make_double2(0.0, 0.0);
+            w.y[g][nt][0] = p.x;
+            w.y[g][nt][1] = p.y;
+          } else {
+            w.y[g][nt][0] = n < R2 ? __ldg(r2 + n) : 0.0;
+            w.y[g][nt][1] = n + 1 < R2 ? __ldg(r2 + n + 1) : 0.0;
+          }
+        }
+      }
+    };
+    double acc = 0.0;
+    auto compute = [&](const T3Rows<KS, NT, G>& w) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        double t = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) dmma884(d0, d1, w.a[g][ks], b[ks][nt]);
+          t = fma(d0, w.y[g][nt][0], t);
+          t = fma(d1, w.y[g][nt][1], t);
+        }
+        acc = fma(w.v[g], t, acc);
+      }
+    };
+    T3Rec<G> rr[3];
+    T3Rows<KS, NT, G> ww[2];
+    load_recs(e0, rr[0]);
+    load_recs(e0 + STEP, rr[1]);
+    load_rows(rr[0], ww[0]);
+    for (int64_t base = e0; base < e1; base += 6 * STEP) {
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const int64_t sb = base + s * STEP;
+        if (sb >= e1) break;
+        load_recs(sb + 2 * STEP, rr[(s + 2) % 3]);
+        load_rows(rr[(s + 1) % 3], ww[(s + 1) % 2]);
+        compute(ww[s % 2]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) slice_out[i0] = acc;
+  }
+}
+
 // Generic order-N Tucker cross term: per nonzero, odometer over the core.
 struct GenPack {
   int ndim;
@@ -357,12 +502,38 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
     k_tucker3<RT, NP><<<blocks, 128, sm, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0, R1,  \
                                               R2, part);                                  \
   } while (0)
-    if (RM <= 4) SKX_T3(4, 4);
-    else if (RM <= 8) SKX_T3(8, 2);
-    else if (RM <= 10) SKX_T3(10, 2);
-    else if (RM <= 16) SKX_T3(16, 1);
-    else if (RM <= 20) SKX_T3(20, 1);
-    else SKX_T3(32, 1);
+    // ranks <= 4: too little work per row for the 8x8x4 tiles (SIMT kernel is faster)
+    if (RM <= 4) {
+      if (RM <= 4) SKX_T3(4, 4);
+      else if (RM <= 8) SKX_T3(8, 2);
+      else if (RM <= 10) SKX_T3(10, 2);
+      else if (RM <= 16) SKX_T3(16, 1);
+      else if (RM <= 20) SKX_T3(20, 1);
+      else SKX_T3(32, 1);
+    } else {
+      // k-steps of 4 over R1, n-tiles of 8 over R2
+      const int KS = (R1 + 3) / 4, NT = (R2 + 7) / 8;
+      const unsigned mb = (unsigned)imin((s0 + 7) / 8, (int64_t)num_sms() * 8);
+#define SKX_T3M(ks, nt)                                                                    \
+  if (KS <= ks && NT == nt) {                                                              \
+    k_tucker3_mma<ks, nt, 2, 0, 0><<<mb, 256, 0, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0, \
+                                                     R1, R2, part);                         \
+  } else
+      if (R1 == 10 && R2 == 10) {
+        k_tucker3_mma<3, 2, 2, 10, 10><<<mb, 256, 0, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0,
+                                                         R1, R2, part);
+      } else if (R1 == 20 && R2 == 20) {
+        k_tucker3_mma<5, 3, 2, 20, 20><<<mb, 256, 0, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0,
+                                                         R1, R2, part);
+      } else
+      SKX_T3M(2, 1) SKX_T3M(3, 1) SKX_T3M(5, 1) SKX_T3M(8, 1)
+      SKX_T3M(2, 2) SKX_T3M(3, 2) SKX_T3M(5, 2) SKX_T3M(8, 2)
+      SKX_T3M(2, 3) SKX_T3M(3, 3) SKX_T3M(5, 3) SKX_T3M(8, 3)
+      SKX_T3M(2, 4) SKX_T3M(3, 4) SKX_T3M(5, 4) SKX_T3M(8, 4) {
+        SKX_REQUIRE(false, "skx_tucker_cross_coo: no kernel for ranks %d x %d", R1, R2);
+      }
+#undef SKX_T3M
+    }
 #undef SKX_T3
     k_final_sum<<<1, 1024, 0, s>>>(part, (int)s0, out);
     return check_launch("k_tucker3", 2);

@@ -347,7 +347,10 @@ def test_dense_gather_and_kron_rows(skx, oracle):
 
 def test_sparse_fitness_order3_and_generic(skx, oracle):
     rng = np.random.default_rng(6)
-    for shape, R in (((50, 40, 30), (3, 4, 5)), ((10, 12, 9, 7), (2, 3, 2, 2)), ((60, 50, 40), (20, 20, 20))):
+    cases = (((50, 40, 30), (3, 4, 5)), ((10, 12, 9, 7), (2, 3, 2, 2)), ((60, 50, 40), (20, 20, 20)),
+             ((40, 50, 60), (10, 10, 10)), ((40, 50, 60), (4, 4, 4)), ((40, 50, 60), (7, 9, 13)),
+             ((40, 50, 60), (12, 32, 17)))
+    for shape, R in cases:
         c, v = _coo_rand(shape, 4000, 3)
         st = skx.SparseTensor(shape, c, v)
         oc = oracle.Coo(shape, c, v)

@@ -21,6 +21,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
+    ap.add_argument("--gantt", type=float, default=0.0,
+                    help="also list, in start order, every kernel longer than this many ms")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -73,6 +75,12 @@ def main():
           f"largest {sorted(gaps)[-5:] if gaps else []} us")
     for nm, (c, d) in sorted(per.items(), key=lambda kv: -kv[1][1])[:30]:
         print(f"{d / 1e3:9.3f} ms {c:5d}  {nm}")
+    if args.gantt > 0:
+        print("start_ms  dur_ms  stream  kernel")
+        for e in sorted(kern, key=lambda e: e["ts"]):
+            if e["dur"] >= args.gantt * 1e3:
+                print(f"{(e['ts'] - t_lo) / 1e3:8.2f} {e['dur'] / 1e3:7.3f} {e['args'].get('stream')!s:>6}  "
+                      f"{e['name'][:60]}")
 
 
 if __name__ == "__main__":
