@@ -275,6 +275,7 @@ __global__ void k_zig_emit(const uint16_t* info, const double* val, int64_t L, L
 }
 
 // ------------------------------------------------------------------ lemire
+constexpr int kScanChunk = 64;  // Philox blocks per thread per CTA
 // Lists the absolute 32-bit positions A = 2*raw + half (half 0 = low word) of
 // every draw in raw words [raw_lo, raw_hi) that Lemire's method would reject
 // for bound k.  Rejection depends only on the drawn value, so the scan can run
@@ -284,9 +285,11 @@ __global__ void k_lemire_scan(uint64_t k0, uint64_t k1, uint64_t raw_lo, uint64_
                               unsigned long long* count) {
   const uint64_t b_first = raw_lo >> 2, b_last = (raw_hi - 1) >> 2;
   const uint64_t nb = b_last - b_first + 1;
-  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (; t < nb; t += stride) {
+  // each CTA owns a contiguous chunk of kScanChunk * blockDim.x blocks and
+  // retires when done: short-lived CTAs let higher-priority streams take SMs
+  const uint64_t c0 = (uint64_t)blockIdx.x * kScanChunk * blockDim.x;
+  const uint64_t c1 = umin64(nb, c0 + (uint64_t)kScanChunk * blockDim.x);
+  for (uint64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
     const uint64_t b = b_first + t;
     const U64x4 blk = philox_block(k0, k1, b + 1);
     // branch-free screen of the 8 halves (rejections are ~1e-8 rare); the
@@ -403,9 +406,9 @@ extern "C" int skx_lemire_scan(uint64_t k0, uint64_t k1, uint64_t raw_lo, uint64
   uint32_t thresh = (uint32_t)((0x100000000ULL - (uint64_t)k) % (uint64_t)k);
   if (thresh == 0 || raw_hi <= raw_lo) return check_launch("lemire(no rejections possible)", 0);
   const uint64_t nb = ((raw_hi - 1) >> 2) - (raw_lo >> 2) + 1;
-  // 4 CTAs (32 warps) per SM saturate the IMAD pipe and leave half of every SM
-  // to memory-bound kernels running concurrently on other streams
-  int blocks = (int)umin64((nb + 255) / 256, (uint64_t)num_sms() * 4);
+  const uint64_t per = (uint64_t)kScanChunk * 256;
+  SKX_REQUIRE((nb + per - 1) / per < (1ULL << 31), "skx_lemire_scan: range too large");
+  const unsigned blocks = (unsigned)((nb + per - 1) / per);
   k_lemire_scan<<<blocks, 256, 0, s>>>(k0, k1, raw_lo, raw_hi, k, thresh, rej, cap, count);
   return check_launch("k_lemire_scan");
 }

@@ -214,26 +214,47 @@ def leverage_scores(a):
 class NormalSource:
     """Device-resident cursor over a Generator's raw stream for
     standard_normal draws (the position lives in HBM, so consecutive draws
-    need no host round trip)."""
+    need no host round trip).
 
-    def __init__(self, gen):
+    numpy's standard_normal keeps no state between calls, so k consecutive
+    draws of sizes n_1..n_k are the first n_1 + ... + n_k normals of the
+    stream.  With batch > 0 the source generates at least `batch` normals at
+    a time and serves later draws from that buffer (one ziggurat pass per
+    sweep instead of one per subproblem)."""
+
+    def __init__(self, gen, batch=0):
         torch = _torch()
         self.gen = gen
         c = rngmod.cursor(gen)
         self.k0, self.k1 = c.k0, c.k1
         self.pos = torch.tensor([c.p], dtype=torch.int64, device="cuda")
+        self.batch = int(batch)
+        self._buf, self._off = None, 0
 
-    def normal(self, shape):
+    def _generate(self, n):
         torch = _torch()
-        n = int(np.prod(shape))
         out = torch.empty(n, dtype=torch.float64, device="cuda")
         nat.call_ws("skx_philox_normal",
                     (ctypes.c_uint64(self.k0), ctypes.c_uint64(self.k1), nat.ptr(self.pos), n,
                      nat.ptr(out), nat.ptr(self.pos)), slot=1)
+        return out
+
+    def normal(self, shape):
+        torch = _torch()
+        n = int(np.prod(shape))
+        left = 0 if self._buf is None else self._buf.numel() - self._off
+        if left < n:
+            fresh = self._generate(max(n - left, self.batch))
+            self._buf = torch.cat([self._buf[self._off:], fresh]) if left else fresh
+            self._off = 0
+        out = self._buf[self._off:self._off + n]
+        self._off += n
         return out.view(*shape)
 
     def sync_host(self):
         """Move the numpy Generator to where numpy would be (one D2H)."""
+        if self._buf is not None and self._off != self._buf.numel():
+            raise RuntimeError("NormalSource.sync_host: buffered normals not consumed")
         rngmod.set_cursor(self.gen, int(self.pos.item()))
 
 

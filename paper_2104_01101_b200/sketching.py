@@ -472,11 +472,14 @@ def _rej_cap(P, k2):
 
 
 class RrfScan:
-    """A Lemire rejection scan over raw words [raw_lo, raw_hi) in flight."""
+    """A Lemire rejection scan over raw words [raw_lo, raw_hi) in flight.
+    `pre` optionally holds a finish already enqueued behind it for a known
+    start cursor (see plan_rrf_scans)."""
 
-    def __init__(self, key, raw_lo, raw_hi, k2, cap, rej, count, stream):
+    def __init__(self, key, raw_lo, raw_hi, k2, cap, rej, count, stream, tag=0):
         self.key, self.raw_lo, self.raw_hi, self.k2, self.cap = key, raw_lo, raw_hi, k2, cap
-        self.rej, self.count, self.stream = rej, count, stream
+        self.rej, self.count, self.stream, self.tag = rej, count, stream, tag
+        self.pre = None
 
 
 def launch_rrf_scan(key, raw_lo, raw_hi, k2, cap, stream=None):
@@ -496,13 +499,11 @@ def launch_rrf_scan(key, raw_lo, raw_hi, k2, cap, stream=None):
     return RrfScan(key, raw_lo, raw_hi, k2, cap, rej, count, st)
 
 
-def finish_rrf_scan(scan, gen, P):
-    """Resolve `scan` for the integers(0,k2,P); integers(0,2,P) call that `gen`
-    makes next: build its d-array, read the rejection count (host waits on the
-    scan's stream only), check the scanned range covered the call (else scan
-    again exactly), and advance `gen` as numpy would."""
+def _enqueue_finish(scan, c, P):
+    """Enqueue skx_lemire_finish for a hash run starting at cursor `c` on the
+    scan's stream, plus a pinned copy of (count, #rejections among the P hash
+    draws) and an event marking both."""
     torch = _torch()
-    c = rngmod.cursor(gen)
     pend_raw = c.p - 1 if c.has else 0
     with torch.cuda.stream(scan.stream):
         d = torch.empty(scan.cap, dtype=torch.int64, device="cuda")
@@ -510,12 +511,28 @@ def finish_rrf_scan(scan, gen, P):
         nat.call_ws("skx_lemire_finish", (nat.ptr(scan.rej), nat.ptr(scan.count), scan.cap,
                                           ctypes.c_uint64(c.p), ctypes.c_uint32(c.has),
                                           ctypes.c_uint64(pend_raw), ctypes.c_uint64(P),
-                                          nat.ptr(d), nat.ptr(n_le)), slot=3)
+                                          nat.ptr(d), nat.ptr(n_le)), slot=3 + 8 * scan.tag)
         host = torch.empty(2, dtype=torch.int64, pin_memory=True)
         host[0:1].copy_(scan.count, non_blocking=True)
         host[1:2].copy_(n_le, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(scan.stream)
+    return (c.p, c.has, P), d, host, ev
+
+
+def finish_rrf_scan(scan, gen, P):
+    """Resolve `scan` for the integers(0,k2,P); integers(0,2,P) call that `gen`
+    makes next: build its d-array, read the rejection count (host waits on the
+    scan's stream only, and only up to this scan's finish if it was enqueued
+    with the scan), check the scanned range covered the call (else scan again
+    exactly), and advance `gen` as numpy would."""
+    torch = _torch()
+    c = rngmod.cursor(gen)
+    pend_raw = c.p - 1 if c.has else 0
+    fin = scan.pre if scan.pre is not None and scan.pre[0] == (c.p, c.has, P) else None
+    if fin is None:
+        fin = _enqueue_finish(scan, c, P)
+    _, d, host, ev = fin
     ev.synchronize()
     count, nrej = int(host[0]), int(host[1])
     need_hi = c.p + (P + nrej - c.has + 1) // 2  # raw words the hash run reads
@@ -555,9 +572,15 @@ def plan_rrf_scans(gen, jobs, stream=None):
     lo = c.p - 1 if c.has else c.p
     hi_start = c.p
     scans = []
-    for P, k2, n_gauss in jobs:
+    for i, (P, k2, n_gauss) in enumerate(jobs):
         cap = _rej_cap(P, k2)
-        scans.append(launch_rrf_scan(key, lo, hi_start + (P + cap) // 2 + 2, k2, cap, stream))
+        sc = launch_rrf_scan(key, lo, hi_start + (P + cap) // 2 + 2, k2, cap, stream)
+        sc.tag = i
+        if i == 0:
+            # the first draw's cursor is known now: its finish goes right behind
+            # its scan, so the host need not wait for the later scans
+            sc.pre = _enqueue_finish(sc, c, P)
+        scans.append(sc)
         # the next call starts after the hash + sign draws and the normals; a
         # buffered high half left by the integers() pair sits *before* the
         # normals, so the next scan starts there (>= lo + P - 2)

@@ -196,7 +196,9 @@ class _Run:
             comm.allreduce(n2)
         self.norm2 = n2[0]
         self.rng_init, self.rng_sketch, self.rng_solve = rngmod.split_rng(config.seed, 3)
-        self.normals = NormalSource(self.rng_solve)
+        # one sweep's Gaussian test matrices (rsvd_lrls: s_n x min(R_n + 10, s_n))
+        per_sweep = sum(s * min(r + 10, s) for s, r in zip(self.shape, self.ranks))
+        self.normals = NormalSource(self.rng_solve, batch=per_sweep)
         self.use_ts = config.sketch == "tensorsketch"
         self.factors = [None] * self.ndim
         self.ts_ops = [None] * self.ndim
@@ -220,8 +222,17 @@ class _Run:
                 self.factors[n] = random_orthonormal_dev(self.shape[n], self.ranks[n], self.rng_init)
             self.prep()
             return
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
+        caller = torch.cuda.current_stream()
+        # the compute-bound scans go to a normal-priority side stream in short
+        # CTAs; everything else runs on a high-priority stream, so the block
+        # scheduler gives the layout sorts and sketches the SMs first and the
+        # scans fill whatever is idle
+        lo_prio, hi_prio = torch.cuda.Stream.priority_range() if hasattr(
+            torch.cuda.Stream, "priority_range") else (0, -1)
+        side = torch.cuda.Stream(priority=lo_prio)
+        main = torch.cuda.Stream(priority=hi_prio)
+        side.wait_stream(caller)
+        main.wait_stream(caller)
         modes = list(range(1, self.ndim))
         dims = []
         for n in modes:
@@ -232,14 +243,17 @@ class _Run:
         # bracketed); they run on the side stream while the main stream builds
         # layouts and TensorSketch right-hand sides
         scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side)
-        if self.sparse:  # layouts first: RRF stage 1 and the TS sketches read them
-            for n in range(self.ndim):
-                self.d.fibre(n)
-        self.prep()
-        for n, scan, (P, k2, width) in zip(modes, scans, dims):
-            tabs = finish_rrf_scan(scan, self.rng_init, P)
-            gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
-            self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm)
+        with torch.cuda.stream(main):
+            if self.sparse:  # layouts first: RRF stage 1 and the TS sketches read them
+                for n in range(self.ndim):
+                    self.d.fibre(n)
+            self.prep()
+            for n, scan, (P, k2, width) in zip(modes, scans, dims):
+                tabs = finish_rrf_scan(scan, self.rng_init, P)
+                gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
+                self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm)
+        caller.wait_stream(main)
+        caller.wait_stream(side)
 
     def build_ts(self, n):
         ext = tuple(self.shape[k] for k in self.others(n))
