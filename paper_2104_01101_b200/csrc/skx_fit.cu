@@ -42,6 +42,78 @@ __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restr
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
+// ---- residual on the FP64 tensor cores.  pred = U Vt is formed 8 x 8 at a
+// time by mma.sync m8n8k4 (KS k-steps of 4 over R, zero padded): A fragment =
+// 8 rows of U (lane holds U[o0 + lane/4][4ks + lane%4]), B fragment = 8
+// columns of Vt (lane holds Vt[4ks + lane%4][x + lane/4]), accumulator lane
+// holds pred[o0 + lane/4][x + 2(lane%4) + {0,1}] -- exactly the 16 bytes of
+// Y it then loads.  A warp owns 8*NT columns (B fragments stay in registers)
+// and walks row groups of 8; a CTA is 4 warps side by side (32*NT columns).
+// grid = (ceil(n_in / (32*NT)), n_split).
+__device__ __forceinline__ void dmma884r(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int KS, int NT>
+__global__ void __launch_bounds__(128) k_resid_mma(const double* __restrict__ U,
+                                                   const double* __restrict__ Vt, int64_t n_out,
+                                                   int64_t n_in, int R, const double* __restrict__ y,
+                                                   int64_t ld, double* __restrict__ part) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane >> 2, c = lane & 3;
+  const int64_t xw = (blockIdx.x * 4 + wid) * (int64_t)(8 * NT);  // first column of the warp
+  double b[NT][KS];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int64_t x = xw + nt * 8 + q;
+      const int r = ks * 4 + c;
+      b[nt][ks] = (x < n_in && r < R) ? __ldg(Vt + (int64_t)r * n_in + x) : 0.0;
+    }
+  const bool vec = (ld & 1) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+  const int64_t per = (((n_out + gridDim.y - 1) / gridDim.y) + 7) & ~int64_t(7);
+  const int64_t oa = imin(blockIdx.y * per, n_out), ob = imin(oa + per, n_out);
+  double acc = 0.0;
+  for (int64_t o0 = oa; o0 < ob; o0 += 8) {
+    const int64_t o = o0 + q;
+    const bool rok = o < ob;
+    double a[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int r = ks * 4 + c;
+      a[ks] = (rok && r < R) ? __ldg(U + o * R + r) : 0.0;
+    }
+    double yv[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int64_t x = xw + nt * 8 + 2 * c;
+      const double* yp = y + o * ld + x;
+      if (vec && rok && x + 1 < n_in) {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(yp));
+        yv[nt][0] = t.x;
+        yv[nt][1] = t.y;
+      } else {
+        yv[nt][0] = (rok && x < n_in) ? __ldcs(yp) : 0.0;
+        yv[nt][1] = (rok && x + 1 < n_in) ? __ldcs(yp + 1) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) dmma884r(d0, d1, a[ks], b[nt][ks]);
+      // padded rows/columns: pred = 0 and y = 0
+      const double e0 = d0 - yv[nt][0], e1 = d1 - yv[nt][1];
+      acc = fma(e0, e0, acc);
+      acc = fma(e1, e1, acc);
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = acc;
+}
+
 // sum_{o,x} (sum_r U[o,r] Vt[r,x] - Y[o*ld + x])^2 -- Y's unit-stride index x
 // is the inner one.  A CTA takes TO outer rows at a time (their U rows staged in
 // shared memory) and sweeps x: the R values Vt[:, x] are loaded once into
@@ -436,29 +508,32 @@ extern "C" int skx_resid_sq(const double* u, const double* vt, int64_t n_out, in
   cudaStream_t st = (cudaStream_t)stream;
   double* part = (double*)ws;
   const int r = (int)R;
-  // (x-blocks) x (row splits) <= kRedBlocks CTAs, fixed for given shapes
-  const int64_t xb = (n_in + kRedThreads - 1) / kRedThreads;
-  const int64_t ys = imax(1, imin(kRedBlocks / imax(xb, 1), (n_out + 15) / 16));
-  dim3 grid((unsigned)xb, (unsigned)ys);
-  int nparts = (int)(xb * ys);
-  if (xb > kRedBlocks) {
-    k_resid_gen<<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-    nparts = kRedBlocks;
-  } else if (R <= 4)
-    k_resid<4, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 8)
-    k_resid<8, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 10)
-    k_resid<10, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 16)
-    k_resid<16, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 20)
-    k_resid<20, 12><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else if (R <= 32)
-    k_resid<32, 8><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-  else {
-    k_resid_gen<<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
-    nparts = kRedBlocks;
+  int nparts = 0;
+  if (R >= 5 && R <= 32) {
+    // 4 warps x 8*NT columns per CTA (NT = 4 up to 3 k-steps, else 2: fewer
+    // registers, more rows in flight); row splits so that CTAs <= kRedBlocks
+    const int KS = (int)((R + 3) / 4);
+    const int NT = KS <= 3 ? 4 : 2;
+    const int64_t xb = (n_in + 32 * NT - 1) / (32 * NT);
+    const int64_t ys = imax(1, imin(kRedBlocks / imax(xb, 1), (n_out + 63) / 64));
+    dim3 grid((unsigned)xb, (unsigned)ys);
+    nparts = (int)(xb * ys);
+#define SKX_RM(ks, nt)                                                                       \
+  if (KS == ks) k_resid_mma<ks, nt><<<grid, 128, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+    SKX_RM(2, 4) SKX_RM(3, 4) SKX_RM(4, 2) SKX_RM(5, 2) SKX_RM(6, 2) SKX_RM(7, 2) SKX_RM(8, 2)
+#undef SKX_RM
+  } else {
+    // (x-blocks) x (row splits) <= kRedBlocks CTAs, fixed for given shapes
+    const int64_t xb = (n_in + kRedThreads - 1) / kRedThreads;
+    const int64_t ys = imax(1, imin(kRedBlocks / imax(xb, 1), (n_out + 15) / 16));
+    dim3 grid((unsigned)xb, (unsigned)ys);
+    nparts = (int)(xb * ys);
+    if (xb > kRedBlocks || R > 32) {
+      k_resid_gen<<<kRedBlocks, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+      nparts = kRedBlocks;
+    } else {
+      k_resid<4, 16><<<grid, kRedThreads, 0, st>>>(u, vt, n_out, n_in, r, y, ld, part);
+    }
   }
   k_final_sum<<<1, 1024, 0, st>>>(part, nparts, out);
   return check_launch("skx_resid_sq", 2);

@@ -89,6 +89,106 @@ __global__ void __launch_bounds__(kTsqrThreads) k_tsqr_block(const double* __res
   }
 }
 
+// ---- register variant for w <= WP <= 32: thread t of the CTA holds row t of
+// the 256-row tile in registers; the step loop is unrolled (k is a compile-
+// time index into the row), so the only shared-memory traffic is the three
+// block reductions per reflector: ||x||^2 below the diagonal, the vector of
+// dot products v^T A[:, k+1:] (warp butterfly reduce-scatter, then a fixed-
+// order sum over the warps) and its broadcast.  Same reflector conventions
+// (dlarfg) as k_tsqr_block, hence the same R up to rounding.
+constexpr int kTsqrRows = 256;
+
+// Butterfly reduce-scatter of NP-vectors (NP a power of two <= 32) over the
+// warp: afterwards lane l holds the warp sum of component l % NP.  Stage h
+// exchanges the half of the live block the partner keeps: NP - 1 shuffles,
+// then 32/NP - 1 more to add the lane groups.
+template <int NP>
+__device__ __forceinline__ double warp_reduce_scatter(double (&p)[NP], int lane) {
+#pragma unroll
+  for (int h = NP / 2; h >= 1; h >>= 1) {
+    const bool upper = (lane & h) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = upper ? p[i] : p[i + h];
+      const double keep = upper ? p[i + h] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  double r = p[0];
+#pragma unroll
+  for (int h = NP; h < 32; h <<= 1) r += __shfl_xor_sync(0xffffffffu, r, h);
+  return r;
+}
+
+template <int WP>
+__global__ void __launch_bounds__(kTsqrRows) k_tsqr_reg(const double* __restrict__ A, int64_t n,
+                                                      int w, int64_t rs, int64_t cs,
+                                                      double* __restrict__ Rout) {
+  __shared__ double red[kTsqrRows / 32][33];
+  __shared__ double dv[32];
+  __shared__ double s_x0;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  constexpr int NW = kTsqrRows / 32;
+  const int64_t r0 = blockIdx.x * (int64_t)kTsqrRows;
+  const int rows = (int)imin(kTsqrRows, n - r0);
+  double a[WP];
+#pragma unroll
+  for (int j = 0; j < WP; ++j)
+    a[j] = (t < rows && j < w) ? A[(r0 + t) * rs + (int64_t)j * cs] : 0.0;
+  const int kmax = min(rows, w);
+#pragma unroll
+  for (int k = 0; k < WP; ++k) {
+    if (k >= kmax) break;
+    // ---- dlarfg on column k, rows k..rows-1
+    double sq = t > k ? a[k] * a[k] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) red[wid][32] = sq;
+    if (t == k) s_x0 = a[k];
+    __syncthreads();
+    double sg = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) sg += red[q][32];
+    const double x0 = s_x0;
+    double tau = 0.0, beta = x0;
+    if (sg != 0.0) {
+      const double nrm = sqrt(fma(x0, x0, sg));
+      beta = x0 >= 0.0 ? -nrm : nrm;
+      tau = (beta - x0) / beta;
+    }
+    if (tau != 0.0) {
+      const double scale = 1.0 / (x0 - beta);
+      const double v = t > k ? a[k] * scale : (t == k ? 1.0 : 0.0);
+      // ---- d_j = sum_t v_t a_t[j], j > k
+      constexpr int NP = WP <= 8 ? 8 : WP <= 16 ? 16 : 32;
+      double p[NP];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) p[j] = (j > k && j < WP) ? v * a[j] : 0.0;
+      const double rsum = warp_reduce_scatter<NP>(p, lane);
+      if (lane < NP) red[wid][lane] = rsum;
+      __syncthreads();
+      if (t < NP) {
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) d += red[q][t];
+        dv[t] = tau * d;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = k + 1; j < WP; ++j) a[j] = fma(-dv[j], v, a[j]);
+    }
+    if (t == k) a[k] = beta;
+    else if (t > k) a[k] = 0.0;
+    __syncthreads();  // red / s_x0 reuse in the next step
+  }
+  double* R = Rout + (int64_t)blockIdx.x * w * w;
+  if (t < w) {
+#pragma unroll
+    for (int j = 0; j < WP; ++j)
+      if (j < w) R[(int64_t)t * w + j] = (j >= t && t < rows) ? a[j] : 0.0;
+  }
+}
+
 }  // namespace skx
 
 using namespace skx;
@@ -97,7 +197,7 @@ extern "C" int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t
                           void* ws, size_t* ws_bytes, void* stream) {
   SKX_REQUIRE(w >= 1 && w <= 64, "skx_tsqr_r: 1 <= w <= 64 columns supported");
   SKX_REQUIRE(ws_bytes != nullptr, "skx_tsqr_r: ws_bytes is NULL");
-  const int BR = w <= 32 ? 256 : 128;
+  const int BR = w <= 32 ? kTsqrRows : 128;
   // level sizes
   int64_t rows = n, total = 0;
   int levels = 0;
@@ -116,9 +216,14 @@ extern "C" int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t
   }
   SKX_REQUIRE(ar.ok(), "skx_tsqr_r: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t smem = (size_t)w * (BR + 1) * sizeof(double);
-  auto kern = BR == 256 ? k_tsqr_block<256> : k_tsqr_block<128>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  size_t smem = (size_t)w * (BR + 1) * sizeof(double);
+  using KF = void (*)(const double*, int64_t, int, int64_t, int64_t, double*);
+  KF kern = k_tsqr_block<128>;
+  if (w <= 8) kern = k_tsqr_reg<8>, smem = 0;
+  else if (w <= 16) kern = k_tsqr_reg<16>, smem = 0;
+  else if (w <= 24) kern = k_tsqr_reg<24>, smem = 0;
+  else if (w <= 32) kern = k_tsqr_reg<32>, smem = 0;
+  if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const double* src = a;
   int64_t srs = rs, scs = cs;
   rows = n;

@@ -171,6 +171,21 @@ def random_orthonormal_dev(n_rows, n_cols, gen):
 
 
 # ------------------------------------------------------------------ driver
+_STREAMS = {}
+
+
+def _init_streams():
+    """(normal-priority, high-priority) streams for the initialisation, created
+    once per device: the caching allocator keys free blocks by stream, so
+    fresh streams every run would defeat reuse of the large layout buffers."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _STREAMS:
+        lo, hi = torch.cuda.Stream.priority_range()
+        _STREAMS[dev] = (torch.cuda.Stream(priority=lo), torch.cuda.Stream(priority=hi))
+    return _STREAMS[dev]
+
+
 class _Run:
     """Device state of one sketched_tucker_als call."""
 
@@ -227,10 +242,7 @@ class _Run:
         # CTAs; everything else runs on a high-priority stream, so the block
         # scheduler gives the layout sorts and sketches the SMs first and the
         # scans fill whatever is idle
-        lo_prio, hi_prio = torch.cuda.Stream.priority_range() if hasattr(
-            torch.cuda.Stream, "priority_range") else (0, -1)
-        side = torch.cuda.Stream(priority=lo_prio)
-        main = torch.cuda.Stream(priority=hi_prio)
+        side, main = _init_streams()
         side.wait_stream(caller)
         main.wait_stream(caller)
         modes = list(range(1, self.ndim))

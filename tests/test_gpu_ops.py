@@ -142,16 +142,28 @@ def test_fitness(golden, skx):
     assert skx.fitness(st, skx.CPModel(cpf, w)) == pytest.approx(float(golden["fitcp_sparse"]), abs=1e-13)
 
 
-@pytest.mark.parametrize("n,w", [(1, 1), (7, 5), (256, 20), (257, 20), (100_000, 20), (3000, 33),
-                                 (50_000, 64)])
+@pytest.mark.parametrize("n,w", [(1, 1), (2, 2), (7, 5), (31, 31), (256, 20), (257, 20), (300, 8),
+                                 (600, 13), (5000, 16), (9000, 24), (70_000, 32), (100_000, 20),
+                                 (3000, 33), (50_000, 64), (1000, -10)])
 def test_tsqr_r_matches_lapack(n, w):
     import torch
     from paper_2104_01101_b200.linalg import tsqr_r_dev
+    deficient = w < 0
+    w = abs(w)
     a = np.random.default_rng(n + w).standard_normal((n, w))
+    if deficient:  # zero column and a repeated column: reflectors with tau = 0
+        a[:, 3] = 0.0
+        a[:, 5] = a[:, 2]
     if n < w:
         return
     r = tsqr_r_dev(torch.from_numpy(a).cuda()).cpu().numpy()
     ref = np.linalg.qr(a, mode="r")
+    if deficient:
+        # R is not unique past a dependent column (the reflector there is built
+        # from rounding noise); check it is an R factor: R^T R = A^T A
+        assert np.allclose(r.T @ r, a.T @ a, rtol=0, atol=1e-10 * np.abs(a.T @ a).max())
+        assert r[3, 3] == 0.0 and np.allclose(np.triu(r), r)
+        return
     assert relerr(np.abs(r), np.abs(ref)) <= 1e-12
     # strided (transposed) input
     rt = tsqr_r_dev(torch.from_numpy(a.T.copy()).cuda().t()).cpu().numpy()
@@ -359,3 +371,31 @@ def test_sparse_fitness_order3_and_generic(skx, oracle):
         got = skx.fitness(st, skx.TuckerModel(core, A))
         exp = oracle.fitness_tucker(oc, core, A)
         assert got == pytest.approx(exp, rel=1e-11, abs=1e-12)
+
+
+@pytest.mark.parametrize("R", [1, 4, 5, 8, 10, 13, 20, 32, 40])
+@pytest.mark.parametrize("orient", ["yt", "rowmajor", "odd_ld"])
+def test_resid_pass(R, orient):
+    """|| Z C A^T - Y ||_F of the rank-constrained solve (src/tucker.py:274) on
+    every kernel path: tensor-core tiles (5 <= R <= 32), SIMT (R <= 4), generic
+    (R > 32); ragged row/column counts and both storage orders of Y."""
+    import torch
+    from paper_2104_01101_b200.linalg import resid_dev
+    rng = np.random.default_rng(R)
+    m, s, r2 = 203, 1037, 24
+    z = rng.standard_normal((m, r2))
+    c = rng.standard_normal((r2, R))
+    a = rng.standard_normal((s, R))
+    y = z @ c @ a.T + 0.1 * rng.standard_normal((m, s))
+    if orient == "yt":        # Y^T stored (s, m) row-major, as the sketches produce it
+        yd = torch.from_numpy(y.T.copy()).cuda().t()
+    elif orient == "rowmajor":
+        yd = torch.from_numpy(y).cuda()
+    else:                     # odd leading dimension (unaligned rows)
+        buf = torch.from_numpy(np.zeros((s, m + 1))).cuda()
+        buf[:, :m] = torch.from_numpy(y.T.copy()).cuda()
+        yd = buf[:, :m].t()
+    got = float(resid_dev(torch.from_numpy(z).cuda(), torch.from_numpy(c).cuda(),
+                          torch.from_numpy(a).cuda(), yd))
+    exp = np.linalg.norm(z @ c @ a.T - y)
+    assert got == pytest.approx(exp, rel=1e-12)
