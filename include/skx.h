@@ -91,13 +91,28 @@ int skx_coo_fibre(int ndim, const int64_t* shape_h, int mode, int64_t nnz, const
                   const double* vals, void* rec_out, int64_t* colptr, void* ws, size_t* ws_bytes,
                   void* stream);
 
+/* Same layout for an order-3 tensor, with mode `mode`'s TensorSketch bucket
+ * and sign folded into each record (tab/tab_off_h/m as skx_ts_rhs_coo): the
+ * second coordinate word holds c1 | bucket << bb | neg << 31 with
+ * bb = ceil(log2 s_b) of the second other mode.  *c1_mask (host) receives
+ * (1 << bb) - 1, the mask every consumer applies to recover c1.  Fails with 1
+ * (invalid argument) when bb + ceil(log2 m) > 31. */
+int skx_coo_fibre_ts(const int64_t* shape_h, int mode, int64_t nnz, const int32_t* coords,
+                     const double* vals, const uint32_t* tab, const int64_t* tab_off_h,
+                     int64_t m, void* rec_out, int64_t* colptr, uint32_t* c1_mask, void* ws,
+                     size_t* ws_bytes, void* stream);
+
 /* Y^T = (S . T_(n)^T)^T for a COO tensor in the fibre-major layout of mode n
  * (skx_coo_fibre); tab = packed tables of the other modes concatenated,
- * tab_off_h offsets.  yt is s_n x m (row i_n = column i_n of the reference's
- * m x s_n output).  Replaces ts_apply_rhs sparse branch, src/sketching.py:150-167. */
+ * tab_off_h offsets; c1_mask recovers the last other coordinate (0xffffffff
+ * for skx_coo_fibre layouts).  packed_bb >= 0: the layout came from
+ * skx_coo_fibre_ts with THIS operator's tables and carries bucket/sign above
+ * bit packed_bb (tab unused).  yt is s_n x m (row i_n = column i_n of the
+ * reference's m x s_n output).  Replaces ts_apply_rhs sparse branch,
+ * src/sketching.py:150-167. */
 int skx_ts_rhs_coo(int n_other, int64_t s_n, const int64_t* colptr, const void* rec,
-                   const uint32_t* tab, const int64_t* tab_off_h, int64_t m, double* yt,
-                   void* stream);
+                   const uint32_t* tab, const int64_t* tab_off_h, int64_t m, uint32_t c1_mask,
+                   int packed_bb, double* yt, void* stream);
 
 /* Same for a dense C-order tensor (ndim, shape_h) and target mode.
  * Replaces ts_apply_rhs dense branch, src/sketching.py:168-175. */
@@ -174,8 +189,8 @@ int skx_gather_fibers_coo(int n_other, const int64_t* ext_h, int64_t s_n, int64_
 int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n, const int64_t* colptr,
                        const void* rec, uint64_t k0, uint64_t k1, uint64_t p0,
                        uint32_t has_pending, uint32_t pending, uint64_t sign_q0,
-                       const uint64_t* rej, int64_t nrej, int64_t k2, double* stage1,
-                       void* stream);
+                       const uint64_t* rej, int64_t nrej, int64_t k2, uint32_t c1_mask,
+                       double* stage1, void* stream);
 
 /* Fill n u64 with UINT64_MAX (pre-fill of a rejection buffer). */
 int skx_fill_u64max(uint64_t* a, int64_t n, void* stream);
@@ -236,13 +251,14 @@ int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_byte
 /* Tucker cross term <ttmc(T,{A}), C> over a lexsorted COO tensor (coords =
  * ndim x nnz SoA int32), factors_h device pointers (s_k x R_k), core C
  * (C-order R_0 x ... x R_{N-1}); colptr0/rec0 (the mode-0 fibre-major layout,
- * may be NULL) enable the order-3 sliced kernel.  out[0] = cross.
+ * may be NULL; c1_mask as skx_ts_rhs_coo) enable the order-3 sliced kernel.
+ * out[0] = cross.
  * Replaces the sparse ttmc + vdot at src/tensors.py:249-258, 351-352. */
 int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h,
                          int64_t nnz, const int32_t* coords, const double* vals,
                          const double* const* factors_h, const double* core,
-                         const int64_t* colptr0, const void* rec0, double* out, void* ws,
-                         size_t* ws_bytes, void* stream);
+                         const int64_t* colptr0, const void* rec0, uint32_t c1_mask, double* out,
+                         void* ws, size_t* ws_bytes, void* stream);
 
 /* CP cross term sum(weights * A_0 .* mttkrp(T, A, 0)) over lexsorted COO.
  * Replaces src/tensors.py:354-357 (+ mttkrp :322-323). */

@@ -32,7 +32,9 @@ _SIGS = {
     "skx_ts_tables": [c_i32, c_p, c_p, c_i64, c_p, c_p],
     "skx_coo_rec_words": [c_i32],
     "skx_coo_fibre": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
-    "skx_ts_rhs_coo": [c_i32, c_i64, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
+    "skx_coo_fibre_ts": [c_p, c_i32, c_i64, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_sz_p,
+                         c_p],
+    "skx_ts_rhs_coo": [c_i32, c_i64, c_p, c_p, c_p, c_p, c_i64, c_u32, c_i32, c_p, c_p],
     "skx_ts_rhs_dense": [c_p, c_i32, c_p, c_i32, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_ts_combine": [c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_p],
     "skx_ts_kron_plan": [c_i32, c_p, c_p, c_p, c_i64, c_p, c_sz_p, c_p, c_sz_p, c_p],
@@ -44,7 +46,7 @@ _SIGS = {
     "skx_gather_fibers_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p,
                               c_i64, c_p, c_sz_p, c_p],
     "skx_rrf_stage1_coo": [c_i32, c_p, c_i64, c_p, c_p, c_u64, c_u64, c_u64, c_u32, c_u32, c_u64,
-                           c_p, c_i64, c_i64, c_p, c_p],
+                           c_p, c_i64, c_i64, c_u32, c_p, c_p],
     "skx_rrf_table": [c_u64, c_u64, c_u64, c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_i64, c_p, c_p],
     "skx_rrf_stage1_dense": [c_p, c_i32, c_p, c_i32, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
@@ -52,8 +54,8 @@ _SIGS = {
     "skx_tsqr_r": [c_p, c_i64, c_i32, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_chol_upper": [c_p, c_i32, c_p, c_p, c_p],
     "skx_jacobi_svd": [c_p, c_i32, c_i64, c_i64, c_p, c_p, c_p, c_p],
-    "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p,
-                             c_p],
+    "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_u32, c_p, c_p,
+                             c_sz_p, c_p],
     "skx_cp_cross_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],

@@ -65,6 +65,30 @@ inline int max_smem_optin() {
   return n;
 }
 
+inline int max_smem_sm() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (n <= 0) n = 228 * 1024;
+  }
+  return n;
+}
+
+// Warps per CTA (<= 8) maximising resident warps per SM when every warp needs
+// `per_warp` bytes of shared memory (1 KB per CTA is reserved by the driver).
+inline int warps_per_cta_for(int64_t per_warp) {
+  int best = 0, best_nw = 0;
+  for (int nw = 1; nw <= 8; ++nw) {
+    const int64_t cta = nw * per_warp;
+    if (cta > max_smem_optin()) break;
+    const int ctas = (int)(max_smem_sm() / (cta + 1024));
+    if (ctas * nw > best) best = ctas * nw, best_nw = nw;
+  }
+  return best_nw;
+}
+
 // Bump-allocator over a caller-provided workspace (no hidden allocations).
 struct Arena {
   char* base;
@@ -167,33 +191,53 @@ __device__ __forceinline__ uint32_t pk_neg(uint32_t e) { return e >> 31; }
 // vector: lanes holding the same bucket are summed in lane order by the lowest
 // lane of the group, which then performs the only write to that bucket.
 // Every lane must call this (full-warp convergent); inactive lanes pass
-// bucket = 0xffffffff.
-// The leader adds the group's values one by one in lane order, so a bucket
-// receives exactly the sequential sum acc + v_l0 + v_l1 + ... (the order
-// numpy's ufunc.at uses when lanes carry consecutive elements).
+// kNoBucket.
+//
+// Duplicate detection: match_any costs ~375 cycles of latency and ~62 SM
+// cycles of issue per call on B200 when the 32 values are distinct (measured;
+// ~2 cycles when they are equal), so with `tags` (one byte per bucket,
+// warp-private, contents irrelevant between calls) every lane first stores
+// its lane id at tags[bucket] and reads it back: if no lane sees a foreign id
+// the buckets are distinct and each lane adds directly; only slices with a
+// real duplicate pay for match_any.
 constexpr uint32_t kNoBucket = 0xffffffffu;
 
+__device__ __forceinline__ void warp_ordered_add_slow(double* acc, uint32_t bucket, double val,
+                                                      double* stage) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(0xffffffffu, bucket);
+  stage[lane] = val;
+  __syncwarp();
+  if (lane == (unsigned)(__ffs(peers) - 1) && bucket != kNoBucket) {
+    double s = acc[bucket];
+    unsigned mask = peers;
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      s += stage[l];
+      mask &= mask - 1;
+    }
+    acc[bucket] = s;
+  }
+}
+
 __device__ __forceinline__ void warp_ordered_add(double* acc, uint32_t bucket, double val,
-                                                 double* stage) {
+                                                 double* stage, uint8_t* tags = nullptr) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
-  unsigned peers = __match_any_sync(full, bucket);
-  const bool solo = peers == (1u << lane) || bucket == kNoBucket;
-  if (__all_sync(full, solo)) {
-    if (bucket != kNoBucket) acc[bucket] += val;
-  } else {
-    stage[lane] = val;
+  const bool has = bucket != kNoBucket;
+  bool distinct;
+  if (tags != nullptr) {
+    if (has) tags[bucket] = (uint8_t)lane;
     __syncwarp();
-    if (lane == (unsigned)(__ffs(peers) - 1) && bucket != kNoBucket) {
-      double s = acc[bucket];
-      unsigned mask = peers;
-      while (mask) {
-        int l = __ffs(mask) - 1;
-        s += stage[l];
-        mask &= mask - 1;
-      }
-      acc[bucket] = s;
-    }
+    distinct = !__any_sync(full, has && tags[bucket] != (uint8_t)lane);
+  } else {
+    const unsigned peers = __match_any_sync(full, bucket);
+    distinct = __all_sync(full, peers == (1u << lane) || !has);
+  }
+  if (distinct) {
+    if (has) acc[bucket] += val;
+  } else {
+    warp_ordered_add_slow(acc, bucket, val, stage);
   }
   __syncwarp();
 }

@@ -193,7 +193,7 @@ __global__ void k_resid_gen(const double* __restrict__ U, const double* __restri
 // read as 16-byte broadcasts shared by the NP nonzeros), t = v . A2[i2,:].
 template <int RT, int NP>
 __global__ void __launch_bounds__(128) k_tucker3(const int64_t* __restrict__ colptr, int64_t s0,
-                                                 const double* __restrict__ rec,
+                                                 const double* __restrict__ rec, uint32_t c1_mask,
                                                  const double* __restrict__ A0,
                                                  const double* __restrict__ A1,
                                                  const double* __restrict__ A2,
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(128) k_tucker3(const int64_t* __restrict__ col
         double xv;
         load_rec<2>(rec, ok ? e : e0, c, xv);
         i1[u] = c[0];
-        i2[u] = c[1];
+        i2[u] = (int)((uint32_t)c[1] & c1_mask);
         x[u] = ok ? xv : 0.0;
       }
 #pragma unroll
@@ -321,7 +321,7 @@ struct T3Rows {
 // time (predicates fold away); 0 reads them at run time.
 template <int KS, int NT, int G, int R1T, int R2T>
 __global__ void __launch_bounds__(256, SKX_T3_MINB) k_tucker3_mma(const int64_t* __restrict__ colptr, int64_t s0,
-                                                     const double* __restrict__ rec,
+                                                     const double* __restrict__ rec, uint32_t c1_mask,
                                                      const double* __restrict__ A0,
                                                      const double* __restrict__ A1,
                                                      const double* __restrict__ A2,
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(256, SKX_T3_MINB) k_tucker3_mma(const int64_t*
         double xv;
         load_rec<2>(rec, ok ? e : e0, cc, xv);
         r.i1[g] = cc[0];
-        r.i2[g] = cc[1];
+        r.i2[g] = (int32_t)((uint32_t)cc[1] & c1_mask);
         r.v[g] = ok ? xv : 0.0;
       }
     };
@@ -542,8 +542,8 @@ extern "C" int skx_resid_sq(const double* u, const double* vt, int64_t n_out, in
 extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h,
                                     int64_t nnz, const int32_t* coords, const double* vals,
                                     const double* const* factors_h, const double* core,
-                                    const int64_t* colptr0, const void* rec0, double* out, void* ws,
-                                    size_t* ws_bytes, void* stream) {
+                                    const int64_t* colptr0, const void* rec0, uint32_t c1_mask,
+                                    double* out, void* ws, size_t* ws_bytes, void* stream) {
   SKX_REQUIRE(ndim >= 1 && ndim <= 8, "skx_tucker_cross_coo: order 1..8");
   SKX_REQUIRE(ws_bytes != nullptr, "skx_tucker_cross_coo: ws_bytes is NULL");
   cudaStream_t s = (cudaStream_t)stream;
@@ -574,7 +574,7 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
     const size_t sm = (size_t)4 * (RT * RT + 2 * 32 * NP * (RT + 1) + 2) * 8;             \
     cudaFuncSetAttribute(k_tucker3<RT, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                          (int)sm);                                                        \
-    k_tucker3<RT, NP><<<blocks, 128, sm, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0, R1,  \
+    k_tucker3<RT, NP><<<blocks, 128, sm, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, R0, R1,  \
                                               R2, part);                                  \
   } while (0)
     // ranks <= 4: too little work per row for the 8x8x4 tiles (SIMT kernel is faster)
@@ -591,14 +591,14 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
       const unsigned mb = (unsigned)imin((s0 + 7) / 8, (int64_t)num_sms() * 8);
 #define SKX_T3M(ks, nt)                                                                    \
   if (KS <= ks && NT == nt) {                                                              \
-    k_tucker3_mma<ks, nt, 2, 0, 0><<<mb, 256, 0, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0, \
+    k_tucker3_mma<ks, nt, 2, 0, 0><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, R0, \
                                                      R1, R2, part);                         \
   } else
       if (R1 == 10 && R2 == 10) {
-        k_tucker3_mma<3, 2, 2, 10, 10><<<mb, 256, 0, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0,
+        k_tucker3_mma<3, 2, 2, 10, 10><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, R0,
                                                          R1, R2, part);
       } else if (R1 == 20 && R2 == 20) {
-        k_tucker3_mma<5, 3, 2, 20, 20><<<mb, 256, 0, s>>>(colptr0, s0, rec, A0, A1, A2, core, R0,
+        k_tucker3_mma<5, 3, 2, 20, 20><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, R0,
                                                          R1, R2, part);
       } else
       SKX_T3M(2, 1) SKX_T3M(3, 1) SKX_T3M(5, 1) SKX_T3M(8, 1)

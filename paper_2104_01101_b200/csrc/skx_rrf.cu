@@ -83,10 +83,12 @@ struct OthExt {
   int64_t ext[15];
 };
 
+// c1_mask: the last other coordinate is rec word & c1_mask (layouts from
+// skx_coo_fibre_ts keep sketch bits above it).
 template <int U, int NO>
 __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t s_n,
                                                  const int64_t* __restrict__ colptr,
-                                                 const double* __restrict__ rec,
+                                                 const double* __restrict__ rec, uint32_t c1_mask,
                                                  double* __restrict__ st1) {
   extern __shared__ double smem[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,7 +116,9 @@ __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t s_
         const bool ok = base + u * 32 + lane < e1;
         uint64_t j = 0;
 #pragma unroll
-        for (int k = 0; k < NO; ++k) j = j * (uint64_t)oe.ext[k] + (uint64_t)c[u][k];
+        for (int k = 0; k < NO; ++k)
+          j = j * (uint64_t)oe.ext[k] +
+              (uint64_t)((uint32_t)c[u][k] & (k == NO - 1 ? c1_mask : 0xffffffffu));
         const uint32_t t = rrf_entry(r, j);
         bk[u] = ok ? pk_bucket(t) : kNoBucket;
         v[u] = pk_neg(t) ? -v[u] : v[u];
@@ -195,7 +199,7 @@ extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n
                                   const int64_t* colptr, const void* rec, uint64_t k0, uint64_t k1,
                                   uint64_t p0, uint32_t has_pending, uint32_t pending,
                                   uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
-                                  double* stage1, void* stream) {
+                                  uint32_t c1_mask, double* stage1, void* stream) {
   SKX_REQUIRE(n_other >= 1 && n_other <= 4, "skx_rrf_stage1_coo: 1..4 other modes");
   const int64_t per = (k2 + 32) * 8;
   int nw = (int)imin(8, (int64_t)(max_smem_optin() - 1024) / per);
@@ -215,7 +219,7 @@ extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t blocks = imin((int64_t)num_sms() * per_sm, (s_n + nw - 1) / nw);
-  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(r, oe, s_n, colptr,
-                                                                  (const double*)rec, stage1);
+  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(
+      r, oe, s_n, colptr, (const double*)rec, c1_mask, stage1);
   return check_launch("k_rrf_coo");
 }

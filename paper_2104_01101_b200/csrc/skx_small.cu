@@ -56,6 +56,75 @@ __global__ void __launch_bounds__(512) k_chol(const double* __restrict__ G, int 
   if (threadIdx.x == 0) *info = bad;
 }
 
+// Register variant (n <= 128): the lower triangle is split over 1024 threads,
+// entry e = t + 1024 q (q < EPT) in column-major packed order, values in
+// registers.  Step k reads column k (left unscaled) from a double-buffered
+// shared column, updates the owned entries right of it with
+// a_ij -= c_i c_j / c_k, and the owners of column k+1 publish it for the next
+// step: one barrier per step.  R row k = c / sqrt(c_k) is written as column k
+// retires.  Same arithmetic as the textbook right-looking algorithm.
+constexpr int kCholThreads = 1024;
+constexpr int kCholEpt = 9;  // ceil(128 * 129 / 2 / 1024)
+
+__global__ void __launch_bounds__(kCholThreads) k_chol_reg(const double* __restrict__ G, int n,
+                                                           double* __restrict__ R,
+                                                           int* __restrict__ info) {
+  __shared__ double col[2][128];
+  const int t = threadIdx.x;
+  const int E = n * (n + 1) / 2;
+  double a[kCholEpt];
+  int ij[kCholEpt];  // i | j << 16
+#pragma unroll
+  for (int q = 0; q < kCholEpt; ++q) {
+    const int e = t + kCholThreads * q;
+    int i = 0, j = 0;
+    if (e < E) {
+      // column-major packed lower triangle: column j holds rows j..n-1, starts
+      // at s_j = j n - j (j - 1) / 2
+      j = (int)((2.0 * n + 1.0 - sqrt((2.0 * n + 1.0) * (2.0 * n + 1.0) - 8.0 * e)) * 0.5);
+      while (j > 0 && j * n - j * (j - 1) / 2 > e) --j;
+      while ((j + 1) * n - (j + 1) * j / 2 <= e) ++j;
+      i = j + (e - (j * n - j * (j - 1) / 2));
+      a[q] = G[(int64_t)i * n + j];
+    } else {
+      j = n;  // never active
+      a[q] = 0.0;
+    }
+    ij[q] = i | (j << 16);
+  }
+  for (int q = t; q < n * n; q += kCholThreads) R[q] = 0.0;  // lower part stays zero
+#pragma unroll
+  for (int q = 0; q < kCholEpt; ++q)
+    if ((ij[q] >> 16) == 0) col[0][ij[q] & 0xffff] = a[q];
+  __syncthreads();
+  int bad = 0;
+  for (int k = 0; k < n; ++k) {
+    const double* ck = col[k & 1];
+    double* cn = col[(k + 1) & 1];
+    const double piv = ck[k];
+    if (!(piv > 0.0)) {  // uniform: every thread reads the same pivot
+      bad = k + 1;
+      break;
+    }
+    const double rp = 1.0 / piv, sq = sqrt(piv), rs = 1.0 / sq;
+#pragma unroll
+    for (int q = 0; q < kCholEpt; ++q) {
+      const int i = ij[q] & 0xffff, j = ij[q] >> 16;
+      if (j == k) {
+        R[(int64_t)k * n + i] = i == k ? sq : a[q] * rs;
+      } else if (j > k && j < n) {
+        a[q] = fma(-ck[i] * ck[j], rp, a[q]);
+        if (j == k + 1) cn[i] = a[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    for (int q = t; q < n * n; q += kCholThreads) R[q] = 0.0;
+  }
+  if (t == 0) *info = bad;
+}
+
 // One-sided Jacobi: columns of A (n x n, shared, column-major) are rotated
 // pairwise (round-robin tournament, n/2 disjoint pairs per step, one warp per
 // pair) until every pair is orthogonal to eps relative; W accumulates the
@@ -170,10 +239,8 @@ using namespace skx;
 
 extern "C" int skx_chol_upper(const double* g, int n, double* r, int* info, void* stream) {
   SKX_REQUIRE(n >= 1 && n <= 128, "skx_chol_upper: 1 <= n <= 128");
-  const size_t smem = (size_t)n * (n | 1) * 8;
-  cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_chol<<<1, 512, smem, (cudaStream_t)stream>>>(g, n, r, info);
-  return check_launch("k_chol");
+  k_chol_reg<<<1, kCholThreads, 0, (cudaStream_t)stream>>>(g, n, r, info);
+  return check_launch("k_chol_reg");
 }
 
 extern "C" int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u,

@@ -58,6 +58,11 @@ struct OtherTabs {
   const uint32_t* t[15];
 };
 
+// shared-memory words (doubles) per warp of the sparse RHS kernel
+__host__ __device__ __forceinline__ int64_t rhs_warp_words(int64_t m) {
+  return (m + 32 + (m + 7) / 8 + 1) & ~int64_t(1);  // even: 16-byte aligned per warp
+}
+
 template <int U, int NO>
 struct RhsRecs {
   int32_t c[U][4];
@@ -80,10 +85,14 @@ __device__ __forceinline__ void rhs_load(const double* __restrict__ rec, int64_t
   }
 }
 
-template <int U, int NO, int PF>
+// PK: the layout carries each record's bucket/sign (skx_coo_fibre_ts, order 3):
+// bucket = (c1 >> bb) & (2^31 - 1) >> bb, sign bit 31; no table lookups.
+// Otherwise the last other coordinate is c1 & c1_mask.
+template <int U, int NO, int PF, bool PK>
 __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
                                                     const int64_t* __restrict__ colptr,
                                                     const double* __restrict__ rec, int64_t m,
+                                                    uint32_t c1_mask, int bb,
                                                     double* __restrict__ yt) {
   extern __shared__ double smem[];
   constexpr int RW = NO <= 2 ? 2 : 3;  // record words
@@ -93,8 +102,10 @@ __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
   const int64_t nnz = colptr[s_n];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  double* acc = smem + (size_t)wid * (m + 32);
+  // per warp: acc (m doubles), stage (32 doubles), duplicate tags (m bytes)
+  double* acc = smem + (size_t)wid * rhs_warp_words(m);
   double* stage = acc + m;
+  uint8_t* tags = reinterpret_cast<uint8_t*>(stage + 32);
   const uint32_t mm = (uint32_t)m;
   const int64_t W = (int64_t)gridDim.x * nw, gw = blockIdx.x * (int64_t)nw + wid;
   auto col_at = [&](int64_t w) -> int64_t {  // first column starting at/after w's share
@@ -138,42 +149,42 @@ __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
       asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
   };
   auto process = [&](int64_t base, const RhsRecs<U, NO>& r) {
-    uint32_t t[U][NO];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int k = 0; k < NO; ++k) t[u][k] = __ldg(ot.t[k] + r.c[u][k]);
     uint32_t hb[U];
     double xs[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // bucket sums reduced mod m by conditional subtraction
-      uint32_t h = 0, neg = 0;
-#pragma unroll
-      for (int k = 0; k < NO; ++k) {
-        h += pk_bucket(t[u][k]);
-        if (h >= mm) h -= mm;
-        neg ^= pk_neg(t[u][k]);
-      }
-      hb[u] = h;
-      xs[u] = neg ? -r.v[u] : r.v[u];
-    }
-    const int64_t nvalid = imin((int64_t)CH, eend - base);
-    if (base >= cbeg && base + nvalid <= cend) {
-      uint32_t b[U];
-      unsigned peers[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) b[u] = u * 32 + lane < nvalid ? hb[u] : kNoBucket;
-#pragma unroll
-      for (int u = 0; u < U; ++u) peers[u] = __match_any_sync(0xffffffffu, b[u]);
+    if (PK) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (__all_sync(0xffffffffu, peers[u] == (1u << lane) || b[u] == kNoBucket)) {
-          if (b[u] != kNoBucket) acc[b[u]] += xs[u];
-          __syncwarp();
-        } else {
-          warp_ordered_add(acc, b[u], xs[u], stage);
-        }
+        const uint32_t w = (uint32_t)r.c[u][NO - 1];
+        hb[u] = (w & 0x7fffffffu) >> bb;
+        xs[u] = (w >> 31) ? -r.v[u] : r.v[u];
       }
+    } else {
+      uint32_t t[U][NO];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < NO; ++k) {
+          const uint32_t c = (uint32_t)r.c[u][k] & (k == NO - 1 ? c1_mask : 0xffffffffu);
+          t[u][k] = __ldg(ot.t[k] + c);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // bucket sums reduced mod m by conditional subtraction
+        uint32_t h = 0, neg = 0;
+#pragma unroll
+        for (int k = 0; k < NO; ++k) {
+          h += pk_bucket(t[u][k]);
+          if (h >= mm) h -= mm;
+          neg ^= pk_neg(t[u][k]);
+        }
+        hb[u] = h;
+        xs[u] = neg ? -r.v[u] : r.v[u];
+      }
+    }
+    const int64_t nvalid = imin((int64_t)CH, eend - base);
+    if (base >= cbeg && base + nvalid <= cend) {  // chunk inside the current column
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        warp_ordered_add(acc, u * 32 + lane < nvalid ? hb[u] : kNoBucket, xs[u], stage, tags);
       return;
     }
 #pragma unroll
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
         const int lo = (int)imax(cbeg - sub, (int64_t)0);
         const int64_t ce = cend - sub;
         const int top = ce < hi ? (int)ce : hi;
-        warp_ordered_add(acc, lane >= lo && lane < top ? hb[u] : kNoBucket, xs[u], stage);
+        warp_ordered_add(acc, lane >= lo && lane < top ? hb[u] : kNoBucket, xs[u], stage, tags);
         if (ce >= hi) break;
         flush();
       }
@@ -400,28 +411,31 @@ int warps_for(int64_t m) {
 }  // namespace
 
 extern "C" int skx_ts_rhs_coo(int n_other, int64_t s_n, const int64_t* colptr, const void* rec,
-                              const uint32_t* tab, const int64_t* tab_off_h, int64_t m, double* yt,
-                              void* stream) {
+                              const uint32_t* tab, const int64_t* tab_off_h, int64_t m,
+                              uint32_t c1_mask, int packed_bb, double* yt, void* stream) {
   SKX_REQUIRE(n_other >= 1 && n_other <= 4, "skx_ts_rhs_coo: 1..4 other modes (sparse order <= 5)");
-  const int nw = warps_for(m);
+  SKX_REQUIRE(packed_bb < 0 || n_other == 2, "skx_ts_rhs_coo: packed layouts are order 3");
+  const int nw = warps_per_cta_for(rhs_warp_words(m) * 8);
   SKX_REQUIRE(nw >= 1, "skx_ts_rhs_coo: sketch size %lld exceeds shared-memory capacity",
               (long long)m);
   if (s_n == 0) return SKX_OK;
   OtherTabs ot{};
   ot.n = n_other;
-  for (int k = 0; k < n_other; ++k) ot.t[k] = tab + tab_off_h[k];
-  const size_t smem = (size_t)nw * (m + 32) * 8;
-  auto kern = n_other == 1 ? k_ts_rhs_coo<4, 1, 8>
-            : n_other == 2 ? k_ts_rhs_coo<4, 2, 8>
-            : n_other == 3 ? k_ts_rhs_coo<4, 3, 8>
-                           : k_ts_rhs_coo<4, 4, 8>;
+  if (packed_bb < 0)
+    for (int k = 0; k < n_other; ++k) ot.t[k] = tab + tab_off_h[k];
+  const size_t smem = (size_t)nw * rhs_warp_words(m) * 8;
+  auto kern = packed_bb >= 0 ? k_ts_rhs_coo<4, 2, 8, true>
+            : n_other == 1   ? k_ts_rhs_coo<4, 1, 8, false>
+            : n_other == 2   ? k_ts_rhs_coo<4, 2, 8, false>
+            : n_other == 3   ? k_ts_rhs_coo<4, 3, 8, false>
+                             : k_ts_rhs_coo<4, 4, 8, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = imin((int64_t)num_sms() * per_sm, (s_n + nw - 1) / nw);
-  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(ot, s_n, colptr,
-                                                                  (const double*)rec, m, yt);
+  kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(
+      ot, s_n, colptr, (const double*)rec, m, c1_mask, packed_bb < 0 ? 0 : packed_bb, yt);
   return check_launch("k_ts_rhs_coo");
 }
 

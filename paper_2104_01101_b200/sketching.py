@@ -212,14 +212,22 @@ def ts_apply_kron(ts, factors, method="auto"):
     return z.cpu().numpy()
 
 
-def ts_rhs_coo_dev(ts, colptr, rec, s_n):
-    """Y^T (s_n x m) from a fibre-major COO layout (DeviceCoo.fibre)."""
+def ts_rhs_coo_dev(ts, colptr, rec, s_n, c1_mask=0xFFFFFFFF, packed_bb=-1):
+    """Y^T (s_n x m) from a fibre-major COO layout (DeviceCoo.fibre); c1_mask /
+    packed_bb describe a layout built with DeviceCoo.fibre(n, ts)."""
     torch = _torch()
     yt = torch.empty((s_n, ts.m), dtype=torch.float64, device="cuda")
     off, op = nat.host_i64(ts.tab_off)
     nat.call("skx_ts_rhs_coo", len(ts.extents), s_n, nat.ptr(colptr), nat.ptr(rec), nat.ptr(ts.tab),
-             op, ts.m, nat.ptr(yt), nat.stream())
+             op, ts.m, ctypes.c_uint32(c1_mask), int(packed_bb), nat.ptr(yt), nat.stream())
     return yt
+
+
+def ts_rhs_mode_dev(ts, d, n):
+    """Y_n^T for mode n of a DeviceCoo, building (or reusing) its layout with
+    ts's buckets folded in when possible."""
+    colptr, rec = d.fibre(n, ts)
+    return ts_rhs_coo_dev(ts, colptr, rec, d.shape[n], d.fibre_mask(n), d.fibre_packed_for(n, ts))
 
 
 def _coo_from_pairs(rows, cols, data, shape):
@@ -266,8 +274,7 @@ def ts_apply_rhs(ts, b, chunk=1 << 20):
         d = DeviceCoo((c,) + tuple(ts.extents),
                       torch.from_numpy(np.ascontiguousarray(cols[:, order].astype(np.int32))).cuda(),
                       torch.from_numpy(np.ascontiguousarray(coo.data[order], dtype=np.float64)).cuda())
-        colptr, rec = d.fibre(0)
-        return ts_rhs_coo_dev(ts, colptr, rec, c).t().cpu().numpy()
+        return ts_rhs_mode_dev(ts, d, 0).t().cpu().numpy()
     bd = _dev(b).contiguous()
     full = ts.full_table()
     out = torch.empty((c, ts.m), dtype=torch.float64, device="cuda")
@@ -632,7 +639,8 @@ def composite_apply(mat, op):
         colptr, rec = _coo_from_pairs(c.row, c.col, c.data, (s, P)).fibre(0)
         off = np.zeros(1, dtype=np.int64)
         nat.call("skx_ts_rhs_coo", 1, s, nat.ptr(colptr), nat.ptr(rec), nat.ptr(tab),
-                 off.ctypes.data_as(ctypes.c_void_p), op.k2, nat.ptr(st1), nat.stream())
+                 off.ctypes.data_as(ctypes.c_void_p), op.k2, ctypes.c_uint32(0xFFFFFFFF), -1,
+                 nat.ptr(st1), nat.stream())
     else:
         md = _dev(mat).contiguous()
         shp, sp_ = nat.host_i64([s, P])

@@ -21,6 +21,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import ctypes
+
 import numpy as np
 
 from . import _native as nat
@@ -219,6 +221,7 @@ class DeviceCoo:
         self.vals = vals          # (nnz,) float64
         self.nnz = int(vals.numel())
         self._fibre = {}
+        self._fibre_meta = {}
         self._keys = {}
         self._norm2 = None
 
@@ -281,10 +284,16 @@ class DeviceCoo:
         return self._norm2
 
     # ---- fibre-major layout for mode n (libskx skx_coo_fibre)
-    def fibre(self, n):
+    def fibre(self, n, ts=None):
         """(colptr, records) of mode n: nonzeros ordered by (i_n, other modes
         ascending) as AoS records {int32 others..., f64 value}, built by one
-        packing pass + a radix sort over ceil(log2 s_n) key bits."""
+        packing pass + a radix sort over ceil(log2 s_n) key bits.
+
+        With `ts` (a TensorSketchOp over mode n's other modes) an order-3
+        layout is built with that operator's bucket/sign folded into the
+        records (skx_coo_fibre_ts) when the bits fit; the RHS sketch then does
+        no table lookups.  Other consumers mask the coordinate
+        (fibre_mask(n)).  An existing layout is reused as is."""
         torch = _torch()
         if n not in self._fibre:
             rw = int(nat.load().skx_coo_rec_words(self.ndim))
@@ -293,10 +302,32 @@ class DeviceCoo:
             rec = torch.empty(max(self.nnz, 1) * rw, dtype=torch.float64, device="cuda")
             colptr = torch.empty(self.shape[n] + 1, dtype=torch.int64, device="cuda")
             shp, sp_ = nat.host_i64(self.shape)
-            nat.call_ws("skx_coo_fibre", (self.ndim, sp_, n, self.nnz, nat.ptr(self.coords),
-                                          nat.ptr(self.vals), nat.ptr(rec), nat.ptr(colptr)), slot=4)
+            mask, owner = 0xFFFFFFFF, None
+            if ts is not None and self.ndim == 3 and _ts_packable(self.shape, n, ts.m):
+                m_out = ctypes.c_uint32(0)
+                off, op = nat.host_i64(ts.tab_off)
+                nat.call_ws("skx_coo_fibre_ts",
+                            (sp_, n, self.nnz, nat.ptr(self.coords), nat.ptr(self.vals),
+                             nat.ptr(ts.tab), op, ts.m, nat.ptr(rec), nat.ptr(colptr),
+                             ctypes.byref(m_out)), slot=4)
+                mask, owner = int(m_out.value), ts
+            else:
+                nat.call_ws("skx_coo_fibre", (self.ndim, sp_, n, self.nnz, nat.ptr(self.coords),
+                                              nat.ptr(self.vals), nat.ptr(rec), nat.ptr(colptr)),
+                            slot=4)
             self._fibre[n] = (colptr, rec)
+            self._fibre_meta[n] = (mask, owner)
         return self._fibre[n]
+
+    def fibre_mask(self, n):
+        """Mask recovering the last other coordinate from mode n's records."""
+        return self._fibre_meta[n][0] if n in self._fibre_meta else 0xFFFFFFFF
+
+    def fibre_packed_for(self, n, ts):
+        """Bit offset of the bucket field if mode n's layout carries `ts`'s
+        buckets/signs, else -1."""
+        mask, owner = self._fibre_meta.get(n, (0xFFFFFFFF, None))
+        return mask.bit_length() if owner is ts and ts is not None else -1
 
     def colptr0(self):
         return self.fibre(0)[0]
@@ -321,7 +352,16 @@ class DeviceCoo:
 
     def release_layouts(self):
         self._fibre.clear()
+        self._fibre_meta.clear()
         self._keys.clear()
+
+
+def _ts_packable(shape, n, m):
+    """skx_coo_fibre_ts bit budget: coordinate bits of the second other mode +
+    bucket bits of m must fit in 31."""
+    b_other = 1 if n == 2 else 2
+    bb = max(int(shape[b_other]) - 1, 0).bit_length()
+    return m >= 1 and bb + max(m - 1, 0).bit_length() <= 31
 
 
 def device_of(t):
@@ -437,7 +477,8 @@ def tucker_cross_dev(d, core, factors):
         cpt, rec0 = d.fibre(0) if d.ndim == 3 else (None, None)
         nat.call_ws("skx_tucker_cross_coo",
                     (d.ndim, sp_, rp, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp,
-                     nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(rec0), nat.ptr(out)))
+                     nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(rec0),
+                     ctypes.c_uint32(d.fibre_mask(0)), nat.ptr(out)))
         return out[0]
     proj = d
     for k, a in enumerate(factors):

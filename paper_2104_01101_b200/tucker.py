@@ -11,6 +11,7 @@ are outside this build's path.
 """
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -22,7 +23,7 @@ from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev,
                      top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather_coo_dev,
                         gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
-                        plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_rhs_coo_dev,
+                        plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_rhs_mode_dev,
                         ts_rhs_dense_dev)
 from .tensors import (DeviceCoo, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
                       matricize, shape_of)
@@ -108,7 +109,8 @@ def rrf_stage1_dev(d, n, tabs):
         others = [k for k in range(d.ndim) if k != n]
         ext, ep = nat.host_i64([shape[k] for k in others])
         nat.call("skx_rrf_stage1_coo", len(others), ep, s_n, nat.ptr(colptr), nat.ptr(rec),
-                 *tabs.args(), tabs.k2, nat.ptr(st1), nat.stream())
+                 *tabs.args(), tabs.k2, ctypes.c_uint32(d.fibre_mask(n)), nat.ptr(st1),
+                 nat.stream())
     else:
         tab = rrf_table_dev(tabs)
         shp, sp_ = nat.host_i64(shape)
@@ -256,9 +258,10 @@ class _Run:
         # layouts and TensorSketch right-hand sides
         scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side)
         with torch.cuda.stream(main):
-            if self.sparse:  # layouts first: RRF stage 1 and the TS sketches read them
-                for n in range(self.ndim):
-                    self.d.fibre(n)
+            self.draw_ts_ops()
+            if self.sparse:  # layouts first (with TS buckets folded in): RRF stage 1 and the
+                for n in range(self.ndim):  # TS sketches read them
+                    self.d.fibre(n, self.ts_ops[n] if self.use_ts else None)
             self.prep()
             for n, scan, (P, k2, width) in zip(modes, scans, dims):
                 tabs = finish_rrf_scan(scan, self.rng_init, P)
@@ -267,22 +270,33 @@ class _Run:
         caller.wait_stream(main)
         caller.wait_stream(side)
 
-    def build_ts(self, n):
+    def _draw_ts(self, n):
         ext = tuple(self.shape[k] for k in self.others(n))
-        op = TensorSketchOp.build(ext, self.m, self.rng_sketch)
-        if self.sparse:
-            colptr, rec = self.d.fibre(n)
-            yt = ts_rhs_coo_dev(op, colptr, rec, self.shape[n])
-        else:
-            yt = ts_rhs_dense_dev(op, self.d, n)
+        return TensorSketchOp.build(ext, self.m, self.rng_sketch)
+
+    def _rhs(self, n, op):
+        # sparse: mode n's layout carries op's buckets when built for it
+        yt = ts_rhs_mode_dev(op, self.d, n) if self.sparse else ts_rhs_dense_dev(op, self.d, n)
         if self.comm is not None:
             self.comm.allreduce(yt)
-        self.ts_ops[n], self.ts_rhs[n] = op, yt
+        return yt
+
+    def draw_ts_ops(self):
+        """All modes' operators, in the reference's draw order (mode 0..N-1)."""
+        if self.use_ts and self.ts_ops[0] is None:
+            for n in range(self.ndim):
+                self.ts_ops[n] = self._draw_ts(n)
+
+    def build_ts(self, n):
+        """Redraw mode n's operator and its right-hand side (src/tucker.py:264-267)."""
+        op = self._draw_ts(n)
+        self.ts_ops[n], self.ts_rhs[n] = op, self._rhs(n, op)
 
     def prep(self):
         if self.use_ts:
+            self.draw_ts_ops()
             for n in range(self.ndim):
-                self.build_ts(n)
+                self.ts_rhs[n] = self._rhs(n, self.ts_ops[n])
 
     def solve_mode(self, n, redraw):
         others = [self.factors[k] for k in self.others(n)]

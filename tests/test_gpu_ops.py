@@ -293,6 +293,49 @@ def test_fibre_layout_matches_stable_sort(skx):
                               np.searchsorted(c[order, n], np.arange(shape[n] + 1)))
 
 
+@pytest.mark.parametrize("shape,m", [((50, 3000, 7), 1600), ((200, 150, 100), 64), ((9, 1, 40), 3)])
+def test_packed_ts_layout(skx, oracle, shape, m):
+    """skx_coo_fibre_ts: records carry mode n's TS bucket/sign above the second
+    coordinate; every consumer (RHS sketch without lookups, RHS sketch with
+    lookups + mask, Tucker cross term, RRF stage 1) matches the plain layout
+    bit for bit."""
+    import torch
+    from paper_2104_01101_b200.sketching import draw_rrf_tables, ts_rhs_coo_dev, ts_rhs_mode_dev
+    from paper_2104_01101_b200.tensors import DeviceCoo, device_of, tucker_cross_dev
+    from paper_2104_01101_b200.tucker import rrf_stage1_dev
+    c, v = _coo_rand(shape, min(20000, int(np.prod(shape)) // 2), 5)
+    st = skx.SparseTensor(shape, c, v)
+    plain = device_of(st)
+    oc = oracle.Coo(shape, c, v)
+    for n in range(3):
+        ext = tuple(shape[k] for k in range(3) if k != n)
+        op = skx.TensorSketchOp.build(ext, m, skx.make_rng(n))
+        packed = DeviceCoo(shape, plain.coords, plain.vals)
+        yt_p = ts_rhs_mode_dev(op, packed, n)
+        assert packed.fibre_packed_for(n, op) >= 0
+        colptr, rec = plain.fibre(n)
+        yt = ts_rhs_coo_dev(op, colptr, rec, shape[n])
+        assert torch.equal(yt_p, yt)
+        hs, ss = oracle.ts_tables(ext, m, oracle.generator(n))
+        assert np.array_equal(yt_p.cpu().numpy().T, oracle.ts_rhs(hs, ss, ext, m, oracle.unfold_t(oc, n)))
+        # lookup path on the packed records (a different operator)
+        op2 = skx.TensorSketchOp.build(ext, m, skx.make_rng(n + 10))
+        assert packed.fibre_packed_for(n, op2) == -1
+        pc, pr = packed.fibre(n)
+        assert torch.equal(ts_rhs_coo_dev(op2, pc, pr, shape[n], packed.fibre_mask(n), -1),
+                           ts_rhs_coo_dev(op2, colptr, rec, shape[n]))
+        # RRF stage 1 on the packed layout
+        P = int(np.prod(ext))
+        t1 = rrf_stage1_dev(packed, n, draw_rrf_tables(skx.make_rng(7), P, 45))
+        t0 = rrf_stage1_dev(plain, n, draw_rrf_tables(skx.make_rng(7), P, 45))
+        assert torch.equal(t1, t0)
+        if n == 0:
+            rng = np.random.default_rng(1)
+            A = [torch.from_numpy(np.linalg.qr(rng.standard_normal((s, 6)))[0]).cuda() for s in shape]
+            core = torch.from_numpy(rng.standard_normal((6, 6, 6))).cuda()
+            assert float(tucker_cross_dev(packed, core, A)) == float(tucker_cross_dev(plain, core, A))
+
+
 @pytest.mark.parametrize("shape,m", [((30, 40, 50), 64), ((12, 13, 14, 15), 256), ((100, 100, 100), 400),
                                      ((3, 200, 5), 4096)])
 def test_dense_ts_rhs_all_modes_vs_oracle(skx, oracle, shape, m):
