@@ -248,8 +248,9 @@ def run_ours(args, cfgd):
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic, "traffic_source": "profiles/r1_traffic.json (ncu --set full)",
                 "alg_bytes_per_launch": int(alg_bytes[roof_k]),
-                "layout": "fibre-major COO: int32 x2 other coords + f64 value = 16 B/nnz; "
-                          "canonical int64 COO would be 32 B/nnz"}
+                "layout": "fibre-major COO records, 16 B/nnz: int32 c_a, int32 (c_b | bucket << bb "
+                          "| sign << 31), f64 value (mode n's TensorSketch bucket/sign folded in "
+                          "when the layout is built); canonical int64 COO would be 32 B/nnz"}
 
     out = {
         "metric": "sketched-ALS sweeps/s (whole sketched_tucker_als call incl. RRF init, TS prep, "

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kCholThreads) k_chol_reg(const double* __restr
 // pairwise (round-robin tournament, n/2 disjoint pairs per step, one warp per
 // pair) until every pair is orthogonal to eps relative; W accumulates the
 // rotations.  s_j = ||a_j||, u_j = a_j / s_j, sorted descending.
-__global__ void __launch_bounds__(512) k_jacobi(const double* __restrict__ Ain, int n, int rs,
+__global__ void __launch_bounds__(1024, 1) k_jacobi(const double* __restrict__ Ain, int n, int rs,
                                                 int cs, double* __restrict__ U,
                                                 double* __restrict__ S,
                                                 double* __restrict__ V) {
@@ -149,14 +149,22 @@ __global__ void __launch_bounds__(512) k_jacobi(const double* __restrict__ Ain, 
   // column 1 + (j - 1 + step) mod (np - 1); pairs are (slot k, slot np-1-k)
   const int nm1 = np - 1;
   const double eps = 2.220446049250313e-16;
-  const double tol = 4.0 * sqrt((double)n) * eps;
+  // rotate while |cos(a_p, a_q)| > 2 n eps: above the rounding noise of the
+  // length-n dot products (a tighter threshold keeps rotating on noise and
+  // runs to the sweep cap), far below what the 1e-10 parity needs
+  const double tol = 2.0 * n * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) changed = 0;
     __syncthreads();
     for (int step = 0; step < np - 1; ++step) {
       for (int pr = wid; pr < np / 2; pr += nw) {
-        int p = pr == 0 ? 0 : 1 + (pr - 1 + step) % nm1;
-        int q = 1 + (np - 2 - pr + step) % nm1;  // slot np-1-pr >= 1
+        // slot j >= 1 holds column 1 + (j - 1 + step) mod (np - 1); both
+        // arguments are < 2 (np - 1): one conditional subtraction each
+        int vp = pr - 1 + step, vq = np - 2 - pr + step;
+        if (vp >= nm1) vp -= nm1;
+        if (vq >= nm1) vq -= nm1;
+        int p = pr == 0 ? 0 : 1 + vp;
+        int q = 1 + vq;  // slot np-1-pr >= 1
         if (p > q) {
           const int t = p;
           p = q;
@@ -249,6 +257,8 @@ extern "C" int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, do
   const int np = n + (n & 1);
   const size_t smem = (size_t)(np * n + np * np) * 8 + (size_t)np * 4 + 16;
   cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_jacobi<<<1, 512, smem, (cudaStream_t)stream>>>(a, n, (int)rs, (int)cs, u, s, v);
+  // one warp per column pair of a round-robin step
+  k_jacobi<<<1, 32 * (np / 2 > 16 ? 32 : np / 2 < 1 ? 1 : np / 2), smem, (cudaStream_t)stream>>>(
+      a, n, (int)rs, (int)cs, u, s, v);
   return check_launch("k_jacobi");
 }

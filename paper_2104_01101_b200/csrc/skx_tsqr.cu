@@ -121,34 +121,41 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&p)[NP], int lane)
 }
 
 template <int WP>
-__global__ void __launch_bounds__(kTsqrRows) k_tsqr_reg(const double* __restrict__ A, int64_t n,
-                                                      int w, int64_t rs, int64_t cs,
-                                                      double* __restrict__ Rout) {
-  __shared__ double red[kTsqrRows / 32][33];
-  __shared__ double dv[32];
+__global__ void __launch_bounds__(kTsqrRows, 1) k_tsqr_reg(const double* __restrict__ A, int64_t n,
+                                                         int w, int64_t rs, int64_t cs,
+                                                         double* __restrict__ Rout) {
+  constexpr int NC = WP <= 32 ? 32 : 64;  // reduction components (dot products)
+  constexpr int NP = WP <= 8 ? 8 : WP <= 16 ? 16 : 32;
+  __shared__ double red[kTsqrRows / 32][NC + 1];
+  __shared__ double dv[NC];
   __shared__ double s_x0;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   constexpr int NW = kTsqrRows / 32;
   const int64_t r0 = blockIdx.x * (int64_t)kTsqrRows;
   const int rows = (int)imin(kTsqrRows, n - r0);
+  double* R = Rout + (int64_t)blockIdx.x * w * w;
+  for (int q = t; q < w * w; q += kTsqrRows) R[q] = 0.0;
+  // a[j] holds column k + j of this thread's row at step k: the row shifts
+  // left by one after every reflector, so the step body has static register
+  // indices without unrolling the step loop (small code, no I-cache thrash)
   double a[WP];
 #pragma unroll
   for (int j = 0; j < WP; ++j)
     a[j] = (t < rows && j < w) ? A[(r0 + t) * rs + (int64_t)j * cs] : 0.0;
   const int kmax = min(rows, w);
-#pragma unroll
-  for (int k = 0; k < WP; ++k) {
-    if (k >= kmax) break;
+#pragma unroll 1
+  for (int k = 0; k < kmax; ++k) {
+    const int rem = w - k;  // live columns a[0..rem)
     // ---- dlarfg on column k, rows k..rows-1
-    double sq = t > k ? a[k] * a[k] : 0.0;
+    double sq = t > k ? a[0] * a[0] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (lane == 0) red[wid][32] = sq;
-    if (t == k) s_x0 = a[k];
+    if (lane == 0) red[wid][NC] = sq;
+    if (t == k) s_x0 = a[0];
     __syncthreads();
     double sg = 0.0;
 #pragma unroll
-    for (int q = 0; q < NW; ++q) sg += red[q][32];
+    for (int q = 0; q < NW; ++q) sg += red[q][NC];
     const double x0 = s_x0;
     double tau = 0.0, beta = x0;
     if (sg != 0.0) {
@@ -156,18 +163,21 @@ __global__ void __launch_bounds__(kTsqrRows) k_tsqr_reg(const double* __restrict
       beta = x0 >= 0.0 ? -nrm : nrm;
       tau = (beta - x0) / beta;
     }
-    if (tau != 0.0) {
+    if (tau != 0.0) {  // uniform
       const double scale = 1.0 / (x0 - beta);
-      const double v = t > k ? a[k] * scale : (t == k ? 1.0 : 0.0);
-      // ---- d_j = sum_t v_t a_t[j], j > k
-      constexpr int NP = WP <= 8 ? 8 : WP <= 16 ? 16 : 32;
-      double p[NP];
+      const double v = t > k ? a[0] * scale : (t == k ? 1.0 : 0.0);
+      // ---- d_j = sum_t v_t a_t[j], 0 < j < rem, in blocks of NP components
 #pragma unroll
-      for (int j = 0; j < NP; ++j) p[j] = (j > k && j < WP) ? v * a[j] : 0.0;
-      const double rsum = warp_reduce_scatter<NP>(p, lane);
-      if (lane < NP) red[wid][lane] = rsum;
+      for (int j0 = 0; j0 < WP; j0 += NP) {
+        if (j0 >= rem) break;
+        double p[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) p[j] = (j0 + j > 0 && j0 + j < rem) ? v * a[j0 + j] : 0.0;
+        const double rsum = warp_reduce_scatter<NP>(p, lane);
+        if (lane < NP) red[wid][j0 + lane] = rsum;
+      }
       __syncthreads();
-      if (t < NP) {
+      if (t < rem) {
         double d = 0.0;
 #pragma unroll
         for (int q = 0; q < NW; ++q) d += red[q][t];
@@ -175,17 +185,19 @@ __global__ void __launch_bounds__(kTsqrRows) k_tsqr_reg(const double* __restrict
       }
       __syncthreads();
 #pragma unroll
-      for (int j = k + 1; j < WP; ++j) a[j] = fma(-dv[j], v, a[j]);
+      for (int j = 1; j < WP; ++j)
+        if (j < rem) a[j] = fma(-dv[j], v, a[j]);
     }
-    if (t == k) a[k] = beta;
-    else if (t > k) a[k] = 0.0;
-    __syncthreads();  // red / s_x0 reuse in the next step
-  }
-  double* R = Rout + (int64_t)blockIdx.x * w * w;
-  if (t < w) {
+    if (t == k) {  // row k of R is final
+      a[0] = beta;
 #pragma unroll
-    for (int j = 0; j < WP; ++j)
-      if (j < w) R[(int64_t)t * w + j] = (j >= t && t < rows) ? a[j] : 0.0;
+      for (int j = 0; j < WP; ++j)
+        if (j < rem) R[(int64_t)k * w + k + j] = a[j];
+    }
+#pragma unroll
+    for (int j = 0; j + 1 < WP; ++j) a[j] = a[j + 1];
+    a[WP - 1] = 0.0;
+    __syncthreads();  // red / dv / s_x0 reuse in the next step
   }
 }
 
@@ -197,7 +209,7 @@ extern "C" int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t
                           void* ws, size_t* ws_bytes, void* stream) {
   SKX_REQUIRE(w >= 1 && w <= 64, "skx_tsqr_r: 1 <= w <= 64 columns supported");
   SKX_REQUIRE(ws_bytes != nullptr, "skx_tsqr_r: ws_bytes is NULL");
-  const int BR = w <= 32 ? kTsqrRows : 128;
+  const int BR = kTsqrRows;
   // level sizes
   int64_t rows = n, total = 0;
   int levels = 0;
@@ -223,6 +235,9 @@ extern "C" int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t
   else if (w <= 16) kern = k_tsqr_reg<16>, smem = 0;
   else if (w <= 24) kern = k_tsqr_reg<24>, smem = 0;
   else if (w <= 32) kern = k_tsqr_reg<32>, smem = 0;
+  else if (w <= 40) kern = k_tsqr_reg<40>, smem = 0;
+  else if (w <= 48) kern = k_tsqr_reg<48>, smem = 0;
+  else kern = k_tsqr_reg<64>, smem = 0;
   if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const double* src = a;
   int64_t srs = rs, scs = cs;
