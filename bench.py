@@ -261,7 +261,8 @@ def run_ours(args, cfgd):
         "data": "synthetic (seeded, generated on GPU)",
         "config": {"workload": cfgd["workload"], "nnz": nnz, "shape": list(shape),
                    "parallelism": f"nnz mode-0 slabs x{world} + NCCL all-reduce" if world > 1 else "single GPU",
-                   "l2": "inputs (3.2 GB) larger than L2 (126 MB)",
+                   "l2": f"inputs ({nnz * 32 / 1e9:.1f} GB canonical COO) larger than L2 (126 MB): "
+                         "no flush needed between steps",
                    "sweeps_per_step": cfgd["sweeps"],
                    "sweeps_per_s_ref_def": round(sweeps / sum(wall_s), 3),
                    "ref_def": "sweeps / sum(SweepTrace.wall_s): N sub-problems + core fold, "

@@ -148,18 +148,19 @@ def _small_svd(r):
     return torch.linalg.svd(r, full_matrices=False)
 
 
-def top_svd_dev(mat, k):
+def top_svd_dev(mat, k, wide=False):
     """Leading k singular triplets of a matrix with one small dimension.
 
     Skinny side <= 64: R from TSQR, SVD of the small R, and the long singular
     vectors recovered as mat V / sigma (or mat^T U / sigma).  Otherwise the
-    cuSOLVER thin SVD."""
+    cuSOLVER thin SVD.  wide=True forces the m < n formulation for a square
+    input (as the caller's larger matrix would take)."""
     torch = _torch()
     m, n = mat.shape
     if min(m, n) > 64:
         u, s, v = thin_svd_dev(mat)
         return u[:, :k], s[:k], v[:, :k]
-    if m >= n:
+    if m >= n and not (wide and m == n):
         r = tsqr_r_dev(mat)
         _, s, vh = _small_svd(r)
         v = vh[:k].transpose(0, 1)
@@ -336,6 +337,62 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
     u, sv, v = top_svd_dev(d, rank)
     core_t = q @ (u * sv)
     return core_t, v.contiguous(), bad
+
+
+def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversample=10,
+                       check=True):
+    """rsvd_lrls_dev for a sparse right-hand side given as leverage-gather hits
+    (row j's entries at hit_col/hit_val[hit_off[j]:hit_off[j+1]], distinct
+    columns per row), plus its residual.  Same algebra as the dense call on
+    the m x s matrix of the hits, restricted to the set H of columns that hold
+    a hit: every product with Y only sees Y's nonzero columns, D = W^T Y is
+    zero outside H, so the SVD is taken of D_H and the factor rows outside H
+    are exactly zero.  The Gaussian test matrix is still drawn s x w, so the
+    rng_solve stream advances exactly as in the reference.  Returns
+    (core_t, a (s x rank), bad, resid)."""
+    torch = _torch()
+    m, r = z.shape
+    if m < r:
+        raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
+    if rank > min(r, s):
+        raise ValueError(f"rank {rank} exceeds min({r}, {s})")
+    qz, rz, bad = sketch_qr_dev(z)
+    if check and bool(bad.item()):
+        raise RankDeficientError("rank-deficient sketched system")
+    width = min(rank + oversample, s)
+    g = normals.normal((s, width))
+    counts = hit_off[1:] - hit_off[:-1]
+    rows = torch.repeat_interleave(torch.arange(m, device="cuda"), counts)
+    cols, inv = torch.unique(hit_col, return_inverse=True)
+    nh = int(cols.numel())
+    yh = torch.zeros((m, max(nh, 1)), dtype=torch.float64, device="cuda")
+    if nh:
+        yh[rows, inv] = hit_val
+    gh = g[cols] if nh else torch.zeros((1, width), dtype=torch.float64, device="cuda")
+    if width < r:
+        c = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ (yh @ gh), upper=True)
+        q, _ = torch.linalg.qr(c, mode="reduced")
+        wm = qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+        dh = wm.transpose(0, 1) @ yh
+    else:
+        xh = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ yh, upper=True)
+        q, _ = torch.linalg.qr(xh @ gh, mode="reduced")
+        dh = q.transpose(0, 1) @ xh
+    # the dense call factors D (w x s, s >= w) through its wide branch; keep
+    # that branch (zero columns appended when |H| < w leave R unchanged)
+    if dh.shape[1] < dh.shape[0]:
+        dh = torch.cat([dh, torch.zeros((dh.shape[0], dh.shape[0] - dh.shape[1]),
+                                        dtype=torch.float64, device="cuda")], dim=1)
+    u, sv, vh = top_svd_dev(dh, rank, wide=True)
+    core_t = q @ (u * sv)
+    a = torch.zeros((s, rank), dtype=torch.float64, device="cuda")
+    if nh:
+        a[cols] = vh[:nh]
+    # residual: Z core_t a^T is zero outside H, so is Y
+    p = z @ core_t
+    resid = torch.linalg.vector_norm(p @ a[cols].transpose(0, 1) - yh[:, :nh]) if nh else \
+        torch.zeros((), dtype=torch.float64, device="cuda")
+    return core_t, a, bad, resid
 
 
 def rsvd_lrls(z, y, rank, rng, oversample=10):

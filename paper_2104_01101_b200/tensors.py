@@ -350,6 +350,11 @@ class DeviceCoo:
                 self._keys[n] = (key, self.vals[perm].contiguous())
         return self._keys[n]
 
+    def drop_fibre(self, n):
+        """Free mode n's fibre-major layout (rebuilt on next use)."""
+        self._fibre.pop(n, None)
+        self._fibre_meta.pop(n, None)
+
     def release_layouts(self):
         self._fibre.clear()
         self._fibre_meta.clear()

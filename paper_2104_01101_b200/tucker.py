@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _native as nat
 from . import rng as rngmod
-from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev,
+from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev, rsvd_lrls_hits_dev,
                      top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather_coo_dev,
                         gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
@@ -173,6 +173,10 @@ def random_orthonormal_dev(n_rows, n_cols, gen):
 
 
 # ------------------------------------------------------------------ driver
+# leverage sampling on sparse tensors: rsvd on the hit columns when the gathered
+# fibres fill less than this fraction of the m x s_n right-hand side
+HITS_DENSITY = 0.05
+
 _STREAMS = {}
 
 
@@ -312,6 +316,11 @@ class _Run:
                 keys, vals = self.d.keys(n)
                 ext = [self.shape[k] for k in self.others(n)]
                 off, col, val = gather_coo_dev(keys, vals, ext, self.shape[n], idx, w)
+                if self.comm is None and col.numel() < HITS_DENSITY * self.m * self.shape[n]:
+                    # mostly-empty sampled fibres: work on the hit columns only
+                    core_t, a, _, res = rsvd_lrls_hits_dev(z, off, col, val, self.shape[n],
+                                                           self.ranks[n], self.normals)
+                    return core_t, a, res
                 y = hits_to_dense(off, col, val, self.m, self.shape[n])
             else:
                 y = gather_dense_dev(self.d, n, idx, w)
@@ -365,6 +374,11 @@ def sketched_tucker_als_dev(t, config, comm=None):
     """Device-resident form: returns (core, factors) as CUDA tensors + trace."""
     run = _Run(t, config, comm)
     run.initialise_and_prep()
+    if run.sparse:
+        # modes >= 1 layouts served the RRF stage 1 and the TS right-hand sides;
+        # the sweeps only read mode 0's (fitness): free the rest (16 B/nnz each)
+        for n in range(1, run.ndim):
+            run.d.drop_fibre(n)
     trace = SweepTrace()
     core = run.sweeps(trace)
     return core, list(run.factors), trace

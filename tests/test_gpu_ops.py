@@ -442,3 +442,33 @@ def test_resid_pass(R, orient):
                           torch.from_numpy(a).cuda(), yd))
     exp = np.linalg.norm(z @ c @ a.T - y)
     assert got == pytest.approx(exp, rel=1e-12)
+
+
+@pytest.mark.parametrize("m,r,s,rank,nh", [(300, 100, 5000, 10, 40), (300, 16, 4000, 8, 400),
+                                           (200, 25, 3000, 5, 7), (64, 9, 800, 3, 4)])
+def test_rsvd_hits_matches_dense(m, r, s, rank, nh):
+    """The hit-column rsvd (sparse leverage right-hand sides) equals the dense
+    rsvd_lrls_dev + residual on the same hits and the same Gaussian stream:
+    both reassociation branches (width < r and width >= r) and |H| < width."""
+    import torch
+    from paper_2104_01101_b200 import rng as rngmod
+    from paper_2104_01101_b200.linalg import NormalSource, resid_dev, rsvd_lrls_dev, rsvd_lrls_hits_dev
+    from paper_2104_01101_b200.sketching import hits_to_dense
+    rng = np.random.default_rng(m + nh)
+    z = torch.from_numpy(rng.standard_normal((m, r))).cuda()
+    hit_cols = rng.choice(s, nh, replace=False)
+    per_row = [np.sort(rng.choice(hit_cols, rng.integers(0, min(nh, 6) + 1), replace=False)) for _ in range(m)]
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum([len(p) for p in per_row])]).astype(np.int64)).cuda()
+    col = torch.from_numpy(np.concatenate(per_row).astype(np.int64)).cuda()
+    val = torch.from_numpy(rng.standard_normal(int(off[-1]))).cuda()
+    y = hits_to_dense(off, col, val, m, s)
+    ct0, a0, _ = rsvd_lrls_dev(z, y, rank, NormalSource(rngmod.make_rng(5)))
+    res0 = float(resid_dev(z, ct0, a0, y))
+    ct1, a1, _, res1 = rsvd_lrls_hits_dev(z, off, col, val, s, rank, NormalSource(rngmod.make_rng(5)))
+    # singular vectors are defined up to sign (the R factors of D and D_H differ
+    # in row signs): compare after the SURVEY 8c canonicalisation
+    (a1c,), c1 = canon([a1.cpu().numpy()], ct1.cpu().numpy().T)
+    (a0c,), c0 = canon([a0.cpu().numpy()], ct0.cpu().numpy().T)
+    assert relerr(a1c, a0c) <= 1e-11
+    assert relerr(c1, c0) <= 1e-11
+    assert float(res1) == pytest.approx(res0, rel=1e-11)

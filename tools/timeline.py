@@ -34,7 +34,8 @@ def main():
 
     cfgd = bench.CONFIGS[args.config]
     coords, vals = planted_cp_coo_device(cfgd["shape"], cfgd["nnz"], rank=10, noise_sd=0.1, seed=0)
-    st = skx.SparseTensor.from_device(cfgd["shape"], coords.t().contiguous(), vals)
+    st = skx.SparseTensor.from_device(cfgd["shape"], coords, vals)
+    del coords, vals
     cfg = skx.TuckerConfig(ranks=cfgd["ranks"], max_sweeps=cfgd["sweeps"], sketch=cfgd["sketch"],
                            sketch_size=cfgd["sketch_size"], seed=0)
     for _ in range(2):
