@@ -52,6 +52,20 @@ class Comm:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
+    def allgather(self, t):
+        """Concatenation of every rank's equally-shaped 1-D tensor `t`, rank order."""
+        if self.world == 1:
+            return t
+        import torch
+        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+        return out
+
+    def split(self, lo, hi):
+        """This rank's contiguous share of the integer range [lo, hi)."""
+        n = hi - lo
+        return lo + n * self.rank // self.world, lo + n * (self.rank + 1) // self.world
+
 
 def shard_device_coo(coords, vals, shape, world, rank):
     """Rank `rank`'s mode-0 slab of a lexsorted (N, nnz) device COO."""

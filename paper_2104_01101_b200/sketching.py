@@ -487,40 +487,55 @@ class RrfScan:
         self.key, self.raw_lo, self.raw_hi, self.k2, self.cap = key, raw_lo, raw_hi, k2, cap
         self.rej, self.count, self.stream, self.tag = rej, count, stream, tag
         self.pre = None
+        self.comm = None
 
 
-def launch_rrf_scan(key, raw_lo, raw_hi, k2, cap, stream=None):
+def launch_rrf_scan(key, raw_lo, raw_hi, k2, cap, stream=None, comm=None):
     """Enqueue the rejection scan of raw words [raw_lo, raw_hi) for bound k2.
     Compute-bound (one Philox block per 4 raw words); meant to run on a side
     stream, overlapping memory-bound work, before the exact start of the
-    integers() call it serves is known."""
+    integers() call it serves is known.  With a multi-rank `comm`
+    every rank scans its 1/world share; the finish gathers the lists."""
     torch = _torch()
     st = stream or torch.cuda.current_stream()
+    lo, hi = comm.split(raw_lo, raw_hi) if comm is not None and comm.world > 1 else (raw_lo, raw_hi)
     with torch.cuda.stream(st):
         rej = torch.empty(cap, dtype=torch.int64, device="cuda")
         nat.call("skx_fill_u64max", nat.ptr(rej), cap, nat.stream())
         count = torch.zeros(1, dtype=torch.int64, device="cuda")
-        nat.call("skx_lemire_scan", ctypes.c_uint64(key[0]), ctypes.c_uint64(key[1]),
-                 ctypes.c_uint64(raw_lo), ctypes.c_uint64(raw_hi), ctypes.c_uint32(k2), nat.ptr(rej),
-                 cap, nat.ptr(count), nat.stream())
-    return RrfScan(key, raw_lo, raw_hi, k2, cap, rej, count, st)
+        if hi > lo:
+            nat.call("skx_lemire_scan", ctypes.c_uint64(key[0]), ctypes.c_uint64(key[1]),
+                     ctypes.c_uint64(lo), ctypes.c_uint64(hi), ctypes.c_uint32(k2), nat.ptr(rej),
+                     cap, nat.ptr(count), nat.stream())
+    sc = RrfScan(key, raw_lo, raw_hi, k2, cap, rej, count, st)
+    sc.comm = comm if comm is not None and comm.world > 1 else None
+    return sc
 
 
 def _enqueue_finish(scan, c, P):
     """Enqueue skx_lemire_finish for a hash run starting at cursor `c` on the
-    scan's stream, plus a pinned copy of (count, #rejections among the P hash
-    draws) and an event marking both."""
+    scan's stream, plus a pinned copy of (largest per-rank count, #rejections
+    among the P hash draws) and an event marking both.  A rank-split scan
+    first gathers every rank's list (the sort inside the finish merges them)."""
     torch = _torch()
     pend_raw = c.p - 1 if c.has else 0
     with torch.cuda.stream(scan.stream):
-        d = torch.empty(scan.cap, dtype=torch.int64, device="cuda")
+        rej, count, cap = scan.rej, scan.count, scan.cap
+        if scan.comm is not None:
+            counts = scan.comm.allgather(scan.count)
+            rej = scan.comm.allgather(scan.rej)
+            cap = int(rej.numel())
+            count, cmax = counts.sum().view(1), counts.max().view(1)
+        else:
+            cmax = count
+        d = torch.empty(cap, dtype=torch.int64, device="cuda")
         n_le = torch.zeros(1, dtype=torch.int64, device="cuda")
-        nat.call_ws("skx_lemire_finish", (nat.ptr(scan.rej), nat.ptr(scan.count), scan.cap,
+        nat.call_ws("skx_lemire_finish", (nat.ptr(rej), nat.ptr(count), cap,
                                           ctypes.c_uint64(c.p), ctypes.c_uint32(c.has),
                                           ctypes.c_uint64(pend_raw), ctypes.c_uint64(P),
                                           nat.ptr(d), nat.ptr(n_le)), slot=3 + 8 * scan.tag)
         host = torch.empty(2, dtype=torch.int64, pin_memory=True)
-        host[0:1].copy_(scan.count, non_blocking=True)
+        host[0:1].copy_(cmax, non_blocking=True)
         host[1:2].copy_(n_le, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(scan.stream)
@@ -541,19 +556,20 @@ def finish_rrf_scan(scan, gen, P):
         fin = _enqueue_finish(scan, c, P)
     _, d, host, ev = fin
     ev.synchronize()
-    count, nrej = int(host[0]), int(host[1])
+    count, nrej = int(host[0]), int(host[1])  # count: largest per-rank list
     need_hi = c.p + (P + nrej - c.has + 1) // 2  # raw words the hash run reads
     covered = (count < scan.cap and c.p >= scan.raw_lo and need_hi <= scan.raw_hi
                and (not c.has or pend_raw >= scan.raw_lo))
     if not covered:  # prediction missed or too many rejections: exact rescan
         cap = max(scan.cap * 4, _rej_cap(P, scan.k2))
         lo = pend_raw if c.has else c.p
-        exact = launch_rrf_scan(scan.key, lo, c.p + (P + cap) // 2 + 2, scan.k2, cap, scan.stream)
+        exact = launch_rrf_scan(scan.key, lo, c.p + (P + cap) // 2 + 2, scan.k2, cap, scan.stream,
+                                scan.comm)
         return finish_rrf_scan(exact, gen, P)
     cur = torch.cuda.current_stream()
     cur.wait_event(ev)
     d.record_stream(cur)
-    tabs = RrfTables(c.k0, c.k1, c.p, c.has, c.pending, d, scan.cap, P + nrej, scan.k2, P)
+    tabs = RrfTables(c.k0, c.k1, c.p, c.has, c.pending, d, int(d.numel()), P + nrej, scan.k2, P)
     rngmod.advance_u32(gen, 2 * P + nrej)
     return tabs
 
@@ -568,7 +584,7 @@ def draw_rrf_tables(gen, P, k2, stream=None):
     return finish_rrf_scan(scan, gen, P)
 
 
-def plan_rrf_scans(gen, jobs, stream=None):
+def plan_rrf_scans(gen, jobs, stream=None, comm=None):
     """Launch the scans of consecutive RRF table draws at once.  jobs =
     [(P, k2, n_gauss)] in draw order, where n_gauss normals follow each pair of
     integers() calls.  Later starts are bracketed (rejections < cap, ziggurat
@@ -581,11 +597,13 @@ def plan_rrf_scans(gen, jobs, stream=None):
     scans = []
     for i, (P, k2, n_gauss) in enumerate(jobs):
         cap = _rej_cap(P, k2)
-        sc = launch_rrf_scan(key, lo, hi_start + (P + cap) // 2 + 2, k2, cap, stream)
+        sc = launch_rrf_scan(key, lo, hi_start + (P + cap) // 2 + 2, k2, cap, stream, comm)
         sc.tag = i
-        if i == 0:
+        if i == 0 and sc.comm is None:
             # the first draw's cursor is known now: its finish goes right behind
-            # its scan, so the host need not wait for the later scans
+            # its scan, so the host need not wait for the later scans.  (Not with
+            # a multi-rank comm: its gather would sit in NCCL's queue ahead of the
+            # right-hand-side all-reduces issued next and stall them behind the scan.)
             sc.pre = _enqueue_finish(sc, c, P)
         scans.append(sc)
         # the next call starts after the hash + sign draws and the normals; a

@@ -260,7 +260,8 @@ class _Run:
         # every mode's rejection scan is enqueued now (their starts are
         # bracketed); they run on the side stream while the main stream builds
         # layouts and TensorSketch right-hand sides
-        scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side)
+        scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
+                               self.comm)
         with torch.cuda.stream(main):
             self.draw_ts_ops()
             if self.sparse:  # layouts first (with TS buckets folded in): RRF stage 1 and the

@@ -120,3 +120,67 @@ def test_gloo_world2_partial_sketches_sum_to_full():
     core = rng.standard_normal((3, 3, 3))
     assert results[0]["cross"] == pytest.approx(float(np.vdot(orc.project_all(full, A), core)), rel=1e-12)
     assert results[1]["n2"] == pytest.approx(float(np.sum(vals ** 2)), rel=1e-13)
+
+
+def _rejections(raw, lo, k):
+    """Absolute 32-bit positions 2r + half of the Lemire rejections for bound k
+    among raw words raw[0..] starting at raw index lo (numpy's buffered u32:
+    low half first)."""
+    thresh = (2 ** 32 - k) % k
+    lo32 = (raw & 0xFFFFFFFF).astype(np.uint64)
+    hi32 = (raw >> np.uint64(32)).astype(np.uint64)
+    out = []
+    for half, v in ((0, lo32), (1, hi32)):
+        idx = np.nonzero(((v * np.uint64(k)) & np.uint64(0xFFFFFFFF)) < thresh)[0]
+        out.append(2 * (lo + idx.astype(np.int64)) + half)
+    return np.sort(np.concatenate(out))
+
+
+def _scan_worker(rank, world, port, lo, hi, k, cap, out_q):
+    import torch
+    import torch.distributed as dist
+    from paper_2104_01101_b200.dist import Comm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Comm()
+    a, b = comm.split(lo, hi)
+    bg = np.random.Philox(key=np.array([11, 22], dtype=np.uint64))
+    raw = bg.random_raw(hi).astype(np.uint64)[a:b]  # raw words a..b-1 of the stream
+    mine = _rejections(raw, a, k)
+    # the device path: fixed-capacity list padded with UINT64_MAX + count
+    buf = torch.full((cap,), -1, dtype=torch.int64)
+    buf[:len(mine)] = torch.from_numpy(mine)
+    count = torch.tensor([len(mine)], dtype=torch.int64)
+    merged = comm.allgather(buf)
+    counts = comm.allgather(count)
+    out_q.put((rank, (a, b, merged.numpy(), counts.numpy())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_split_rejection_scan():
+    """Rank-split RRF rejection scan (sketching.launch_rrf_scan with a comm):
+    each rank scans its Comm.split share of the raw range; the gathered,
+    padded lists merged by the finish's sort equal the single-rank list."""
+    import multiprocessing as mp
+    lo, cap = 1000, 4096
+    k = 2 ** 31 + 5  # large bound: rejection probability ~1/2, many positions
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_scan_worker, args=(r, 2, port, lo, lo + 2000, k, cap, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (a0, b0, m0, c0), (a1, b1, m1, c1) = res[0], res[1]
+    assert (a0, b1) == (lo, lo + 2000) and b0 == a1  # disjoint cover of the range
+    assert np.array_equal(m0, m1) and np.array_equal(c0, c1)
+    merged = np.sort(m0.astype(np.uint64))[: int(c0.sum())].astype(np.int64)
+    bg = np.random.Philox(key=np.array([11, 22], dtype=np.uint64))
+    ref = _rejections(bg.random_raw(lo + 2000).astype(np.uint64)[lo:], lo, k)
+    assert np.array_equal(merged, ref)
