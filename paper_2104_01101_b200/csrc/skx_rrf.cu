@@ -63,6 +63,27 @@ struct RrfRng {
   uint32_t k2;
 };
 
+// q(j) from a shared-memory bucket table: cnt[b] = #{d_i < b << shift}
+// (kRrfBuckets buckets over the column range), then the few d entries inside
+// j's bucket (usually none: ~1e2 rejections over 4096 buckets).
+constexpr int kRrfBuckets = 4096;
+
+__device__ __forceinline__ uint64_t count_le_tab(const RrfRng& r, const uint32_t* cnt, int shift,
+                                                uint64_t j) {
+  const uint64_t b = j >> shift;
+  uint32_t i = cnt[b];
+  const uint32_t e = cnt[b + 1];
+  while (i < e && r.d[i] <= j) ++i;
+  return i;
+}
+
+__device__ __forceinline__ uint32_t rrf_entry_q(const RrfRng& r, uint64_t j, uint64_t q) {
+  const uint32_t hu = r.st.at(q);
+  const uint32_t h = (uint32_t)(((uint64_t)hu * r.k2) >> 32);
+  const uint32_t su = r.st.at(r.sign_q0 + j);
+  return h | (su & 0x80000000u);  // integers(0,2) = u >> 31; sign = 1 - 2g
+}
+
 __device__ __forceinline__ uint32_t rrf_entry(const RrfRng& r, uint64_t j) {
   const uint64_t q = j + count_le(r.d, r.nd, j);
   const uint32_t hu = r.st.at(q);
@@ -96,6 +117,22 @@ __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t s_
   const int64_t k2 = r.k2;
   double* acc = smem + (size_t)wid * (k2 + 32);
   double* stage = acc + k2;
+  // bucket table of the sorted rejection offsets (after the accumulators)
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + (size_t)nw * (k2 + 32));
+  uint64_t P = 1;
+  for (int k = 0; k < NO; ++k) P *= (uint64_t)oe.ext[k];
+  int shift = 0;
+  while ((P >> shift) >= (uint64_t)kRrfBuckets) ++shift;
+  for (int b = threadIdx.x; b <= kRrfBuckets; b += blockDim.x) {
+    const uint64_t v = (uint64_t)b << shift;  // count d_i < v
+    int64_t lo = 0, hi = r.nd;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (r.d[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    cnt[b] = (uint32_t)lo;
+  }
+  __syncthreads();
   const int64_t gw = blockIdx.x * (int64_t)nw + wid;
   const int64_t tw = (int64_t)gridDim.x * nw;
   for (int64_t col = gw; col < s_n; col += tw) {
@@ -119,7 +156,7 @@ __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t s_
         for (int k = 0; k < NO; ++k)
           j = j * (uint64_t)oe.ext[k] +
               (uint64_t)((uint32_t)c[u][k] & (k == NO - 1 ? c1_mask : 0xffffffffu));
-        const uint32_t t = rrf_entry(r, j);
+        const uint32_t t = rrf_entry_q(r, j, j + count_le_tab(r, cnt, shift, j));
         bk[u] = ok ? pk_bucket(t) : kNoBucket;
         v[u] = pk_neg(t) ? -v[u] : v[u];
       }
@@ -202,14 +239,16 @@ extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n
                                   uint32_t c1_mask, double* stage1, void* stream) {
   SKX_REQUIRE(n_other >= 1 && n_other <= 4, "skx_rrf_stage1_coo: 1..4 other modes");
   const int64_t per = (k2 + 32) * 8;
-  int nw = (int)imin(8, (int64_t)(max_smem_optin() - 1024) / per);
+  const int64_t tab_bytes = (kRrfBuckets + 1) * 4;
+  int nw = (int)imin(8, (int64_t)(max_smem_optin() - 1024 - tab_bytes) / per);
   SKX_REQUIRE(nw >= 1, "skx_rrf_stage1_coo: k2 too large for shared memory");
+  SKX_REQUIRE(nrej < (int64_t(1) << 32), "skx_rrf_stage1_coo: rejection list too long");
   if (s_n == 0) return SKX_OK;
   RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
   OthExt oe{};
   oe.n = n_other;
   for (int k = 0; k < n_other; ++k) oe.ext[k] = ext_h[k];
-  const size_t smem = (size_t)nw * per;
+  const size_t smem = (size_t)nw * per + tab_bytes;
   auto kern = n_other == 1 ? k_rrf_coo<4, 1>
             : n_other == 2 ? k_rrf_coo<4, 2>
             : n_other == 3 ? k_rrf_coo<4, 3>
