@@ -57,9 +57,14 @@ class Comm:
         if self.world == 1:
             return t
         import torch
-        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
-        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        return out
+        t = t.contiguous()
+        if self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t, group=self.group)
+        return torch.cat(parts)
 
     def split(self, lo, hi):
         """This rank's contiguous share of the integer range [lo, hi)."""

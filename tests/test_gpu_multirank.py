@@ -1,0 +1,87 @@
+"""GPU: the multi-rank driver path against the single-process run.
+
+Two processes share the one GPU of the test box and talk over gloo (host-side
+collectives, so no kernel waits on another rank's kernel): each rank holds its
+mode-0 slab of the nonzeros, splits the RRF rejection scans, and all-reduces
+its partial sketches; the model must equal the single-process model to
+rounding (the partial sums are added in a different order)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests.conftest import canon, relerr
+
+pytestmark = pytest.mark.gpu
+
+SHAPE = (120, 90, 70)
+NNZ = 40_000
+CONFIGS = {
+    "ts": dict(ranks=(4, 5, 3), max_sweeps=3, sketch="tensorsketch", sketch_size=400, seed=3),
+    "lev": dict(ranks=(4, 5, 3), max_sweeps=3, sketch="leverage-random", sketch_size=600, seed=4),
+}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    import paper_2104_01101_b200 as skx
+    from paper_2104_01101_b200.dist import Comm, shard_device_coo
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from paper_2104_01101_b200.tucker import sketched_tucker_als_dev
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Comm()
+    c, v = planted_cp_coo_host(SHAPE, NNZ, rank=3, seed=1)
+    coords = torch.from_numpy(c.T.astype(np.int32)).cuda()
+    vals = torch.from_numpy(v).cuda()
+    cs, vs, _ = shard_device_coo(coords, vals, SHAPE, world, rank)
+    st = skx.SparseTensor.from_device(SHAPE, cs, vs)
+    out = {}
+    for tag, cfg in CONFIGS.items():
+        core, fac, tr = sketched_tucker_als_dev(st, skx.TuckerConfig(**cfg), comm)
+        out[tag] = (core.cpu().numpy(), [a.cpu().numpy() for a in fac], tr.fitness, tr.residuals)
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_match_single_process():
+    import multiprocessing as mp
+    import paper_2104_01101_b200 as skx
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c, v = planted_cp_coo_host(SHAPE, NNZ, rank=3, seed=1)
+    st = skx.SparseTensor(SHAPE, c, v)
+    for tag, cfg in CONFIGS.items():
+        model, tr = skx.sketched_tucker_als(st, skx.TuckerConfig(**cfg))
+        ref_f, ref_c = canon(model.factors, model.core)
+        for r in (0, 1):
+            core, fac, fit, resid = res[r][tag]
+            got_f, got_c = canon(fac, core)
+            for a, b in zip(got_f, ref_f):
+                assert relerr(a, b) <= 1e-10, (tag, r, relerr(a, b))
+            assert relerr(got_c, ref_c) <= 1e-10
+            assert np.allclose(fit, tr.fitness, rtol=0, atol=1e-12)
+            assert np.allclose(resid, tr.residuals, rtol=1e-10)
