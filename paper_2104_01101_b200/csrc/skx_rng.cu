@@ -292,15 +292,23 @@ __global__ void k_lemire_scan(uint64_t k0, uint64_t k1, uint64_t raw_lo, uint64_
   for (uint64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
     const uint64_t b = b_first + t;
     const U64x4 blk = philox_block(k0, k1, b + 1);
-    // branch-free screen of the 8 halves (rejections are ~1e-8 rare); the
-    // range checks only run for a block that has a candidate
-    uint32_t flag = 0;
+    // branch-free screen of the 8 halves (rejections are ~1e-8 rare): the
+    // minimum low product (integer min on the ALU pipe, which the Philox
+    // multiplies leave idle) decides; the per-half flags and range checks only
+    // run for a block that has a candidate
+    uint32_t mn = 0xffffffffu;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      flag |= (uint32_t)((uint32_t)blk.v[w] * k < thresh) << (2 * w);
-      flag |= (uint32_t)((uint32_t)(blk.v[w] >> 32) * k < thresh) << (2 * w + 1);
+      mn = min(mn, (uint32_t)blk.v[w] * k);
+      mn = min(mn, (uint32_t)(blk.v[w] >> 32) * k);
     }
-    if (flag) {
+    if (mn < thresh) {
+      uint32_t flag = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        flag |= (uint32_t)((uint32_t)blk.v[w] * k < thresh) << (2 * w);
+        flag |= (uint32_t)((uint32_t)(blk.v[w] >> 32) * k < thresh) << (2 * w + 1);
+      }
       for (int bit = 0; bit < 8; ++bit) {
         if (!((flag >> bit) & 1)) continue;
         const uint64_t r = 4 * b + (bit >> 1);

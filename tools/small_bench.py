@@ -37,5 +37,16 @@ def main():
         print(f"jacobi n={n} (rank 10): {timeit(lambda: jacobi_svd_dev(lr)):.1f} us")
 
 
+
+
+def torch_chol():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    z = torch.randn(1600, 100, dtype=torch.float64, device="cuda", generator=g)
+    gram = z.t() @ z
+    print(f"torch.linalg.cholesky_ex n=100: {timeit(lambda: torch.linalg.cholesky_ex(gram, upper=True)):.1f} us")
+    print(f"chol_upper_dev n=100: {timeit(lambda: chol_upper_dev(gram)):.1f} us")
+
+
 if __name__ == "__main__":
     main()
+    torch_chol()
