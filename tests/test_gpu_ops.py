@@ -472,3 +472,52 @@ def test_rsvd_hits_matches_dense(m, r, s, rank, nh):
     assert relerr(a1c, a0c) <= 1e-11
     assert relerr(c1, c0) <= 1e-11
     assert float(res1) == pytest.approx(res0, rel=1e-11)
+
+
+def test_integration_md_ctypes_binding(skx, oracle):
+    """The raw ctypes binding shown in INTEGRATION.md (no package code on the
+    call path: skx_ts_tables, skx_coo_fibre_ts, skx_ts_rhs_coo) reproduces the
+    reference's ts_apply_rhs bit for bit."""
+    import ctypes
+    import torch
+    from paper_2104_01101_b200 import _native as nat
+    lib = ctypes.CDLL(nat.lib_path())
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    lib.skx_ts_tables.argtypes = [ctypes.c_int, vp, vp, i64, vp, vp]
+    lib.skx_coo_fibre_ts.argtypes = [vp, ctypes.c_int, i64, vp, vp, vp, vp, i64, vp, vp,
+                                     ctypes.POINTER(ctypes.c_uint32), vp,
+                                     ctypes.POINTER(ctypes.c_size_t), vp]
+    lib.skx_ts_rhs_coo.argtypes = [ctypes.c_int, i64, vp, vp, vp, vp, i64, ctypes.c_uint32,
+                                   ctypes.c_int, vp, vp]
+    shape, m, mode = (60, 70, 80), 300, 1
+    c, v = _coo_rand(shape, 20000, 11)
+    ext = np.array([s for k, s in enumerate(shape) if k != mode], dtype=np.int64)
+    shp = np.array(shape, dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(ext)[:-1]]).astype(np.int64)
+    g = skx.make_rng(4)
+    coeffs = np.stack([np.concatenate([g.integers(0, 2 ** 31 - 1, 4, dtype=np.int64),
+                                       g.integers(0, 2 ** 31 - 1, 5, dtype=np.int64)])
+                       for _ in range(2)])
+    dc = torch.from_numpy(np.ascontiguousarray(c.T.astype(np.int32))).cuda()
+    dv = torch.from_numpy(v).cuda()
+    tab = torch.empty(int(ext.sum()), dtype=torch.int32, device="cuda")
+    assert lib.skx_ts_tables(2, ext.ctypes.data_as(vp), coeffs.ctypes.data_as(vp), m,
+                             vp(tab.data_ptr()), None) == 0
+    rec = torch.empty(2 * len(v), dtype=torch.float64, device="cuda")
+    colptr = torch.empty(shape[mode] + 1, dtype=torch.int64, device="cuda")
+    mask, ws_n = ctypes.c_uint32(0), ctypes.c_size_t(0)
+    args = (shp.ctypes.data_as(vp), mode, len(v), vp(dc.data_ptr()), vp(dv.data_ptr()),
+            vp(tab.data_ptr()), off.ctypes.data_as(vp), m, vp(rec.data_ptr()),
+            vp(colptr.data_ptr()), ctypes.byref(mask))
+    assert lib.skx_coo_fibre_ts(*args, None, ctypes.byref(ws_n), None) == 0
+    ws = torch.empty(ws_n.value, dtype=torch.uint8, device="cuda")
+    assert lib.skx_coo_fibre_ts(*args, vp(ws.data_ptr()), ctypes.byref(ws_n), None) == 0
+    yt = torch.empty((shape[mode], m), dtype=torch.float64, device="cuda")
+    assert lib.skx_ts_rhs_coo(2, shape[mode], vp(colptr.data_ptr()), vp(rec.data_ptr()),
+                              vp(tab.data_ptr()), off.ctypes.data_as(vp), m, mask.value,
+                              mask.value.bit_length(), vp(yt.data_ptr()), None) == 0
+    torch.cuda.synchronize()
+    # the same operator through the reference's own draw order and the oracle
+    hs, ss = oracle.ts_tables(tuple(ext), m, oracle.generator(4))
+    ref = oracle.ts_rhs(hs, ss, tuple(ext), m, oracle.unfold_t(oracle.Coo(shape, c, v), mode))
+    assert np.array_equal(yt.cpu().numpy().T, ref)
