@@ -29,6 +29,20 @@ from . import _native as nat
 
 
 # ============================================================ host types
+# SparseTensor(shape, coords, values) with at least this many nonzeros is
+# sorted and validated on the GPU (same result as the host lexsort)
+DEVICE_INGEST_NNZ = 1 << 20
+
+
+def _device_ingest_ok(shape):
+    if any(int(x) >= (1 << 31) for x in shape) or float(np.prod([float(x) for x in shape])) >= 2.0 ** 62:
+        return False
+    try:
+        return _torch().cuda.is_available()
+    except Exception:
+        return False
+
+
 class SparseTensor:
     """Order-N COO tensor (src/tensors.py:26-98): coords (nnz, N) int64
     lexsorted, duplicates rejected, immutable."""
@@ -45,6 +59,12 @@ class SparseTensor:
             raise ValueError("coordinate width does not match tensor order")
         if coords.shape[0] != values.shape[0]:
             raise ValueError("number of coordinates does not match number of values")
+        if coords.shape[0] >= DEVICE_INGEST_NNZ and _device_ingest_ok(shape):
+            # large inputs: validate, lexsort and deduplicate-check on the GPU
+            # (SURVEY 8f rank 1); the host arrays are materialised on demand
+            self._init(shape, None, None)
+            self._device = DeviceCoo.ingest(shape, coords, values)
+            return
         if coords.size and ((coords < 0).any() or (coords >= np.asarray(shape)).any()):
             raise ValueError("coordinate out of range")
         order = np.lexsort(coords.T[::-1])
@@ -239,6 +259,30 @@ class DeviceCoo:
         cd = c64.to("cuda", non_blocking=True)
         vd = v.to("cuda", non_blocking=True)
         return cls(st.shape, cd.t().to(torch.int32).contiguous(), vd)
+
+    @classmethod
+    def ingest(cls, shape, coords, values):
+        """Unsorted host COO -> lexsorted DeviceCoo (src/tensors.py:35-60
+        semantics: range check, lexsort, duplicate rejection) on the GPU: the
+        linearised int64 key (C order) is radix-sorted and adjacent keys are
+        compared."""
+        torch = _torch()
+        shape = tuple(int(x) for x in shape)
+        nd = len(shape)
+        c = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.int64)).cuda()
+        v = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).cuda()
+        ext = torch.tensor(shape, dtype=torch.int64, device="cuda")
+        if bool(((c < 0) | (c >= ext)).any()):
+            raise ValueError("coordinate out of range")
+        key = torch.zeros(c.shape[0], dtype=torch.int64, device="cuda")
+        for k in range(nd):
+            key = key * shape[k] + c[:, k]
+        key, perm = torch.sort(key)
+        if key.numel() > 1 and bool((key[1:] == key[:-1]).any()):
+            raise ValueError("duplicate coordinates")
+        del key
+        cs = c.t()[:, perm].to(torch.int32).contiguous()
+        return cls(shape, cs, v[perm].contiguous())
 
     @classmethod
     def from_torch(cls, shape, coords, vals, validate=True):

@@ -521,3 +521,28 @@ def test_integration_md_ctypes_binding(skx, oracle):
     hs, ss = oracle.ts_tables(tuple(ext), m, oracle.generator(4))
     ref = oracle.ts_rhs(hs, ss, tuple(ext), m, oracle.unfold_t(oracle.Coo(shape, c, v), mode))
     assert np.array_equal(yt.cpu().numpy().T, ref)
+
+
+def test_device_ingest_matches_host_lexsort(skx, monkeypatch):
+    """SparseTensor(shape, coords, values) above DEVICE_INGEST_NNZ sorts and
+    validates on the GPU: same arrays as the host
+    np.lexsort path, same errors for duplicates and out-of-range coordinates."""
+    from paper_2104_01101_b200 import tensors
+    rng = np.random.default_rng(12)
+    shape = (300, 200, 150)
+    lin = rng.choice(int(np.prod(shape)), 50_000, replace=False)
+    coords = np.stack(np.unravel_index(lin, shape), axis=1).astype(np.int64)
+    vals = rng.standard_normal(len(lin))
+    host = skx.SparseTensor(shape, coords, vals)          # below threshold: host lexsort
+    monkeypatch.setattr(tensors, "DEVICE_INGEST_NNZ", 1000)
+    dev = skx.SparseTensor(shape, coords, vals)
+    assert dev._device is not None
+    assert np.array_equal(dev.coords, host.coords) and np.array_equal(dev.values, host.values)
+    bad = coords.copy()
+    bad[7] = bad[3]
+    with pytest.raises(ValueError, match="duplicate"):
+        skx.SparseTensor(shape, bad, vals)
+    bad = coords.copy()
+    bad[5, 1] = shape[1]
+    with pytest.raises(ValueError, match="out of range"):
+        skx.SparseTensor(shape, bad, vals)
