@@ -282,28 +282,40 @@ def resid_dev(z, core_t, a, y):
 
 def sketch_qr_dev(z):
     """Reduced QR of the sketched system Z (m x r) with the reference's rank
-    test.  r <= 128: CholeskyQR2 (two small Grams, two one-CTA Choleskys, two
-    TRSMs -- no LAPACK panel); it is used only when safe (both Choleskys
-    succeed and diag(R) spans < 1e6, i.e. cond(Z) far below eps^-1/2),
-    otherwise the Householder QR of cuSOLVER runs, giving the same rank
-    decision as src/linalg.py:44-52.  One host sync decides."""
+    test.  r <= 128: Cholesky QR (small Gram, one-CTA Cholesky, TRSM -- no
+    LAPACK panel).  One pass already gives Q orthonormal to 1e-13 for the
+    well-conditioned Z a TensorSketch of orthonormal factors produces (the
+    orthogonality defect of Q is measured, not assumed); otherwise a second
+    pass (CholeskyQR2), and when even that is unsafe (first Cholesky fails or
+    diag(R) spans >= 1e6, i.e. cond(Z) near eps^-1/2) the Householder QR of
+    cuSOLVER runs -- the same rank decision as src/linalg.py:44-52.  One host
+    sync decides (a second only on the CholeskyQR2 path)."""
     torch = _torch()
     m, r = z.shape
     if r > 128 or m < r:
         return qr_flag_dev(z)
-    r1, i1 = chol_upper_dev(z.transpose(0, 1) @ z)
+    g1 = z.transpose(0, 1) @ z
+    r1, i1 = chol_upper_dev(g1)
     z1 = torch.linalg.solve_triangular(r1, z, upper=True, left=False)
-    r2, i2 = chol_upper_dev(z1.transpose(0, 1) @ z1)
-    q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
-    rz = r2 @ r1
+    g2 = z1.transpose(0, 1) @ z1
     d1 = torch.diagonal(r1)
-    unsafe = (i1[0] != 0) | (i2[0] != 0) | ~(d1.max() < 1e6 * d1.min())
-    tol = 1e-12 * torch.linalg.vector_norm(z)
-    bad = (torch.diagonal(rz).abs() < tol).any()
-    flags = torch.stack([unsafe, bad]).cpu()
+    unsafe = (i1[0] != 0) | ~(d1.max() < 1e6 * d1.min())
+    one_pass = (g2 - torch.eye(r, dtype=g2.dtype, device=g2.device)).abs().max() < 1e-13
+    tol = 1e-12 * torch.sqrt(torch.trace(g1))  # ||Z||_F
+    bad1 = (d1.abs() < tol).any()
+    flags = torch.stack([unsafe, one_pass, bad1]).cpu()
     if bool(flags[0]):
         return qr_flag_dev(z)
-    return q, rz, flags[1]
+    if bool(flags[1]):
+        return z1, r1, flags[2]
+    r2, i2 = chol_upper_dev(g2)
+    q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
+    rz = r2 @ r1
+    bad = (torch.diagonal(rz).abs() < tol).any()
+    flags2 = torch.stack([i2[0] != 0, bad]).cpu()
+    if bool(flags2[0]):
+        return qr_flag_dev(z)
+    return q, rz, flags2[1]
 
 
 def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
