@@ -230,10 +230,11 @@ class _Run:
         return [k for k in range(self.ndim) if k != n]
 
     def initialise_and_prep(self):
-        """RRF init of modes 1..N-1 plus the TensorSketch prep, scheduled so the
-        compute-bound rejection scans (side stream) overlap the memory-bound
-        layout builds and right-hand-side sketches (main stream).  Host draws
-        keep the reference order: per mode hash, signs, then Gaussian."""
+        """RRF init of modes 1..N-1 plus the TensorSketch prep: layouts and
+        right-hand sides (high-priority stream), then the compute-bound
+        rejection scans (normal-priority side stream) with each mode's RRF
+        stage 1 overlapping the next mode's scan.  Host draws keep the
+        reference order: per mode hash, signs, then Gaussian."""
         torch = _torch()
         init = self.cfg.init or "rrf"
         if init not in ("rrf", "random"):
@@ -246,8 +247,7 @@ class _Run:
         caller = torch.cuda.current_stream()
         # the compute-bound scans go to a normal-priority side stream in short
         # CTAs; everything else runs on a high-priority stream, so the block
-        # scheduler gives the layout sorts and sketches the SMs first and the
-        # scans fill whatever is idle
+        # scheduler gives RRF stage 1 the SMs ahead of the next scan
         side, main = _init_streams()
         side.wait_stream(caller)
         main.wait_stream(caller)
@@ -257,17 +257,21 @@ class _Run:
             width = self.cfg.resolved_rrf_width(self.ranks[n])
             P, k2 = _rrf_dims(self.shape, n, self.ranks[n], width)
             dims.append((P, k2, width))
-        # every mode's rejection scan is enqueued now (their starts are
-        # bracketed); they run on the side stream while the main stream builds
-        # layouts and TensorSketch right-hand sides
-        scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
-                               self.comm)
         with torch.cuda.stream(main):
             self.draw_ts_ops()
             if self.sparse:  # layouts first (with TS buckets folded in): RRF stage 1 and the
                 for n in range(self.ndim):  # TS sketches read them
                     self.d.fibre(n, self.ts_ops[n] if self.use_ts else None)
             self.prep()
+            # the scans start once the layouts and right-hand sides are done: the
+            # IMAD-bound scans and the memory/latency-bound layout work barely
+            # overlap on the same SMs (co-running gained < 1 ms at config 4), and
+            # alone the sketch kernels run at full speed.  Every mode's scan is
+            # enqueued now (later starts bracketed) on the normal-priority side
+            # stream; RRF stage 1 of mode n (high priority) overlaps scan n+1.
+            side.wait_stream(main)
+            scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
+                                   self.comm)
             for n, scan, (P, k2, width) in zip(modes, scans, dims):
                 tabs = finish_rrf_scan(scan, self.rng_init, P)
                 gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
