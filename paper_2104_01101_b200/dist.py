@@ -71,6 +71,52 @@ class Comm:
         n = hi - lo
         return lo + n * self.rank // self.world, lo + n * (self.rank + 1) // self.world
 
+    def row_chunk(self, s):
+        """Rows per rank of an s-row matrix split for reduce-scatter/all-gather
+        (equal chunks; the last rank's chunk is padded)."""
+        return -(-s // self.world)
+
+    def row_slab(self, s):
+        """[lo, hi) rows of an s-row matrix owned by this rank."""
+        c = self.row_chunk(s)
+        return min(self.rank * c, s), min((self.rank + 1) * c, s)
+
+    def reduce_scatter_rows(self, t):
+        """Sum over ranks of the (s, ...) tensor t, returning this rank's row slab
+        (row_slab(s)) -- half the traffic of an all-reduce, and every rank keeps
+        only its part."""
+        import torch
+        s = t.shape[0]
+        c = self.row_chunk(s)
+        if self.world == 1:
+            return t
+        flat = t.reshape(s, -1)
+        if c * self.world != s:
+            flat = torch.cat([flat, flat.new_zeros((c * self.world - s, flat.shape[1]))])
+        out = flat.new_empty((c, flat.shape[1]))
+        if self.dist.get_backend(self.group) == "nccl":
+            self.dist.reduce_scatter_tensor(out, flat.contiguous(), op=self.dist.ReduceOp.SUM,
+                                            group=self.group)
+        else:  # gloo has no reduce-scatter: all-reduce and keep the slab
+            full = flat.contiguous().clone()
+            self.dist.all_reduce(full, op=self.dist.ReduceOp.SUM, group=self.group)
+            out.copy_(full[self.rank * c:(self.rank + 1) * c])
+        lo, hi = self.row_slab(s)
+        return out[:hi - lo].reshape((hi - lo,) + tuple(t.shape[1:]))
+
+    def allgather_rows(self, t, s):
+        """Inverse of the row split: every rank's (row_slab) rows -> the full
+        (s, ...) tensor on all ranks."""
+        import torch
+        if self.world == 1:
+            return t
+        c = self.row_chunk(s)
+        flat = t.reshape(t.shape[0], -1)
+        if flat.shape[0] < c:
+            flat = torch.cat([flat, flat.new_zeros((c - flat.shape[0], flat.shape[1]))])
+        full = self.allgather(flat.contiguous().reshape(-1)).reshape(self.world * c, -1)[:s]
+        return full.reshape((s,) + tuple(t.shape[1:]))
+
 
 def shard_device_coo(coords, vals, shape, world, rank):
     """Rank `rank`'s mode-0 slab of a lexsorted (N, nnz) device COO."""

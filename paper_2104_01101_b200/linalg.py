@@ -351,11 +351,64 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
     return core_t, v.contiguous(), bad
 
 
+def rsvd_lrls_rows_dev(z, yt_loc, row_lo, s, rank, normals, comm, oversample=10, check=True):
+    """rsvd_lrls_dev + residual with the right-hand side split by columns over
+    ranks: this rank holds Y^T rows [row_lo, row_lo + rows) as
+    yt_loc.  Column-separable steps run on the local block -- Y G (all-reduced,
+    m x w), D^T = Y^T W (local rows), the residual (all-reduced scalar) -- and
+    the SVD of D goes through a TSQR whose leaves are the ranks' R factors
+    (all-gathered, w x w each).  Returns (core_t, a_loc (rows x rank), bad,
+    resid); the caller all-gathers a_loc."""
+    torch = _torch()
+    m, r = z.shape
+    if m < r:
+        raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
+    if rank > min(r, s):
+        raise ValueError(f"rank {rank} exceeds min({r}, {s})")
+    qz, rz, bad = sketch_qr_dev(z)
+    if check and bool(bad.item()):
+        raise RankDeficientError("rank-deficient sketched system")
+    width = min(rank + oversample, s)
+    g = normals.normal((s, width))  # the whole stream is drawn on every rank
+    rows = yt_loc.shape[0]
+    g_loc = g[row_lo:row_lo + rows]
+    y_loc = yt_loc.t()  # m x rows
+    if width < r:
+        yg = comm.allreduce((y_loc @ g_loc).contiguous())
+        c = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ yg, upper=True)
+        q, _ = torch.linalg.qr(c, mode="reduced")
+        wm = qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+        dt_loc = yt_loc @ wm  # rows x w  (= (W^T Y)^T on this block)
+    else:
+        xt_loc = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ y_loc, upper=True).t()
+        xg = comm.allreduce((xt_loc.t() @ g_loc).contiguous())
+        q, _ = torch.linalg.qr(xg, mode="reduced")
+        dt_loc = xt_loc @ q
+    # SVD of D (wd x s, wd = q's width): TSQR over the ranks' row blocks of D^T
+    wd = int(dt_loc.shape[1])
+    if rows >= wd:
+        r_loc = tsqr_r_dev(dt_loc.contiguous())
+    else:
+        pad = torch.zeros((wd, wd), dtype=torch.float64, device="cuda")
+        pad[:rows] = dt_loc
+        r_loc = tsqr_r_dev(pad)
+    r_all = comm.allgather(r_loc.contiguous().reshape(-1)).reshape(-1, wd)
+    rr = tsqr_r_dev(r_all)
+    u, sv, _ = _small_svd(rr.transpose(0, 1))
+    u = u[:, :rank]
+    sk = sv[:rank]
+    a_loc = (dt_loc @ u) / torch.where(sk > 0, sk, torch.ones_like(sk))
+    core_t = q @ (u * sk)
+    res2 = resid_dev(z, core_t, a_loc.contiguous(), y_loc) ** 2
+    res = torch.sqrt(comm.allreduce(res2.reshape(1))[0])
+    return core_t, a_loc, bad, res
+
+
 def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversample=10,
-                       check=True):
+                       check=True, hit_row=None):
     """rsvd_lrls_dev for a sparse right-hand side given as leverage-gather hits
     (row j's entries at hit_col/hit_val[hit_off[j]:hit_off[j+1]], distinct
-    columns per row), plus its residual.  Same algebra as the dense call on
+    columns per row; or explicit rows in hit_row), plus its residual.  Same algebra as the dense call on
     the m x s matrix of the hits, restricted to the set H of columns that hold
     a hit: every product with Y only sees Y's nonzero columns, D = W^T Y is
     zero outside H, so the SVD is taken of D_H and the factor rows outside H
@@ -373,8 +426,11 @@ def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversampl
         raise RankDeficientError("rank-deficient sketched system")
     width = min(rank + oversample, s)
     g = normals.normal((s, width))
-    counts = hit_off[1:] - hit_off[:-1]
-    rows = torch.repeat_interleave(torch.arange(m, device="cuda"), counts)
+    if hit_row is None:
+        counts = hit_off[1:] - hit_off[:-1]
+        rows = torch.repeat_interleave(torch.arange(m, device="cuda"), counts)
+    else:  # explicit (row, col, val) triples (e.g. gathered from several ranks)
+        rows = hit_row
     cols, inv = torch.unique(hit_col, return_inverse=True)
     nh = int(cols.numel())
     yh = torch.zeros((m, max(nh, 1)), dtype=torch.float64, device="cuda")

@@ -20,7 +20,7 @@ import numpy as np
 from . import _native as nat
 from . import rng as rngmod
 from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev, rsvd_lrls_hits_dev,
-                     top_svd_dev)
+                     rsvd_lrls_rows_dev, top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather_coo_dev,
                         gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
                         plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_rhs_mode_dev,
@@ -287,7 +287,9 @@ class _Run:
         # sparse: mode n's layout carries op's buckets when built for it
         yt = ts_rhs_mode_dev(op, self.d, n) if self.sparse else ts_rhs_dense_dev(op, self.d, n)
         if self.comm is not None:
-            self.comm.allreduce(yt)
+            # sum the partial sketches and keep this rank's rows (columns of Y_n):
+            # every later step on Y_n is column-separable
+            yt = self.comm.reduce_scatter_rows(yt)
         return yt
 
     def draw_ts_ops(self):
@@ -313,6 +315,12 @@ class _Run:
             if redraw:
                 self.build_ts(n)
             z = ts_kron_dev(self.ts_ops[n], others)
+            if self.comm is not None:  # this rank holds Y_n^T rows row_slab(s_n)
+                s_n = self.shape[n]
+                lo, _ = self.comm.row_slab(s_n)
+                core_t, a_loc, _, res = rsvd_lrls_rows_dev(z, self.ts_rhs[n], lo, s_n,
+                                                           self.ranks[n], self.normals, self.comm)
+                return core_t, self.comm.allgather_rows(a_loc.contiguous(), s_n), res
             y = self.ts_rhs[n].t()
         else:
             idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
@@ -321,18 +329,53 @@ class _Run:
                 keys, vals = self.d.keys(n)
                 ext = [self.shape[k] for k in self.others(n)]
                 off, col, val = gather_coo_dev(keys, vals, ext, self.shape[n], idx, w)
-                if self.comm is None and col.numel() < HITS_DENSITY * self.m * self.shape[n]:
+                row = None
+                total = col.numel()
+                if self.comm is not None:
+                    # every rank gathered the sampled fibres from its own shard:
+                    # the hits are disjoint, so their union is the full sample
+                    row, col, val = self._gather_hits(off, col, val)
+                    total = col.numel()
+                if total < HITS_DENSITY * self.m * self.shape[n]:
                     # mostly-empty sampled fibres: work on the hit columns only
                     core_t, a, _, res = rsvd_lrls_hits_dev(z, off, col, val, self.shape[n],
-                                                           self.ranks[n], self.normals)
+                                                           self.ranks[n], self.normals,
+                                                           hit_row=row)
                     return core_t, a, res
-                y = hits_to_dense(off, col, val, self.m, self.shape[n])
+                if row is None:
+                    y = hits_to_dense(off, col, val, self.m, self.shape[n])
+                else:
+                    torch = _torch()
+                    y = torch.zeros((self.m, self.shape[n]), dtype=torch.float64, device="cuda")
+                    y[row, col] = val
+                    return self._finish_dense(z, y, n)
             else:
                 y = gather_dense_dev(self.d, n, idx, w)
             if self.comm is not None:
                 self.comm.allreduce(y)
+        return self._finish_dense(z, y, n)
+
+    def _finish_dense(self, z, y, n):
         core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals)
         return core_t, a, resid_dev(z, core_t, a, y)
+
+    def _gather_hits(self, off, col, val):
+        """All ranks' sampled-fibre hits as (row, col, val) triples."""
+        torch = _torch()
+        counts = off[1:] - off[:-1]
+        row = torch.repeat_interleave(torch.arange(self.m, device="cuda"), counts)
+        n_loc = torch.tensor([col.numel()], dtype=torch.int64, device="cuda")
+        n_all = self.comm.allgather(n_loc)
+        cap = int(n_all.max().item())
+        def pad(t):
+            out = t.new_zeros(max(cap, 1))
+            out[:t.numel()] = t
+            return out
+        rows = self.comm.allgather(pad(row))
+        cols = self.comm.allgather(pad(col))
+        vals = self.comm.allgather(pad(val))
+        keep = torch.cat([torch.arange(max(cap, 1), device="cuda") < k for k in n_all.tolist()])
+        return rows[keep], cols[keep], vals[keep]
 
     def fold_core(self, core_t):
         ranks = self.ranks

@@ -184,3 +184,43 @@ def test_gloo_world2_split_rejection_scan():
     bg = np.random.Philox(key=np.array([11, 22], dtype=np.uint64))
     ref = _rejections(bg.random_raw(lo + 2000).astype(np.uint64)[lo:], lo, k)
     assert np.array_equal(merged, ref)
+
+
+def _rows_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2104_01101_b200.dist import Comm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Comm()
+    s = 7  # not divisible by the world size: padded chunks
+    t = torch.arange(s * 3, dtype=torch.float64).reshape(s, 3) * (rank + 1)
+    slab = comm.reduce_scatter_rows(t)
+    lo, hi = comm.row_slab(s)
+    back = comm.allgather_rows(slab * 2, s)
+    q.put((rank, (lo, hi, slab.numpy(), back.numpy())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_row_slabs():
+    """Comm.reduce_scatter_rows / allgather_rows (the column-sharded rsvd's
+    collectives): each rank gets its row slab of the sum; gathering the slabs
+    rebuilds the full matrix on every rank."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = np.arange(21, dtype=np.float64).reshape(7, 3) * 3  # (1 + 2) x
+    (lo0, hi0, s0, b0), (lo1, hi1, s1, b1) = res[0], res[1]
+    assert (lo0, hi0, lo1, hi1) == (0, 4, 4, 7)
+    assert np.array_equal(s0, full[0:4]) and np.array_equal(s1, full[4:7])
+    assert np.array_equal(b0, 2 * full) and np.array_equal(b1, 2 * full)

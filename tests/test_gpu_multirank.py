@@ -20,7 +20,12 @@ NNZ = 40_000
 CONFIGS = {
     "ts": dict(ranks=(4, 5, 3), max_sweeps=3, sketch="tensorsketch", sketch_size=400, seed=3),
     "lev": dict(ranks=(4, 5, 3), max_sweeps=3, sketch="leverage-random", sketch_size=600, seed=4),
+    "lev_dense": dict(ranks=(4, 5, 3), max_sweeps=2, sketch="leverage-random", sketch_size=500,
+                      seed=5),
 }
+# lev_dense forces the dense sampled right-hand side (all-reduced) instead of
+# the gathered-hits path
+DENSE_TAGS = ("lev_dense",)
 
 
 def _free_port():
@@ -49,8 +54,10 @@ def _worker(rank, world, port, q):
     vals = torch.from_numpy(v).cuda()
     cs, vs, _ = shard_device_coo(coords, vals, SHAPE, world, rank)
     st = skx.SparseTensor.from_device(SHAPE, cs, vs)
+    from paper_2104_01101_b200 import tucker
     out = {}
     for tag, cfg in CONFIGS.items():
+        tucker.HITS_DENSITY = 0.0 if tag in DENSE_TAGS else 0.05
         core, fac, tr = sketched_tucker_als_dev(st, skx.TuckerConfig(**cfg), comm)
         out[tag] = (core.cpu().numpy(), [a.cpu().numpy() for a in fac], tr.fitness, tr.residuals)
     q.put((rank, out))
@@ -74,7 +81,9 @@ def test_two_ranks_match_single_process():
         assert p.exitcode == 0
     c, v = planted_cp_coo_host(SHAPE, NNZ, rank=3, seed=1)
     st = skx.SparseTensor(SHAPE, c, v)
+    from paper_2104_01101_b200 import tucker
     for tag, cfg in CONFIGS.items():
+        tucker.HITS_DENSITY = 0.0 if tag in DENSE_TAGS else 0.05
         model, tr = skx.sketched_tucker_als(st, skx.TuckerConfig(**cfg))
         ref_f, ref_c = canon(model.factors, model.core)
         for r in (0, 1):
@@ -85,3 +94,4 @@ def test_two_ranks_match_single_process():
             assert relerr(got_c, ref_c) <= 1e-10
             assert np.allclose(fit, tr.fitness, rtol=0, atol=1e-12)
             assert np.allclose(resid, tr.residuals, rtol=1e-10)
+    tucker.HITS_DENSITY = 0.05
