@@ -260,7 +260,8 @@ def run_ours(args, cfgd):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, generated on GPU)",
         "config": {"workload": cfgd["workload"], "nnz": nnz, "shape": list(shape),
-                   "parallelism": f"nnz mode-0 slabs x{world} + NCCL all-reduce" if world > 1 else "single GPU",
+                   "parallelism": (f"nnz mode-0 slabs x{world}; NCCL reduce-scatter of Y_n by columns, "
+                                   "column-sharded rsvd, split RRF scans") if world > 1 else "single GPU",
                    "l2": f"inputs ({nnz * 32 / 1e9:.1f} GB canonical COO) larger than L2 (126 MB): "
                          "no flush needed between steps",
                    "sweeps_per_step": cfgd["sweeps"],
