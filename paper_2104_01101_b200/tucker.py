@@ -123,9 +123,11 @@ def _rrf_finish(d, n, rank, tabs, gauss, comm=None):
     """Composite sketch B = (T_(n) T_cs) G and its leading left singular vectors."""
     torch = _torch()
     st1 = rrf_stage1_dev(d, n, tabs)
-    if comm is not None:
-        comm.allreduce(st1)
     b = st1 @ torch.from_numpy(gauss).cuda()
+    if comm is not None:
+        # the Gaussian stage is linear: reduce the s_n x k1 product of each
+        # rank's partial stage 1 instead of the s_n x k2 stage 1 (SURVEY 8e)
+        comm.allreduce(b)
     if min(b.shape) < rank:
         raise ValueError(f"cannot extract {rank} directions from a {tuple(b.shape)} sketch")
     u, _, _ = top_svd_dev(b, rank)
