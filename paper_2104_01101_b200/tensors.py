@@ -524,10 +524,12 @@ def tucker_cross_dev(d, core, factors):
         fa = [f.contiguous() for f in factors]
         arr, fp = nat.host_ptrs(fa)
         cpt, rec0 = d.fibre(0) if d.ndim == 3 else (None, None)
+        # own workspace slot: the fitness may run on a side stream concurrently
+        # with the next sweep's sub-problems
         nat.call_ws("skx_tucker_cross_coo",
                     (d.ndim, sp_, rp, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp,
                      nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(rec0),
-                     ctypes.c_uint32(d.fibre_mask(0)), nat.ptr(out)))
+                     ctypes.c_uint32(d.fibre_mask(0)), nat.ptr(out)), slot=5)
         return out[0]
     proj = d
     for k, a in enumerate(factors):

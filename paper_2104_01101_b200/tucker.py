@@ -194,6 +194,19 @@ def _init_streams():
     return _STREAMS[dev]
 
 
+_FIT_STREAMS = {}
+
+
+def _fit_stream():
+    """Low-priority stream for the overlapped per-sweep fitness (one per device)."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _FIT_STREAMS:
+        lo, _ = torch.cuda.Stream.priority_range()
+        _FIT_STREAMS[dev] = torch.cuda.Stream(priority=lo)
+    return _FIT_STREAMS[dev]
+
+
 class _Run:
     """Device state of one sketched_tucker_als call."""
 
@@ -388,6 +401,29 @@ class _Run:
         torch = _torch()
         core = None
         res_dev, fit_dev, ev = [], [], []
+        # overlap the per-sweep fitness with the next sweep unless an early stop
+        # needs its value first (or collectives would interleave across streams):
+        # the sub-problems run on the high-priority stream, the fitness on a
+        # low-priority one, so the block scheduler serves the solves first
+        overlap = self.cfg.convergence_tol <= 0 and self.comm is None and self.sparse
+        fs = _fit_stream() if overlap else None
+        caller = torch.cuda.current_stream()
+        hi = _init_streams()[1] if overlap else caller
+        hi.wait_stream(caller)
+        with torch.cuda.stream(hi):
+            core = self._sweep_loop(trace, res_dev, fit_dev, ev, fs, overlap)
+        caller.wait_stream(hi)
+        if fs is not None:
+            caller.wait_stream(fs)
+        torch.cuda.synchronize()
+        trace.residuals.extend(torch.stack(res_dev).cpu().tolist() if res_dev else [])
+        trace.fitness.extend(torch.stack(fit_dev).cpu().tolist() if fit_dev else [])
+        trace.wall_s.extend(a.elapsed_time(b) / 1e3 for a, b in ev)
+        return core
+
+    def _sweep_loop(self, trace, res_dev, fit_dev, ev, fs, overlap):
+        torch = _torch()
+        core = None
         for _ in range(self.cfg.max_sweeps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -408,15 +444,22 @@ class _Run:
             core = self.fold_core(core_t)
             e1.record()
             ev.append((e0, e1))
-            f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, self.comm)
+            if overlap:
+                # the fitness of this sweep (a pass over the nonzeros) runs on a
+                # low-priority stream while the next sweep's sub-problems --
+                # mostly single-CTA and latency-bound -- proceed; they only read
+                # factors that are replaced (not overwritten) by later solves
+                fs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(fs):
+                    f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, self.comm)
+                for t in [core] + list(self.factors):
+                    t.record_stream(fs)
+            else:
+                f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, self.comm)
             fit_dev.append(f)
             if self.cfg.convergence_tol > 0 and len(fit_dev) > 1:
                 if abs(float(fit_dev[-1].item()) - float(fit_dev[-2].item())) < self.cfg.convergence_tol:
                     break
-        torch.cuda.synchronize()
-        trace.residuals.extend(torch.stack(res_dev).cpu().tolist() if res_dev else [])
-        trace.fitness.extend(torch.stack(fit_dev).cpu().tolist() if fit_dev else [])
-        trace.wall_s.extend(a.elapsed_time(b) / 1e3 for a, b in ev)
         return core
 
 
