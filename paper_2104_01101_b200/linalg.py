@@ -240,6 +240,13 @@ class NormalSource:
                      nat.ptr(out), nat.ptr(self.pos)), slot=1)
         return out
 
+    def prefetch(self):
+        """Generate the next batch now (e.g. while the GPU is otherwise busy
+        with compute-bound work) so the next draws are served from memory."""
+        left = 0 if self._buf is None else self._buf.numel() - self._off
+        if self.batch and left == 0:
+            self._buf, self._off = self._generate(self.batch), 0
+
     def normal(self, shape):
         torch = _torch()
         n = int(np.prod(shape))

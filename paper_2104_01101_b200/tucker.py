@@ -23,8 +23,8 @@ from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev,
                      rsvd_lrls_rows_dev, top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather_coo_dev,
                         gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
-                        plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_rhs_mode_dev,
-                        ts_rhs_dense_dev)
+                        plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
+                        ts_rhs_dense_dev, ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
                       matricize, shape_of)
 
@@ -287,6 +287,13 @@ class _Run:
             side.wait_stream(main)
             scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
                                    self.comm)
+            # small first-sweep inputs that do not depend on the RRF factors,
+            # built while the scans occupy the GPU: the Kronecker-sketch plans
+            # and the first batch of Gaussian test matrices
+            if self.use_ts:
+                for op in self.ts_ops:
+                    ts_kron_plan_dev(op)
+            self.normals.prefetch()
             for n, scan, (P, k2, width) in zip(modes, scans, dims):
                 tabs = finish_rrf_scan(scan, self.rng_init, P)
                 gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
