@@ -301,9 +301,6 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-#ifndef SKX_T3_MINB
-#define SKX_T3_MINB 1
-#endif
 template <int G>
 struct T3Rec {
   int32_t i1[G], i2[G];
@@ -320,7 +317,7 @@ struct T3Rows {
 // copied while its load is in flight.  R1T/R2T > 0 fix the ranks at compile
 // time (predicates fold away); 0 reads them at run time.
 template <int KS, int NT, int G, int R1T, int R2T>
-__global__ void __launch_bounds__(256, SKX_T3_MINB) k_tucker3_mma(const int64_t* __restrict__ colptr, int64_t s0,
+__global__ void __launch_bounds__(256) k_tucker3_mma(const int64_t* __restrict__ colptr, int64_t s0,
                                                      const double* __restrict__ rec, uint32_t c1_mask,
                                                      const double* __restrict__ A0,
                                                      const double* __restrict__ A1,
