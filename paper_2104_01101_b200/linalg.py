@@ -289,8 +289,8 @@ def resid_dev(z, core_t, a, y):
 
 def sketch_qr_dev(z):
     """Reduced QR of the sketched system Z (m x r) with the reference's rank
-    test.  r <= 128: Cholesky QR (small Gram, one-CTA Cholesky, TRSM -- no
-    LAPACK panel).  One pass already gives Q orthonormal to 1e-13 for the
+    test.  Cholesky QR (small Gram, Cholesky -- one-CTA libskx kernel up to
+    r = 128, cuSOLVER potrf beyond -- TRSM; no LAPACK Householder panel).  One pass already gives Q orthonormal to 1e-13 for the
     well-conditioned Z a TensorSketch of orthonormal factors produces (the
     orthogonality defect of Q is measured, not assumed); otherwise a second
     pass (CholeskyQR2), and when even that is unsafe (first Cholesky fails or
@@ -299,10 +299,17 @@ def sketch_qr_dev(z):
     sync decides (a second only on the CholeskyQR2 path)."""
     torch = _torch()
     m, r = z.shape
-    if r > 128 or m < r:
+    if m < r:
         return qr_flag_dev(z)
+
+    def chol(g):  # one-CTA libskx kernel up to 128; cuSOLVER potrf beyond (no host sync)
+        if r <= 128:
+            return chol_upper_dev(g)
+        u, info = torch.linalg.cholesky_ex(g, upper=True)
+        return u, info.view(1)
+
     g1 = z.transpose(0, 1) @ z
-    r1, i1 = chol_upper_dev(g1)
+    r1, i1 = chol(g1)
     z1 = torch.linalg.solve_triangular(r1, z, upper=True, left=False)
     g2 = z1.transpose(0, 1) @ z1
     d1 = torch.diagonal(r1)
@@ -315,7 +322,7 @@ def sketch_qr_dev(z):
         return qr_flag_dev(z)
     if bool(flags[1]):
         return z1, r1, flags[2]
-    r2, i2 = chol_upper_dev(g2)
+    r2, i2 = chol(g2)
     q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
     rz = r2 @ r1
     bad = (torch.diagonal(rz).abs() < tol).any()

@@ -17,6 +17,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+DENSE = {
+    1: dict(shape=(100,) * 3, ranks=(5,) * 3, sketch="tensorsketch", sketch_size=400, sweeps=5,
+            noise=1e-2),
+    2: dict(shape=(400,) * 3, ranks=(10,) * 3, sketch="leverage-random", sketch_size=3200,
+            sweeps=10, noise=1e-2),
+    3: dict(shape=(120,) * 4, ranks=(8,) * 4, sketch="tensorsketch", sketch_size=4096, sweeps=10,
+            noise=1e-3),
+}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
@@ -32,17 +42,32 @@ def main():
     from paper_2104_01101_b200.synth import planted_cp_coo_device
     from paper_2104_01101_b200.tucker import sketched_tucker_als_dev
 
-    cfgd = bench.CONFIGS[args.config]
-    coords, vals = planted_cp_coo_device(cfgd["shape"], cfgd["nnz"], rank=10, noise_sd=0.1, seed=0)
-    st = skx.SparseTensor.from_device(cfgd["shape"], coords, vals)
-    del coords, vals
+    if args.config in bench.CONFIGS:
+        cfgd = bench.CONFIGS[args.config]
+        coords, vals = planted_cp_coo_device(cfgd["shape"], cfgd["nnz"], rank=10, noise_sd=0.1,
+                                             seed=0)
+        st = skx.SparseTensor.from_device(cfgd["shape"], coords, vals)
+        del coords, vals
+    else:  # dense configs 1-3 (BASELINE.json), planted Tucker generated on the GPU
+        cfgd = DENSE[args.config]
+        g = torch.Generator(device="cuda").manual_seed(0)
+        r = cfgd["ranks"][0]
+        t = torch.randn((r,) * len(cfgd["shape"]), dtype=torch.float64, device="cuda", generator=g)
+        for n, s_n in enumerate(cfgd["shape"]):
+            q, _ = torch.linalg.qr(torch.randn(s_n, r, dtype=torch.float64, device="cuda", generator=g))
+            t = torch.movedim(torch.tensordot(q, t, dims=([1], [n])), 0, n)
+        e = torch.randn(t.shape, dtype=torch.float64, device="cuda", generator=g)
+        st = (t + e * (cfgd["noise"] * torch.linalg.vector_norm(t) / torch.linalg.vector_norm(e))).contiguous()
     cfg = skx.TuckerConfig(ranks=cfgd["ranks"], max_sweeps=cfgd["sweeps"], sketch=cfgd["sketch"],
                            sketch_size=cfgd["sketch_size"], seed=0)
+    sparse = not torch.is_tensor(st)
     for _ in range(2):
-        st._device.release_layouts()
+        if sparse:
+            st._device.release_layouts()
         sketched_tucker_als_dev(st, cfg)
     torch.cuda.synchronize()
-    st._device.release_layouts()
+    if sparse:
+        st._device.release_layouts()
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         t0 = time.perf_counter()
         sketched_tucker_als_dev(st, cfg)
