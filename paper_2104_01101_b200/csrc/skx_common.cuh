@@ -229,7 +229,36 @@ __device__ __forceinline__ void warp_ordered_add(double* acc, uint32_t bucket, d
   if (tags != nullptr) {
     if (has) tags[bucket] = (uint8_t)lane;
     __syncwarp();
-    distinct = !__any_sync(full, has && tags[bucket] != (uint8_t)lane);
+    // lanes whose tag store was overwritten share their bucket with another lane
+    const unsigned lose = __ballot_sync(full, has && tags[bucket] != (uint8_t)lane);
+    if (lose == 0u) {
+      if (has) acc[bucket] += val;
+    } else {
+      // rare collision path: resolve one group per losing lane (shfl + ballot,
+      // ~10x cheaper than match_any on 32 distinct values); each group's
+      // lowest lane adds its members in lane order, everyone else directly
+      stage[lane] = val;
+      __syncwarp();
+      unsigned pend = lose, grouped = 0u;
+      while (pend) {
+        const uint32_t bl = __shfl_sync(full, bucket, __ffs(pend) - 1);
+        const unsigned peers = __ballot_sync(full, bucket == bl);
+        grouped |= peers;
+        pend &= ~peers;
+        if (lane == (unsigned)(__ffs(peers) - 1)) {
+          double s = acc[bl];
+          unsigned mask = peers;
+          while (mask) {
+            s += stage[__ffs(mask) - 1];
+            mask &= mask - 1;
+          }
+          acc[bl] = s;
+        }
+      }
+      if (has && !((grouped >> lane) & 1u)) acc[bucket] += val;
+    }
+    __syncwarp();
+    return;
   } else {
     const unsigned peers = __match_any_sync(full, bucket);
     distinct = __all_sync(full, peers == (1u << lane) || !has);

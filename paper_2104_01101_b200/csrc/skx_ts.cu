@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_ts_rhs_coo(OtherTabs ot, int64_t s_n,
       for (int u = 0; u < U; ++u) {
         const uint32_t w = (uint32_t)r.c[u][NO - 1];
         hb[u] = (w & 0x7fffffffu) >> bb;
-        xs[u] = (w >> 31) ? -r.v[u] : r.v[u];
+        xs[u] = __longlong_as_double(__double_as_longlong(r.v[u]) ^ ((unsigned long long)(w >> 31) << 63));
       }
     } else {
       uint32_t t[U][NO];
@@ -244,73 +244,163 @@ __device__ __forceinline__ uint32_t dense_bucket(const uint32_t* tA, const uint3
   return h >= (uint32_t)m ? h - (uint32_t)m : h;
 }
 
-// Work item = (i_n, chunk) where chunk is a contiguous range of j of length
-// `chunk`; the CTA's warps split it into contiguous pieces, accumulate in
-// order, and the CTA writes acc_0 + acc_1 + ... (warp order) to part[item].
-template <bool FULL, int U>
-__global__ void __launch_bounds__(256) k_dense_rows(const double* __restrict__ t, DenseView v,
+// Row form: the flat (i_n, j) index space (j = a B + b over the other modes,
+// i_n-major) is split into equal contiguous ranges, one per warp of a
+// persistent grid.  A warp walks its range in chunks of 32 U values with a
+// private shared-memory accumulator (ordered adds, as in the sparse kernel),
+// the next chunk already in registers and the one PF chunks ahead prefetched
+// into L2; when its range crosses into the next i_n it streams the
+// accumulator out to part[(warp + i_n) m ..] (injective: ranges are ordered)
+// and k_sum_flat adds each i_n's pieces in warp order.
+template <bool FULL, int U, int PF>
+__global__ void __launch_bounds__(256) k_dense_flat(const double* __restrict__ t, DenseView v,
                                                     const uint32_t* __restrict__ tA,
                                                     const uint32_t* __restrict__ tB, int64_t m,
-                                                    int64_t chunk, int64_t nch,
-                                                    double* __restrict__ part) {
+                                                    int64_t per, double* __restrict__ part) {
   extern __shared__ double smem[];
+  constexpr int64_t CH = 32 * U;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  double* acc = smem + (size_t)wid * (m + 32);
+  const int64_t ww = rhs_warp_words(m);  // acc (m), stage (32), duplicate tags (m bytes)
+  double* acc = smem + (size_t)wid * ww;
   double* stage = acc + m;
-  const int64_t P = v.A * v.B;
-  const int64_t items = v.s_n * nch;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int64_t in = item / nch, ch = item % nch;
-    const int64_t j0 = ch * chunk, j1 = imin(j0 + chunk, P);
-    const int64_t per = (j1 - j0 + nw - 1) / nw;
-    const int64_t g0 = imin(j0 + wid * per, j1), g1 = imin(g0 + per, j1);
-    for (int64_t h = lane; h < m; h += 32) acc[h] = 0.0;
-    __syncwarp();
-    int64_t g = g0;
-    while (g < g1) {
-      const int64_t a = g / v.B, b0 = g - a * v.B;
-      const int64_t len = imin(v.B - b0, g1 - g);
-      const double* row = t + (a * v.s_n + in) * v.B + b0;
-      for (int64_t o = 0; o < len; o += 32 * U) {
-        uint32_t bk[U];
-        double x[U];
+  // tag-based duplicate detection pays off once collisions among 32 lanes are
+  // rare; small sketches (RRF, k2 ~ 1e2) take the match_any path throughout
+  uint8_t* tags = m >= 1024 ? reinterpret_cast<uint8_t*>(stage + 32) : nullptr;
+  const int64_t B = v.B, P = v.A * v.B, total = v.s_n * P;
+  const int64_t rs = v.s_n * B;                                 // stride of a
+  const uint32_t qc = (uint32_t)(CH / B), rc = (uint32_t)(CH % B);  // a, b advance per chunk
+  const int64_t dstep = (int64_t)qc * rs + rc, wrap = rs - B;   // pointer advance, wrap fix
+  const uint32_t Bu = (uint32_t)B;
+  const int64_t gw = blockIdx.x * (int64_t)nw + wid;
+  int64_t f = imin(gw * per, total);
+  const int64_t fend = imin(f + per, total);
+  if (f >= fend) return;
+  for (int64_t h = lane; h < m; h += 32) acc[h] = 0.0;
+  __syncwarp();
+  int64_t in = f / P;
+  while (f < fend) {
+    const int64_t jend = imin((in + 1) * P, fend) - in * P;
+    int64_t j = f - in * P;
+    const double* base = t + in * B;
+    // per slice u: element pointer, b (and a for the split tables; the full
+    // table is indexed by j itself), advanced incrementally by one chunk
+    const double* p[U];
+    uint32_t a[U], b[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t e = o + u * 32 + lane;
-          bk[u] = kNoBucket;
+    for (int u = 0; u < U; ++u) {
+      const int64_t jj = j + u * 32 + lane;
+      const int64_t aa = jj / B;
+      a[u] = (uint32_t)aa;
+      b[u] = (uint32_t)(jj - aa * B);
+      p[u] = base + aa * rs + b[u];
+    }
+    const uint32_t* tp = tA + j + lane;  // FULL table, slice u at tp + 32 u
+    // L2 prefetch cursor: 16 lanes x 128 bytes = one chunk, PF chunks ahead
+    int64_t pj = j + PF * CH + (lane & 15) * 16;
+    const double* pp;
+    uint32_t pb;
+    {
+      const int64_t pa = pj / B;
+      pb = (uint32_t)(pj - pa * B);
+      pp = base + pa * rs + pb;
+    }
+    auto step = [&](const double*& q, uint32_t& bb, uint32_t& aa) {
+      q += dstep;
+      bb += rc;
+      aa += qc;
+      if (bb >= Bu) {
+        bb -= Bu;
+        q += wrap;
+        ++aa;
+      }
+    };
+    // raw loads only: value and table words are consumed one chunk later
+    auto load = [&](int64_t j0, double (&x)[U], uint32_t (&ka)[U], uint32_t (&kb)[U]) {
+      const bool whole = j0 + CH <= jend;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (whole || j0 + u * 32 + lane < jend) {
+          if (FULL) {
+            ka[u] = __ldg(tp + u * 32);
+          } else {
+            ka[u] = __ldg(tA + a[u]);
+            kb[u] = __ldg(tB + b[u]);
+          }
+          x[u] = __ldcs(p[u]);
+        } else {
+          ka[u] = kNoBucket;
+          kb[u] = 0;
           x[u] = 0.0;
-          if (e < len) {
-            uint32_t neg;
-            bk[u] = dense_bucket<FULL>(tA, tB, a, b0 + e, v.B, m, neg);
-            const double xv = __ldcs(row + e);
-            x[u] = neg ? -xv : xv;
+        }
+        step(p[u], b[u], a[u]);
+      }
+      tp += CH;
+    };
+    auto process = [&](const double (&x)[U], const uint32_t (&ka)[U], const uint32_t (&kb)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t bk = kNoBucket, neg = 0;
+        if (ka[u] != kNoBucket) {
+          if (FULL) {
+            bk = pk_bucket(ka[u]);
+            neg = pk_neg(ka[u]);
+          } else {
+            const uint32_t h = pk_bucket(ka[u]) + pk_bucket(kb[u]);
+            bk = h >= (uint32_t)m ? h - (uint32_t)m : h;
+            neg = pk_neg(ka[u]) ^ pk_neg(kb[u]);
           }
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) warp_ordered_add(acc, bk[u], x[u], stage);
+        // sign flip on the high word (one LOP3 instead of two selects)
+        const double sx = __longlong_as_double(__double_as_longlong(x[u]) ^
+                                               ((unsigned long long)neg << 63));
+        warp_ordered_add(acc, bk, sx, stage, tags);
       }
-      g += len;
+    };
+    auto ahead = [&](int64_t j0, double (&x)[U], uint32_t (&ka)[U], uint32_t (&kb)[U]) {
+      load(j0, x, ka, kb);
+      if (lane < 16 && pj < jend) asm volatile("prefetch.global.L2 [%0];" ::"l"(pp));
+      uint32_t dummy = 0;
+      step(pp, pb, dummy);
+      pj += CH;
+    };
+    double xc[U], xn[U];
+    uint32_t ac[U], bc[U], an[U], bn[U];
+    load(j, xc, ac, bc);
+    while (true) {
+      const bool more = j + CH < jend;
+      if (more) ahead(j + CH, xn, an, bn);
+      process(xc, ac, bc);
+      j += CH;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xc[u] = xn[u];
+        ac[u] = an[u];
+        bc[u] = bn[u];
+      }
     }
-    __syncthreads();
-    double* dst = part + item * m;
-    for (int64_t h = threadIdx.x; h < m; h += blockDim.x) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += smem[(size_t)w * (m + 32) + h];
-      dst[h] = s;
+    double* dst = part + (gw + in) * m;
+    for (int64_t h = lane; h < m; h += 32) {
+      dst[h] = acc[h];
+      acc[h] = 0.0;
     }
-    __syncthreads();
+    __syncwarp();
+    f = (in + 1) * P;
+    ++in;
   }
 }
 
-// yt[i_n, :] = sum over chunks (in order) of part[(i_n, ch), :]
-__global__ void k_sum_chunks(const double* __restrict__ part, int64_t s_n, int64_t nch, int64_t m,
-                             double* __restrict__ yt) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// yt[i_n, h] = sum over the warps w whose range meets i_n (in order) of
+// part[(w + i_n) m + h]
+__global__ void k_sum_flat(const double* __restrict__ part, int64_t s_n, int64_t P, int64_t per,
+                           int64_t m, double* __restrict__ yt) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= s_n * m) return;
   const int64_t in = idx / m, h = idx - in * m;
+  const int64_t w0 = in * P / per, w1 = ((in + 1) * P - 1) / per;
   double s = 0.0;
-  for (int64_t c = 0; c < nch; ++c) s += part[(in * nch + c) * m + h];
+  for (int64_t w = w0; w <= w1; ++w) s += part[(w + in) * m + h];
   yt[idx] = s;
 }
 
@@ -339,6 +429,62 @@ __global__ void k_run_bounds(const uint32_t* __restrict__ keys, int64_t n, int64
     if ((int64_t)keys[mid] < c) lo = mid + 1; else hi = mid;
   }
   start[c] = lo;
+}
+
+// Segmented variant: task = (bucket c, segment k, column block); segment k
+// covers rows [k seg, (k+1) seg) of c's run, the last segment the rest; the
+// partial sums are then added segment by segment (fixed order) by
+// k_sum_segs.  Keeps the GPU busy when the bucket count m is small (RRF:
+// k2 ~ 1e2 buckets) or the runs are long.
+template <int CPL>
+__global__ void __launch_bounds__(256) k_gather_rows_seg(const double* __restrict__ t, int64_t s_n,
+                                                         const int64_t* __restrict__ start,
+                                                         const uint32_t* __restrict__ list,
+                                                         const uint32_t* __restrict__ neg_of,
+                                                         int64_t m, int64_t seg, int64_t nseg,
+                                                         double* __restrict__ part) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ncb = (s_n + 32 * CPL - 1) / (32 * CPL);
+  const int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + wid;
+  if (task >= m * nseg * ncb) return;
+  const int64_t cb = task % ncb, ck = task / ncb;
+  const int64_t c = ck / nseg, k = ck - c * nseg;
+  const int64_t col0 = cb * 32 * CPL;
+  double acc[CPL];
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
+  const int64_t rs = start[c], re = start[c + 1];
+  const int64_t r0 = imin(rs + k * seg, re), r1 = k == nseg - 1 ? re : imin(r0 + seg, re);
+  for (int64_t r = r0; r < r1; ++r) {
+    const uint32_t a = list[r];
+    const bool ng = neg_of[a] != 0;
+    const double* row = t + (int64_t)a * s_n;
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+      const int64_t col = col0 + u * 32 + lane;
+      if (col < s_n) {
+        const double x = __ldcs(row + col);
+        acc[u] += ng ? -x : x;
+      }
+    }
+  }
+  double* dst = part + ck * s_n;
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) {
+    const int64_t col = col0 + u * 32 + lane;
+    if (col < s_n) dst[col] = acc[u];
+  }
+}
+
+// yt[col, c] = sum_k part[(c, k), col], k ascending
+__global__ void k_sum_segs(const double* __restrict__ part, int64_t m, int64_t nseg, int64_t s_n,
+                           double* __restrict__ yt) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= m * s_n) return;
+  const int64_t col = idx / m, c = idx - col * m;
+  double s = 0.0;
+  for (int64_t k = 0; k < nseg; ++k) s += part[(c * nseg + k) * s_n + col];
+  yt[col * m + c] = s;
 }
 
 template <int CPL>
@@ -401,15 +547,6 @@ extern "C" int skx_ts_tables(int nmodes, const int64_t* extents_h, const int64_t
   return check_launch("k_ts_tables");
 }
 
-namespace {
-int warps_for(int64_t m) {
-  const int64_t per = (m + 32) * 8;
-  int64_t w = (int64_t)(max_smem_optin() - 1024) / per;
-  if (w > 8) w = 8;
-  return (int)w;
-}
-}  // namespace
-
 extern "C" int skx_ts_rhs_coo(int n_other, int64_t s_n, const int64_t* colptr, const void* rec,
                               const uint32_t* tab, const int64_t* tab_off_h, int64_t m,
                               uint32_t c1_mask, int packed_bb, double* yt, void* stream) {
@@ -458,6 +595,10 @@ static int dense_sketch(bool full, const double* t, int ndim, const int64_t* sha
     uint32_t* v_out = ar.take<uint32_t>(P);
     uint32_t* neg = ar.take<uint32_t>(P);
     int64_t* start = ar.take<int64_t>(m + 1);
+    // segments of kSeg rows (about 2 x the mean run length / kSeg per bucket)
+    constexpr int64_t kSeg = 256;
+    const int64_t nseg = imax(1, 2 * ((P / imax(m, 1) + kSeg - 1) / kSeg));
+    double* part = ar.take<double>((size_t)m * nseg * v.s_n);
     size_t cub_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, k_in, k_out, v_in, v_out, (int)P, 0, 32, s);
     void* cub_tmp = ar.take<char>(cub_bytes);
@@ -479,39 +620,42 @@ static int dense_sketch(bool full, const double* t, int ndim, const int64_t* sha
     k_run_bounds<<<(unsigned)((m + 1 + 255) / 256), 256, 0, s>>>(k_out, P, m, start);
     const int64_t s_n = v.s_n;
     if (s_n <= 32 * 4) {
-      const int64_t tasks = m * ((s_n + 127) / 128);
-      k_gather_rows<4><<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(t, s_n, start, v_out, neg, m, yt);
+      const int64_t tasks = m * nseg * ((s_n + 127) / 128);
+      k_gather_rows_seg<4><<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(t, s_n, start, v_out, neg, m,
+                                                                       kSeg, nseg, part);
     } else {
-      const int64_t tasks = m * ((s_n + 255) / 256);
-      k_gather_rows<8><<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(t, s_n, start, v_out, neg, m, yt);
+      const int64_t tasks = m * nseg * ((s_n + 255) / 256);
+      k_gather_rows_seg<8><<<(unsigned)((tasks + 7) / 8), 256, 0, s>>>(t, s_n, start, v_out, neg, m,
+                                                                       kSeg, nseg, part);
     }
-    return check_launch("dense sketch (gather form)", 4);
+    k_sum_segs<<<(unsigned)((m * s_n + 255) / 256), 256, 0, s>>>(part, m, nseg, s_n, yt);
+    return check_launch("dense sketch (gather form)", 5);
   }
-  const int nw = warps_for(m);
+  const int nw = warps_per_cta_for(rhs_warp_words(m) * 8);
   SKX_REQUIRE(nw >= 1, "dense sketch: sketch size %lld exceeds shared-memory capacity",
               (long long)m);
-  // chunk so that there are >= ~4 items per SM but each chunk is >= 64K values
-  int64_t chunk = imax(int64_t(1) << 16, (v.s_n * P) / ((int64_t)num_sms() * 4));
-  chunk = imin(chunk, int64_t(1) << 22);
-  if (chunk > P) chunk = P;
-  if (chunk < 1) chunk = 1;
-  const int64_t nch = (P + chunk - 1) / chunk;
-  double* part = ar.take<double>((size_t)v.s_n * nch * m);
+  SKX_REQUIRE(v.A < (int64_t(1) << 31) && v.B < (int64_t(1) << 31),
+              "dense sketch: other-mode extents too large for the row form");
+  const size_t smem = (size_t)nw * rhs_warp_words(m) * 8;
+  auto kern = full ? k_dense_flat<true, 8, 6> : k_dense_flat<false, 8, 6>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  // one range per resident warp, but at least 16K values per range
+  const int64_t total = v.s_n * P;
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  blocks = imax(1, imin(blocks, (total + 16384 * nw - 1) / (16384 * nw)));
+  const int64_t W = blocks * nw;
+  const int64_t per = (total + W - 1) / W;
+  double* part = ar.take<double>((size_t)(W + v.s_n) * m);
   if (ws == nullptr) {
     *ws_bytes = ar.used + 256;
     return SKX_OK;
   }
   SKX_REQUIRE(ar.ok(), "dense sketch: workspace too small");
-  const size_t smem = (size_t)nw * (m + 32) * 8;
-  auto kern = full ? k_dense_rows<true, 8> : k_dense_rows<false, 8>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t items = v.s_n * nch;
-  const int64_t blocks = imin((int64_t)num_sms() * per_sm, items);
-  kern<<<(unsigned)blocks, nw * 32, smem, s>>>(t, v, tA, tB, m, chunk, nch, part);
-  k_sum_chunks<<<(unsigned)((v.s_n * m + 255) / 256), 256, 0, s>>>(part, v.s_n, nch, m, yt);
+  kern<<<(unsigned)blocks, nw * 32, smem, s>>>(t, v, tA, tB, m, per, part);
+  k_sum_flat<<<(unsigned)((v.s_n * m + 255) / 256), 256, 0, s>>>(part, v.s_n, P, per, m, yt);
   return check_launch("dense sketch (row form)", 2);
 }
 

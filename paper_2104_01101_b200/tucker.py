@@ -25,7 +25,7 @@ from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather
                         gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
                         plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
                         ts_rhs_dense_dev, ts_rhs_mode_dev)
-from .tensors import (DeviceCoo, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
+from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
                       matricize, shape_of)
 
 SKETCH_KINDS = (None, "tensorsketch", "leverage-random", "leverage-deterministic")
@@ -224,13 +224,17 @@ class _Run:
         self.m = config.resolved_sketch_size()
         _check_sketch_size(self.m, self.ranks)
         self.cfg = config
-        self.d = device_of(t)
-        self.sparse = is_sparse_dev(self.d)
         self.comm = comm
-        n2 = self.d.norm2().clone() if self.sparse else (self.d * self.d).sum().view(1)
-        if comm is not None:
-            comm.allreduce(n2)
-        self.norm2 = n2[0]
+        self._host = None
+        if (isinstance(t, SparseTensor) and t._device is None and comm is None
+                and (config.init or "rrf") == "rrf" and self.ndim > 1):
+            # host COO: the upload is deferred into initialise_and_prep, where
+            # it overlaps the data-independent rejection scans
+            self._host = t
+            self.d = None
+            self.sparse = True
+        else:
+            self._attach(device_of(t))
         self.rng_init, self.rng_sketch, self.rng_solve = rngmod.split_rng(config.seed, 3)
         # one sweep's Gaussian test matrices (rsvd_lrls: s_n x min(R_n + 10, s_n))
         per_sweep = sum(s * min(r + 10, s) for s, r in zip(self.shape, self.ranks))
@@ -240,6 +244,14 @@ class _Run:
         self.ts_ops = [None] * self.ndim
         self.ts_rhs = [None] * self.ndim
         self.events = []
+
+    def _attach(self, d):
+        self.d = d
+        self.sparse = is_sparse_dev(d)
+        n2 = d.norm2().clone() if self.sparse else (d * d).sum().view(1)
+        if self.comm is not None:
+            self.comm.allreduce(n2)
+        self.norm2 = n2[0]
 
     def others(self, n):
         return [k for k in range(self.ndim) if k != n]
@@ -272,6 +284,17 @@ class _Run:
             width = self.cfg.resolved_rrf_width(self.ranks[n])
             P, k2 = _rrf_dims(self.shape, n, self.ranks[n], width)
             dims.append((P, k2, width))
+        scans = None
+        if self._host is not None:
+            # host input: the scans depend only on rng_init's position, so they
+            # run while the copy engine streams the COO arrays in
+            scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
+                                   self.comm)
+            with torch.cuda.stream(main):
+                self.draw_ts_ops()
+                self._host._device = DeviceCoo.from_host(self._host)
+                self._attach(self._host._device)
+                self._host = None
         with torch.cuda.stream(main):
             self.draw_ts_ops()
             if self.sparse:  # layouts first (with TS buckets folded in): RRF stage 1 and the
@@ -284,9 +307,10 @@ class _Run:
             # alone the sketch kernels run at full speed.  Every mode's scan is
             # enqueued now (later starts bracketed) on the normal-priority side
             # stream; RRF stage 1 of mode n (high priority) overlaps scan n+1.
-            side.wait_stream(main)
-            scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
-                                   self.comm)
+            if scans is None:
+                side.wait_stream(main)
+                scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims],
+                                       side, self.comm)
             # small first-sweep inputs that do not depend on the RRF factors,
             # built while the scans occupy the GPU: the Kronecker-sketch plans
             # and the first batch of Gaussian test matrices

@@ -1,5 +1,8 @@
 """Time the dense TensorSketch right-hand side (skx_ts_rhs_dense, K1d) on the
-config-3 shape (120^4 float64, m = 4096) per mode with CUDA events."""
+config-3 shape (120^4 float64, m = 4096) per mode with CUDA events.
+
+    python tools/dense_bench.py [shape=120,120,120,120] [m=4096] [modes=0,1,2,3]
+"""
 import os
 import sys
 
@@ -16,7 +19,8 @@ def main():
     m = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
     g = torch.Generator(device="cuda").manual_seed(0)
     t = torch.randn(shape, dtype=torch.float64, device="cuda", generator=g)
-    for n in range(len(shape)):
+    modes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else range(len(shape))
+    for n in modes:
         ext = tuple(shape[k] for k in range(len(shape)) if k != n)
         op = skx.TensorSketchOp.build(ext, m, skx.make_rng(n))
         ts_rhs_dense_dev(op, t, n)
