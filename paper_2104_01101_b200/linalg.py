@@ -231,6 +231,7 @@ class NormalSource:
         self.pos = torch.tensor([c.p], dtype=torch.int64, device="cuda")
         self.batch = int(batch)
         self._buf, self._off = None, 0
+        self._pending = []  # [(buffer, event)]: following batches, made on a side stream
 
     def _generate(self, n):
         torch = _torch()
@@ -247,10 +248,36 @@ class NormalSource:
         if self.batch and left == 0:
             self._buf, self._off = self._generate(self.batch), 0
 
+    def prefetch_async(self, stream):
+        """Enqueue one more batch on `stream` (the draws are data-independent)
+        unless a full batch beyond the buffered normals is already on its way;
+        the caller's stream waits for it only when it is first used."""
+        torch = _torch()
+        if not self.batch:
+            return
+        left = 0 if self._buf is None else self._buf.numel() - self._off
+        left += sum(b.numel() for b, _ in self._pending)
+        if left >= 2 * self.batch:
+            return
+        stream.wait_stream(torch.cuda.current_stream())  # device cursor order
+        with torch.cuda.stream(stream):
+            nxt = self._generate(self.batch)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self._pending.append((nxt, ev))
+
     def normal(self, shape):
         torch = _torch()
         n = int(np.prod(shape))
         left = 0 if self._buf is None else self._buf.numel() - self._off
+        while left < n and self._pending:
+            nxt, ev = self._pending.pop(0)
+            cur = torch.cuda.current_stream()
+            cur.wait_event(ev)
+            nxt.record_stream(cur)
+            self._buf = torch.cat([self._buf[self._off:], nxt]) if left else nxt
+            self._off = 0
+            left = self._buf.numel()
         if left < n:
             fresh = self._generate(max(n - left, self.batch))
             self._buf = torch.cat([self._buf[self._off:], fresh]) if left else fresh
@@ -261,7 +288,7 @@ class NormalSource:
 
     def sync_host(self):
         """Move the numpy Generator to where numpy would be (one D2H)."""
-        if self._buf is not None and self._off != self._buf.numel():
+        if self._pending or (self._buf is not None and self._off != self._buf.numel()):
             raise RuntimeError("NormalSource.sync_host: buffered normals not consumed")
         rngmod.set_cursor(self.gen, int(self.pos.item()))
 

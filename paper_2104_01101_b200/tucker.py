@@ -455,10 +455,14 @@ class _Run:
     def _sweep_loop(self, trace, res_dev, fit_dev, ev, fs, overlap):
         torch = _torch()
         core = None
-        for _ in range(self.cfg.max_sweeps):
+        for sweep in range(self.cfg.max_sweeps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
+            if overlap and sweep + 1 < self.cfg.max_sweeps:
+                # the next sweep's Gaussian test matrices, on the low-priority
+                # stream behind the previous fitness
+                self.normals.prefetch_async(fs)
             core_t = None
             for n in range(self.ndim):
                 try:
