@@ -244,6 +244,14 @@ int skx_chol_upper(const double* g, int n, double* r, int* info, void* stream);
 int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u, double* s,
                    double* v, void* stream);
 
+/* Middle step of the associated rsvd_lrls (src/linalg.py:105-110) for a test
+ * width w < r: with B = Q_z^T (Y G) (r x w, row-major) and the upper R_z
+ * (r x r, row-major), q = thin-Q of R_z^-1 B (Householder, LAPACK sign
+ * convention) and x = R_z^-T q, both r x w row-major.  One CTA; r <= 128,
+ * w <= 32.  Replaces np.linalg.solve / np.linalg.qr on the small operands. */
+int skx_lrls_mid(const double* rz, const double* b, int r, int w, double* q, double* x,
+                 void* stream);
+
 /* out[0] = sum(x^2) with a fixed-order reduction. */
 int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,
               void* stream);

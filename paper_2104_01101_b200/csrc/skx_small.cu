@@ -241,6 +241,143 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(const double* __restrict__ A
   for (int k = threadIdx.x; k < n; k += blockDim.x) S[k] = sv[ord[k]];
 }
 
+// Middle of Algorithm 5 (rsvd_lrls, src/linalg.py:87-113) for the associated
+// form used when the test width w < r:  C = R^-1 B (B = Q_z^T Y G, r x w),
+// C = Q T (Householder, as LAPACK geqr2/org2r), X = R^-T Q.  One CTA of w
+// warps, warp k owning column k: the triangular solves need only warp syncs;
+// R sits in shared memory with an odd leading dimension so that both its
+// row and its column walks are bank-conflict free.  Replaces two cuBLAS
+// TRSMs and a ~25-launch cuSOLVER QR.
+__global__ void __launch_bounds__(1024, 1) k_lrls_mid(const double* __restrict__ Rg,
+                                                     const double* __restrict__ Bg, int r, int w,
+                                                     double* __restrict__ Qg,
+                                                     double* __restrict__ Xg) {
+  extern __shared__ double sm[];
+  const int ld = r | 1;
+  double* R = sm;             // r x r upper, row-major, ld odd
+  double* C = R + r * ld;     // column-major, ld r
+  double* Q = C + r * w;      // column-major, ld r
+  double* tau = Q + r * w;    // w
+  double* rinv = tau + w;     // 1 / R_ii
+  const int tid = threadIdx.x, lane = tid & 31, k = tid >> 5;
+  for (int i = k; i < r; i += blockDim.x >> 5)
+    for (int j = lane; j < r; j += 32) R[i * ld + j] = Rg[(int64_t)i * r + j];
+  for (int i = tid; i < r; i += blockDim.x) rinv[i] = 1.0 / Rg[(int64_t)i * r + i];
+  for (int i = lane; i < r; i += 32) C[k * r + i] = Bg[(int64_t)i * w + k];
+  __syncthreads();
+  // 1. back substitution, warp k on column k held in registers (lane l owns
+  //    rows l, l + 32, ...): C <- R^-1 C
+  constexpr int kSl = 4;  // r <= 128
+  {
+    double* ck = C + k * r;
+    double c[kSl];
+#pragma unroll
+    for (int t = 0; t < kSl; ++t) c[t] = lane + 32 * t < r ? ck[lane + 32 * t] : 0.0;
+    // row i = 32 ti + ii lives in register slot ti (static after unrolling)
+#pragma unroll
+    for (int ti = kSl - 1; ti >= 0; --ti) {
+      for (int ii = 31; ii >= 0; --ii) {
+        const int i = 32 * ti + ii;
+        if (i >= r) continue;
+        const double xi = __shfl_sync(0xffffffffu, c[ti], ii) * rinv[i];
+#pragma unroll
+        for (int t = 0; t <= ti; ++t) {
+          const int l = lane + 32 * t;
+          const double upd = fma(-R[min(l, r - 1) * ld + i], xi, c[t]);
+          c[t] = l < i ? upd : (l == i ? xi : c[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kSl; ++t)
+      if (lane + 32 * t < r) ck[lane + 32 * t] = c[t];
+  }
+  __syncthreads();
+  // 2. Householder QR of C: v_j = [1; C[j+1:, j]], H_j = I - tau_j v v^T
+  for (int j = 0; j < w; ++j) {
+    if (k == j) {
+      double* cj = C + j * r;
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < r; i += 32) ss = fma(cj[i], cj[i], ss);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const double alpha = cj[j];
+      double t = 0.0, beta = alpha, scale = 0.0;
+      if (ss != 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+        t = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      __syncwarp();
+      for (int i = j + 1 + lane; i < r; i += 32) cj[i] *= scale;
+      if (lane == 0) {
+        cj[j] = beta;
+        tau[j] = t;
+      }
+    }
+    __syncthreads();
+    if (k > j) {
+      const double tj = tau[j];
+      const double* v = C + j * r;
+      double* ck = C + k * r;
+      double d = 0.0;
+      for (int i = j + 1 + lane; i < r; i += 32) d = fma(v[i], ck[i], d);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      d = tj * (ck[j] + d);
+      __syncwarp();
+      if (lane == 0) ck[j] -= d;
+      for (int i = j + 1 + lane; i < r; i += 32) ck[i] = fma(-d, v[i], ck[i]);
+    }
+    __syncthreads();
+  }
+  // 3. thin Q = H_0 ... H_{w-1} [I_w; 0], warp k on column k
+  {
+    double* qk = Q + k * r;
+    for (int i = lane; i < r; i += 32) qk[i] = i == k ? 1.0 : 0.0;
+    __syncwarp();
+    for (int j = k; j >= 0; --j) {  // H_j leaves column k untouched for j > k
+      const double tj = tau[j];
+      const double* v = C + j * r;
+      double d = 0.0;
+      for (int i = j + 1 + lane; i < r; i += 32) d = fma(v[i], qk[i], d);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      d = tj * (qk[j] + d);
+      __syncwarp();
+      if (lane == 0) qk[j] -= d;
+      for (int i = j + 1 + lane; i < r; i += 32) qk[i] = fma(-d, v[i], qk[i]);
+      __syncwarp();
+    }
+    for (int i = lane; i < r; i += 32) Qg[(int64_t)i * w + k] = qk[i];
+    __syncwarp();
+    // 4. X = R^-T Q: forward substitution with L = R^T (L[l][i] = R[i][l]),
+    //    column in registers as in step 1
+    double c[kSl];
+#pragma unroll
+    for (int t = 0; t < kSl; ++t) c[t] = lane + 32 * t < r ? qk[lane + 32 * t] : 0.0;
+#pragma unroll
+    for (int ti = 0; ti < kSl; ++ti) {
+      for (int ii = 0; ii < 32; ++ii) {
+        const int i = 32 * ti + ii;
+        if (i >= r) break;
+        const double xi = __shfl_sync(0xffffffffu, c[ti], ii) * rinv[i];
+#pragma unroll
+        for (int t = ti; t < kSl; ++t) {
+          const int l = lane + 32 * t;
+          const double upd = fma(-R[i * ld + min(l, r - 1)], xi, c[t]);
+          c[t] = (l > i && l < r) ? upd : (l == i ? xi : c[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kSl; ++t)
+      if (lane + 32 * t < r) qk[lane + 32 * t] = c[t];
+    __syncwarp();
+    for (int i = lane; i < r; i += 32) Xg[(int64_t)i * w + k] = qk[i];
+  }
+}
+
 }  // namespace skx
 
 using namespace skx;
@@ -261,4 +398,14 @@ extern "C" int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, do
   k_jacobi<<<1, 32 * (np / 2 > 16 ? 32 : np / 2 < 1 ? 1 : np / 2), smem, (cudaStream_t)stream>>>(
       a, n, (int)rs, (int)cs, u, s, v);
   return check_launch("k_jacobi");
+}
+
+extern "C" int skx_lrls_mid(const double* rz, const double* b, int r, int w, double* q,
+                            double* x, void* stream) {
+  SKX_REQUIRE(r >= 1 && w >= 1 && w <= r && r <= 128 && w <= 32,
+              "skx_lrls_mid: need 1 <= w <= min(r, 32), r <= 128");
+  const size_t smem = ((size_t)r * (r | 1) + 2 * (size_t)r * w + w + r) * 8;
+  cudaFuncSetAttribute(k_lrls_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_lrls_mid<<<1, 32 * w, smem, (cudaStream_t)stream>>>(rz, b, r, w, q, x);
+  return check_launch("k_lrls_mid");
 }

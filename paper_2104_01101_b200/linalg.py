@@ -359,6 +359,25 @@ def sketch_qr_dev(z):
     return q, rz, flags2[1]
 
 
+def assoc_mid_dev(qz, rz, yg):
+    """(q, W) of the associated rsvd_lrls form: c = R_z^-1 Q_z^T (Y G) and its
+    thin Q (src/linalg.py:105-109: x_ls G = R^-1 Q^T (Y G)), W = Q_z R_z^-T q.
+    One libskx CTA does both triangular solves and the Householder QR when
+    r <= 128 and the width <= 32 (cuBLAS TRSM + cuSOLVER QR beyond)."""
+    torch = _torch()
+    r, w = rz.shape[0], yg.shape[1]
+    b = qz.transpose(0, 1) @ yg
+    if r <= 128 and w <= 32 and w <= r:
+        q = torch.empty((r, w), dtype=torch.float64, device="cuda")
+        x = torch.empty((r, w), dtype=torch.float64, device="cuda")
+        nat.call("skx_lrls_mid", nat.ptr(rz.contiguous()), nat.ptr(b.contiguous()), r, w,
+                 nat.ptr(q), nat.ptr(x), nat.stream())
+        return q, qz @ x
+    c = torch.linalg.solve_triangular(rz, b, upper=True)
+    q, _ = torch.linalg.qr(c, mode="reduced")
+    return q, qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+
+
 def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
     """Algorithm 5 (src/linalg.py:87-113) on device.
     z: (m, r) CUDA tensor (any strides), y: (m, s) CUDA tensor view.
@@ -379,9 +398,7 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
         # Same algebra, associated so that Y (m x s, the big operand) only meets
         # width-column matrices: X_ls G = R^-1 Q_z^T (Y G) and
         # Q^T X_ls = (Q_z R^-T Q)^T Y.  2.5x fewer flops at configs 2/4/5.
-        c = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ (y @ g), upper=True)
-        q, _ = torch.linalg.qr(c, mode="reduced")
-        wm = qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+        q, wm = assoc_mid_dev(qz, rz, y @ g)
         d = wm.transpose(0, 1) @ y
     else:
         x = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ y, upper=True)
@@ -416,9 +433,7 @@ def rsvd_lrls_rows_dev(z, yt_loc, row_lo, s, rank, normals, comm, oversample=10,
     y_loc = yt_loc.t()  # m x rows
     if width < r:
         yg = comm.allreduce((y_loc @ g_loc).contiguous())
-        c = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ yg, upper=True)
-        q, _ = torch.linalg.qr(c, mode="reduced")
-        wm = qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+        q, wm = assoc_mid_dev(qz, rz, yg)
         dt_loc = yt_loc @ wm  # rows x w  (= (W^T Y)^T on this block)
     else:
         xt_loc = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ y_loc, upper=True).t()
@@ -479,9 +494,7 @@ def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversampl
         yh[rows, inv] = hit_val
     gh = g[cols] if nh else torch.zeros((1, width), dtype=torch.float64, device="cuda")
     if width < r:
-        c = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ (yh @ gh), upper=True)
-        q, _ = torch.linalg.qr(c, mode="reduced")
-        wm = qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+        q, wm = assoc_mid_dev(qz, rz, yh @ gh)
         dh = wm.transpose(0, 1) @ yh
     else:
         xh = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ yh, upper=True)

@@ -284,12 +284,17 @@ class _Run:
             width = self.cfg.resolved_rrf_width(self.ranks[n])
             P, k2 = _rrf_dims(self.shape, n, self.ranks[n], width)
             dims.append((P, k2, width))
-        scans = None
+        # The rejection scans depend only on rng_init's position: every mode's
+        # scan is enqueued first (later starts bracketed) on the normal-priority
+        # side stream, in short CTAs.  The layouts and right-hand sides (high
+        # priority) take SMs ahead of them as CTAs retire, and the IMAD-bound
+        # scans fill in around the memory/latency-bound layout work (config 4:
+        # the first scan ends ~2 ms earlier than if started after the layouts);
+        # with a host input they also run while the COO arrays are uploaded.
+        # RRF stage 1 of mode n (high priority) overlaps scan n+1.
+        scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
+                               self.comm)
         if self._host is not None:
-            # host input: the scans depend only on rng_init's position, so they
-            # run while the copy engine streams the COO arrays in
-            scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
-                                   self.comm)
             with torch.cuda.stream(main):
                 self.draw_ts_ops()
                 self._host._device = DeviceCoo.from_host(self._host)
@@ -301,16 +306,6 @@ class _Run:
                 for n in range(self.ndim):  # TS sketches read them
                     self.d.fibre(n, self.ts_ops[n] if self.use_ts else None)
             self.prep()
-            # the scans start once the layouts and right-hand sides are done: the
-            # IMAD-bound scans and the memory/latency-bound layout work barely
-            # overlap on the same SMs (co-running gained < 1 ms at config 4), and
-            # alone the sketch kernels run at full speed.  Every mode's scan is
-            # enqueued now (later starts bracketed) on the normal-priority side
-            # stream; RRF stage 1 of mode n (high priority) overlaps scan n+1.
-            if scans is None:
-                side.wait_stream(main)
-                scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims],
-                                       side, self.comm)
             # small first-sweep inputs that do not depend on the RRF factors,
             # built while the scans occupy the GPU: the Kronecker-sketch plans
             # and the first batch of Gaussian test matrices

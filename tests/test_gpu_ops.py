@@ -546,3 +546,28 @@ def test_device_ingest_matches_host_lexsort(skx, monkeypatch):
     bad[5, 1] = shape[1]
     with pytest.raises(ValueError, match="out of range"):
         skx.SparseTensor(shape, bad, vals)
+
+
+@pytest.mark.parametrize("m,r,w", [(1600, 100, 20), (400, 25, 15), (300, 128, 32), (40, 7, 7),
+                                   (64, 33, 1)])
+def test_assoc_mid_vs_lapack(skx, m, r, w):
+    """libskx one-CTA middle step (two triangular solves + Householder QR) vs
+    scipy/numpy on the same operands (src/linalg.py:105-110)."""
+    import scipy.linalg
+    import torch
+    from paper_2104_01101_b200.linalg import assoc_mid_dev
+    rng = np.random.default_rng(m + r + w)
+    z = rng.standard_normal((m, r))
+    qz, rz = np.linalg.qr(z)
+    yg = rng.standard_normal((m, w))
+    q, wm = assoc_mid_dev(torch.from_numpy(qz).cuda(), torch.from_numpy(rz).cuda(),
+                          torch.from_numpy(yg).cuda())
+    c = scipy.linalg.solve_triangular(rz, qz.T @ yg, lower=False)
+    q_ref, _ = np.linalg.qr(c)
+    wm_ref = qz @ scipy.linalg.solve_triangular(rz.T, q_ref, lower=True)
+    q, wm = q.cpu().numpy(), wm.cpu().numpy()
+    sgn = np.sign(np.sum(q * q_ref, axis=0))
+    assert np.all(sgn != 0)
+    assert relerr(q * sgn, q_ref) <= 1e-12
+    assert relerr(wm * sgn, wm_ref) <= 1e-12
+    assert np.abs(q.T @ q - np.eye(w)).max() <= 1e-13

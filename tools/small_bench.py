@@ -7,6 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
+from paper_2104_01101_b200 import _native as nat  # noqa: E402
 from paper_2104_01101_b200.linalg import chol_upper_dev, jacobi_svd_dev, tsqr_r_dev  # noqa: E402
 
 
@@ -35,6 +36,16 @@ def main():
         lr = torch.randn(n, 10, dtype=torch.float64, device="cuda", generator=g) @ torch.randn(
             10, n, dtype=torch.float64, device="cuda", generator=g)
         print(f"jacobi n={n} (rank 10): {timeit(lambda: jacobi_svd_dev(lr)):.1f} us")
+    qz, rz = torch.linalg.qr(z)
+    for w in (20, 30):
+        b = torch.randn(100, w, dtype=torch.float64, device="cuda", generator=g)
+        q = torch.empty_like(b)
+        x = torch.empty_like(b)
+
+        def mid():
+            nat.call("skx_lrls_mid", nat.ptr(rz), nat.ptr(b), 100, w, nat.ptr(q), nat.ptr(x),
+                     nat.stream())
+        print(f"lrls_mid r=100 w={w}: {timeit(mid):.1f} us")
 
 
 
