@@ -138,7 +138,7 @@ def call(name, *args):
         e0.record(s)
         rc = getattr(lib, name)(*args)
         e1.record(s)
-        hook.append((e0, e1))
+        hook.append((e0, e1, args))
     else:
         rc = getattr(lib, name)(*args)
     if rc != 0:
