@@ -178,6 +178,17 @@ int skx_gather_fibers_coo(int n_other, const int64_t* ext_h, int64_t s_n, int64_
                           const double* w, int64_t m, int64_t* hit_off, int64_t* hit_col,
                           double* hit_val, int64_t cap, void* ws, size_t* ws_bytes, void* stream);
 
+/* The nonzeros of a lexsorted COO tensor (coords_h[k]: int32 coordinates of
+ * mode k, extents shape_h) whose other-mode flat index is in sflat (m values,
+ * sorted ascending, unique): their keys flat * s_mode + i_mode and values, in
+ * no particular order (the caller sorts the few hits), at most cap of them;
+ * *count (device) = the number found.  One pass over the coordinates replaces
+ * the sorted key array of skx_gather_fibers_coo (src/sketching.py:262-264). */
+int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode, int64_t nnz,
+                          const int32_t* const* coords_h, const double* vals, const int64_t* sflat,
+                          int64_t m, int64_t* out_key, double* out_val, int64_t cap,
+                          uint64_t* count, void* stream);
+
 /* ------------------------------------------------- K4: range finder */
 
 /* stage1[i_n, c] = sum_j T_(n)[i_n, j] sign_j [hash_j == c] where hash/sign are

@@ -43,6 +43,8 @@ _SIGS = {
     "skx_lev_sample": [c_i32, c_p, c_p, c_p, c_i64, c_u64, c_u64, c_u64, c_p, c_p, c_p],
     "skx_kron_rows": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
     "skx_gather_fibers_dense": [c_p, c_i32, c_p, c_i32, c_p, c_p, c_i64, c_p, c_p],
+    "skx_filter_fibers_coo": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_i64, c_p, c_p, c_i64, c_p,
+                              c_p],
     "skx_gather_fibers_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_p,
                               c_i64, c_p, c_sz_p, c_p],
     "skx_rrf_stage1_coo": [c_i32, c_p, c_i64, c_p, c_p, c_u64, c_u64, c_u64, c_u32, c_u32, c_u64,

@@ -6,27 +6,43 @@
 
 namespace skx {
 
-// Single-CTA: p = max(s,0)/sum; cdf = cumsum(p); cdf /= cdf[-1].
-// Fixed-order chunked scan (deterministic; rounding differs from numpy's
-// sequential cumsum only in the last bits).
-__global__ void __launch_bounds__(1024) k_lev_prepare(const double* __restrict__ sc, int64_t s,
-                                                      double* __restrict__ p, double* __restrict__ cdf) {
-  __shared__ double part[1024];
-  __shared__ double total;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t per = (s + nt - 1) / nt;
-  const int64_t lo = imin(tid * per, s), hi = imin(lo + per, s);
+// p = max(s,0)/sum; cdf = cumsum(p); cdf /= cdf[-1] over kLevChunks fixed
+// chunks (deterministic; rounding differs from numpy's sequential cumsum only
+// in the last bits).  Each chunk is one thread's sequential pass; the chunks
+// are spread over kLevChunks/32 one-warp CTAs so the ~2 s IEEE divisions run on
+// many SMs, and the two cross-chunk sums are a single thread's fixed-order
+// loop (k_lev_total, k_lev_offsets).
+constexpr int kLevChunks = 1024;
+
+__device__ __forceinline__ void lev_chunk(int64_t s, int t, int64_t& lo, int64_t& hi) {
+  const int64_t per = (s + kLevChunks - 1) / kLevChunks;
+  lo = imin(t * per, s);
+  hi = imin(lo + per, s);
+}
+
+__global__ void k_lev_sums(const double* __restrict__ sc, int64_t s, double* __restrict__ part) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t lo, hi;
+  lev_chunk(s, t, lo, hi);
   double acc = 0.0;
   for (int64_t i = lo; i < hi; ++i) acc += fmax(sc[i], 0.0);
-  part[tid] = acc;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int i = 0; i < nt; ++i) t += part[i];
-    total = t;
-  }
-  __syncthreads();
-  const double tot = total;
+  part[t] = acc;
+}
+
+__global__ void k_lev_total(double* __restrict__ part, double* __restrict__ tot) {
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (int i = 0; i < kLevChunks; ++i) t += part[i];
+  tot[0] = t;
+}
+
+__global__ void k_lev_scan(const double* __restrict__ sc, int64_t s, const double* __restrict__ tot_p,
+                           double* __restrict__ p, double* __restrict__ cdf,
+                           double* __restrict__ part) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t lo, hi;
+  lev_chunk(s, t, lo, hi);
+  const double tot = tot_p[0];
   double run = 0.0;
   for (int64_t i = lo; i < hi; ++i) {
     const double pi = fmax(sc[i], 0.0) / tot;
@@ -34,26 +50,31 @@ __global__ void __launch_bounds__(1024) k_lev_prepare(const double* __restrict__
     run += pi;
     cdf[i] = run;
   }
-  __syncthreads();
-  part[tid] = run;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int i = 0; i < nt; ++i) {
-      const double v = part[i];
-      part[i] = t;
-      t += v;
-    }
+  part[t] = run;
+}
+
+// exclusive prefix of the chunk totals; tot[1] = cdf[s-1] after the offsets
+__global__ void k_lev_offsets(int64_t s, double* __restrict__ part, double* __restrict__ tot) {
+  if (threadIdx.x != 0) return;
+  const int64_t per = (s + kLevChunks - 1) / kLevChunks;
+  const int c_last = (int)((s - 1) / per);
+  double t = 0.0, last = 0.0;
+  for (int i = 0; i < kLevChunks; ++i) {
+    const double v = part[i];
+    part[i] = t;
+    if (i == c_last) last = v + t;  // the last element's run plus its offset
+    t += v;
   }
-  __syncthreads();
-  const double offs = part[tid];
-  for (int64_t i = lo; i < hi; ++i) cdf[i] += offs;
-  __syncthreads();
-  __shared__ double last;
-  if (tid == 0) last = cdf[s - 1];
-  __syncthreads();
-  const double L = last;
-  for (int64_t i = lo; i < hi; ++i) cdf[i] /= L;
+  tot[1] = last;
+}
+
+__global__ void k_lev_final(int64_t s, const double* __restrict__ part,
+                            const double* __restrict__ tot, double* __restrict__ cdf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t lo, hi;
+  lev_chunk(s, t, lo, hi);
+  const double offs = part[t], L = tot[1];
+  for (int64_t i = lo; i < hi; ++i) cdf[i] = (cdf[i] + offs) / L;
 }
 
 struct PtrPack {
@@ -168,19 +189,126 @@ __global__ void k_gather_coo_write(const int64_t* __restrict__ keys, const doubl
   }
 }
 
+// ---- sparse gather without a sorted key array: one pass over the lexsorted
+// COO keeps the nonzeros whose other-mode index is among the sampled ones
+// (~m nnz / P_n of them: ~160 at config 5).  A 64 Kbit shared-memory bitmap of
+// the sampled flats rejects almost every nonzero with one shared load; the
+// rare bitmap hits are confirmed by binary search in the sorted flats.  The
+// bitmap is a two-probe Bloom filter over 2^18 bits (32 KB): at m = 6400 about
+// 0.2% of the nonzeros reach the (L2-latency-bound) binary search.
+struct CoordPack {
+  const int32_t* c[8];
+  int64_t ext[8];
+};
+
+constexpr int kBloomBits = 18;
+
+__device__ __forceinline__ uint2 flat_hash2(uint64_t f) {
+  const uint64_t a = f * 0x9E3779B97F4A7C15ull, b = (f ^ (f >> 29)) * 0xBF58476D1CE4E5B9ull;
+  return make_uint2((uint32_t)(a >> (64 - kBloomBits)), (uint32_t)(b >> (64 - kBloomBits)));
+}
+
+__global__ void __launch_bounds__(256) k_filter_fibers(int ndim, int mode, CoordPack cp,
+                                                       int64_t nnz, const double* __restrict__ vals,
+                                                       const int64_t* __restrict__ sflat, int64_t m,
+                                                       int64_t* __restrict__ out_key,
+                                                       double* __restrict__ out_val, int64_t cap,
+                                                       unsigned long long* __restrict__ count) {
+  __shared__ uint32_t bits[1 << (kBloomBits - 5)];
+  for (int i = threadIdx.x; i < (1 << (kBloomBits - 5)); i += blockDim.x) bits[i] = 0u;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    const uint2 h = flat_hash2((uint64_t)sflat[j]);
+    atomicOr(&bits[h.x >> 5], 1u << (h.x & 31));
+    atomicOr(&bits[h.y >> 5], 1u << (h.y & 31));
+  }
+  __syncthreads();
+  const int64_t s_n = cp.ext[mode];
+  constexpr int U = 4;  // elements per thread per pass, loads issued first
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < nnz; e0 += U * stride) {
+    int64_t flat[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) flat[u] = 0;
+    for (int k = 0; k < ndim; ++k) {
+      if (k == mode) continue;
+      int32_t c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = e0 + u * stride;
+        c[u] = e < nnz ? __ldcs(cp.c[k] + e) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) flat[u] = flat[u] * cp.ext[k] + c[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * stride;
+      const uint2 h = flat_hash2((uint64_t)flat[u]);
+      if (e >= nnz || !((bits[h.x >> 5] >> (h.x & 31)) & (bits[h.y >> 5] >> (h.y & 31)) & 1u))
+        continue;
+      int64_t lo = 0, hi = m;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sflat[mid] < flat[u]) lo = mid + 1; else hi = mid;
+      }
+      if (lo < m && sflat[lo] == flat[u]) {
+        const unsigned long long slot = atomicAdd(count, 1ull);
+        if ((int64_t)slot < cap) {
+          out_key[slot] = flat[u] * s_n + cp.c[mode][e];
+          out_val[slot] = vals[e];
+        }
+      }
+    }
+  }
+}
+
 }  // namespace skx
 
 using namespace skx;
 
+extern "C" int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode, int64_t nnz,
+                                     const int32_t* const* coords_h, const double* vals,
+                                     const int64_t* sflat, int64_t m, int64_t* out_key,
+                                     double* out_val, int64_t cap, uint64_t* count,
+                                     void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 8 && mode >= 0 && mode < ndim,
+              "skx_filter_fibers_coo: order 2..8 and a valid mode");
+  SKX_REQUIRE(m >= 1, "skx_filter_fibers_coo: empty sample");
+  cudaStream_t s = (cudaStream_t)stream;
+  CoordPack cp{};
+  for (int k = 0; k < ndim; ++k) {
+    cp.c[k] = coords_h[k];
+    cp.ext[k] = shape_h[k];
+  }
+  cudaMemsetAsync(count, 0, sizeof(uint64_t), s);
+  if (nnz == 0) return check_launch("skx_filter_fibers_coo");
+  const int64_t blocks = imin((nnz + 1023) / 1024, (int64_t)num_sms() * 16);
+  k_filter_fibers<<<(unsigned)blocks, 256, 0, s>>>(ndim, mode, cp, nnz, vals, sflat, m, out_key,
+                                                   out_val, cap, (unsigned long long*)count);
+  return check_launch("k_filter_fibers");
+}
+
 extern "C" int skx_lev_prepare(const double* scores, int64_t s, double* p, double* cdf, void* ws,
                                size_t* ws_bytes, void* stream) {
   SKX_REQUIRE(s >= 1, "skx_lev_prepare: empty score vector");
-  if (ws_bytes && ws == nullptr) {
-    *ws_bytes = 0;
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_lev_prepare: ws_bytes is NULL");
+  Arena ar(ws, *ws_bytes);
+  double* part = ar.take<double>(kLevChunks);
+  double* tot = ar.take<double>(2);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
     return SKX_OK;
   }
-  k_lev_prepare<<<1, 1024, 0, (cudaStream_t)stream>>>(scores, s, p, cdf);
-  return check_launch("k_lev_prepare");
+  SKX_REQUIRE(ar.ok(), "skx_lev_prepare: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned g = kLevChunks / 32;
+  k_lev_sums<<<g, 32, 0, st>>>(scores, s, part);
+  k_lev_total<<<1, 32, 0, st>>>(part, tot);
+  k_lev_scan<<<g, 32, 0, st>>>(scores, s, tot, p, cdf, part);
+  k_lev_offsets<<<1, 32, 0, st>>>(s, part, tot);
+  k_lev_final<<<g, 32, 0, st>>>(s, part, tot, cdf);
+  return check_launch("lev_prepare", 5);
 }
 
 extern "C" int skx_lev_sample(int n_other, const int64_t* ext_h, const double* const* p_h,

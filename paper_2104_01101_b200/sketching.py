@@ -317,8 +317,8 @@ def lev_sample_dev(factors, m, gen, check=True):
     for sc in scores:
         p = torch.empty_like(sc)
         cdf = torch.empty_like(sc)
-        nat.call("skx_lev_prepare", nat.ptr(sc), int(sc.numel()), nat.ptr(p), nat.ptr(cdf), None,
-                 None, nat.stream())
+        nat.call_ws("skx_lev_prepare", (nat.ptr(sc), int(sc.numel()), nat.ptr(p), nat.ptr(cdf)),
+                    slot=6)
         ps.append(p)
         cdfs.append(cdf)
     k = len(factors)
@@ -400,6 +400,39 @@ def gather_coo_dev(keys, vals, ext_others, s_n, idx, w):
                                           nat.ptr(idx), nat.ptr(w), m, nat.ptr(hit_off),
                                           nat.ptr(hit_col), nat.ptr(hit_val), total))
     return hit_off, hit_col[:total], hit_val[:total]
+
+
+FILTER_CAP0 = 1 << 16
+
+
+def filter_fibers_dev(d, n, idx):
+    """(keys, vals) of the nonzeros of DeviceCoo d lying in the sampled mode-n
+    fibres (other-mode multi-indices = rows of idx), sorted by key = flat_other *
+    s_n + i_n: the slice of d.keys(n) that gather_coo_dev reads, found with one
+    pass over the coordinates instead of a full sort (src/sketching.py:262-264)."""
+    torch = _torch()
+    others = [k for k in range(d.ndim) if k != n]
+    flat = torch.zeros(idx.shape[0], dtype=torch.int64, device="cuda")
+    for c, k in enumerate(others):
+        flat = flat * d.shape[k] + idx[:, c]
+    sflat = torch.unique(flat)
+    shape_a, shape_p = nat.host_i64(d.shape)
+    rows = [d.coords[k] for k in range(d.ndim)]
+    ptr_a, ptr_p = nat.host_ptrs(rows)
+    cap = FILTER_CAP0
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    while True:
+        keys = torch.empty(cap, dtype=torch.int64, device="cuda")
+        vals = torch.empty(cap, dtype=torch.float64, device="cuda")
+        nat.call("skx_filter_fibers_coo", d.ndim, shape_p, n, d.nnz, ptr_p, nat.ptr(d.vals),
+                 nat.ptr(sflat), int(sflat.numel()), nat.ptr(keys), nat.ptr(vals), cap,
+                 nat.ptr(count), nat.stream())
+        found = int(count.item())
+        if found <= cap:
+            break
+        cap = found
+    keys, order = torch.sort(keys[:found])
+    return keys, vals[:found][order].contiguous()
 
 
 def hits_to_dense(hit_off, hit_col, hit_val, m, s_n):

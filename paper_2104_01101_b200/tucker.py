@@ -21,8 +21,8 @@ from . import _native as nat
 from . import rng as rngmod
 from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev, rsvd_lrls_hits_dev,
                      rsvd_lrls_rows_dev, top_svd_dev)
-from .sketching import (TensorSketchOp, draw_rrf_tables, finish_rrf_scan, gather_coo_dev,
-                        gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
+from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, finish_rrf_scan,
+                        gather_coo_dev, gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
                         plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
                         ts_rhs_dense_dev, ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
@@ -367,7 +367,7 @@ class _Run:
             idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
             z = kron_rows_dev(others, idx, w)
             if self.sparse:
-                keys, vals = self.d.keys(n)
+                keys, vals = filter_fibers_dev(self.d, n, idx)
                 ext = [self.shape[k] for k in self.others(n)]
                 off, col, val = gather_coo_dev(keys, vals, ext, self.shape[n], idx, w)
                 row = None

@@ -571,3 +571,32 @@ def test_assoc_mid_vs_lapack(skx, m, r, w):
     assert relerr(q * sgn, q_ref) <= 1e-12
     assert relerr(wm * sgn, wm_ref) <= 1e-12
     assert np.abs(q.T @ q - np.eye(w)).max() <= 1e-13
+
+
+@pytest.mark.parametrize("shape,nnz,mode", [((50, 40, 30), 20000, 0), ((50, 40, 30), 20000, 1),
+                                            ((50, 40, 30), 20000, 2), ((12, 9, 7, 5), 3000, 2)])
+def test_filter_fibers_matches_sorted_keys(skx, shape, nnz, mode):
+    """One-pass fibre filter + gather == gather over the fully sorted key array
+    (bit-exact), with repeated sampled fibres and empty ones."""
+    import torch
+    from paper_2104_01101_b200.sketching import filter_fibers_dev, gather_coo_dev
+    from paper_2104_01101_b200.tensors import device_of
+    rng = np.random.default_rng(nnz + mode)
+    lin = rng.choice(int(np.prod(shape)), size=nnz, replace=False)
+    coords = np.stack(np.unravel_index(np.sort(lin), shape), axis=1)
+    st = skx.SparseTensor(shape, coords, rng.standard_normal(nnz))
+    d = device_of(st)
+    others = [k for k in range(len(shape)) if k != mode]
+    m = 300
+    idx = np.stack([rng.integers(0, shape[k], m) for k in others], axis=1)
+    idx[m // 2:m // 2 + 20] = idx[:20]  # repeated fibres
+    idx_d = torch.from_numpy(idx).cuda()
+    w = torch.from_numpy(rng.random(m) + 0.5).cuda()
+    ext = [shape[k] for k in others]
+    keys, vals = d.keys(mode)
+    ref = gather_coo_dev(keys, vals, ext, shape[mode], idx_d, w)
+    fk, fv = filter_fibers_dev(d, mode, idx_d)
+    got = gather_coo_dev(fk, fv, ext, shape[mode], idx_d, w)
+    for a, b in zip(got, ref):
+        assert torch.equal(a, b)
+    assert got[2].numel() > 0
