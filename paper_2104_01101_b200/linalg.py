@@ -220,8 +220,10 @@ class NormalSource:
     numpy's standard_normal keeps no state between calls, so k consecutive
     draws of sizes n_1..n_k are the first n_1 + ... + n_k normals of the
     stream.  With batch > 0 the source generates at least `batch` normals at
-    a time and serves later draws from that buffer (one ziggurat pass per
-    sweep instead of one per subproblem)."""
+    a time and serves later draws from those segments (one ziggurat pass per
+    sweep instead of one per subproblem).  Generated segments are kept until
+    commit(), so snapshot()/restore() can rewind the consumption point (a
+    replayed speculative sweep re-reads the same normals)."""
 
     def __init__(self, gen, batch=0):
         torch = _torch()
@@ -230,8 +232,8 @@ class NormalSource:
         self.k0, self.k1 = c.k0, c.k1
         self.pos = torch.tensor([c.p], dtype=torch.int64, device="cuda")
         self.batch = int(batch)
-        self._buf, self._off = None, 0
-        self._pending = []  # [(buffer, event)]: following batches, made on a side stream
+        self._segs = []  # [(tensor, event or None)] in stream order
+        self._i, self._off = 0, 0  # consumption point: segment, offset
 
     def _generate(self, n):
         torch = _torch()
@@ -241,54 +243,66 @@ class NormalSource:
                      nat.ptr(out), nat.ptr(self.pos)), slot=1)
         return out
 
+    def _left(self):
+        return sum(t.numel() for t, _ in self._segs[self._i:]) - self._off
+
     def prefetch(self):
         """Generate the next batch now (e.g. while the GPU is otherwise busy
         with compute-bound work) so the next draws are served from memory."""
-        left = 0 if self._buf is None else self._buf.numel() - self._off
-        if self.batch and left == 0:
-            self._buf, self._off = self._generate(self.batch), 0
+        if self.batch and self._left() == 0:
+            self._segs.append((self._generate(self.batch), None))
 
     def prefetch_async(self, stream):
         """Enqueue one more batch on `stream` (the draws are data-independent)
         unless a full batch beyond the buffered normals is already on its way;
         the caller's stream waits for it only when it is first used."""
         torch = _torch()
-        if not self.batch:
-            return
-        left = 0 if self._buf is None else self._buf.numel() - self._off
-        left += sum(b.numel() for b, _ in self._pending)
-        if left >= 2 * self.batch:
+        if not self.batch or self._left() >= 2 * self.batch:
             return
         stream.wait_stream(torch.cuda.current_stream())  # device cursor order
         with torch.cuda.stream(stream):
             nxt = self._generate(self.batch)
             ev = torch.cuda.Event()
             ev.record(stream)
-        self._pending.append((nxt, ev))
+        self._segs.append((nxt, ev))
 
     def normal(self, shape):
         torch = _torch()
         n = int(np.prod(shape))
-        left = 0 if self._buf is None else self._buf.numel() - self._off
-        while left < n and self._pending:
-            nxt, ev = self._pending.pop(0)
-            cur = torch.cuda.current_stream()
-            cur.wait_event(ev)
-            nxt.record_stream(cur)
-            self._buf = torch.cat([self._buf[self._off:], nxt]) if left else nxt
-            self._off = 0
-            left = self._buf.numel()
+        left = self._left()
         if left < n:
-            fresh = self._generate(max(n - left, self.batch))
-            self._buf = torch.cat([self._buf[self._off:], fresh]) if left else fresh
-            self._off = 0
-        out = self._buf[self._off:self._off + n]
-        self._off += n
+            self._segs.append((self._generate(max(n - left, self.batch)), None))
+        cur = torch.cuda.current_stream()
+        parts, need = [], n
+        while need > 0:
+            t, ev = self._segs[self._i]
+            if ev is not None:
+                cur.wait_event(ev)
+                t.record_stream(cur)
+            take = min(need, t.numel() - self._off)
+            parts.append(t[self._off:self._off + take])
+            need -= take
+            self._off += take
+            if self._off == t.numel():
+                self._i, self._off = self._i + 1, 0
+        out = parts[0] if len(parts) == 1 else torch.cat(parts)
         return out.view(*shape)
+
+    def snapshot(self):
+        """Consumption point to return to if a speculative sweep is replayed."""
+        return (self._i, self._off)
+
+    def restore(self, snap):
+        self._i, self._off = snap
+
+    def commit(self):
+        """Release the fully consumed segments (no rewind before this point)."""
+        del self._segs[:self._i]
+        self._i = 0
 
     def sync_host(self):
         """Move the numpy Generator to where numpy would be (one D2H)."""
-        if self._pending or (self._buf is not None and self._off != self._buf.numel()):
+        if self._left() != 0:
             raise RuntimeError("NormalSource.sync_host: buffered normals not consumed")
         rngmod.set_cursor(self.gen, int(self.pos.item()))
 
@@ -314,7 +328,7 @@ def resid_dev(z, core_t, a, y):
     return torch.sqrt(out[0])
 
 
-def sketch_qr_dev(z):
+def sketch_qr_dev(z, defer=None):
     """Reduced QR of the sketched system Z (m x r) with the reference's rank
     test.  Cholesky QR (small Gram, Cholesky -- one-CTA libskx kernel up to
     r = 128, cuSOLVER potrf beyond -- TRSM; no LAPACK Householder panel).  One pass already gives Q orthonormal to 1e-13 for the
@@ -323,7 +337,12 @@ def sketch_qr_dev(z):
     pass (CholeskyQR2), and when even that is unsafe (first Cholesky fails or
     diag(R) spans >= 1e6, i.e. cond(Z) near eps^-1/2) the Householder QR of
     cuSOLVER runs -- the same rank decision as src/linalg.py:44-52.  One host
-    sync decides (a second only on the CholeskyQR2 path)."""
+    sync decides (a second only on the CholeskyQR2 path).
+
+    defer (a list): speculative form without the host sync -- the one-pass
+    factors are returned and a device flag "this sub-problem must be redone
+    on the checked path" (unsafe, second pass needed, or rank-deficient) is
+    appended; the caller verifies the flags later and replays on failure."""
     torch = _torch()
     m, r = z.shape
     if m < r:
@@ -344,6 +363,9 @@ def sketch_qr_dev(z):
     one_pass = (g2 - torch.eye(r, dtype=g2.dtype, device=g2.device)).abs().max() < 1e-13
     tol = 1e-12 * torch.sqrt(torch.trace(g1))  # ||Z||_F
     bad1 = (d1.abs() < tol).any()
+    if defer is not None:
+        defer.append(unsafe | ~one_pass | bad1)
+        return z1, r1, None
     flags = torch.stack([unsafe, one_pass, bad1]).cpu()
     if bool(flags[0]):
         return qr_flag_dev(z)
@@ -378,10 +400,11 @@ def assoc_mid_dev(qz, rz, yg):
     return q, qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
 
 
-def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
+def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None):
     """Algorithm 5 (src/linalg.py:87-113) on device.
     z: (m, r) CUDA tensor (any strides), y: (m, s) CUDA tensor view.
-    Returns (core_t (r, rank), a (s, rank), rank_bad flag)."""
+    Returns (core_t (r, rank), a (s, rank), rank_bad flag).  defer: see
+    sketch_qr_dev (the rank check is then the caller's)."""
     torch = _torch()
     m, r = z.shape
     s = y.shape[1]
@@ -389,8 +412,8 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True):
         raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
     if rank > min(r, s):
         raise ValueError(f"rank {rank} exceeds min({r}, {s})")
-    qz, rz, bad = sketch_qr_dev(z)
-    if check and bool(bad.item()):
+    qz, rz, bad = sketch_qr_dev(z, defer)
+    if check and defer is None and bool(bad.item()):
         raise RankDeficientError("rank-deficient sketched system")
     width = min(rank + oversample, s)
     g = normals.normal((s, width))

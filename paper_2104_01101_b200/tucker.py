@@ -350,7 +350,7 @@ class _Run:
             for n in range(self.ndim):
                 self.ts_rhs[n] = self._rhs(n, self.ts_ops[n])
 
-    def solve_mode(self, n, redraw):
+    def solve_mode(self, n, redraw, defer=None):
         others = [self.factors[k] for k in self.others(n)]
         if self.use_ts:
             if redraw:
@@ -363,6 +363,7 @@ class _Run:
                                                            self.ranks[n], self.normals, self.comm)
                 return core_t, self.comm.allgather_rows(a_loc.contiguous(), s_n), res
             y = self.ts_rhs[n].t()
+            return self._finish_dense(z, y, n, defer)
         else:
             idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
             z = kron_rows_dev(others, idx, w)
@@ -396,8 +397,8 @@ class _Run:
                 self.comm.allreduce(y)
         return self._finish_dense(z, y, n)
 
-    def _finish_dense(self, z, y, n):
-        core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals)
+    def _finish_dense(self, z, y, n, defer=None):
+        core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals, defer=defer)
         return core_t, a, resid_dev(z, core_t, a, y)
 
     def _gather_hits(self, off, col, val):
@@ -450,6 +451,13 @@ class _Run:
     def _sweep_loop(self, trace, res_dev, fit_dev, ev, fs, overlap):
         torch = _torch()
         core = None
+        # TensorSketch sweeps run speculatively: every sub-problem takes the
+        # one-pass Cholesky QR without a host round trip and records a device
+        # flag; one sync per sweep checks them all, and a flagged sweep is
+        # replayed from its starting state on the checked path (second QR
+        # pass / Householder / rank-deficiency redraw), so results are those
+        # of the checked path either way
+        speculate = self.use_ts and self.comm is None
         for sweep in range(self.cfg.max_sweeps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -459,18 +467,35 @@ class _Run:
                 # stream behind the previous fitness
                 self.normals.prefetch_async(fs)
             core_t = None
-            for n in range(self.ndim):
-                try:
-                    core_t, a, res = self.solve_mode(n, redraw=False)
-                except RankDeficientError:
+            done = False
+            if speculate:
+                start = (list(self.factors), self.normals.snapshot(), len(res_dev))
+                flags, sweep_res = [], []
+                for n in range(self.ndim):
+                    core_t, a, res = self.solve_mode(n, redraw=False, defer=flags)
+                    self.factors[n] = a
+                    sweep_res.append(res)
+                if not bool(torch.stack(flags).any()):
+                    res_dev.extend(sweep_res)
+                    done = True
+                else:
+                    self.factors = list(start[0])
+                    self.normals.restore(start[1])
+                    del res_dev[start[2]:]
+            if not done:
+                for n in range(self.ndim):
                     try:
-                        core_t, a, res = self.solve_mode(n, redraw=True)
-                    except RankDeficientError as exc:
-                        raise RankDeficientError(
-                            f"mode-{n} sketched system rank-deficient after redraw "
-                            f"(m={self.m}, sketch={self.cfg.sketch}): {exc}") from exc
-                self.factors[n] = a
-                res_dev.append(res)
+                        core_t, a, res = self.solve_mode(n, redraw=False)
+                    except RankDeficientError:
+                        try:
+                            core_t, a, res = self.solve_mode(n, redraw=True)
+                        except RankDeficientError as exc:
+                            raise RankDeficientError(
+                                f"mode-{n} sketched system rank-deficient after redraw "
+                                f"(m={self.m}, sketch={self.cfg.sketch}): {exc}") from exc
+                    self.factors[n] = a
+                    res_dev.append(res)
+            self.normals.commit()
             core = self.fold_core(core_t)
             e1.record()
             ev.append((e0, e1))

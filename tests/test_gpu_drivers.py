@@ -97,3 +97,41 @@ def test_sparse_reduced_config_vs_oracle(oracle, skx, kind):
     # residuals are sketch-space quantities: compare directly
     assert np.allclose(trace.residuals, tr.residuals, rtol=1e-8), (trace.residuals, tr.residuals)
     assert np.allclose(trace.fitness, tr.fitness, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_speculative_sweep_replay_is_exact(skx, sparse, monkeypatch):
+    """A flagged speculative sweep is replayed from its starting state on the
+    checked path: forcing the flag on the first sub-problem of every sweep
+    must give bitwise the same model and trace as the unforced run."""
+    import torch
+    from paper_2104_01101_b200 import linalg
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from paper_2104_01101_b200.tucker import sketched_tucker_als_dev
+    shape = (60, 50, 40)
+    if sparse:
+        c, v = planted_cp_coo_host(shape, 20_000, rank=3, seed=2)
+        t = skx.SparseTensor(shape, c, v)
+    else:
+        t = np.random.default_rng(2).standard_normal(shape)
+    cfg = skx.TuckerConfig(ranks=(4, 5, 3), max_sweeps=3, sketch="tensorsketch",
+                           sketch_size=400, seed=9)
+    core0, fac0, tr0 = sketched_tucker_als_dev(t, cfg)
+    orig = linalg.sketch_qr_dev
+    forced = []
+
+    def forcing(z, defer=None):
+        out = orig(z, defer)
+        if defer is not None and len(defer) == 1:
+            defer.append(torch.ones((), dtype=torch.bool, device="cuda"))
+            forced.append(1)
+        return out
+    monkeypatch.setattr(linalg, "sketch_qr_dev", forcing)
+    if sparse:
+        t._device = None
+    core1, fac1, tr1 = sketched_tucker_als_dev(t, cfg)
+    assert len(forced) == 3  # every sweep was replayed
+    assert torch.equal(core0, core1)
+    for a, b in zip(fac0, fac1):
+        assert torch.equal(a, b)
+    assert tr0.residuals == tr1.residuals and tr0.fitness == tr1.fitness
