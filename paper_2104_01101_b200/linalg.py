@@ -356,7 +356,13 @@ def sketch_qr_dev(z, defer=None):
 
     g1 = z.transpose(0, 1) @ z
     r1, i1 = chol(g1)
-    z1 = torch.linalg.solve_triangular(r1, z, upper=True, left=False)
+    if r <= 128:
+        z1 = torch.linalg.solve_triangular(r1, z, upper=True, left=False)
+    else:
+        # large r: one TRSM for R^-1 (r right-hand sides, parallel) and a GEMM,
+        # instead of a latency-bound TRSM with the m x r operand
+        eye = torch.eye(r, dtype=z.dtype, device=z.device)
+        z1 = z @ torch.linalg.solve_triangular(r1, eye, upper=True)
     g2 = z1.transpose(0, 1) @ z1
     d1 = torch.diagonal(r1)
     unsafe = (i1[0] != 0) | ~(d1.max() < 1e6 * d1.min())
@@ -395,9 +401,11 @@ def assoc_mid_dev(qz, rz, yg):
         nat.call("skx_lrls_mid", nat.ptr(rz.contiguous()), nat.ptr(b.contiguous()), r, w,
                  nat.ptr(q), nat.ptr(x), nat.stream())
         return q, qz @ x
-    c = torch.linalg.solve_triangular(rz, b, upper=True)
-    q, _ = torch.linalg.qr(c, mode="reduced")
-    return q, qz @ torch.linalg.solve_triangular(rz.transpose(0, 1), q, upper=False)
+    # r > 128: R^-1 once (one TRSM with r right-hand sides), then GEMMs
+    rinv = torch.linalg.solve_triangular(rz, torch.eye(r, dtype=rz.dtype, device=rz.device),
+                                         upper=True)
+    q, _ = torch.linalg.qr(rinv @ b, mode="reduced")
+    return q, qz @ (rinv.transpose(0, 1) @ q)
 
 
 def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None):
