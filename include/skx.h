@@ -263,6 +263,17 @@ int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u, do
 int skx_lrls_mid(const double* rz, const double* b, int r, int w, double* q, double* x,
                  void* stream);
 
+/* Skip-mode sparse TTMc of an order-3 COO tensor (ttmc(t, factors, skip=n),
+ * src/tensors.py:261-277): from mode n's fibre-major layout (skx_coo_fibre /
+ * skx_coo_fibre_ts with c1_mask), out (s_n x R1*R2, row-major; column
+ * k1*R2 + k2) = sum over each column's nonzeros of v * A1[i1,k1] * A2[i2,k2]
+ * in layout order, products and sums unfused (numpy's rounding).  A1 (s_1 x
+ * R1) and A2 (s_2 x R2) are the first and second other modes' factors,
+ * row-major; R1*R2 <= 1024. */
+int skx_ttmc3_skip_coo(int64_t s_n, const int64_t* colptr, const void* rec, uint32_t c1_mask,
+                       const double* a1, int r1, const double* a2, int r2, double* out,
+                       void* stream);
+
 /* out[0] = sum(x^2) with a fixed-order reduction. */
 int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,
               void* stream);

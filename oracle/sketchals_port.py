@@ -157,6 +157,88 @@ def project_all(t, factors):
     return out
 
 
+def ttmc(t, factors, skip=None, chunk=1 << 16):
+    """Tensor times matrix-chain (src/tensors.py:217-247): contract every mode
+    m != skip with factors[m]^T.  Sparse skip-mode: per chunk of the nonzeros
+    (mode-`skip` stable order), each nonzero's Kronecker row product
+    (first other mode slowest), segment sums, added into the unfolded output
+    (src/tensors.py:261-277)."""
+    if skip is None:
+        return project_all(t, factors)
+    if not isinstance(t, Coo):
+        out = np.asarray(t)
+        for k in range(out.ndim):
+            if k != skip:
+                out = mode_product(out, factors[k].T, k)
+        return out
+    others = _rest(t.ndim, skip)
+    cols = int(np.prod([factors[k].shape[1] for k in others]))
+    out = np.zeros((t.shape[skip], cols))
+    shp = [t.shape[k] if k == skip else factors[k].shape[1] for k in range(t.ndim)]
+    if t.nnz == 0:
+        return fold(out, skip, shp)
+    order = np.argsort(t.coords[:, skip], kind="stable")
+    rows = t.coords[order, skip]
+    for lo in range(0, t.nnz, chunk):
+        hi = min(lo + chunk, t.nnz)
+        idx = order[lo:hi]
+        contrib = t.values[idx][:, None]
+        for k in others:
+            fk = factors[k][t.coords[idx, k]]
+            contrib = (contrib[:, :, None] * fk[:, None, :]).reshape(hi - lo, -1)
+        seg = rows[lo:hi]
+        starts = np.flatnonzero(np.r_[True, seg[1:] != seg[:-1]])
+        out[seg[starts]] += np.add.reduceat(contrib, starts, axis=0)
+    return fold(out, skip, shp)
+
+
+def hosvd_init(t, ranks):
+    """Leading eigenvectors of the mode Grams (src/tucker.py:112-126)."""
+    out = []
+    for n, r in enumerate(ranks):
+        tn = unfold(t, n)
+        gram = (tn @ tn.T).toarray() if sp.issparse(tn) else tn @ tn.T
+        _, vecs = np.linalg.eigh(gram)
+        out.append(vecs[:, ::-1][:, :r])
+    return out
+
+
+def hooi(t, ranks, max_sweeps=5, init="hosvd", seed=0, tol=0.0):
+    """Exact Tucker-ALS (src/tucker.py:155-193): per mode the leading left
+    singular vectors of the skip-mode TTMc unfolding; residual from the
+    captured energy; core from the last mode's contraction."""
+    import time
+
+    shape = tuple(t.shape)
+    nd = len(shape)
+    rng = generator(seed)
+    if init == "hosvd":
+        A = hosvd_init(t, ranks)
+    elif init == "random":
+        A = [np.linalg.qr(rng.standard_normal((shape[n], ranks[n])))[0][:, :ranks[n]]
+             for n in range(nd)]
+    else:
+        raise ValueError("unknown init")
+    nt2 = norm_of(t) ** 2
+    tr = Trace()
+    core = None
+    for _ in range(max_sweeps):
+        t0 = time.perf_counter()
+        y = None
+        for n in range(nd):
+            y = ttmc(t, A, skip=n)
+            u, sv, _ = np.linalg.svd(unfold(y, n), full_matrices=False)
+            A[n] = u[:, :ranks[n]]
+            tr.residuals.append(np.sqrt(max(nt2 - float(np.sum(sv[:ranks[n]] ** 2)), 0.0)))
+        core = mode_product(y, A[nd - 1].T, nd - 1)
+        fit = 1.0 - np.sqrt(max(nt2 - float(np.vdot(core, core)), 0.0)) / np.sqrt(nt2)
+        tr.wall_s.append(time.perf_counter() - t0)
+        tr.fitness.append(float(fit))
+        if len(tr.fitness) > 1 and abs(tr.fitness[-1] - tr.fitness[-2]) < tol:
+            break
+    return core, A, tr
+
+
 def khatri_rao(mats):
     """src/tensors.py:288-301 (first matrix slowest)."""
     out = np.asarray(mats[0])
@@ -561,9 +643,10 @@ def cp_on_core(core, rank, sweeps=25, seed=0):
 
 
 def cp_via_tucker(t, rank, tucker_sweeps=5, cp_sweeps=None, sketch_size=None,
-                  sketch_factor=None, seed=0, tucker_rank=None):
-    """Alg. 6 as at src/cp.py:177-224 (sketched branch).  tucker_rank=None ties
-    the Tucker ranks to the CP rank exactly like the reference; config 5 of
+                  sketch_factor=None, seed=0, tucker_rank=None, sketch="leverage-random"):
+    """Alg. 6 as at src/cp.py:177-224 (sketch=None: the exact-HOOI compression
+    stage with HOSVD init, src/cp.py:195-205).  tucker_rank=None ties the
+    Tucker ranks to the CP rank exactly like the reference; config 5 of
     BASELINE.json sets tucker_rank=20 with rank=10."""
     shape = tuple(t.shape)
     nd = len(shape)
@@ -571,9 +654,13 @@ def cp_via_tucker(t, rank, tucker_sweeps=5, cp_sweeps=None, sketch_size=None,
         raise ValueError("rank exceeds a tensor extent")
     s_t, s_c = (c.generate_state(1)[0] for c in np.random.SeedSequence(seed).spawn(2))
     tr_rank = rank if tucker_rank is None else tucker_rank
-    core, B, ttr = sketched_tucker(t, (tr_rank,) * nd, "leverage-random",
-                                   max_sweeps=tucker_sweeps, sketch_size=sketch_size,
-                                   sketch_factor=sketch_factor, init="rrf", seed=int(s_t))
+    if sketch:
+        core, B, ttr = sketched_tucker(t, (tr_rank,) * nd, "leverage-random",
+                                       max_sweeps=tucker_sweeps, sketch_size=sketch_size,
+                                       sketch_factor=sketch_factor, init="rrf", seed=int(s_t))
+    else:
+        core, B, ttr = hooi(t, (tr_rank,) * nd, max_sweeps=tucker_sweeps, init="hosvd",
+                            seed=int(s_t))
     A, w, ctr = cp_on_core(core, rank, sweeps=25 if cp_sweeps is None else cp_sweeps,
                            seed=int(s_c))
     fac = [b @ a for b, a in zip(B, A)]

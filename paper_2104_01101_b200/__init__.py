@@ -8,13 +8,13 @@ libskx.so (hand-written sm_100a CUDA, include/skx.h) plus cuBLAS/cuSOLVER for
 dense factorisations; there is no CPU fallback.
 """
 from .tensors import (CPModel, SparseTensor, TuckerModel, fitness, fold, khatri_rao,
-                      matricize, matricize_t, mttkrp, tensor_norm, ttm)
+                      matricize, matricize_t, mttkrp, tensor_norm, ttm, ttmc)
 from .linalg import (LeverageProfile, RankDeficientError, SvdResult, leverage_scores,
                      reduced_qr, rsvd_lrls, thin_svd, truncated_svd)
 from .sketching import (CompositeSketchOp, CountSketchOp, LevSamplerOp, TensorSketchOp,
                         composite_apply, lev_apply, lev_apply_krp, lev_build, ts_apply_kron,
                         ts_apply_rhs)
-from .tucker import (SweepTrace, TuckerConfig, hosvd_init, init_rrf, sketched_tucker_als)
+from .tucker import (SweepTrace, TuckerConfig, hooi, hosvd_init, init_rrf, sketched_tucker_als)
 from .cp import CPConfig, cp_als, cp_via_sketched_tucker, sketched_cp_als
 from .rng import make_rng, split_rng
 

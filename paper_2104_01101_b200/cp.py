@@ -22,7 +22,7 @@ import numpy as np
 
 from . import rng as rngmod
 from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, shape_of)
-from .tucker import SweepTrace, TuckerConfig, hosvd_init_dev, sketched_tucker_als_dev
+from .tucker import SweepTrace, TuckerConfig, hooi_dev, hosvd_init_dev, sketched_tucker_als_dev
 
 
 def _torch():
@@ -165,15 +165,17 @@ def cp_via_sketched_tucker(t, config):
     rank = config.rank
     if any(rank > s for s in shape):
         raise ValueError("rank exceeds a tensor extent")
-    if not config.sketch:
-        raise NotImplementedError("the exact-HOOI compression stage is outside this build's hot path")
     seed_tucker, seed_cp = (s.generate_state(1)[0] for s in np.random.SeedSequence(config.seed).spawn(2))
     tr_rank = rank if config.tucker_rank is None else int(config.tucker_rank)
     tucker_cfg = TuckerConfig(ranks=(tr_rank,) * ndim, max_sweeps=config.tucker_sweeps,
-                              sketch="leverage-random", sketch_size=config.sketch_size,
-                              sketch_factor=config.sketch_factor, init="rrf", seed=int(seed_tucker))
+                              sketch="leverage-random" if config.sketch else None,
+                              sketch_size=config.sketch_size, sketch_factor=config.sketch_factor,
+                              init="rrf" if config.sketch else "hosvd", seed=int(seed_tucker))
     d = device_of(t)
-    core, tfac, ttrace = sketched_tucker_als_dev(d, tucker_cfg)
+    if config.sketch:
+        core, tfac, ttrace = sketched_tucker_als_dev(d, tucker_cfg)
+    else:  # exact HOOI compression stage (src/cp.py:203-204)
+        core, tfac, ttrace = hooi_dev(d, tucker_cfg)
     core_cfg = replace(config, sketch=None, sketch_size=None, sketch_factor=None,
                        init="hosvd-of-core", seed=int(seed_cp))
     cfac, cw, ctrace = cp_als_dev(core, core_cfg, on_core=True)

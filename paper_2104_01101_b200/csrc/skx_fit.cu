@@ -429,6 +429,66 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_mma(const int64_t* __restri
   }
 }
 
+// Skip-mode sparse TTMc for order 3 (src/tensors.py:261-277): row i_n of the
+// s_n x (R1 R2) unfolding is sum_e (v_e A1[i1_e, k1]) A2[i2_e, k2] over the
+// column's records in layout order (= the reference's mode_sort order), with
+// the products and sums unfused so the rounding follows numpy's.  Warp per
+// column; lane owns output entries k = lane + 32 t (k1 = k / R2, k2 = k % R2)
+// and accumulates them in registers; the column's records are loaded 32 at a
+// time and broadcast by shuffles.
+template <int T>
+__global__ void __launch_bounds__(256) k_ttmc3_skip(int64_t s_n, const int64_t* __restrict__ colptr,
+                                                    const double* __restrict__ rec, uint32_t c1_mask,
+                                                    const double* __restrict__ A1, int R1,
+                                                    const double* __restrict__ A2, int R2,
+                                                    double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int RR = R1 * R2;
+  int o1[T], o2[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int k = lane + 32 * t;
+    o1[t] = k < RR ? k / R2 : 0;
+    o2[t] = k < RR ? k % R2 : 0;
+  }
+  for (int64_t col = gw; col < s_n; col += tw) {
+    double acc[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = 0.0;
+    const int64_t e0 = colptr[col], e1 = colptr[col + 1];
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int64_t e = base + lane;
+      int32_t ca = 0, cb = 0;
+      double v = 0.0;
+      if (e < e1) {
+        int32_t cc[4];
+        load_rec<2>(rec, e, cc, v);
+        ca = cc[0];
+        cb = (int32_t)((uint32_t)cc[1] & c1_mask);
+      }
+      const int n = (int)imin(32, e1 - base);
+      for (int q = 0; q < n; ++q) {
+        const int64_t ia = __shfl_sync(0xffffffffu, ca, q);
+        const int64_t ib = __shfl_sync(0xffffffffu, cb, q);
+        const double vv = __shfl_sync(0xffffffffu, v, q);
+        const double* a1 = A1 + ia * R1;
+        const double* a2 = A2 + ib * R2;
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          acc[t] = __dadd_rn(acc[t], __dmul_rn(__dmul_rn(vv, __ldg(a1 + o1[t])), __ldg(a2 + o2[t])));
+      }
+    }
+    double* dst = out + col * (int64_t)RR;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int k = lane + 32 * t;
+      if (k < RR) dst[k] = acc[t];
+    }
+  }
+}
+
 // Generic order-N Tucker cross term: per nonzero, odometer over the core.
 struct GenPack {
   int ndim;
@@ -653,4 +713,26 @@ extern "C" int skx_cp_cross_coo(int ndim, const int64_t* shape_h, int64_t R, int
   k_cp_cross<<<kRedBlocks, kRedThreads, 0, s>>>(g, R, nnz, vals, weights, part);
   k_final_sum<<<1, 1024, 0, s>>>(part, kRedBlocks, out);
   return check_launch("k_cp_cross", 2);
+}
+
+extern "C" int skx_ttmc3_skip_coo(int64_t s_n, const int64_t* colptr, const void* rec,
+                                  uint32_t c1_mask, const double* a1, int r1, const double* a2,
+                                  int r2, double* out, void* stream) {
+  SKX_REQUIRE(r1 >= 1 && r2 >= 1 && r1 * r2 <= 1024,
+              "skx_ttmc3_skip_coo: need 1 <= R1 R2 <= 1024");
+  if (s_n == 0) return SKX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int rr = r1 * r2;
+  const int64_t blocks = imin((s_n + 7) / 8, (int64_t)num_sms() * 16);
+  const double* rc = (const double*)rec;
+#define SKX_TT(T) k_ttmc3_skip<T><<<(unsigned)blocks, 256, 0, s>>>(s_n, colptr, rc, c1_mask, a1, r1, \
+                                                                  a2, r2, out)
+  if (rr <= 32) SKX_TT(1);
+  else if (rr <= 64) SKX_TT(2);
+  else if (rr <= 128) SKX_TT(4);
+  else if (rr <= 256) SKX_TT(8);
+  else if (rr <= 512) SKX_TT(16);
+  else SKX_TT(32);
+#undef SKX_TT
+  return check_launch("k_ttmc3_skip");
 }

@@ -19,9 +19,8 @@ Device side (HBM layout):
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
-
 import ctypes
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -498,6 +497,76 @@ def ttm(t, mat, n):
     out = ttm_dev(torch.from_numpy(np.ascontiguousarray(t)).cuda(),
                   torch.from_numpy(np.ascontiguousarray(mat)).cuda(), n)
     return out.contiguous().cpu().numpy()
+
+
+def _ttmc_skip_sparse_dev(d, factors, skip, chunk=1 << 16):
+    """Skip-mode TTMc of a DeviceCoo: (s_skip, prod R_others) unfolding."""
+    torch = _torch()
+    others = [k for k in range(d.ndim) if k != skip]
+    s_n = d.shape[skip]
+    rr = int(np.prod([factors[k].shape[1] for k in others]))
+    if d.ndim == 3 and rr <= 1024:
+        out = torch.empty((s_n, rr), dtype=torch.float64, device="cuda")
+        colptr, rec = d.fibre(skip)
+        a1, a2 = (factors[k].contiguous() for k in others)
+        nat.call("skx_ttmc3_skip_coo", s_n, nat.ptr(colptr), nat.ptr(rec),
+                 ctypes.c_uint32(d.fibre_mask(skip)), nat.ptr(a1), int(a1.shape[1]), nat.ptr(a2),
+                 int(a2.shape[1]), nat.ptr(out), nat.stream())
+        return out
+    # other orders: the same per-nonzero Kronecker rows on the device, summed
+    # per output row in the reference's (mode-stable) order, chunk by chunk
+    out = torch.zeros((s_n, rr), dtype=torch.float64, device="cuda")
+    rows_all = d.coords[skip].long()
+    order = torch.argsort(rows_all, stable=True)
+    for lo in range(0, d.nnz, chunk):
+        idx = order[lo:lo + chunk]
+        contrib = d.vals[idx][:, None]
+        for k in others:
+            fk = factors[k][d.coords[k][idx].long()]
+            contrib = (contrib[:, :, None] * fk[:, None, :]).reshape(idx.numel(), -1)
+        rows, counts = torch.unique_consecutive(rows_all[idx], return_counts=True)
+        out[rows] += torch.segment_reduce(contrib, "sum", lengths=counts, axis=0)
+    return out
+
+
+def ttmc_dev(d, factors, skip=None):
+    """ttmc on device (src/tensors.py:217-258).  Dense: mode products in
+    ascending mode order.  Sparse, skip = n: the libskx kernel (order 3) over
+    mode n's fibre-major layout; skip = None: the mode-0 skip result
+    contracted with A_0^T (same sum, associated around the small side)."""
+    torch = _torch()
+    nd = d.ndim
+    if not is_sparse_dev(d):
+        out = d
+        for k in range(nd):
+            if k != skip:
+                out = ttm_dev(out, factors[k].t(), k)
+        return out
+    if skip is not None:
+        y = _ttmc_skip_sparse_dev(d, factors, skip)
+        shp = [d.shape[k] if k == skip else factors[k].shape[1] for k in range(nd)]
+        return fold(y, skip, shp)
+    y0 = _ttmc_skip_sparse_dev(d, factors, 0)
+    core = factors[0].t() @ y0
+    return core.reshape([factors[k].shape[1] for k in range(nd)])
+
+
+def ttmc(t, factors, skip=None, chunk=1 << 16):
+    """Tensor times matrix-chain: contract every mode m != skip with
+    factors[m]^T (src/tensors.py:217-247); numpy result."""
+    nd = t.ndim if isinstance(t, SparseTensor) else np.asarray(t).ndim
+    if skip is not None and not 0 <= skip < nd:
+        raise ValueError(f"skip mode {skip} out of range")
+    shape = tuple(t.shape)
+    for m in range(nd):
+        if m == skip:
+            continue
+        if np.shape(factors[m])[0] != shape[m]:
+            raise ValueError(
+                f"ttmc mode {m}: factor has {np.shape(factors[m])[0]} rows, tensor extent is {shape[m]}")
+    d = device_of(t)
+    fs = [_to_dev_mat(f) for f in factors]
+    return ttmc_dev(d, fs, skip).contiguous().cpu().numpy()
 
 
 def khatri_rao(mats):

@@ -26,7 +26,7 @@ from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, fini
                         plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
                         ts_rhs_dense_dev, ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
-                      matricize, shape_of)
+                      matricize, shape_of, ttm_dev, ttmc_dev)
 
 SKETCH_KINDS = (None, "tensorsketch", "leverage-random", "leverage-deterministic")
 
@@ -538,19 +538,111 @@ def sketched_tucker_als(t, config):
     return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace
 
 
+def _sparse_gram_dev(d, n, max_side=1 << 15):
+    """T_(n) T_(n)^T (s_n x s_n, dense) of a DeviceCoo, deterministically: the
+    products of every pair of nonzeros in the same mode-n fibre, sorted by
+    their Gram cell and summed per cell in that order."""
+    torch = _torch()
+    s_n = d.shape[n]
+    if s_n > max_side:
+        raise ValueError(f"hosvd_init: mode-{n} Gram of a sparse tensor needs s_n <= {max_side} "
+                         f"(got {s_n}); the reference forms it densely as well")
+    keys, vals = d.keys(n)  # flat_other * s_n + i_n, ascending
+    g = torch.zeros(s_n * s_n, dtype=torch.float64, device="cuda")
+    if vals.numel() == 0:
+        return g.view(s_n, s_n)
+    fib = keys // s_n
+    row = keys % s_n
+    _, counts = torch.unique_consecutive(fib, return_counts=True)
+    starts = torch.cumsum(counts, 0) - counts
+    # every (e, e') pair inside a fibre: e repeated len(fibre) times
+    reps = torch.repeat_interleave(counts, counts)
+    e = torch.repeat_interleave(torch.arange(vals.numel(), device="cuda"), reps)
+    first = torch.repeat_interleave(torch.repeat_interleave(starts, counts), reps)
+    offs = torch.arange(e.numel(), device="cuda") - torch.repeat_interleave(
+        torch.cumsum(reps, 0) - reps, reps)
+    e2 = first + offs
+    cell = row[e] * s_n + row[e2]
+    prod = vals[e] * vals[e2]
+    cell, order = torch.sort(cell, stable=True)
+    cells, cnt = torch.unique_consecutive(cell, return_counts=True)
+    g[cells] = torch.segment_reduce(prod[order], "sum", lengths=cnt, axis=0)
+    return g.view(s_n, s_n)
+
+
 def hosvd_init_dev(t, ranks):
     """Leading eigenvectors of the mode Grams (src/tucker.py:112-126), device."""
     torch = _torch()
     out = []
     for n, rank in enumerate(ranks):
-        tn = t.movedim(n, 0).reshape(t.shape[n], -1)
-        _, vecs = torch.linalg.eigh(tn @ tn.t())
+        if is_sparse_dev(t):
+            gram = _sparse_gram_dev(t, n)
+        else:
+            tn = t.movedim(n, 0).reshape(t.shape[n], -1)
+            gram = tn @ tn.t()
+        _, vecs = torch.linalg.eigh(gram)
         out.append(vecs.flip(1)[:, :rank].contiguous())
     return out
 
 
 def hosvd_init(t, ranks, rng=None):
+    """Leading left singular vectors of every unfolding via the mode Grams
+    (src/tucker.py:112-126); rng is accepted for interface parity."""
     d = device_of(t)
-    if is_sparse_dev(d):
-        raise NotImplementedError("hosvd_init of a sparse tensor is outside this build's hot path")
     return [a.cpu().numpy() for a in hosvd_init_dev(d, ranks)]
+
+
+def hooi_dev(t, config):
+    """Exact Tucker-ALS (src/tucker.py:155-193) on device: per mode the
+    leading left singular vectors of the skip-mode TTMc unfolding (libskx
+    kernel for sparse order 3), residual from the captured energy, core from
+    the last mode's contraction.  Returns (core, factors, trace)."""
+    import time
+    torch = _torch()
+    if config.sketch is not None:
+        raise ValueError("hooi is the unsketched driver; got a sketch config")
+    shape = tuple(int(s) for s in t.shape)
+    ndim = len(shape)
+    ranks = config.ranks
+    _validate_ranks(shape, ranks)
+    rng = rngmod.make_rng(config.seed)
+    init = config.init or "hosvd"
+    d = device_of(t)
+    if init == "hosvd":
+        factors = hosvd_init_dev(d, ranks)
+    elif init == "random":
+        factors = [random_orthonormal_dev(shape[n], ranks[n], rng) for n in range(ndim)]
+    else:
+        raise ValueError(f"unknown init {init!r} for hooi")
+    n2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
+    norm_t = math.sqrt(float(n2.item()))
+    norm_t_sq = norm_t ** 2
+    trace = SweepTrace()
+    core = None
+    for _ in range(config.max_sweeps):
+        tic = time.perf_counter()
+        y = None
+        captured = []
+        for n in range(ndim):
+            y = ttmc_dev(d, factors, skip=n)
+            yn = y.movedim(n, 0).reshape(shape[n], -1)
+            u, sv, _ = top_svd_dev(yn, ranks[n])
+            factors[n] = u[:, :ranks[n]].contiguous()
+            captured.append((sv[:ranks[n]] ** 2).sum())
+        core = ttm_dev(y, factors[ndim - 1].t(), ndim - 1).contiguous()
+        cap = torch.stack(captured + [(core * core).sum()]).cpu().tolist()
+        for c in cap[:-1]:
+            trace.residuals.append(math.sqrt(max(norm_t_sq - c, 0.0)))
+        fit = 1.0 - math.sqrt(max(norm_t_sq - cap[-1], 0.0)) / norm_t
+        trace.wall_s.append(time.perf_counter() - tic)
+        trace.fitness.append(float(fit))
+        if (len(trace.fitness) > 1
+                and abs(trace.fitness[-1] - trace.fitness[-2]) < config.convergence_tol):
+            break
+    return core, factors, trace
+
+
+def hooi(t, config):
+    """Exact Tucker-ALS (src/tucker.py:155-193)."""
+    core, factors, trace = hooi_dev(t, config)
+    return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace

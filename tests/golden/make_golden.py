@@ -183,10 +183,67 @@ def drivers():
     put("cpt_split", np.array(trace.stage_split))
 
 
+TTMC_CASES = {
+    # tag: (kind, shape, nnz or None, ranks, seed)
+    "ttd3": ("dense", (6, 5, 4), None, (2, 3, 2), 21),
+    "tts3": ("sparse", (15, 12, 10), 300, (3, 2, 4), 22),
+    "ttd4": ("dense", (5, 4, 3, 4), None, (2, 2, 3, 2), 23),
+    "tts4": ("sparse", (8, 7, 6, 5), 200, (2, 3, 2, 2), 24),
+}
+
+HOOI_CASES = {
+    "hooid": (("dense", (30, 30, 30), 3, 1e-2, 1), dict(ranks=(3, 3, 3), max_sweeps=4, seed=0)),
+    "hoois": (("sparse", (40, 40, 40), 3000, 3), dict(ranks=(4, 4, 4), max_sweeps=3, seed=0)),
+    "hooir": (("dense", (20, 18, 16), 2, 1e-2, 6),
+              dict(ranks=(2, 3, 2), max_sweeps=3, init="random", seed=5)),
+}
+
+
+def ttmc_input(kind, shape, nnz, seed):
+    gen = np.random.default_rng(seed)
+    if kind == "dense":
+        return gen.standard_normal(shape)
+    lin = np.sort(gen.choice(int(np.prod(shape)), size=nnz, replace=False))
+    coords = np.stack(np.unravel_index(lin, shape), axis=1)
+    return ref.SparseTensor(shape, coords, gen.standard_normal(nnz))
+
+
+def ttmc_cases():
+    for tag, (kind, shape, nnz, ranks, seed) in TTMC_CASES.items():
+        t = ttmc_input(kind, shape, nnz, seed)
+        gen = np.random.default_rng(seed + 100)
+        fs = [gen.standard_normal((s, r)) for s, r in zip(shape, ranks)]
+        for k, f in enumerate(fs):
+            put(f"{tag}_f{k}", f)
+        put(f"{tag}_all", ref.ttmc(t, fs, skip=None))
+        for n in range(len(shape)):
+            put(f"{tag}_skip{n}", ref.ttmc(t, fs, skip=n))
+
+
+def hooi_cases():
+    for tag, (spec, cfg) in HOOI_CASES.items():
+        t = make_input(spec)
+        model, trace = ref.hooi(t, ref.TuckerConfig(**cfg))
+        store_run(tag, model, trace)
+    # CP via Tucker with the exact-HOOI compression stage (sketch=None)
+    c, v = planted_cp_coo_host((30, 30, 30), 4000, rank=3, seed=5)
+    st = ref.SparseTensor((30, 30, 30), c, v)
+    cfg = ref.CPConfig(rank=3, sketch=None, tucker_sweeps=3, max_sweeps=10, seed=12)
+    model, trace = ref.cp_via_sketched_tucker(st, cfg)
+    for k, a in enumerate(model.factors):
+        put(f"cph_a{k}", a)
+    put("cph_w", model.weights)
+    put("cph_fitness", np.array(trace.fitness))
+    put("cph_residuals", np.array(trace.residuals))
+    put("cph_split", np.array(trace.stage_split))
+
+
 def main():
     tables()
     operators()
     drivers()
+    ttmc_cases()
+    hooi_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")

@@ -135,3 +135,66 @@ def test_speculative_sweep_replay_is_exact(skx, sparse, monkeypatch):
     for a, b in zip(fac0, fac1):
         assert torch.equal(a, b)
     assert tr0.residuals == tr1.residuals and tr0.fitness == tr1.fitness
+
+
+# ---- ttmc and exact HOOI (SURVEY 8b operator list, 8f rank 2) vs the reference
+from tests.test_oracle_golden import HOOI, TTMC, ttmc_factors, ttmc_input  # noqa: E402
+
+
+@pytest.mark.parametrize("tag", list(TTMC))
+def test_ttmc_vs_reference_golden(golden, skx, tag):
+    kind, shape, nnz, ranks, seed = TTMC[tag]
+    x = ttmc_input(kind, shape, nnz, seed)
+    t = x if kind == "dense" else skx.SparseTensor(shape, *x)
+    fs = ttmc_factors(shape, ranks, seed)
+    got = skx.ttmc(t, fs)
+    assert got.shape == golden[f"{tag}_all"].shape
+    assert relerr(got, golden[f"{tag}_all"]) <= 1e-13
+    for n in range(len(shape)):
+        got = skx.ttmc(t, fs, skip=n)
+        ref = golden[f"{tag}_skip{n}"]
+        assert got.shape == ref.shape
+        # sparse order 3: same unfused products in the same order as the
+        # reference; its np.add.reduceat sums differ only in the last bit
+        assert relerr(got, ref) <= (1e-15 if kind == "sparse" and len(shape) == 3 else 1e-13)
+    with pytest.raises(ValueError):
+        skx.ttmc(t, fs, skip=len(shape))
+    with pytest.raises(ValueError):
+        skx.ttmc(t, [f[:-1] for f in fs], skip=0)
+
+
+def test_ttmc_sparse_kernel_at_scale(skx, oracle):
+    """libskx skip-mode TTMc on a larger COO tensor against the oracle."""
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    shape = (300, 200, 250)
+    c, v = planted_cp_coo_host(shape, 200_000, rank=4, seed=8)
+    t = skx.SparseTensor(shape, c, v)
+    ot = oracle.Coo(shape, c, v)
+    g = np.random.default_rng(3)
+    fs = [g.standard_normal((s, r)) for s, r in zip(shape, (7, 12, 9))]
+    for n in range(3):
+        assert relerr(skx.ttmc(t, fs, skip=n), oracle.ttmc(ot, fs, skip=n)) <= 1e-13
+
+
+@pytest.mark.parametrize("tag", list(HOOI))
+def test_hooi_vs_reference_golden(golden, oracle, skx, tag):
+    spec, cfg = HOOI[tag]
+    t = _as_api_input(skx, oracle, spec)
+    model, trace = skx.hooi(t, skx.TuckerConfig(**cfg))
+    _compare_model(model, trace, golden, tag)
+    with pytest.raises(ValueError):
+        skx.hooi(t, skx.TuckerConfig(ranks=cfg["ranks"], sketch="tensorsketch"))
+
+
+def test_cp_via_tucker_hooi_stage_vs_reference_golden(golden, skx):
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    c, v = planted_cp_coo_host((30, 30, 30), 4000, rank=3, seed=5)
+    st = skx.SparseTensor((30, 30, 30), c, v)
+    cfg = skx.CPConfig(rank=3, sketch=None, tucker_sweeps=3, max_sweeps=10, seed=12)
+    model, trace = skx.cp_via_sketched_tucker(st, cfg)
+    assert trace.stage_split == int(golden["cph_split"])
+    assert np.allclose(trace.fitness, golden["cph_fitness"], rtol=0, atol=1e-9)
+    assert np.allclose(trace.residuals, golden["cph_residuals"], rtol=1e-8, atol=1e-12)
+    for k in range(3):
+        assert relerr(np.abs(model.factors[k]), np.abs(golden[f"cph_a{k}"])) <= 1e-8
+    assert relerr(np.abs(model.weights), np.abs(golden["cph_w"])) <= 1e-8

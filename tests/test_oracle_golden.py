@@ -154,3 +154,71 @@ def test_cp_via_tucker(golden, oracle):
     for k in range(3):
         assert relerr(np.abs(fac[k]), np.abs(golden[f"cpt_a{k}"])) <= 1e-9
     assert relerr(np.abs(w), np.abs(golden["cpt_w"])) <= 1e-9
+
+
+# ---- ttmc, HOOI, CP via exact-HOOI compression
+TTMC = {
+    "ttd3": ("dense", (6, 5, 4), None, (2, 3, 2), 21),
+    "tts3": ("sparse", (15, 12, 10), 300, (3, 2, 4), 22),
+    "ttd4": ("dense", (5, 4, 3, 4), None, (2, 2, 3, 2), 23),
+    "tts4": ("sparse", (8, 7, 6, 5), 200, (2, 3, 2, 2), 24),
+}
+HOOI = {
+    "hooid": (("dense", (30, 30, 30), 3, 1e-2, 1), dict(ranks=(3, 3, 3), max_sweeps=4, seed=0)),
+    "hoois": (("sparse", (40, 40, 40), 3000, 3), dict(ranks=(4, 4, 4), max_sweeps=3, seed=0)),
+    "hooir": (("dense", (20, 18, 16), 2, 1e-2, 6),
+              dict(ranks=(2, 3, 2), max_sweeps=3, init="random", seed=5)),
+}
+
+
+def ttmc_input(kind, shape, nnz, seed):
+    """(dense array | (coords, values)) as tests/golden/make_golden.py draws them."""
+    g = np.random.default_rng(seed)
+    if kind == "dense":
+        return g.standard_normal(shape)
+    lin = np.sort(g.choice(int(np.prod(shape)), size=nnz, replace=False))
+    return np.stack(np.unravel_index(lin, shape), axis=1), g.standard_normal(nnz)
+
+
+def ttmc_factors(shape, ranks, seed):
+    g = np.random.default_rng(seed + 100)
+    return [g.standard_normal((s, r)) for s, r in zip(shape, ranks)]
+
+
+@pytest.mark.parametrize("tag", list(TTMC))
+def test_ttmc(golden, oracle, tag):
+    kind, shape, nnz, ranks, seed = TTMC[tag]
+    x = ttmc_input(kind, shape, nnz, seed)
+    t = x if kind == "dense" else oracle.Coo(shape, *x)
+    fs = ttmc_factors(shape, ranks, seed)
+    assert relerr(oracle.ttmc(t, fs), golden[f"{tag}_all"]) <= 1e-13
+    for n in range(len(shape)):
+        assert relerr(oracle.ttmc(t, fs, skip=n), golden[f"{tag}_skip{n}"]) <= 1e-13
+
+
+@pytest.mark.parametrize("tag", list(HOOI))
+def test_hooi_driver(golden, oracle, tag):
+    spec, cfg = HOOI[tag]
+    t = make_input(oracle, spec)
+    core, fac, tr = oracle.hooi(t, cfg["ranks"], max_sweeps=cfg["max_sweeps"],
+                                init=cfg.get("init", "hosvd"), seed=cfg["seed"])
+    got_f, got_c = canon(fac, core)
+    ref_f, ref_c = canon([golden[f"{tag}_a{k}"] for k in range(3)], golden[f"{tag}_core"])
+    for a, b in zip(got_f, ref_f):
+        assert relerr(a, b) <= 1e-10
+    assert relerr(got_c, ref_c) <= 1e-10
+    assert np.allclose(tr.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-12)
+    assert np.allclose(tr.residuals, golden[f"{tag}_residuals"], rtol=1e-9, atol=1e-12)
+
+
+def test_cp_via_tucker_hooi_stage(golden, oracle):
+    c, v = planted_cp_coo_host((30, 30, 30), 4000, rank=3, seed=5)
+    st = oracle.Coo((30, 30, 30), c, v)
+    fac, w, tr, _ = oracle.cp_via_tucker(st, 3, tucker_sweeps=3, cp_sweeps=10, seed=12,
+                                         sketch=None)
+    assert tr.stage_split == int(golden["cph_split"])
+    assert np.allclose(tr.fitness, golden["cph_fitness"], rtol=0, atol=1e-10)
+    assert np.allclose(tr.residuals, golden["cph_residuals"], rtol=1e-9, atol=1e-12)
+    for k in range(3):
+        assert relerr(np.abs(fac[k]), np.abs(golden[f"cph_a{k}"])) <= 1e-9
+    assert relerr(np.abs(w), np.abs(golden["cph_w"])) <= 1e-9
