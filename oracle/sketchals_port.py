@@ -642,6 +642,59 @@ def cp_on_core(core, rank, sweeps=25, seed=0):
     return A, w, tr
 
 
+def sketched_cp(t, rank, max_sweeps=30, sketch_size=None, sketch_factor=None, seed=0,
+                init="rrf"):
+    """Leverage-sampled CP-ALS on the full tensor (src/cp.py:110-116,
+    119-174 sketched branch): RRF (or random) init of every mode from the
+    first of two seed streams; per mode a random leverage sample of the
+    Khatri-Rao rows (second stream), weighted Hadamard rows and fibres,
+    least squares (numpy lstsq), column normalisation; fitness per sweep and
+    residual (1 - fit) ||T||."""
+    import time
+
+    shape = tuple(t.shape)
+    nd = len(shape)
+    nt = norm_of(t)
+    r_init, r_sketch = streams(seed, 2)
+    width = None
+    if sketch_factor is not None:
+        width = max(rank, int(math.ceil(math.sqrt(sketch_factor) * rank)))
+    elif sketch_size is not None:
+        width = max(rank, int(math.ceil(math.sqrt(sketch_size / rank ** 2) * rank)))
+    if init == "random":
+        A = [r_init.uniform(size=(shape[n], rank)) for n in range(nd)]
+    else:
+        w0 = width or max(rank + 8, 2 * rank)
+        A = [init_rrf(unfold(t, n), rank, min(w0, shape[n]), r_init) if shape[n] > rank
+             else np.linalg.qr(r_init.standard_normal((shape[n], rank)))[0] for n in range(nd)]
+    A = [np.asarray(a, dtype=np.float64) for a in A]
+    w = np.ones(rank)
+    m = int(sketch_size) if sketch_size is not None else int(math.ceil(sketch_factor * rank ** 2))
+    bts = [unfold_t(t, n) for n in range(nd)]
+    tr = Trace()
+    for _ in range(max_sweeps):
+        t0 = time.perf_counter()
+        for n in range(nd):
+            others = [A[k] for k in _rest(nd, n)]
+            ext = tuple(shape[k] for k in _rest(nd, n))
+            idx, wt, _ = lev_sample(others, m, r_sketch)
+            z = others[0][idx[:, 0]].copy()
+            for k in range(1, len(others)):
+                z *= others[k][idx[:, k]]
+            z = wt[:, None] * z
+            flat = np.ravel_multi_index(idx.T, ext)
+            bt = bts[n]
+            y = np.asarray(bt.tocsr()[flat].todense()) if sp.issparse(bt) else np.asarray(bt)[flat]
+            y = wt[:, None] * y
+            sol, *_ = np.linalg.lstsq(z, y, rcond=None)
+            A[n], w = _unit_columns(sol.T)
+        fit = fitness_cp(t, [a.copy() for a in A], w.copy())
+        tr.residuals.append((1.0 - fit) * nt)
+        tr.wall_s.append(time.perf_counter() - t0)
+        tr.fitness.append(float(fit))
+    return A, w, tr
+
+
 def cp_via_tucker(t, rank, tucker_sweeps=5, cp_sweeps=None, sketch_size=None,
                   sketch_factor=None, seed=0, tucker_rank=None, sketch="leverage-random"):
     """Alg. 6 as at src/cp.py:177-224 (sketch=None: the exact-HOOI compression

@@ -5,8 +5,8 @@ sampling) to compress, exact CP-ALS on the small core (hosvd-of-core init),
 then the factor chains multiplied back and renormalised, with the final
 fitness measured against the full tensor (src/cp.py:177-224).  ``cp_als`` is
 the exact normal-equations CP-ALS (src/cp.py:119-174) on a dense tensor held
-on the GPU -- used on the core.  ``sketched_cp_als`` (leverage-sampled CP on
-the full tensor) is a different algorithm outside this build's path.
+on the GPU -- used on the core.  ``sketched_cp_als`` is leverage-sampled
+CP-ALS on the full tensor (src/cp.py:110-116).
 
 Extension: ``CPConfig.tucker_rank`` (default None = the reference's tie of the
 Tucker ranks to the CP rank) lets config 5 of BASELINE.json request Tucker
@@ -90,28 +90,7 @@ def cp_als_dev(t, config, on_core=False):
         raise ValueError("CP decomposition of a zero-norm tensor is undefined")
     rng_init, _ = rngmod.split_rng(config.seed, 2)
     init = config.init or ("hosvd-of-core" if on_core else "rrf")
-    if init == "hosvd-of-core":
-        factors = hosvd_init_dev(t, [min(rank, s) for s in shape])
-    elif init == "random":
-        factors = [torch.from_numpy(rng_init.uniform(size=(shape[n], rank))).cuda() for n in range(ndim)]
-    elif init == "rrf":
-        # src/cp.py:72-87 with the rrf width of src/cp.py:559-564
-        from .tucker import init_rrf_dev
-        width = None
-        if config.sketch_factor is not None:
-            width = max(rank, int(math.ceil(math.sqrt(config.sketch_factor) * rank)))
-        elif config.sketch_size is not None:
-            width = max(rank, int(math.ceil(math.sqrt(config.sketch_size / rank ** 2) * rank)))
-        width = width or max(rank + 8, 2 * rank)
-        factors = []
-        for n in range(ndim):
-            if shape[n] > rank:
-                factors.append(init_rrf_dev(t, n, rank, min(width, shape[n]), rng_init))
-            else:
-                g = torch.from_numpy(rng_init.standard_normal((shape[n], rank))).cuda()
-                factors.append(torch.linalg.qr(g, mode="reduced")[0].contiguous())
-    else:
-        raise ValueError(f"unknown init {init!r} for CP")
+    factors = _init_factors_dev(t, config, init, rng_init)
     weights = torch.ones(rank, dtype=torch.float64, device="cuda")
     grams = [a.t() @ a for a in factors]
     res_dev, fit_dev, walls = [], [], []
@@ -141,6 +120,37 @@ def cp_als_dev(t, config, on_core=False):
     return factors, weights, trace
 
 
+def _init_factors_dev(t, config, init, rng_init):
+    """src/cp.py:72-87 on device (t dense CUDA tensor or DeviceCoo)."""
+    torch = _torch()
+    shape = shape_of(t)
+    ndim = len(shape)
+    rank = config.rank
+    if init == "hosvd-of-core":
+        factors = hosvd_init_dev(t, [min(rank, s) for s in shape])
+    elif init == "random":
+        factors = [torch.from_numpy(rng_init.uniform(size=(shape[n], rank))).cuda() for n in range(ndim)]
+    elif init == "rrf":
+        # src/cp.py:72-87 with the rrf width of src/cp.py:559-564
+        from .tucker import init_rrf_dev
+        width = None
+        if config.sketch_factor is not None:
+            width = max(rank, int(math.ceil(math.sqrt(config.sketch_factor) * rank)))
+        elif config.sketch_size is not None:
+            width = max(rank, int(math.ceil(math.sqrt(config.sketch_size / rank ** 2) * rank)))
+        width = width or max(rank + 8, 2 * rank)
+        factors = []
+        for n in range(ndim):
+            if shape[n] > rank:
+                factors.append(init_rrf_dev(t, n, rank, min(width, shape[n]), rng_init))
+            else:
+                g = torch.from_numpy(rng_init.standard_normal((shape[n], rank))).cuda()
+                factors.append(torch.linalg.qr(g, mode="reduced")[0].contiguous())
+    else:
+        raise ValueError(f"unknown init {init!r} for CP")
+    return factors
+
+
 def cp_als(t, config, on_core=False):
     """Exact CP-ALS (src/cp.py:102-107) for dense tensors on the GPU."""
     if config.sketch is not None:
@@ -152,9 +162,64 @@ def cp_als(t, config, on_core=False):
     return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
 
 
+def sketched_cp_als_dev(d, config):
+    """Leverage-sampled CP-ALS on the full tensor (src/cp.py:110-174, sketched
+    branch) on device: per mode a random leverage sample of the Khatri-Rao
+    rows (bit-exact index sets, libskx K3), weighted Hadamard rows and the
+    sampled fibres (dense gather or one-pass sparse filter), least squares by
+    QR, column normalisation; fitness each sweep, residual (1 - fit) ||T||."""
+    from .sketching import (filter_fibers_dev, gather_coo_dev, gather_dense_dev, hits_to_dense,
+                            lev_sample_dev)
+    torch = _torch()
+    shape = shape_of(d)
+    ndim = len(shape)
+    rank = config.rank
+    if rank < 1:
+        raise ValueError("rank must be positive")
+    sparse = is_sparse_dev(d)
+    norm_t2 = d.norm2()[0] if sparse else (d * d).sum()
+    nt = math.sqrt(float(norm_t2.item()))
+    if nt == 0.0:
+        raise ValueError("CP decomposition of a zero-norm tensor is undefined")
+    rng_init, rng_sketch = rngmod.split_rng(config.seed, 2)
+    factors = _init_factors_dev(d, config, config.init or "rrf", rng_init)
+    factors = [a.to(torch.float64).contiguous() for a in factors]
+    weights = torch.ones(rank, dtype=torch.float64, device="cuda")
+    m = config.resolved_sketch_size()
+    if m < rank:
+        raise ValueError(f"sketch size {m} below rank {rank}")
+    trace = SweepTrace()
+    for _ in range(config.resolved_sweeps(False)):
+        tic = time.perf_counter()
+        for n in range(ndim):
+            others = [factors[k] for k in range(ndim) if k != n]
+            ext = [shape[k] for k in range(ndim) if k != n]
+            idx, w, _, _ = lev_sample_dev(others, m, rng_sketch)
+            z = others[0][idx[:, 0]].clone()
+            for c in range(1, len(others)):
+                z *= others[c][idx[:, c]]
+            z = w[:, None] * z
+            if sparse:
+                keys, vals = filter_fibers_dev(d, n, idx)
+                off, col, val = gather_coo_dev(keys, vals, ext, shape[n], idx, w)
+                y = hits_to_dense(off, col, val, m, shape[n])
+            else:
+                y = gather_dense_dev(d, n, idx, w)
+            sol = torch.linalg.lstsq(z, y).solution
+            factors[n], weights = _normalize_columns_dev(sol.t().contiguous())
+        fit = float(fitness_cp_dev(d, factors, weights, norm_t2).item())
+        trace.residuals.append((1.0 - fit) * nt)
+        trace.wall_s.append(time.perf_counter() - tic)
+        trace.fitness.append(fit)
+    return factors, weights, trace
+
+
 def sketched_cp_als(t, config):
-    raise NotImplementedError("sketched_cp_als (leverage-sampled CP on the full tensor) is outside "
-                              "this build's hot path (SURVEY 2.1 / 8f)")
+    """Leverage-score sketched CP-ALS (src/cp.py:110-116)."""
+    if config.sketch != "leverage-random":
+        raise ValueError("sketched_cp_als needs sketch='leverage-random'")
+    factors, weights, trace = sketched_cp_als_dev(device_of(t), config)
+    return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
 
 
 def cp_via_sketched_tucker(t, config):

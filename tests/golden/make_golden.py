@@ -238,12 +238,32 @@ def hooi_cases():
     put("cph_split", np.array(trace.stage_split))
 
 
+SCP_CASES = {
+    "scpd": (("dense", (20, 18, 16), 3, 1e-2, 7),
+             dict(rank=3, sketch="leverage-random", sketch_factor=16, max_sweeps=5, seed=13)),
+    "scps": (("sparse", (30, 30, 30), 4000, 5),
+             dict(rank=3, sketch="leverage-random", sketch_size=200, max_sweeps=4, seed=14)),
+}
+
+
+def sketched_cp_cases():
+    for tag, (spec, cfg) in SCP_CASES.items():
+        t = make_input(spec)
+        model, trace = ref.sketched_cp_als(t, ref.CPConfig(**cfg))
+        for k, a in enumerate(model.factors):
+            put(f"{tag}_a{k}", a)
+        put(f"{tag}_w", model.weights)
+        put(f"{tag}_fitness", np.array(trace.fitness))
+        put(f"{tag}_residuals", np.array(trace.residuals))
+
+
 def main():
     tables()
     operators()
     drivers()
     ttmc_cases()
     hooi_cases()
+    sketched_cp_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")

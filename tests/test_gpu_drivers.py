@@ -198,3 +198,22 @@ def test_cp_via_tucker_hooi_stage_vs_reference_golden(golden, skx):
     for k in range(3):
         assert relerr(np.abs(model.factors[k]), np.abs(golden[f"cph_a{k}"])) <= 1e-8
     assert relerr(np.abs(model.weights), np.abs(golden["cph_w"])) <= 1e-8
+
+
+from tests.test_oracle_golden import SCP  # noqa: E402
+
+
+@pytest.mark.parametrize("tag", list(SCP))
+def test_sketched_cp_als_vs_reference_golden(golden, oracle, skx, tag):
+    spec, cfg = SCP[tag]
+    t = _as_api_input(skx, oracle, spec)
+    model, trace = skx.sketched_cp_als(t, skx.CPConfig(**cfg))
+    # column signs follow the RRF init's singular-vector signs (SVD convention):
+    # the model is the same up to sign flips that cancel across modes
+    for k in range(3):
+        assert relerr(np.abs(model.factors[k]), np.abs(golden[f"{tag}_a{k}"])) <= 1e-8, (tag, k)
+    assert relerr(np.abs(model.weights), np.abs(golden[f"{tag}_w"])) <= 1e-8
+    assert np.allclose(trace.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-9)
+    assert np.allclose(trace.residuals, golden[f"{tag}_residuals"], rtol=1e-7, atol=1e-10)
+    with pytest.raises(ValueError):
+        skx.sketched_cp_als(t, skx.CPConfig(rank=3, sketch=None))

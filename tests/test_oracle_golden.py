@@ -222,3 +222,25 @@ def test_cp_via_tucker_hooi_stage(golden, oracle):
     for k in range(3):
         assert relerr(np.abs(fac[k]), np.abs(golden[f"cph_a{k}"])) <= 1e-9
     assert relerr(np.abs(w), np.abs(golden["cph_w"])) <= 1e-9
+
+
+SCP = {
+    "scpd": (("dense", (20, 18, 16), 3, 1e-2, 7),
+             dict(rank=3, sketch="leverage-random", sketch_factor=16, max_sweeps=5, seed=13)),
+    "scps": (("sparse", (30, 30, 30), 4000, 5),
+             dict(rank=3, sketch="leverage-random", sketch_size=200, max_sweeps=4, seed=14)),
+}
+
+
+@pytest.mark.parametrize("tag", list(SCP))
+def test_sketched_cp(golden, oracle, tag):
+    spec, cfg = SCP[tag]
+    t = make_input(oracle, spec)
+    fac, w, tr = oracle.sketched_cp(t, cfg["rank"], max_sweeps=cfg["max_sweeps"],
+                                    sketch_size=cfg.get("sketch_size"),
+                                    sketch_factor=cfg.get("sketch_factor"), seed=cfg["seed"])
+    for k in range(3):
+        assert relerr(fac[k], golden[f"{tag}_a{k}"]) <= 1e-9
+    assert relerr(w, golden[f"{tag}_w"]) <= 1e-9
+    assert np.allclose(tr.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-10)
+    assert np.allclose(tr.residuals, golden[f"{tag}_residuals"], rtol=1e-8, atol=1e-12)
