@@ -274,6 +274,13 @@ int skx_ttmc3_skip_coo(int64_t s_n, const int64_t* colptr, const void* rec, uint
                        const double* a1, int r1, const double* a2, int r2, double* out,
                        void* stream);
 
+/* Decision flags of the sketched Cholesky QR (src/linalg.py:44-52 and the
+ * orthogonality check of the one-pass factor), all r x r row-major: G1 = Z^T Z,
+ * its Cholesky factor R1 (+ info), G2 = Q1^T Q1.  out[0] unsafe, out[1] one
+ * pass suffices, out[2] rank-deficient, out[3] = out[0] | !out[1] | out[2]. */
+int skx_cholqr_flags(const double* g1, const double* r1, const int* info, const double* g2, int r,
+                     int* out, void* stream);
+
 /* out[0] = sum(x^2) with a fixed-order reduction. */
 int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,
               void* stream);

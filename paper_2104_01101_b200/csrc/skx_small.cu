@@ -391,6 +391,75 @@ __global__ void __launch_bounds__(1024, 1) k_lrls_mid(const double* __restrict__
   }
 }
 
+// Decision flags of the Cholesky QR of the sketched system (src/linalg.py:44-52
+// rank test plus the orthogonality check), in one CTA instead of ~20 small
+// tensor kernels: out[0] = unsafe (Cholesky failed, or diag(R) not finite or
+// spanning >= 1e6), out[1] = one pass suffices (max |Q^T Q - I| < 1e-13),
+// out[2] = rank-deficient (some |R_ii| < 1e-12 ||Z||_F), out[3] = the
+// speculative sweep must be replayed (out[0] | !out[1] | out[2]).  NaNs count
+// as failures, as the comparisons in torch do.
+__global__ void __launch_bounds__(256) k_cholqr_flags(const double* __restrict__ g1,
+                                                      const double* __restrict__ r1,
+                                                      const int* __restrict__ info,
+                                                      const double* __restrict__ g2, int r,
+                                                      int* __restrict__ out) {
+  __shared__ double s_max[8], s_min[8], s_tr[8], s_dev[8];
+  __shared__ int s_nan[8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double dmax = -INFINITY, dmin = INFINITY, tr = 0.0, dev = 0.0;
+  int nan = 0;
+  for (int i = tid; i < r; i += blockDim.x) {
+    const double d = r1[(int64_t)i * r + i];
+    if (d != d) nan = 1;
+    dmax = fmax(dmax, d);
+    dmin = fmin(dmin, d);
+    tr += g1[(int64_t)i * r + i];
+  }
+  for (int64_t q = tid; q < (int64_t)r * r; q += blockDim.x) {
+    const int64_t i = q / r, j = q - i * r;
+    const double e = fabs(g2[q] - (i == j ? 1.0 : 0.0));
+    if (e != e) nan |= 2;
+    dev = fmax(dev, e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+  }
+  if (lane == 0) {
+    s_max[wid] = dmax;
+    s_min[wid] = dmin;
+    s_tr[wid] = tr;
+    s_dev[wid] = dev;
+    s_nan[wid] = nan;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int nw = blockDim.x >> 5;
+    double a = -INFINITY, b = INFINITY, t = 0.0, dv = 0.0;
+    int nn = 0;
+    for (int w = 0; w < nw; ++w) {
+      a = fmax(a, s_max[w]);
+      b = fmin(b, s_min[w]);
+      t += s_tr[w];
+      dv = fmax(dv, s_dev[w]);
+      nn |= s_nan[w];
+    }
+    const double tol = 1e-12 * sqrt(t);
+    int bad = (t != t) ? 1 : 0;
+    for (int i = 0; i < r && !bad; ++i) bad = fabs(r1[(int64_t)i * r + i]) < tol;
+    const int unsafe = info[0] != 0 || (nn & 1) || !(a < 1e6 * b);
+    const int one = !(nn & 2) && dv < 1e-13;
+    out[0] = unsafe;
+    out[1] = one;
+    out[2] = bad;
+    out[3] = unsafe || !one || bad;
+  }
+}
+
 }  // namespace skx
 
 using namespace skx;
@@ -421,4 +490,11 @@ extern "C" int skx_lrls_mid(const double* rz, const double* b, int r, int w, dou
   cudaFuncSetAttribute(k_lrls_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_lrls_mid<<<1, 32 * w, smem, (cudaStream_t)stream>>>(rz, b, r, w, q, x);
   return check_launch("k_lrls_mid");
+}
+
+extern "C" int skx_cholqr_flags(const double* g1, const double* r1, const int* info,
+                                const double* g2, int r, int* out, void* stream) {
+  SKX_REQUIRE(r >= 1, "skx_cholqr_flags: empty system");
+  k_cholqr_flags<<<1, 256, 0, (cudaStream_t)stream>>>(g1, r1, info, g2, r, out);
+  return check_launch("k_cholqr_flags");
 }

@@ -364,15 +364,14 @@ def sketch_qr_dev(z, defer=None):
         eye = torch.eye(r, dtype=z.dtype, device=z.device)
         z1 = z @ torch.linalg.solve_triangular(r1, eye, upper=True)
     g2 = z1.transpose(0, 1) @ z1
-    d1 = torch.diagonal(r1)
-    unsafe = (i1[0] != 0) | ~(d1.max() < 1e6 * d1.min())
-    one_pass = (g2 - torch.eye(r, dtype=g2.dtype, device=g2.device)).abs().max() < 1e-13
-    tol = 1e-12 * torch.sqrt(torch.trace(g1))  # ||Z||_F
-    bad1 = (d1.abs() < tol).any()
+    # unsafe / one pass suffices / rank-deficient (+ replay flag) in one libskx CTA
+    fl = torch.empty(4, dtype=torch.int32, device="cuda")
+    nat.call("skx_cholqr_flags", nat.ptr(g1.contiguous()), nat.ptr(r1.contiguous()),
+             nat.ptr(i1.to(torch.int32)), nat.ptr(g2.contiguous()), r, nat.ptr(fl), nat.stream())
     if defer is not None:
-        defer.append(unsafe | ~one_pass | bad1)
+        defer.append(fl[3])
         return z1, r1, None
-    flags = torch.stack([unsafe, one_pass, bad1]).cpu()
+    flags = fl[:3].cpu()
     if bool(flags[0]):
         return qr_flag_dev(z)
     if bool(flags[1]):
@@ -380,6 +379,7 @@ def sketch_qr_dev(z, defer=None):
     r2, i2 = chol(g2)
     q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
     rz = r2 @ r1
+    tol = 1e-12 * torch.sqrt(torch.trace(g1))  # ||Z||_F
     bad = (torch.diagonal(rz).abs() < tol).any()
     flags2 = torch.stack([i2[0] != 0, bad]).cpu()
     if bool(flags2[0]):
