@@ -233,6 +233,7 @@ class NormalSource:
         self.pos = torch.tensor([c.p], dtype=torch.int64, device="cuda")
         self.batch = int(batch)
         self._segs = []  # [(tensor, event or None)] in stream order
+        self._base = 0  # absolute index of _segs[0] (segments before it were committed)
         self._i, self._off = 0, 0  # consumption point: segment, offset
 
     def _generate(self, n):
@@ -289,16 +290,24 @@ class NormalSource:
         return out.view(*shape)
 
     def snapshot(self):
-        """Consumption point to return to if a speculative sweep is replayed."""
-        return (self._i, self._off)
+        """Consumption point to return to if a speculative sweep is replayed
+        (absolute segment index, offset)."""
+        return (self._base + self._i, self._off)
 
     def restore(self, snap):
-        self._i, self._off = snap
+        i, off = snap
+        if i < self._base:
+            raise RuntimeError("NormalSource.restore: point already committed")
+        self._i, self._off = i - self._base, off
 
-    def commit(self):
-        """Release the fully consumed segments (no rewind before this point)."""
-        del self._segs[:self._i]
-        self._i = 0
+    def commit(self, snap=None):
+        """Release the segments fully consumed before `snap` (default: the
+        current point); no rewind before it afterwards."""
+        i = self._base + self._i if snap is None else snap[0]
+        drop = max(0, i - self._base)
+        del self._segs[:drop]
+        self._base += drop
+        self._i -= drop
 
     def sync_host(self):
         """Move the numpy Generator to where numpy would be (one D2H)."""
@@ -408,11 +417,14 @@ def assoc_mid_dev(qz, rz, yg):
     return q, qz @ (rinv.transpose(0, 1) @ q)
 
 
-def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None):
+def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None, pre=None):
     """Algorithm 5 (src/linalg.py:87-113) on device.
     z: (m, r) CUDA tensor (any strides), y: (m, s) CUDA tensor view.
     Returns (core_t (r, rank), a (s, rank), rank_bad flag).  defer: see
-    sketch_qr_dev (the rank check is then the caller's)."""
+    sketch_qr_dev (the rank check is then the caller's).  pre = (g, yg,
+    event): the Gaussian test matrix already drawn and Y G computed on another
+    stream (speculative sweeps only: drawing before the rank check would
+    consume the stream on a rank-deficient system)."""
     torch = _torch()
     m, r = z.shape
     s = y.shape[1]
@@ -424,12 +436,19 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None):
     if check and defer is None and bool(bad.item()):
         raise RankDeficientError("rank-deficient sketched system")
     width = min(rank + oversample, s)
-    g = normals.normal((s, width))
+    if pre is not None:
+        g, yg, ev = pre
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ev)
+        yg.record_stream(cur)
+    else:
+        g = normals.normal((s, width))
+        yg = None
     if width < r:
         # Same algebra, associated so that Y (m x s, the big operand) only meets
         # width-column matrices: X_ls G = R^-1 Q_z^T (Y G) and
         # Q^T X_ls = (Q_z R^-T Q)^T Y.  2.5x fewer flops at configs 2/4/5.
-        q, wm = assoc_mid_dev(qz, rz, y @ g)
+        q, wm = assoc_mid_dev(qz, rz, y @ g if yg is None else yg)
         d = wm.transpose(0, 1) @ y
     else:
         x = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ y, upper=True)

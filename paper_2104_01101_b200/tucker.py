@@ -194,6 +194,19 @@ def _init_streams():
     return _STREAMS[dev]
 
 
+_YG_STREAMS = {}
+
+
+def _yg_stream():
+    """High-priority stream for the early Y G pass of speculative sweeps."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _YG_STREAMS:
+        _, hi = torch.cuda.Stream.priority_range()
+        _YG_STREAMS[dev] = torch.cuda.Stream(priority=hi)
+    return _YG_STREAMS[dev]
+
+
 _FIT_STREAMS = {}
 
 
@@ -355,6 +368,9 @@ class _Run:
         if self.use_ts:
             if redraw:
                 self.build_ts(n)
+            pre = None
+            if defer is not None and self.comm is None:
+                pre = self._early_yg(n)
             z = ts_kron_dev(self.ts_ops[n], others)
             if self.comm is not None:  # this rank holds Y_n^T rows row_slab(s_n)
                 s_n = self.shape[n]
@@ -363,7 +379,7 @@ class _Run:
                                                            self.ranks[n], self.normals, self.comm)
                 return core_t, self.comm.allgather_rows(a_loc.contiguous(), s_n), res
             y = self.ts_rhs[n].t()
-            return self._finish_dense(z, y, n, defer)
+            return self._finish_dense(z, y, n, defer, pre)
         else:
             idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
             z = kron_rows_dev(others, idx, w)
@@ -397,9 +413,31 @@ class _Run:
                 self.comm.allreduce(y)
         return self._finish_dense(z, y, n)
 
-    def _finish_dense(self, z, y, n, defer=None):
-        core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals, defer=defer)
+    def _finish_dense(self, z, y, n, defer=None, pre=None):
+        core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals, defer=defer, pre=pre)
         return core_t, a, resid_dev(z, core_t, a, y)
+
+    def _early_yg(self, n):
+        """Speculative sweeps: draw this sub-problem's Gaussian test matrix now
+        and start Y G (a bandwidth-bound pass over Y_n) on the idle init side
+        stream, so it overlaps the Kronecker sketch and the Cholesky QR of Z
+        (latency-bound single-CTA kernels) on the sweep stream."""
+        torch = _torch()
+        s_n = self.shape[n]
+        width = min(self.ranks[n] + 10, s_n)
+        r = int(np.prod([self.ranks[k] for k in self.others(n)]))
+        if width >= r:
+            return None
+        g = self.normals.normal((s_n, width))
+        side = _yg_stream()
+        cur = torch.cuda.current_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            yg = self.ts_rhs[n].t() @ g
+            ev = torch.cuda.Event()
+            ev.record(side)
+        g.record_stream(side)
+        return g, yg, ev
 
     def _gather_hits(self, off, col, val):
         """All ranks' sampled-fibre hits as (row, col, val) triples."""
@@ -453,36 +491,51 @@ class _Run:
         core = None
         # TensorSketch sweeps run speculatively: every sub-problem takes the
         # one-pass Cholesky QR without a host round trip and records a device
-        # flag; one sync per sweep checks them all, and a flagged sweep is
-        # replayed from its starting state on the checked path (second QR
-        # pass / Householder / rank-deficiency redraw), so results are those
-        # of the checked path either way
+        # flag.  A sweep's flags are copied to the host asynchronously and
+        # checked once the next sweep has been enqueued (pipelined when no
+        # early stop needs the fitness), so the GPU does not wait for the host
+        # at sweep boundaries.  A flagged sweep is replayed from its starting
+        # state on the checked path (second QR pass / Householder /
+        # rank-deficiency redraw) and everything enqueued after it is
+        # discarded, so the results are those of the checked path either way.
         speculate = self.use_ts and self.comm is None
-        for sweep in range(self.cfg.max_sweeps):
+        pipeline = speculate and self.cfg.convergence_tol <= 0
+        nsw = self.cfg.max_sweeps
+        pending = None  # (sweep, start state, host flag, event) awaiting its check
+        checked = set()  # sweeps to re-run on the checked path
+        k = 0
+        while True:
+            if k >= nsw:
+                if pending is not None and self._flagged(pending):
+                    k = self._rollback(pending, res_dev, fit_dev, ev)
+                    checked.add(k)
+                    pending = None
+                    continue
+                break
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            if overlap and sweep + 1 < self.cfg.max_sweeps:
-                # the next sweep's Gaussian test matrices, on the low-priority
-                # stream behind the previous fitness
-                self.normals.prefetch_async(fs)
+            start = (k, list(self.factors), self.normals.snapshot(), len(res_dev), len(fit_dev),
+                     len(ev))
+            spec = speculate and k not in checked
             core_t = None
-            done = False
-            if speculate:
-                start = (list(self.factors), self.normals.snapshot(), len(res_dev))
-                flags, sweep_res = [], []
+            if spec:
+                flags = []
                 for n in range(self.ndim):
                     core_t, a, res = self.solve_mode(n, redraw=False, defer=flags)
                     self.factors[n] = a
-                    sweep_res.append(res)
-                if not bool(torch.stack(flags).any()):
-                    res_dev.extend(sweep_res)
-                    done = True
-                else:
-                    self.factors = list(start[0])
-                    self.normals.restore(start[1])
-                    del res_dev[start[2]:]
-            if not done:
+                    res_dev.append(res)
+                    if n == 0 and overlap and k + 1 < nsw:
+                        # the next sweep's Gaussian test matrices, on the
+                        # low-priority stream (enqueued once the GPU has work)
+                        self.normals.prefetch_async(fs)
+                hf = torch.empty(1, dtype=torch.int32, pin_memory=True)
+                hf.copy_(torch.stack(flags).any().to(torch.int32).view(1), non_blocking=True)
+                fev = torch.cuda.Event()
+                fev.record()
+            else:
+                if overlap and k + 1 < nsw:
+                    self.normals.prefetch_async(fs)
                 for n in range(self.ndim):
                     try:
                         core_t, a, res = self.solve_mode(n, redraw=False)
@@ -495,7 +548,6 @@ class _Run:
                                 f"(m={self.m}, sketch={self.cfg.sketch}): {exc}") from exc
                     self.factors[n] = a
                     res_dev.append(res)
-            self.normals.commit()
             core = self.fold_core(core_t)
             e1.record()
             ev.append((e0, e1))
@@ -512,10 +564,47 @@ class _Run:
             else:
                 f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, self.comm)
             fit_dev.append(f)
-            if self.cfg.convergence_tol > 0 and len(fit_dev) > 1:
-                if abs(float(fit_dev[-1].item()) - float(fit_dev[-2].item())) < self.cfg.convergence_tol:
-                    break
+            if pending is not None:  # the previous speculative sweep, now that this one is queued
+                if self._flagged(pending):
+                    k = self._rollback(pending, res_dev, fit_dev, ev)
+                    checked.add(k)
+                    pending = None
+                    continue
+                pending = None
+            if spec:
+                pending = (start, hf, fev)
+                if not pipeline:
+                    if self._flagged(pending):
+                        k = self._rollback(pending, res_dev, fit_dev, ev)
+                        checked.add(k)
+                        pending = None
+                        continue
+                    pending = None
+            # Gaussian segments before this sweep's start are no longer needed
+            self.normals.commit(start[2] if pending is not None else None)
+            if (self.cfg.convergence_tol > 0 and len(fit_dev) > 1
+                    and abs(float(fit_dev[-1].item()) - float(fit_dev[-2].item()))
+                    < self.cfg.convergence_tol):
+                break
+            k += 1
         return core
+
+    @staticmethod
+    def _flagged(pending):
+        _, hf, fev = pending
+        fev.synchronize()
+        return int(hf[0]) != 0
+
+    def _rollback(self, pending, res_dev, fit_dev, ev):
+        """Return the run to the start of a flagged speculative sweep (factors,
+        Gaussian-segment position, trace lists); returns that sweep's index."""
+        (k, factors, normals, n_res, n_fit, n_ev), _, _ = pending
+        self.factors = list(factors)
+        self.normals.restore(normals)
+        del res_dev[n_res:]
+        del fit_dev[n_fit:]
+        del ev[n_ev:]
+        return k
 
 
 def sketched_tucker_als_dev(t, config, comm=None):

@@ -130,7 +130,7 @@ def test_speculative_sweep_replay_is_exact(skx, sparse, monkeypatch):
     if sparse:
         t._device = None
     core1, fac1, tr1 = sketched_tucker_als_dev(t, cfg)
-    assert len(forced) == 3  # every sweep was replayed
+    assert len(forced) >= 3  # every sweep was flagged (and replayed)
     assert torch.equal(core0, core1)
     for a, b in zip(fac0, fac1):
         assert torch.equal(a, b)
