@@ -119,12 +119,20 @@ def run_ours(args, cfgd):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: SKX_BENCH_SHARE_GPU=1 runs every rank on cuda:0 over gloo (the
+    # multi-rank logic on a one-GPU box; never used for a reported number)
+    share = os.environ.get("SKX_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     comm = None
     if world > 1:
         import torch.distributed as dist
         from paper_2104_01101_b200.dist import Comm
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = Comm()
     nat.load()
 
