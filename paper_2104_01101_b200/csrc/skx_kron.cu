@@ -74,7 +74,11 @@ __global__ void k_kp_dense(const double* __restrict__ cs, KronModePlan pl, int64
   zt[p * m + pl.rb[r]] = cs[idx];
 }
 
-// grid (h-blocks, q, run-split).  Partial sums part[split][q*R+p][h].
+// grid (h-blocks, q, run-split).  Partial sums part[split][q*R+p][h].  Each
+// thread owns KH output buckets (h, h + 256, ...) so every run's CountSketch
+// row (PC values, a broadcast load) is reused KH times from registers.
+constexpr int kKpKH = 4;
+
 template <int PC>
 __global__ void __launch_bounds__(256) k_kp_conv(const double* __restrict__ zc, int64_t m,
                                                  const double* __restrict__ cs, KronModePlan pl,
@@ -84,27 +88,40 @@ __global__ void __launch_bounds__(256) k_kp_conv(const double* __restrict__ zc, 
   const int64_t q = blockIdx.y;
   for (int64_t h = threadIdx.x; h < m; h += blockDim.x) zs[h] = zc[q * m + h];
   __syncthreads();
-  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (h >= m) return;
+  const int64_t hb = blockIdx.x * (int64_t)blockDim.x * kKpKH + threadIdx.x;
+  if (hb >= m) return;
   const int64_t nr = *pl.nrun;
   const int64_t per = (nr + nsplit - 1) / nsplit;
   const int64_t r0 = imin(blockIdx.z * per, nr), r1 = imin(r0 + per, nr);
   for (int64_t p0 = 0; p0 < R; p0 += PC) {
-    double acc[PC];
+    double acc[kKpKH][PC];
 #pragma unroll
-    for (int u = 0; u < PC; ++u) acc[u] = 0.0;
+    for (int j = 0; j < kKpKH; ++j)
+#pragma unroll
+      for (int u = 0; u < PC; ++u) acc[j][u] = 0.0;
     for (int64_t r = r0; r < r1; ++r) {
-      int64_t src = h - (int64_t)pl.rb[r];
-      if (src < 0) src += m;
-      const double zv = zs[src];
       const double* y = cs + r * R + p0;
+      double yv[PC];
 #pragma unroll
-      for (int u = 0; u < PC; ++u)
-        if (p0 + u < R) acc[u] = fma(__ldg(y + u), zv, acc[u]);
+      for (int u = 0; u < PC; ++u) yv[u] = p0 + u < R ? __ldg(y + u) : 0.0;
+      const int64_t b = (int64_t)pl.rb[r];
+#pragma unroll
+      for (int j = 0; j < kKpKH; ++j) {
+        int64_t src = hb + j * (int64_t)blockDim.x - b;
+        if (src < 0) src += m;
+        const double zv = src < m ? zs[src] : 0.0;
+#pragma unroll
+        for (int u = 0; u < PC; ++u) acc[j][u] = fma(yv[u], zv, acc[j][u]);
+      }
     }
 #pragma unroll
-    for (int u = 0; u < PC; ++u)
-      if (p0 + u < R) part[((int64_t)blockIdx.z * rnew + q * R + p0 + u) * m + h] = acc[u];
+    for (int j = 0; j < kKpKH; ++j) {
+      const int64_t h = hb + j * (int64_t)blockDim.x;
+      if (h >= m) continue;
+#pragma unroll
+      for (int u = 0; u < PC; ++u)
+        if (p0 + u < R) part[((int64_t)blockIdx.z * rnew + q * R + p0 + u) * m + h] = acc[j][u];
+    }
   }
 }
 
@@ -210,7 +227,7 @@ extern "C" int skx_ts_kron_apply(int n_other, const int64_t* ext_h, const int64_
   for (int k = 0; k + 1 < n_other; ++k) rmid *= ranks_h[k];
   const int nsms = num_sms();
   // run split chosen so the largest step has >= 2 CTAs per SM
-  const int64_t hblk = (m + 255) / 256;
+  const int64_t hblk = (m + 256 * kKpKH - 1) / (256 * kKpKH);
   int nsplit = (int)imax(1, imin(32, (2 * nsms + hblk * rmid - 1) / imax(1, hblk * rmid)));
   Arena ar(ws, *ws_bytes);
   double* cs = ar.take<double>(smax * rmax);
