@@ -487,42 +487,6 @@ __global__ void k_sum_segs(const double* __restrict__ part, int64_t m, int64_t n
   yt[col * m + c] = s;
 }
 
-template <int CPL>
-__global__ void __launch_bounds__(256) k_gather_rows(const double* __restrict__ t, int64_t s_n,
-                                                     const int64_t* __restrict__ start,
-                                                     const uint32_t* __restrict__ list,
-                                                     const uint32_t* __restrict__ neg_of,
-                                                     int64_t m, double* __restrict__ yt) {
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ncb = (s_n + 32 * CPL - 1) / (32 * CPL);
-  const int64_t task = blockIdx.x * (int64_t)(blockDim.x >> 5) + wid;
-  if (task >= m * ncb) return;
-  const int64_t c = task / ncb, cb = task - c * ncb;
-  const int64_t col0 = cb * 32 * CPL;
-  double acc[CPL];
-#pragma unroll
-  for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
-  const int64_t r0 = start[c], r1 = start[c + 1];
-  for (int64_t r = r0; r < r1; ++r) {
-    const uint32_t a = list[r];
-    const bool ng = neg_of[a] != 0;
-    const double* row = t + (int64_t)a * s_n;
-#pragma unroll
-    for (int u = 0; u < CPL; ++u) {
-      const int64_t col = col0 + u * 32 + lane;
-      if (col < s_n) {
-        const double x = __ldcs(row + col);
-        acc[u] += ng ? -x : x;
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < CPL; ++u) {
-    const int64_t col = col0 + u * 32 + lane;
-    if (col < s_n) yt[col * m + c] = acc[u];
-  }
-}
-
 }  // namespace skx
 
 using namespace skx;
