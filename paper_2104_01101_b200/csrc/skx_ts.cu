@@ -405,8 +405,8 @@ __global__ void k_sum_flat(const double* __restrict__ part, int64_t s_n, int64_t
 }
 
 // ---- gather form for B == 1 (target mode is the fastest-varying one): rows
-// of s_n contiguous values share one bucket; a warp owns a bucket and adds the
-// rows of its (ascending) list -- exactly numpy's add.at order.
+// of s_n contiguous values share one bucket; the columns are sorted by bucket
+// (ascending index inside a bucket) and each bucket's rows are summed.
 template <bool FULL>
 __global__ void k_bucket_keys(const uint32_t* __restrict__ tA, int64_t A, uint32_t* keys,
                               uint32_t* idx, uint32_t* neg) {
@@ -431,9 +431,9 @@ __global__ void k_run_bounds(const uint32_t* __restrict__ keys, int64_t n, int64
   start[c] = lo;
 }
 
-// Segmented variant: task = (bucket c, segment k, column block); segment k
-// covers rows [k seg, (k+1) seg) of c's run, the last segment the rest; the
-// partial sums are then added segment by segment (fixed order) by
+// Task = (bucket c, segment k, column block); segment k covers rows
+// [k seg, (k+1) seg) of c's run, the last segment the rest; the partial sums
+// are then added segment by segment (fixed order, deterministic) by
 // k_sum_segs.  Keeps the GPU busy when the bucket count m is small (RRF:
 // k2 ~ 1e2 buckets) or the runs are long.
 template <int CPL>
