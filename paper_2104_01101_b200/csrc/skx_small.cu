@@ -398,13 +398,13 @@ __global__ void __launch_bounds__(1024, 1) k_lrls_mid(const double* __restrict__
 // out[2] = rank-deficient (some |R_ii| < 1e-12 ||Z||_F), out[3] = the
 // speculative sweep must be replayed (out[0] | !out[1] | out[2]).  NaNs count
 // as failures, as the comparisons in torch do.
-__global__ void __launch_bounds__(256) k_cholqr_flags(const double* __restrict__ g1,
+__global__ void __launch_bounds__(1024) k_cholqr_flags(const double* __restrict__ g1,
                                                       const double* __restrict__ r1,
                                                       const int* __restrict__ info,
                                                       const double* __restrict__ g2, int r,
                                                       int* __restrict__ out) {
-  __shared__ double s_max[8], s_min[8], s_tr[8], s_dev[8];
-  __shared__ int s_nan[8];
+  __shared__ double s_max[32], s_min[32], s_tr[32], s_dev[32];
+  __shared__ int s_nan[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double dmax = -INFINITY, dmin = INFINITY, tr = 0.0, dev = 0.0;
   int nan = 0;
@@ -415,11 +415,13 @@ __global__ void __launch_bounds__(256) k_cholqr_flags(const double* __restrict__
     dmin = fmin(dmin, d);
     tr += g1[(int64_t)i * r + i];
   }
-  for (int64_t q = tid; q < (int64_t)r * r; q += blockDim.x) {
-    const int64_t i = q / r, j = q - i * r;
-    const double e = fabs(g2[q] - (i == j ? 1.0 : 0.0));
-    if (e != e) nan |= 2;
-    dev = fmax(dev, e);
+  for (int i = wid; i < r; i += blockDim.x >> 5) {  // warp per row, lanes along it
+    const double* row = g2 + (int64_t)i * r;
+    for (int j = lane; j < r; j += 32) {
+      const double e = fabs(row[j] - (i == j ? 1.0 : 0.0));
+      if (e != e) nan |= 2;
+      dev = fmax(dev, e);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -495,6 +497,6 @@ extern "C" int skx_lrls_mid(const double* rz, const double* b, int r, int w, dou
 extern "C" int skx_cholqr_flags(const double* g1, const double* r1, const int* info,
                                 const double* g2, int r, int* out, void* stream) {
   SKX_REQUIRE(r >= 1, "skx_cholqr_flags: empty system");
-  k_cholqr_flags<<<1, 256, 0, (cudaStream_t)stream>>>(g1, r1, info, g2, r, out);
+  k_cholqr_flags<<<1, r > 128 ? 1024 : 256, 0, (cudaStream_t)stream>>>(g1, r1, info, g2, r, out);
   return check_launch("k_cholqr_flags");
 }

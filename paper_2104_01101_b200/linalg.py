@@ -371,7 +371,9 @@ def sketch_qr_dev(z, defer=None):
         # large r: one TRSM for R^-1 (r right-hand sides, parallel) and a GEMM,
         # instead of a latency-bound TRSM with the m x r operand
         eye = torch.eye(r, dtype=z.dtype, device=z.device)
-        z1 = z @ torch.linalg.solve_triangular(r1, eye, upper=True)
+        r1inv = torch.linalg.solve_triangular(r1, eye, upper=True)
+        z1 = z @ r1inv
+        r1._skx_inv = r1inv  # reused by assoc_mid_dev when the one-pass R is kept
     g2 = z1.transpose(0, 1) @ z1
     # unsafe / one pass suffices / rank-deficient (+ replay flag) in one libskx CTA
     fl = torch.empty(4, dtype=torch.int32, device="cuda")
@@ -410,9 +412,12 @@ def assoc_mid_dev(qz, rz, yg):
         nat.call("skx_lrls_mid", nat.ptr(rz.contiguous()), nat.ptr(b.contiguous()), r, w,
                  nat.ptr(q), nat.ptr(x), nat.stream())
         return q, qz @ x
-    # r > 128: R^-1 once (one TRSM with r right-hand sides), then GEMMs
-    rinv = torch.linalg.solve_triangular(rz, torch.eye(r, dtype=rz.dtype, device=rz.device),
-                                         upper=True)
+    # r > 128: R^-1 once (one TRSM with r right-hand sides, or the one-pass
+    # Cholesky QR's own), then GEMMs
+    rinv = getattr(rz, "_skx_inv", None)
+    if rinv is None:
+        rinv = torch.linalg.solve_triangular(rz, torch.eye(r, dtype=rz.dtype, device=rz.device),
+                                             upper=True)
     q, _ = torch.linalg.qr(rinv @ b, mode="reduced")
     return q, qz @ (rinv.transpose(0, 1) @ q)
 
