@@ -519,7 +519,7 @@ def rsvd_lrls_rows_dev(z, yt_loc, row_lo, s, rank, normals, comm, oversample=10,
 
 
 def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversample=10,
-                       check=True, hit_row=None):
+                       check=True, hit_row=None, defer=None):
     """rsvd_lrls_dev for a sparse right-hand side given as leverage-gather hits
     (row j's entries at hit_col/hit_val[hit_off[j]:hit_off[j+1]], distinct
     columns per row; or explicit rows in hit_row), plus its residual.  Same algebra as the dense call on
@@ -535,8 +535,8 @@ def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversampl
         raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
     if rank > min(r, s):
         raise ValueError(f"rank {rank} exceeds min({r}, {s})")
-    qz, rz, bad = sketch_qr_dev(z)
-    if check and bool(bad.item()):
+    qz, rz, bad = sketch_qr_dev(z, defer)
+    if check and defer is None and bool(bad.item()):
         raise RankDeficientError("rank-deficient sketched system")
     width = min(rank + oversample, s)
     g = normals.normal((s, width))

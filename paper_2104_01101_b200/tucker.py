@@ -381,7 +381,11 @@ class _Run:
             y = self.ts_rhs[n].t()
             return self._finish_dense(z, y, n, defer, pre)
         else:
-            idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
+            if defer is not None:  # rank check of the factors deferred with the rest
+                idx, w, _, lbad = lev_sample_dev(others, self.m, self.rng_sketch, check=False)
+                defer.append(lbad)
+            else:
+                idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
             z = kron_rows_dev(others, idx, w)
             if self.sparse:
                 keys, vals = filter_fibers_dev(self.d, n, idx)
@@ -398,7 +402,7 @@ class _Run:
                     # mostly-empty sampled fibres: work on the hit columns only
                     core_t, a, _, res = rsvd_lrls_hits_dev(z, off, col, val, self.shape[n],
                                                            self.ranks[n], self.normals,
-                                                           hit_row=row)
+                                                           hit_row=row, defer=defer)
                     return core_t, a, res
                 if row is None:
                     y = hits_to_dense(off, col, val, self.m, self.shape[n])
@@ -406,12 +410,12 @@ class _Run:
                     torch = _torch()
                     y = torch.zeros((self.m, self.shape[n]), dtype=torch.float64, device="cuda")
                     y[row, col] = val
-                    return self._finish_dense(z, y, n)
+                    return self._finish_dense(z, y, n, defer)
             else:
                 y = gather_dense_dev(self.d, n, idx, w)
             if self.comm is not None:
                 self.comm.allreduce(y)
-        return self._finish_dense(z, y, n)
+        return self._finish_dense(z, y, n, defer)
 
     def _finish_dense(self, z, y, n, defer=None, pre=None):
         core_t, a, _ = rsvd_lrls_dev(z, y, self.ranks[n], self.normals, defer=defer, pre=pre)
@@ -498,7 +502,7 @@ class _Run:
         # state on the checked path (second QR pass / Householder /
         # rank-deficiency redraw) and everything enqueued after it is
         # discarded, so the results are those of the checked path either way.
-        speculate = self.use_ts and self.comm is None
+        speculate = self.comm is None
         pipeline = speculate and self.cfg.convergence_tol <= 0
         nsw = self.cfg.max_sweeps
         pending = None  # (sweep, start state, host flag, event) awaiting its check
@@ -516,7 +520,7 @@ class _Run:
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             start = (k, list(self.factors), self.normals.snapshot(), len(res_dev), len(fit_dev),
-                     len(ev))
+                     len(ev), self.rng_sketch.bit_generator.state)
             spec = speculate and k not in checked
             core_t = None
             if spec:
@@ -598,9 +602,10 @@ class _Run:
     def _rollback(self, pending, res_dev, fit_dev, ev):
         """Return the run to the start of a flagged speculative sweep (factors,
         Gaussian-segment position, trace lists); returns that sweep's index."""
-        (k, factors, normals, n_res, n_fit, n_ev), _, _ = pending
+        (k, factors, normals, n_res, n_fit, n_ev, rs), _, _ = pending
         self.factors = list(factors)
         self.normals.restore(normals)
+        self.rng_sketch.bit_generator.state = rs
         del res_dev[n_res:]
         del fit_dev[n_fit:]
         del ev[n_ev:]

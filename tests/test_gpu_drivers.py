@@ -99,8 +99,9 @@ def test_sparse_reduced_config_vs_oracle(oracle, skx, kind):
     assert np.allclose(trace.fitness, tr.fitness, rtol=0, atol=1e-9)
 
 
+@pytest.mark.parametrize("sketch", ["tensorsketch", "leverage-random"])
 @pytest.mark.parametrize("sparse", [False, True])
-def test_speculative_sweep_replay_is_exact(skx, sparse, monkeypatch):
+def test_speculative_sweep_replay_is_exact(skx, sparse, sketch, monkeypatch):
     """A flagged speculative sweep is replayed from its starting state on the
     checked path: forcing the flag on the first sub-problem of every sweep
     must give bitwise the same model and trace as the unforced run."""
@@ -114,15 +115,16 @@ def test_speculative_sweep_replay_is_exact(skx, sparse, monkeypatch):
         t = skx.SparseTensor(shape, c, v)
     else:
         t = np.random.default_rng(2).standard_normal(shape)
-    cfg = skx.TuckerConfig(ranks=(4, 5, 3), max_sweeps=3, sketch="tensorsketch",
+    cfg = skx.TuckerConfig(ranks=(4, 5, 3), max_sweeps=3, sketch=sketch,
                            sketch_size=400, seed=9)
     core0, fac0, tr0 = sketched_tucker_als_dev(t, cfg)
     orig = linalg.sketch_qr_dev
-    forced = []
+    forced, seen = [], set()
 
     def forcing(z, defer=None):
         out = orig(z, defer)
-        if defer is not None and len(defer) == 1:
+        if defer is not None and id(defer) not in seen:  # first sub-problem of a sweep
+            seen.add(id(defer))
             defer.append(torch.ones((), dtype=torch.bool, device="cuda"))
             forced.append(1)
         return out
