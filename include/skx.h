@@ -281,6 +281,12 @@ int skx_ttmc3_skip_coo(int64_t s_n, const int64_t* colptr, const void* rec, uint
 int skx_cholqr_flags(const double* g1, const double* r1, const int* info, const double* g2, int r,
                      int* out, void* stream);
 
+/* Mode-last copy of a dense C-order tensor: out has mode `mode` moved to the
+ * fastest-varying position, the other modes in their order (the layout in
+ * which every dense sketch of that mode takes the gather form). */
+int skx_mode_last(const double* t, int ndim, const int64_t* shape_h, int mode, double* out,
+                  void* stream);
+
 /* out[0] = sum(x^2) with a fixed-order reduction. */
 int skx_sumsq(const double* x, int64_t n, double* out, void* ws, size_t* ws_bytes,
               void* stream);

@@ -58,6 +58,7 @@ _SIGS = {
     "skx_jacobi_svd": [c_p, c_i32, c_i64, c_i64, c_p, c_p, c_p, c_p],
     "skx_ttmc3_skip_coo": [c_i64, c_p, c_p, c_u32, c_p, c_i32, c_p, c_i32, c_p, c_p],
     "skx_cholqr_flags": [c_p, c_p, c_p, c_p, c_i32, c_p, c_p],
+    "skx_mode_last": [c_p, c_i32, c_p, c_i32, c_p, c_p],
     "skx_lrls_mid": [c_p, c_p, c_i32, c_i32, c_p, c_p, c_p],
     "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_u32, c_p, c_p,
                              c_sz_p, c_p],

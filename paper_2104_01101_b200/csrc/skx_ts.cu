@@ -623,6 +623,48 @@ static int dense_sketch(bool full, const double* t, int ndim, const int64_t* sha
   return check_launch("dense sketch (row form)", 2);
 }
 
+namespace skx {
+// Mode-last copy of a dense tensor viewed as [A, S, B]: out[a, b, s] = in[a, s, b]
+// (batched transposes of S x B panels through 32 x 32 shared-memory tiles,
+// coalesced on both sides).  Feeds the gather form of the dense sketches.
+__global__ void __launch_bounds__(256) k_mode_last(const double* __restrict__ in, int64_t S,
+                                                   int64_t B, double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const int64_t a = blockIdx.z;
+  const int64_t s0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  const double* src = in + a * S * B;
+  double* dst = out + a * S * B;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t s = s0 + ty + k, b = b0 + tx;
+    if (s < S && b < B) tile[ty + k][tx] = __ldcs(src + s * B + b);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t b = b0 + ty + k, s = s0 + tx;
+    if (s < S && b < B) dst[b * S + s] = tile[tx][ty + k];
+  }
+}
+
+}  // namespace skx
+
+extern "C" int skx_mode_last(const double* t, int ndim, const int64_t* shape_h, int mode,
+                             double* out, void* stream) {
+  using namespace skx;
+  SKX_REQUIRE(ndim >= 1 && mode >= 0 && mode < ndim, "skx_mode_last: bad mode");
+  int64_t A = 1, B = 1;
+  for (int k = 0; k < mode; ++k) A *= shape_h[k];
+  for (int k = mode + 1; k < ndim; ++k) B *= shape_h[k];
+  const int64_t S = shape_h[mode];
+  if (A * S * B == 0) return SKX_OK;
+  SKX_REQUIRE(A < 65536, "skx_mode_last: leading extent product too large for the grid");
+  dim3 grid((unsigned)((B + 31) / 32), (unsigned)((S + 31) / 32), (unsigned)A);
+  k_mode_last<<<grid, 256, 0, (cudaStream_t)stream>>>(t, S, B, out);
+  return check_launch("k_mode_last");
+}
+
 // Partial TS tables for the [A, s_n, B] split of a dense tensor: combine the
 // per-mode tables of modes before / after the target mode.
 namespace skx {

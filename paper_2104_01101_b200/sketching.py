@@ -241,9 +241,35 @@ def _coo_from_pairs(rows, cols, data, shape):
                                                            dtype=np.float64)).cuda())
 
 
-def ts_rhs_dense_dev(ts, t, mode):
-    """Y^T (s_n x m) for mode `mode` of a dense CUDA tensor."""
+# a mode-last copy of a dense tensor turns its sketches into the gather form
+# (each other-mode index owns one contiguous s_n-vector): one permuting copy
+# plus a bucket-sorted gather beat the shared-memory row form at large m
+MODE_LAST_MAX_BYTES = 24 << 30
+
+
+def mode_last_dev(t, mode):
+    """(tensor, mode) with `mode` moved to the fastest-varying position when
+    that is worth a copy (dense, not already last, small enough)."""
     torch = _torch()
+    nd = t.dim()
+    if mode == nd - 1 or t.numel() * 8 > MODE_LAST_MAX_BYTES:
+        return t, mode
+    a = int(np.prod(t.shape[:mode]))
+    if a >= 65536:
+        return t.movedim(mode, -1).contiguous(), nd - 1
+    shape = tuple(t.shape)
+    out = torch.empty(shape[:mode] + shape[mode + 1:] + (shape[mode],), dtype=torch.float64,
+                      device="cuda")
+    shp, sp_ = nat.host_i64(shape)
+    nat.call("skx_mode_last", nat.ptr(t.contiguous()), nd, sp_, mode, nat.ptr(out), nat.stream())
+    return out, nd - 1
+
+
+def ts_rhs_dense_dev(ts, t, mode):
+    """Y^T (s_n x m) for mode `mode` of a dense CUDA tensor (the other modes
+    keep their order in the mode-last copy, so the tables apply unchanged)."""
+    torch = _torch()
+    t, mode = mode_last_dev(t, mode)
     shape = tuple(t.shape)
     yt = torch.empty((shape[mode], ts.m), dtype=torch.float64, device="cuda")
     shp, sp_ = nat.host_i64(shape)

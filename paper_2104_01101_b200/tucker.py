@@ -23,6 +23,7 @@ from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev,
                      rsvd_lrls_rows_dev, top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, finish_rrf_scan,
                         gather_coo_dev, gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
+                        mode_last_dev,
                         plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
                         ts_rhs_dense_dev, ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
@@ -113,9 +114,10 @@ def rrf_stage1_dev(d, n, tabs):
                  nat.stream())
     else:
         tab = rrf_table_dev(tabs)
-        shp, sp_ = nat.host_i64(shape)
-        nat.call_ws("skx_rrf_stage1_dense", (nat.ptr(d), len(shape), sp_, n, nat.ptr(tab), tabs.k2,
-                                             nat.ptr(st1)))
+        dl, nl = mode_last_dev(d, n)  # gather form on a mode-last copy
+        shp, sp_ = nat.host_i64(tuple(dl.shape))
+        nat.call_ws("skx_rrf_stage1_dense", (nat.ptr(dl), len(shape), sp_, nl, nat.ptr(tab),
+                                             tabs.k2, nat.ptr(st1)))
     return st1
 
 
