@@ -455,7 +455,29 @@ __global__ void __launch_bounds__(256) k_gather_rows_seg(const double* __restric
   for (int u = 0; u < CPL; ++u) acc[u] = 0.0;
   const int64_t rs = start[c], re = start[c + 1];
   const int64_t r0 = imin(rs + k * seg, re), r1 = k == nseg - 1 ? re : imin(r0 + seg, re);
-  for (int64_t r = r0; r < r1; ++r) {
+  // RB rows in flight per iteration (loads first, then the adds in row order)
+  constexpr int RB = 4;
+  int64_t r = r0;
+  for (; r + RB <= r1; r += RB) {
+    double x[RB][CPL];
+    bool ng[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const uint32_t a = list[r + q];
+      ng[q] = neg_of[a] != 0;
+      const double* row = t + (int64_t)a * s_n;
+#pragma unroll
+      for (int u = 0; u < CPL; ++u) {
+        const int64_t col = col0 + u * 32 + lane;
+        x[q][u] = col < s_n ? __ldcs(row + col) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q)
+#pragma unroll
+      for (int u = 0; u < CPL; ++u) acc[u] += ng[q] ? -x[q][u] : x[q][u];
+  }
+  for (; r < r1; ++r) {
     const uint32_t a = list[r];
     const bool ng = neg_of[a] != 0;
     const double* row = t + (int64_t)a * s_n;
