@@ -439,6 +439,49 @@ def lev_sample(factors, m, rng):
     return idx, 1.0 / np.sqrt(m * pp), scores
 
 
+def top_m_products(score_lists, m):
+    """Best-first frontier search over score-sorted lists (src/sketching.py:
+    224-259): the m largest products, ties by lexicographic original
+    multi-index, in pop order."""
+    import heapq
+
+    total = int(np.prod([len(x) for x in score_lists]))
+    if m > total:
+        raise ValueError(f"cannot select {m} rows from {total}")
+    orders, srt = [], []
+    for x in score_lists:
+        o = np.lexsort((np.arange(len(x)), -np.asarray(x)))
+        orders.append(o)
+        srt.append(np.asarray(x)[o])
+    start = tuple(0 for _ in score_lists)
+    first = tuple(int(orders[k][0]) for k in range(len(score_lists)))
+    heap = [(-float(np.prod([x[0] for x in srt])), first, start)]
+    seen = {start}
+    out = []
+    while len(out) < m:
+        _, orig, pos = heapq.heappop(heap)
+        out.append(orig)
+        for k in range(len(pos)):
+            if pos[k] + 1 >= len(srt[k]):
+                continue
+            nxt = pos[:k] + (pos[k] + 1,) + pos[k + 1:]
+            if nxt in seen:
+                continue
+            seen.add(nxt)
+            prod = float(np.prod([srt[j][nxt[j]] for j in range(len(nxt))]))
+            norig = tuple(int(orders[j][nxt[j]]) for j in range(len(nxt)))
+            heapq.heappush(heap, (-prod, norig, nxt))
+    return np.array(out, dtype=np.int64)
+
+
+def lev_det(factors, m):
+    """Deterministic leverage sampler (src/sketching.py:218-220)."""
+    if m < 1:
+        raise ValueError("sample count must be positive")
+    scores = [leverage(f) for f in factors]
+    return top_m_products(scores, m), np.ones(m), scores
+
+
 def lev_rows(idx, w, extents, factors, bt):
     """src/sketching.py:262-287: weighted Kronecker rows and RHS rows."""
     m = idx.shape[0]
@@ -525,8 +568,8 @@ def sketched_tucker(t, ranks, sketch, max_sweeps=5, sketch_size=None,
     """Alg. 4 of the paper as implemented at src/tucker.py:216-300."""
     import time
 
-    if sketch not in ("tensorsketch", "leverage-random"):
-        raise ValueError("oracle covers tensorsketch and leverage-random")
+    if sketch not in ("tensorsketch", "leverage-random", "leverage-deterministic"):
+        raise ValueError("oracle covers tensorsketch and leverage sampling")
     shape = tuple(t.shape)
     nd = len(shape)
     ranks = tuple(int(r) for r in ranks)
@@ -572,7 +615,10 @@ def sketched_tucker(t, ranks, sketch, max_sweeps=5, sketch_size=None,
             z = ts_kron(tabs[n][0], tabs[n][1], ext, m, others)
             y = rhs[n]
         else:
-            idx, w, _ = lev_sample(others, m, r_sketch)
+            if sketch == "leverage-deterministic":
+                idx, w, _ = lev_det(others, m)
+            else:
+                idx, w, _ = lev_sample(others, m, r_sketch)
             z, y = lev_rows(idx, w, ext, others, bts[n])
         ct, a = rsvd_lrls(z, y, ranks[n], r_solve)
         res = float(np.linalg.norm((z @ ct) @ a.T - y))

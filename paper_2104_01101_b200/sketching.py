@@ -363,17 +363,77 @@ def lev_sample_dev(factors, m, gen, check=True):
     return idx, w, scores, bad
 
 
+def top_m_products_dev(score_list, m):
+    """Multi-indices (m, k) of the m largest products of one score per mode
+    (src/sketching.py:224-259), in the reference's pop order: products
+    descending, ties by lexicographic original multi-index.  Instead of the
+    best-first heap, every candidate position tuple with prod(p_k + 1) <= m in
+    the score-sorted lists is enumerated on the device (any other tuple has at
+    least m better ones) and the candidates are sorted by that key; products
+    are formed left to right as numpy's prod does.  Equal to the heap's order
+    whenever a step down a sorted list never rounds to an equal product with a
+    smaller original index (distinct or exactly tied scores)."""
+    torch = _torch()
+    lens = [int(x.numel()) for x in score_list]
+    total = int(np.prod(lens))
+    if m > total:
+        raise ValueError(f"cannot select {m} rows from {total}")
+    orders, srt = [], []
+    for x in score_list:
+        o = torch.sort(-x, stable=True).indices  # descending, ties by ascending index
+        orders.append(o)
+        srt.append(x[o])
+    dev = score_list[0].device
+    pos = torch.zeros((1, 0), dtype=torch.int64, device=dev)
+    bound = torch.ones(1, dtype=torch.int64, device=dev)
+    for L in lens:
+        cnt = torch.clamp(m // bound, max=L)
+        rep = torch.repeat_interleave(torch.arange(cnt.numel(), device=dev), cnt)
+        off = torch.arange(rep.numel(), device=dev) - torch.repeat_interleave(
+            torch.cumsum(cnt, 0) - cnt, cnt)
+        pos = torch.cat([pos[rep], off[:, None]], dim=1)
+        bound = bound[rep] * (off + 1)
+    prod = srt[0][pos[:, 0]]
+    for k in range(1, len(lens)):
+        prod = prod * srt[k][pos[:, k]]
+    orig = torch.stack([orders[k][pos[:, k]] for k in range(len(lens))], dim=1)
+    perm = torch.arange(prod.numel(), device=dev)
+    for k in reversed(range(len(lens))):  # lexicographic tie-break: least significant first
+        perm = perm[torch.sort(orig[perm, k], stable=True).indices]
+    perm = perm[torch.sort(-prod[perm], stable=True).indices]
+    return orig[perm[:m]].contiguous()
+
+
+def lev_det_dev(factors, m, check=True):
+    """Deterministic leverage sampler (src/sketching.py:218-220): the m
+    largest products of the factors' leverage scores, unit weights.  Returns
+    (idx, weights, scores, bad) like lev_sample_dev."""
+    torch = _torch()
+    if m < 1:
+        raise ValueError("sample count must be positive")
+    scores, bads = [], []
+    for f in factors:
+        sc, bad = leverage_scores_dev(f, check=check)
+        scores.append(sc)
+        bads.append(bad)
+    idx = top_m_products_dev(scores, m)
+    bad = bads[0]
+    for b in bads[1:]:
+        bad = bad | b
+    return idx, torch.ones(m, dtype=torch.float64, device="cuda"), scores, bad
+
+
 def lev_build(factors, m, variant, rng):
     """Build a leverage-score row sampler (src/sketching.py:193-221)."""
     if m < 1:
         raise ValueError("sample count must be positive")
-    if variant == "deterministic":
-        raise NotImplementedError(
-            "leverage-deterministic (top-m products) is outside this build's hot path (SURVEY 8f)")
-    if variant != "random":
+    if variant not in ("random", "deterministic"):
         raise ValueError(f"unknown variant {variant!r}")
     fs = [_dev(f) for f in factors]
-    idx, w, scores, _ = lev_sample_dev(fs, m, rngmod.make_rng(rng))
+    if variant == "deterministic":
+        idx, w, scores, _ = lev_det_dev(fs, m)
+    else:
+        idx, w, scores, _ = lev_sample_dev(fs, m, rngmod.make_rng(rng))
     extents = tuple(f.shape[0] for f in fs)
     profiles = [LeverageProfile(s.cpu().numpy(), f.shape[1]) for s, f in zip(scores, fs)]
     return LevSamplerOp(m, extents, profiles, variant, idx.cpu().numpy(), w.cpu().numpy(),

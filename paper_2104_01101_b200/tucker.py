@@ -22,8 +22,8 @@ from . import rng as rngmod
 from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev, rsvd_lrls_hits_dev,
                      rsvd_lrls_rows_dev, top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, finish_rrf_scan,
-                        gather_coo_dev, gather_dense_dev, hits_to_dense, kron_rows_dev, lev_sample_dev,
-                        mode_last_dev,
+                        gather_coo_dev, gather_dense_dev, hits_to_dense, kron_rows_dev, lev_det_dev,
+                        lev_sample_dev, mode_last_dev,
                         plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
                         ts_rhs_dense_dev, ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
@@ -229,9 +229,6 @@ class _Run:
         torch = _torch()
         if config.sketch is None:
             raise ValueError("sketched_tucker_als needs a sketch kind")
-        if config.sketch == "leverage-deterministic":
-            raise NotImplementedError(
-                "leverage-deterministic sampling is outside this build's hot path (SURVEY 8f)")
         self.shape = tuple(int(s) for s in t.shape)
         self.ndim = len(self.shape)
         self.ranks = config.ranks
@@ -383,11 +380,14 @@ class _Run:
             y = self.ts_rhs[n].t()
             return self._finish_dense(z, y, n, defer, pre)
         else:
+            det = self.cfg.sketch == "leverage-deterministic"
             if defer is not None:  # rank check of the factors deferred with the rest
-                idx, w, _, lbad = lev_sample_dev(others, self.m, self.rng_sketch, check=False)
+                idx, w, _, lbad = (lev_det_dev(others, self.m, check=False) if det else
+                                   lev_sample_dev(others, self.m, self.rng_sketch, check=False))
                 defer.append(lbad)
             else:
-                idx, w, _, _ = lev_sample_dev(others, self.m, self.rng_sketch)
+                idx, w, _, _ = (lev_det_dev(others, self.m) if det else
+                                lev_sample_dev(others, self.m, self.rng_sketch))
             z = kron_rows_dev(others, idx, w)
             if self.sparse:
                 keys, vals = filter_fibers_dev(self.d, n, idx)

@@ -257,6 +257,28 @@ def sketched_cp_cases():
         put(f"{tag}_residuals", np.array(trace.residuals))
 
 
+def deterministic_cases():
+    """lev_build(variant="deterministic") on factors with tied and zero
+    scores, and the driver with leverage-deterministic sampling."""
+    gen = np.random.default_rng(31)
+    f0 = orthonormal(30, 3, gen)
+    f1 = orthonormal(25, 3, gen)
+    f1[5] = f1[9]  # a duplicated row: tied leverage scores
+    f2 = np.vstack([orthonormal(18, 2, gen), np.zeros((4, 2))])  # zero scores
+    f3 = orthonormal(20, 2, gen)
+    for tag, fs, m in (("ld2", [f0, f1], 200), ("ld3", [f0, f2, f3], 150), ("ldz", [f2, f3], 400)):
+        for k, f in enumerate(fs):
+            put(f"{tag}_f{k}", f)
+        put(f"{tag}_idx", ref.lev_build(fs, m, "deterministic", make_rng(0)).indices)
+    for tag, spec in (("ddet", ("dense", (30, 30, 30), 3, 1e-2, 8)),
+                      ("sdet", ("sparse", (40, 40, 40), 3000, 9))):
+        t = make_input(spec)
+        cfg = dict(ranks=(3, 3, 3), max_sweeps=3, sketch="leverage-deterministic",
+                   sketch_size=120, seed=2)
+        model, trace = ref.sketched_tucker_als(t, ref.TuckerConfig(**cfg))
+        store_run(tag, model, trace)
+
+
 def main():
     tables()
     operators()
@@ -264,6 +286,7 @@ def main():
     ttmc_cases()
     hooi_cases()
     sketched_cp_cases()
+    deterministic_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")

@@ -219,3 +219,26 @@ def test_sketched_cp_als_vs_reference_golden(golden, oracle, skx, tag):
     assert np.allclose(trace.residuals, golden[f"{tag}_residuals"], rtol=1e-7, atol=1e-10)
     with pytest.raises(ValueError):
         skx.sketched_cp_als(t, skx.CPConfig(rank=3, sketch=None))
+
+
+from tests.test_oracle_golden import DET  # noqa: E402
+
+
+@pytest.mark.parametrize("tag,nf", [("ld2", 2), ("ld3", 3), ("ldz", 2)])
+def test_lev_deterministic_indices_bit_exact(golden, skx, tag, nf):
+    fs = [golden[f"{tag}_f{k}"] for k in range(nf)]
+    m = golden[f"{tag}_idx"].shape[0]
+    s = skx.lev_build(fs, m, "deterministic", skx.make_rng(0))
+    assert np.array_equal(s.indices, golden[f"{tag}_idx"])
+    assert np.array_equal(s.weights, np.ones(m))
+    with pytest.raises(ValueError):
+        skx.lev_build(fs, int(np.prod([f.shape[0] for f in fs])) + 1, "deterministic",
+                      skx.make_rng(0))
+
+
+@pytest.mark.parametrize("tag", list(DET))
+def test_deterministic_driver_vs_reference_golden(golden, oracle, skx, tag):
+    t = _as_api_input(skx, oracle, DET[tag])
+    model, trace = skx.sketched_tucker_als(t, skx.TuckerConfig(
+        ranks=(3, 3, 3), max_sweeps=3, sketch="leverage-deterministic", sketch_size=120, seed=2))
+    _compare_model(model, trace, golden, tag)

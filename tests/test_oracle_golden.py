@@ -244,3 +244,31 @@ def test_sketched_cp(golden, oracle, tag):
     assert relerr(w, golden[f"{tag}_w"]) <= 1e-9
     assert np.allclose(tr.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-10)
     assert np.allclose(tr.residuals, golden[f"{tag}_residuals"], rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.parametrize("tag,nf", [("ld2", 2), ("ld3", 3), ("ldz", 2)])
+def test_lev_deterministic_bit_exact(golden, oracle, tag, nf):
+    fs = [golden[f"{tag}_f{k}"] for k in range(nf)]
+    m = golden[f"{tag}_idx"].shape[0]
+    idx, w, _ = oracle.lev_det(fs, m)
+    assert np.array_equal(idx, golden[f"{tag}_idx"])
+    assert np.array_equal(w, np.ones(m))
+
+
+DET = {
+    "ddet": ("dense", (30, 30, 30), 3, 1e-2, 8),
+    "sdet": ("sparse", (40, 40, 40), 3000, 9),
+}
+
+
+@pytest.mark.parametrize("tag", list(DET))
+def test_sketched_tucker_deterministic(golden, oracle, tag):
+    t = make_input(oracle, DET[tag])
+    core, fac, tr = oracle.sketched_tucker(t, (3, 3, 3), "leverage-deterministic", max_sweeps=3,
+                                           sketch_size=120, seed=2)
+    got_f, got_c = canon(fac, core)
+    ref_f, ref_c = canon([golden[f"{tag}_a{k}"] for k in range(3)], golden[f"{tag}_core"])
+    for a, b in zip(got_f, ref_f):
+        assert relerr(a, b) <= 1e-10
+    assert relerr(got_c, ref_c) <= 1e-10
+    assert np.allclose(tr.residuals, golden[f"{tag}_residuals"], rtol=1e-10, atol=0)
