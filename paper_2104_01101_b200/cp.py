@@ -4,8 +4,8 @@
 sampling) to compress, exact CP-ALS on the small core (hosvd-of-core init),
 then the factor chains multiplied back and renormalised, with the final
 fitness measured against the full tensor (src/cp.py:177-224).  ``cp_als`` is
-the exact normal-equations CP-ALS (src/cp.py:119-174) on a dense tensor held
-on the GPU -- used on the core.  ``sketched_cp_als`` is leverage-sampled
+the exact normal-equations CP-ALS (src/cp.py:119-174) on a dense or sparse
+tensor held on the GPU (also used on the core).  ``sketched_cp_als`` is leverage-sampled
 CP-ALS on the full tensor (src/cp.py:110-116).
 
 Extension: ``CPConfig.tucker_rank`` (default None = the reference's tie of the
@@ -21,7 +21,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import rng as rngmod
-from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, shape_of)
+from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, mttkrp_dev, shape_of)
 from .tucker import SweepTrace, TuckerConfig, hooi_dev, hosvd_init_dev, sketched_tucker_als_dev
 
 
@@ -66,25 +66,16 @@ def _normalize_columns_dev(a):
     return a / safe, nrm
 
 
-def _mttkrp_dense_dev(t, factors, n):
-    nd = t.dim()
-    others = [k for k in range(nd) if k != n]
-    R = factors[others[0]].shape[1]
-    kr = factors[others[0]]
-    for k in others[1:]:
-        kr = (kr[:, None, :] * factors[k][None, :, :]).reshape(-1, R)
-    return t.movedim(n, 0).reshape(t.shape[n], -1) @ kr
-
-
 def cp_als_dev(t, config, on_core=False):
-    """Exact CP-ALS on a dense CUDA tensor (src/cp.py:119-174, unsketched)."""
+    """Exact CP-ALS (src/cp.py:119-174, unsketched) on a dense CUDA tensor or a
+    DeviceCoo."""
     torch = _torch()
     shape = tuple(t.shape)
     ndim = len(shape)
     rank = config.rank
     if rank < 1:
         raise ValueError("rank must be positive")
-    norm_t2 = (t * t).sum()
+    norm_t2 = t.norm2()[0] if is_sparse_dev(t) else (t * t).sum()
     nt2 = float(norm_t2.item())
     if nt2 == 0.0:
         raise ValueError("CP decomposition of a zero-norm tensor is undefined")
@@ -103,7 +94,7 @@ def cp_als_dev(t, config, on_core=False):
             for k in range(ndim):
                 if k != n:
                     go = go * grams[k]
-            mm = _mttkrp_dense_dev(t, factors, n)
+            mm = mttkrp_dev(t, factors, n)
             sc = mm @ torch.linalg.pinv(go, rtol=1e-12)
             cross = (sc * mm).sum()
             mod = ((sc.t() @ sc) * go).sum()
@@ -152,12 +143,10 @@ def _init_factors_dev(t, config, init, rng_init):
 
 
 def cp_als(t, config, on_core=False):
-    """Exact CP-ALS (src/cp.py:102-107) for dense tensors on the GPU."""
+    """Exact CP-ALS (src/cp.py:102-107) on the GPU (dense or sparse input)."""
     if config.sketch is not None:
         raise ValueError("cp_als is the unsketched driver; got a sketch config")
     d = device_of(t)
-    if is_sparse_dev(d):
-        raise NotImplementedError("direct CP-ALS on a sparse tensor is outside this build's hot path")
     factors, weights, trace = cp_als_dev(d, config, on_core=on_core)
     return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
 

@@ -679,27 +679,49 @@ def fitness(t, model):
     return float(f.item())
 
 
-def mttkrp(t, factors, n):
-    """T_(n) @ khatri_rao(others) on device (src/tensors.py:307-336)."""
+def mttkrp_dev(d, factors, n):
+    """T_(n) @ khatri_rao(factors except n) on device (src/tensors.py:307-336);
+    factors: device matrices for every mode.  Sparse: per-nonzero Hadamard
+    rows summed per mode-n index in the (stable) mode-n order -- deterministic,
+    no atomics."""
     torch = _torch()
-    d = device_of(t)
     nd = len(shape_of(d))
     others = [k for k in range(nd) if k != n]
-    fs = [_to_dev_mat(factors[k]) for k in others]
+    fs = [factors[k] for k in others]
     R = fs[0].shape[1]
-    for k, f in zip(others, fs):
-        if f.shape[0] != shape_of(d)[k]:
-            raise ValueError(f"mttkrp mode {k}: factor has {f.shape[0]} rows, extent is {shape_of(d)[k]}")
-        if f.shape[1] != R:
-            raise ValueError("mttkrp factors must share the column count")
     if is_sparse_dev(d):
-        prod = d.vals[:, None].expand(-1, R).clone()
-        for k, f in zip(others, fs):
-            prod *= f[d.coords[k].long()]
         out = torch.zeros((d.shape[n], R), dtype=torch.float64, device="cuda")
-        out.index_add_(0, d.coords[n].long(), prod)
-        return out.cpu().numpy()
+        if d.nnz == 0:
+            return out
+        rows_all = d.coords[n].long()
+        order = torch.argsort(rows_all, stable=True)
+        chunk = 1 << 22
+        for lo in range(0, d.nnz, chunk):
+            idx = order[lo:lo + chunk]
+            prod = d.vals[idx][:, None].expand(-1, R).clone()
+            for k, f in zip(others, fs):
+                prod *= f[d.coords[k][idx].long()]
+            rows, counts = torch.unique_consecutive(rows_all[idx], return_counts=True)
+            out[rows] += torch.segment_reduce(prod, "sum", lengths=counts, axis=0)
+        return out
     kr = fs[0]
     for f in fs[1:]:
         kr = (kr[:, None, :] * f[None, :, :]).reshape(-1, R)
-    return (d.movedim(n, 0).reshape(d.shape[n], -1) @ kr).cpu().numpy()
+    return d.movedim(n, 0).reshape(d.shape[n], -1) @ kr
+
+
+def mttkrp(t, factors, n):
+    """T_(n) @ khatri_rao(others) (src/tensors.py:307-336); numpy result."""
+    d = device_of(t)
+    nd = len(shape_of(d))
+    fs = [_to_dev_mat(f) for f in factors]
+    others = [k for k in range(nd) if k != n]
+    R = fs[others[0]].shape[1]
+    for k in others:
+        if fs[k].shape[0] != shape_of(d)[k]:
+            raise ValueError(f"mttkrp mode {k}: factor has {fs[k].shape[0]} rows, extent is {shape_of(d)[k]}")
+        if fs[k].shape[1] != R:
+            raise ValueError("mttkrp factors must share the column count")
+    return mttkrp_dev(d, fs, n).cpu().numpy()
+
+

@@ -279,6 +279,19 @@ def deterministic_cases():
         store_run(tag, model, trace)
 
 
+def cp_als_cases():
+    """Exact CP-ALS on a sparse tensor (rrf init) and on a dense one."""
+    c, v = planted_cp_coo_host((30, 30, 30), 3000, rank=3, seed=21)
+    for tag, t in (("cpas", ref.SparseTensor((30, 30, 30), c, v)),
+                   ("cpad", planted_tucker_dense((20, 18, 16), 3, 1e-2, 22))):
+        model, trace = ref.cp_als(t, ref.CPConfig(rank=3, max_sweeps=6, seed=23))
+        for k, a in enumerate(model.factors):
+            put(f"{tag}_a{k}", a)
+        put(f"{tag}_w", model.weights)
+        put(f"{tag}_fitness", np.array(trace.fitness))
+        put(f"{tag}_residuals", np.array(trace.residuals))
+
+
 def main():
     tables()
     operators()
@@ -287,6 +300,7 @@ def main():
     hooi_cases()
     sketched_cp_cases()
     deterministic_cases()
+    cp_als_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")

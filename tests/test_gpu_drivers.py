@@ -242,3 +242,21 @@ def test_deterministic_driver_vs_reference_golden(golden, oracle, skx, tag):
     model, trace = skx.sketched_tucker_als(t, skx.TuckerConfig(
         ranks=(3, 3, 3), max_sweeps=3, sketch="leverage-deterministic", sketch_size=120, seed=2))
     _compare_model(model, trace, golden, tag)
+
+
+@pytest.mark.parametrize("tag", ["cpas", "cpad"])
+def test_cp_als_vs_reference_golden(golden, skx, tag):
+    """Exact CP-ALS (src/cp.py:102-174) on a sparse (device mttkrp, no atomics)
+    and a dense tensor."""
+    from paper_2104_01101_b200.synth import planted_cp_coo_host, planted_tucker_dense
+    if tag == "cpas":
+        c, v = planted_cp_coo_host((30, 30, 30), 3000, rank=3, seed=21)
+        t = skx.SparseTensor((30, 30, 30), c, v)
+    else:
+        t = planted_tucker_dense((20, 18, 16), 3, 1e-2, 22)
+    model, trace = skx.cp_als(t, skx.CPConfig(rank=3, max_sweeps=6, seed=23))
+    for k in range(3):
+        assert relerr(np.abs(model.factors[k]), np.abs(golden[f"{tag}_a{k}"])) <= 1e-8, k
+    assert relerr(np.abs(model.weights), np.abs(golden[f"{tag}_w"])) <= 1e-8
+    assert np.allclose(trace.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-9)
+    assert np.allclose(trace.residuals, golden[f"{tag}_residuals"], rtol=1e-8, atol=1e-10)
