@@ -645,10 +645,11 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
     } else {
       // k-steps of 4 over R1, n-tiles of 8 over R2
       const int KS = (R1 + 3) / 4, NT = (R2 + 7) / 8;
-      // short CTAs (about two slices per warp): when the fitness runs on a
+      // short CTAs (one slice per warp): when the fitness runs on a
       // low-priority stream beside a sweep, SMs free up every few tens of
       // microseconds for the sweep's kernels instead of once per wave
-      const unsigned mb = (unsigned)imax(1, (s0 + 15) / 16);
+      // (persistent grids measured 2-6 ms slower per config-4 call)
+      const unsigned mb = (unsigned)imax(1, (s0 + 7) / 8);
 #define SKX_T3M(ks, nt)                                                                    \
   if (KS <= ks && NT == nt) {                                                              \
     k_tucker3_mma<ks, nt, 2, 0, 0><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, R0, \
