@@ -84,22 +84,10 @@ __global__ void k_bounds_i32(const int32_t* __restrict__ keys, int64_t n, int64_
   colptr[c] = lo;
 }
 
-template <class Rec>
-__global__ void k_iota(uint32_t* __restrict__ v, int64_t n) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
-
-template <class Rec>
-__global__ void k_gather_rec(const Rec* __restrict__ src, const uint32_t* __restrict__ idx,
-                             int64_t n, Rec* __restrict__ dst) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = src[__ldg(idx + i)];
-}
-
-// Modes >= 1: records are packed in input order, the (i_n, position) pairs are
-// radix-sorted (8-byte elements through the sort passes instead of 20), and
-// the records gathered once in sorted order -- a stable sort by i_n.
+// Modes >= 1: records are packed in input order with their i_n keys and
+// radix-sorted as (key, record) pairs -- a stable sort by i_n.  (Sorting
+// (key, position) pairs and gathering the records afterwards moves fewer bytes
+// per pass, but the random 16-byte gather measured slower at 1e8-1e9 nnz.)
 template <class Rec>
 static int build(int ndim, const int64_t* shape_h, int mode, int64_t nnz, const int32_t* coords,
                  const double* vals, void* rec_out, int64_t* colptr, void* ws, size_t* ws_bytes,
@@ -108,18 +96,15 @@ static int build(int ndim, const int64_t* shape_h, int mode, int64_t nnz, const 
   Arena ar(ws, *ws_bytes);
   uint32_t* k_in = nullptr;
   uint32_t* k_out = nullptr;
-  uint32_t* i_in = nullptr;
-  uint32_t* i_out = nullptr;
   Rec* r_in = nullptr;
   void* tmp = nullptr;
   size_t cb = 0;
   if (mode != 0) {
     k_in = ar.take<uint32_t>(nnz);
     k_out = ar.take<uint32_t>(nnz);
-    i_in = ar.take<uint32_t>(nnz);
-    i_out = ar.take<uint32_t>(nnz);
     r_in = ar.take<Rec>(nnz);
-    cub::DeviceRadixSort::SortPairs(nullptr, cb, k_in, k_out, i_in, i_out, (int64_t)nnz, 0, 32, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, cb, k_in, k_out, r_in, (Rec*)rec_out, (int64_t)nnz, 0,
+                                    32, s);
     tmp = ar.take<char>(cb);
   }
   if (ws == nullptr) {
@@ -135,21 +120,13 @@ static int build(int ndim, const int64_t* shape_h, int mode, int64_t nnz, const 
     k_bounds_i32<<<gb, 256, 0, s>>>(coords, nnz, sn, colptr);
     return check_launch("skx_coo_fibre(mode 0)", 2);
   }
-  int launches = 1;
-  if (nnz) {
-    k_pack<Rec><<<g, 256, 0, s>>>(ndim, mode, nnz, coords, vals, k_in, r_in, tp);
-    k_iota<Rec><<<g, 256, 0, s>>>(i_in, nnz);
-    launches += 2;
-  }
   int bits = 1;
   while ((int64_t(1) << bits) < sn) ++bits;
-  cub::DeviceRadixSort::SortPairs(tmp, cb, k_in, k_out, i_in, i_out, (int64_t)nnz, 0, bits, s);
-  if (nnz) {
-    k_gather_rec<Rec><<<g, 256, 0, s>>>(r_in, i_out, nnz, (Rec*)rec_out);
-    ++launches;
-  }
+  if (nnz) k_pack<Rec><<<g, 256, 0, s>>>(ndim, mode, nnz, coords, vals, k_in, r_in, tp);
+  cub::DeviceRadixSort::SortPairs(tmp, cb, k_in, k_out, r_in, (Rec*)rec_out, (int64_t)nnz, 0, bits,
+                                  s);
   k_bounds_u32<<<gb, 256, 0, s>>>(k_out, nnz, sn, colptr);
-  return check_launch("skx_coo_fibre", launches);
+  return check_launch("skx_coo_fibre", 3);
 }
 
 }  // namespace skx
