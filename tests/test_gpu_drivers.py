@@ -260,3 +260,30 @@ def test_cp_als_vs_reference_golden(golden, skx, tag):
     assert relerr(np.abs(model.weights), np.abs(golden[f"{tag}_w"])) <= 1e-8
     assert np.allclose(trace.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-9)
     assert np.allclose(trace.residuals, golden[f"{tag}_residuals"], rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+@pytest.mark.parametrize("sketch", ["tensorsketch", "leverage-random"])
+def test_early_stop_and_random_init_vs_oracle(skx, oracle, sparse, sketch):
+    """convergence_tol > 0 (the non-pipelined speculative path: each sweep is
+    verified before the fitness decides) and init="random" against the
+    oracle: same number of sweeps, same model."""
+    from paper_2104_01101_b200.synth import planted_cp_coo_host, planted_tucker_dense
+    shape = (40, 36, 30)
+    if sparse:
+        c, v = planted_cp_coo_host(shape, 6000, rank=3, seed=4)
+        t, tr_ = skx.SparseTensor(shape, c, v), oracle.Coo(shape, c, v)
+    else:
+        t = tr_ = planted_tucker_dense(shape, 3, 1e-2, 4)
+    for init, tol in (("rrf", 1e-4), ("random", 0.0)):
+        cfg = dict(ranks=(3, 3, 3), max_sweeps=8, sketch=sketch, sketch_size=200, seed=6,
+                   init=init, convergence_tol=tol)
+        model, trace = skx.sketched_tucker_als(t, skx.TuckerConfig(**cfg))
+        core, fac, otr = oracle.sketched_tucker(tr_, (3, 3, 3), sketch, max_sweeps=8,
+                                                sketch_size=200, seed=6, init=init, tol=tol)
+        assert len(trace.fitness) == len(otr.fitness)
+        gf, gc = canon(model.factors, model.core)
+        rf, rc = canon(fac, core)
+        for a, b in zip(gf, rf):
+            assert relerr(a, b) <= 1e-9
+        assert relerr(gc, rc) <= 1e-9
