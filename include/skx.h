@@ -158,6 +158,16 @@ int skx_lev_sample(int n_other, const int64_t* ext_h, const double* const* p_h,
                    const double* const* cdf_h, int64_t m, uint64_t k0, uint64_t k1, uint64_t p0,
                    int64_t* idx, double* w, void* stream);
 
+/* Deterministic leverage sampling: idx (m x k, int64) = the original
+ * multi-indices of the m largest products of one score per list, in the pop
+ * order of the reference's best-first heap (products descending, ties by
+ * lexicographic multi-index, a tuple entering the frontier only once a
+ * predecessor was popped) -- src/sketching.py:224-259 `_top_m_products`,
+ * used by lev_build(variant="deterministic") at :218-220. scores_h: host
+ * array of k device pointers (len_h[j] doubles each). */
+int skx_top_m_products(int k, const int64_t* len_h, const double* const* scores_h, int64_t m,
+                       int64_t* idx, void* ws, size_t* ws_bytes, void* stream);
+
 /* Z[j,:] = w_j kron_k A_k[idx_jk,:], column-major m x prod(R)
  * (src/sketching.py:280-285). */
 int skx_kron_rows(int n_other, const int64_t* ranks_h, const double* const* factors_h,
@@ -309,6 +319,23 @@ int skx_cp_cross_coo(int ndim, const int64_t* shape_h, int64_t R, int64_t nnz,
                      const int32_t* coords, const double* vals, const double* const* factors_h,
                      const double* weights, double* out, void* ws, size_t* ws_bytes,
                      void* stream);
+
+/* ------------------------------------------------ K8: CP-ALS on the core */
+
+/* CP-ALS of a dense order-3 core (dims_h = I, J, K; C-order) in one CTA:
+ * hosvd-of-core init (leading eigenvectors of the unfolding Grams,
+ * src/tucker.py:112-126), `sweeps` sweeps of the normal-equations update
+ * A_n = mttkrp(C, A, n) pinv(hadamard of the other Grams, rcond=1e-12) with
+ * column normalisation into weights (src/cp.py:119-174 with on_core=True),
+ * the sub-problem residuals (src/cp.py:96-99; residuals = 3*sweeps) and the
+ * CP fitness after each sweep (src/tensors.py:339-368; fitness = sweeps).
+ * factors receives I*R + J*R + K*R doubles (row-major, mode after mode),
+ * weights R; *info = 0 ok, 1 zero-norm core.  Needs rank <= min(I,J,K) <= 32
+ * and skx_cp_core_smem_bytes(dims_h, rank) within the shared-memory limit. */
+int skx_cp_core_als(const int64_t* dims_h, int rank, int sweeps, const double* core,
+                    double* factors, double* weights, double* residuals, double* fitness,
+                    int* info, void* stream);
+size_t skx_cp_core_smem_bytes(const int64_t* dims_h, int rank);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,7 @@ _SIGS = {
     "skx_ts_kron_apply": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_lev_prepare": [c_p, c_i64, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_lev_sample": [c_i32, c_p, c_p, c_p, c_i64, c_u64, c_u64, c_u64, c_p, c_p, c_p],
+    "skx_top_m_products": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_kron_rows": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
     "skx_gather_fibers_dense": [c_p, c_i32, c_p, c_i32, c_p, c_p, c_i64, c_p, c_p],
     "skx_filter_fibers_coo": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_i64, c_p, c_p, c_i64, c_p,
@@ -63,11 +64,14 @@ _SIGS = {
     "skx_tucker_cross_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_u32, c_p, c_p,
                              c_sz_p, c_p],
     "skx_cp_cross_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_cp_core_als": [c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "skx_cp_core_smem_bytes": [c_p, c_i32],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],
 }
-_RET = {"skx_last_error": ctypes.c_char_p, "skx_launch_count": ctypes.c_longlong}
+_RET = {"skx_last_error": ctypes.c_char_p, "skx_launch_count": ctypes.c_longlong,
+        "skx_cp_core_smem_bytes": ctypes.c_size_t, "skx_coo_rec_words": ctypes.c_int}
 
 EXPORTS = tuple(_SIGS)
 
@@ -177,19 +181,31 @@ def host_ptrs(tensors):
 
 
 class Workspace:
-    """Grow-only per-device scratch buffer shared by stream-ordered calls."""
+    """Grow-only per-device scratch buffers (slots) shared by stream-ordered
+    calls.  Each slot remembers the streams it was handed to; when a slot
+    grows, the old buffer is marked used on those streams (record_stream), so
+    the caching allocator cannot hand it out again before their queued work
+    has finished."""
 
     def __init__(self):
         self._buf = {}
+        self._streams = {}
 
     def get(self, nbytes, slot=0):
         import torch
         dev = torch.cuda.current_device()
         key = (dev, slot)
+        cur = torch.cuda.current_stream()
         buf = self._buf.get(key)
+        users = self._streams.setdefault(key, {})
         if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                for st in users.values():
+                    buf.record_stream(st)
+                users.clear()
             buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
             self._buf[key] = buf
+        users[cur.cuda_stream] = cur
         return buf
 
 

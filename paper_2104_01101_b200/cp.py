@@ -66,15 +66,66 @@ def _normalize_columns_dev(a):
     return a / safe, nrm
 
 
+def _core_kernel_ok(t, rank, init):
+    """K8 (libskx skx_cp_core_als) covers the on-core stage of Algorithm 6:
+    a dense order-3 core, hosvd-of-core init, rank <= every extent <= 32."""
+    from . import _native as nat
+    if is_sparse_dev(t) or t.dim() != 3 or init != "hosvd-of-core":
+        return False
+    shape = tuple(int(x) for x in t.shape)
+    if not all(rank <= x <= 32 for x in shape):
+        return False
+    dims, dp = nat.host_i64(shape)
+    return int(nat.load().skx_cp_core_smem_bytes(dp, rank)) <= 227 * 1024
+
+
+def cp_core_als_dev(core, config):
+    """CP-ALS on a small dense order-3 core in one libskx CTA (K8): the whole
+    on-core stage of src/cp.py:119-174 (hosvd-of-core init, sweeps of
+    Gram-Hadamard / core MTTKRP / pinv / normalisation, residuals and the
+    fitness per sweep).  One launch and one small D2H for the trace."""
+    from . import _native as nat
+    torch = _torch()
+    shape = tuple(int(x) for x in core.shape)
+    rank = config.rank
+    sweeps = config.resolved_sweeps(True)
+    fac = torch.empty(sum(shape) * rank, dtype=torch.float64, device="cuda")
+    w = torch.empty(rank, dtype=torch.float64, device="cuda")
+    res = torch.empty(max(3 * sweeps, 1), dtype=torch.float64, device="cuda")
+    fit = torch.empty(max(sweeps, 1), dtype=torch.float64, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    dims, dp = nat.host_i64(shape)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nat.call("skx_cp_core_als", dp, rank, sweeps, nat.ptr(core.contiguous()), nat.ptr(fac),
+             nat.ptr(w), nat.ptr(res), nat.ptr(fit), nat.ptr(info), nat.stream())
+    e1.record()
+    host = torch.cat([info.to(torch.float64), res[:3 * sweeps], fit[:sweeps]]).cpu().tolist()
+    if int(host[0]) != 0:
+        raise ValueError("CP decomposition of a zero-norm tensor is undefined")
+    factors, off = [], 0
+    for x in shape:
+        factors.append(fac[off:off + x * rank].view(x, rank))
+        off += x * rank
+    total = e0.elapsed_time(e1) / 1e3
+    trace = SweepTrace(fitness=host[1 + 3 * sweeps:], residuals=host[1:1 + 3 * sweeps],
+                       wall_s=[total / max(sweeps, 1)] * sweeps)
+    return factors, w, trace
+
+
 def cp_als_dev(t, config, on_core=False):
     """Exact CP-ALS (src/cp.py:119-174, unsketched) on a dense CUDA tensor or a
-    DeviceCoo."""
+    DeviceCoo.  On a small dense order-3 core with hosvd-of-core init the
+    whole stage is the one-CTA libskx kernel K8 (cp_core_als_dev)."""
     torch = _torch()
     shape = tuple(t.shape)
     ndim = len(shape)
     rank = config.rank
     if rank < 1:
         raise ValueError("rank must be positive")
+    if _core_kernel_ok(t, rank, config.init or ("hosvd-of-core" if on_core else "rrf")):
+        return cp_core_als_dev(t, config)
     norm_t2 = t.norm2()[0] if is_sparse_dev(t) else (t * t).sum()
     nt2 = float(norm_t2.item())
     if nt2 == 0.0:
@@ -151,6 +202,29 @@ def cp_als(t, config, on_core=False):
     return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
 
 
+def _lstsq_min_norm_dev(z, y):
+    """Minimum-norm least squares min ||z x - y|| as np.linalg.lstsq(z, y,
+    rcond=None) (LAPACK gelsd: singular values below eps * max(m, R) * s_max
+    are treated as zero), so a rank-deficient sampled system (repeated
+    leverage rows) stays finite as in the reference.  z (m x R) = Q R by
+    TSQR, R = U_r diag(s) V^T by one-sided Jacobi (R <= 64), U = z V / s;
+    x = V diag(1/s) U^T y over the kept singular values.  No host sync."""
+    from .linalg import jacobi_svd_dev, tsqr_r_dev
+    torch = _torch()
+    m, r = z.shape
+    if r <= 64 and m >= r:
+        rf = tsqr_r_dev(z.contiguous())
+        _, sv, v = jacobi_svd_dev(rf)
+    else:
+        _, sv, vh = torch.linalg.svd(z, full_matrices=False)
+        v = vh.transpose(0, 1)
+    tol = np.finfo(np.float64).eps * max(m, r) * sv[0]
+    inv = torch.where(sv > tol, 1.0 / torch.where(sv > 0, sv, torch.ones_like(sv)),
+                      torch.zeros_like(sv))
+    u = (z @ v) * inv
+    return v @ (inv[:, None] * (u.transpose(0, 1) @ y))
+
+
 def sketched_cp_als_dev(d, config):
     """Leverage-sampled CP-ALS on the full tensor (src/cp.py:110-174, sketched
     branch) on device: per mode a random leverage sample of the Khatri-Rao
@@ -194,7 +268,7 @@ def sketched_cp_als_dev(d, config):
                 y = hits_to_dense(off, col, val, m, shape[n])
             else:
                 y = gather_dense_dev(d, n, idx, w)
-            sol = torch.linalg.lstsq(z, y).solution
+            sol = _lstsq_min_norm_dev(z, y)
             factors[n], weights = _normalize_columns_dev(sol.t().contiguous())
         fit = float(fitness_cp_dev(d, factors, weights, norm_t2).item())
         trace.residuals.append((1.0 - fit) * nt)
@@ -211,8 +285,15 @@ def sketched_cp_als(t, config):
     return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
 
 
-def cp_via_sketched_tucker(t, config):
-    """CP through sketched Tucker compression (Alg. 6, src/cp.py:177-224)."""
+def cp_via_sketched_tucker_dev(t, config, comm=None):
+    """Algorithm 6 on the device (src/cp.py:177-224).  Returns (factors,
+    weights, trace) with CUDA tensors.  t: SparseTensor (a host-resident one
+    is uploaded inside the Tucker stage, overlapping its rejection scans),
+    DeviceCoo or dense array/tensor.  Stages: sketched Tucker-ALS with
+    leverage sampling (or exact HOOI), CP-ALS on the core (K8, one CTA), the
+    factor chains B_n A_n renormalised, and the CP fitness against the full
+    tensor (one pass over the nonzeros).  comm: nonzeros sharded over ranks
+    (SURVEY 8e); the core stage is replicated."""
     torch = _torch()
     shape = tuple(int(s) for s in t.shape)
     ndim = len(shape)
@@ -225,10 +306,13 @@ def cp_via_sketched_tucker(t, config):
                               sketch="leverage-random" if config.sketch else None,
                               sketch_size=config.sketch_size, sketch_factor=config.sketch_factor,
                               init="rrf" if config.sketch else "hosvd", seed=int(seed_tucker))
-    d = device_of(t)
     if config.sketch:
-        core, tfac, ttrace = sketched_tucker_als_dev(d, tucker_cfg)
+        # a host SparseTensor goes in as is: the Tucker stage uploads it while
+        # the data-independent RRF rejection scans run
+        core, tfac, ttrace = sketched_tucker_als_dev(t, tucker_cfg, comm)
+        d = device_of(t)
     else:  # exact HOOI compression stage (src/cp.py:203-204)
+        d = device_of(t)
         core, tfac, ttrace = hooi_dev(d, tucker_cfg)
     core_cfg = replace(config, sketch=None, sketch_size=None, sketch_factor=None,
                        init="hosvd-of-core", seed=int(seed_cp))
@@ -239,9 +323,20 @@ def cp_via_sketched_tucker(t, config):
         unit, nrm = _normalize_columns_dev(b @ a)
         out.append(unit)
         weights = weights * nrm
-    norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
-    fin = float(fitness_cp_dev(d, out, weights, norm2).item())
+    if is_sparse_dev(d):
+        norm2 = d.norm2()[0].clone()
+        if comm is not None:
+            norm2 = comm.allreduce(norm2.view(1))[0]
+    else:
+        norm2 = (d * d).sum()
+    fin = float(fitness_cp_dev(d, out, weights, norm2, comm).item())
     trace = SweepTrace(fitness=list(ttrace.fitness) + [fin], residuals=list(ctrace.residuals),
                        wall_s=list(ttrace.wall_s) + [sum(ctrace.wall_s)],
                        stage_split=len(ttrace.fitness))
+    return out, weights, trace
+
+
+def cp_via_sketched_tucker(t, config):
+    """CP through sketched Tucker compression (Alg. 6, src/cp.py:177-224)."""
+    out, weights, trace = cp_via_sketched_tucker_dev(t, config)
     return CPModel([a.cpu().numpy() for a in out], weights.cpu().numpy()), trace

@@ -254,6 +254,10 @@ class NormalSource:
         """Generate the next batch now (e.g. while the GPU is otherwise busy
         with compute-bound work) so the next draws are served from memory."""
         if self.batch and self._left() == 0:
+            cur = _torch().cuda.current_stream()
+            for _, ev in self._segs:
+                if ev is not None:
+                    cur.wait_event(ev)
             self._segs.append((self._generate(self.batch), None))
 
     def prefetch_async(self, stream):
@@ -274,9 +278,14 @@ class NormalSource:
         torch = _torch()
         n = int(np.prod(shape))
         left = self._left()
-        if left < n:
-            self._segs.append((self._generate(max(n - left, self.batch)), None))
         cur = torch.cuda.current_stream()
+        if left < n:
+            # the device cursor (and workspace slot 1) may still be in use by a
+            # segment generated on another stream: order after all of them
+            for _, ev in self._segs:
+                if ev is not None:
+                    cur.wait_event(ev)
+            self._segs.append((self._generate(max(n - left, self.batch)), None))
         parts, need = [], n
         while need > 0:
             t, ev = self._segs[self._i]

@@ -365,43 +365,21 @@ def lev_sample_dev(factors, m, gen, check=True):
 
 def top_m_products_dev(score_list, m):
     """Multi-indices (m, k) of the m largest products of one score per mode
-    (src/sketching.py:224-259), in the reference's pop order: products
-    descending, ties by lexicographic original multi-index.  Instead of the
-    best-first heap, every candidate position tuple with prod(p_k + 1) <= m in
-    the score-sorted lists is enumerated on the device (any other tuple has at
-    least m better ones) and the candidates are sorted by that key; products
-    are formed left to right as numpy's prod does.  Equal to the heap's order
-    whenever a step down a sorted list never rounds to an equal product with a
-    smaller original index (distinct or exactly tied scores)."""
+    (src/sketching.py:224-259), in the reference's pop order: libskx sorts each
+    list (descending, ties by index) and replays the best-first search on the
+    device, so tied products (zero or repeated scores) come out exactly as the
+    reference's heap pops them."""
     torch = _torch()
     lens = [int(x.numel()) for x in score_list]
     total = int(np.prod(lens))
     if m > total:
         raise ValueError(f"cannot select {m} rows from {total}")
-    orders, srt = [], []
-    for x in score_list:
-        o = torch.sort(-x, stable=True).indices  # descending, ties by ascending index
-        orders.append(o)
-        srt.append(x[o])
-    dev = score_list[0].device
-    pos = torch.zeros((1, 0), dtype=torch.int64, device=dev)
-    bound = torch.ones(1, dtype=torch.int64, device=dev)
-    for L in lens:
-        cnt = torch.clamp(m // bound, max=L)
-        rep = torch.repeat_interleave(torch.arange(cnt.numel(), device=dev), cnt)
-        off = torch.arange(rep.numel(), device=dev) - torch.repeat_interleave(
-            torch.cumsum(cnt, 0) - cnt, cnt)
-        pos = torch.cat([pos[rep], off[:, None]], dim=1)
-        bound = bound[rep] * (off + 1)
-    prod = srt[0][pos[:, 0]]
-    for k in range(1, len(lens)):
-        prod = prod * srt[k][pos[:, k]]
-    orig = torch.stack([orders[k][pos[:, k]] for k in range(len(lens))], dim=1)
-    perm = torch.arange(prod.numel(), device=dev)
-    for k in reversed(range(len(lens))):  # lexicographic tie-break: least significant first
-        perm = perm[torch.sort(orig[perm, k], stable=True).indices]
-    perm = perm[torch.sort(-prod[perm], stable=True).indices]
-    return orig[perm[:m]].contiguous()
+    sc = [x.to(torch.float64).contiguous() for x in score_list]
+    idx = torch.empty((m, len(sc)), dtype=torch.int64, device="cuda")
+    ln, lp = nat.host_i64(lens)
+    arr, sp_ = nat.host_ptrs(sc)
+    nat.call_ws("skx_top_m_products", (len(sc), lp, sp_, m, nat.ptr(idx)), slot=6)
+    return idx
 
 
 def lev_det_dev(factors, m, check=True):

@@ -279,6 +279,33 @@ def deterministic_cases():
         store_run(tag, model, trace)
 
 
+def topm_cases():
+    """The reference's best-first top-m selection on score lists with ties:
+    zero scores mid-list, repeated scores, three modes (src/sketching.py:
+    224-259).  tm0 is the 2 x 2 case where a candidate-sort selection differs
+    from the heap's pop order."""
+    from sketchals.sketching import _top_m_products
+    cases = [([np.array([0.0, 0.7]), np.array([0.4, 0.6])], 3)]
+    gen = np.random.default_rng(77)
+    for i in range(12):
+        k = 2 + (i % 2)
+        lists = []
+        for _ in range(k):
+            n = int(gen.integers(3, 12))
+            x = gen.uniform(size=n)
+            x[gen.uniform(size=n) < 0.3] = 0.0
+            if i % 3 == 0:
+                x[gen.integers(0, n)] = x[gen.integers(0, n)]  # a repeated score
+            lists.append(x)
+        total = int(np.prod([len(x) for x in lists]))
+        cases.append((lists, int(gen.integers(1, total + 1))))
+    for i, (lists, m) in enumerate(cases):
+        for k, x in enumerate(lists):
+            put(f"tm{i}_s{k}", x)
+        put(f"tm{i}_idx", _top_m_products(lists, m))
+    put("tm_count", np.array(len(cases)))
+
+
 def cp_als_cases():
     """Exact CP-ALS on a sparse tensor (rrf init) and on a dense one."""
     c, v = planted_cp_coo_host((30, 30, 30), 3000, rank=3, seed=21)
@@ -293,6 +320,13 @@ def cp_als_cases():
 
 
 def main():
+    if sys.argv[1:] == ["topm"]:  # add just these cases to an existing file
+        path = os.path.join(HERE, "golden.npz")
+        OUT.update(dict(np.load(path)))
+        topm_cases()
+        np.savez_compressed(path, **OUT)
+        print("wrote", path, len(OUT), "arrays")
+        return
     tables()
     operators()
     drivers()
@@ -301,6 +335,7 @@ def main():
     sketched_cp_cases()
     deterministic_cases()
     cp_als_cases()
+    topm_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")

@@ -236,6 +236,18 @@ def test_lev_deterministic_indices_bit_exact(golden, skx, tag, nf):
                       skx.make_rng(0))
 
 
+def test_top_m_products_ties_vs_reference_golden(golden, skx):
+    """Device best-first search (skx_top_m_products) vs the reference heap on
+    score lists with zero / repeated scores (a candidate sort
+    differs there)."""
+    import torch
+    from paper_2104_01101_b200.sketching import top_m_products_dev
+    from tests.test_oracle_golden import _tm_cases
+    for i, lists, want in _tm_cases(golden):
+        got = top_m_products_dev([torch.from_numpy(x).cuda() for x in lists], want.shape[0])
+        assert np.array_equal(got.cpu().numpy(), want), i
+
+
 @pytest.mark.parametrize("tag", list(DET))
 def test_deterministic_driver_vs_reference_golden(golden, oracle, skx, tag):
     t = _as_api_input(skx, oracle, DET[tag])

@@ -255,6 +255,22 @@ def test_lev_deterministic_bit_exact(golden, oracle, tag, nf):
     assert np.array_equal(w, np.ones(m))
 
 
+def _tm_cases(golden):
+    for i in range(int(golden["tm_count"])):
+        lists, k = [], 0
+        while f"tm{i}_s{k}" in golden:
+            lists.append(golden[f"tm{i}_s{k}"])
+            k += 1
+        yield i, lists, golden[f"tm{i}_idx"]
+
+
+def test_top_m_products_ties_bit_exact(golden, oracle):
+    """Best-first top-m with zero and repeated scores (pop order, not a sort)."""
+    for i, lists, want in _tm_cases(golden):
+        got = oracle.top_m_products(lists, want.shape[0])
+        assert np.array_equal(got, want), i
+
+
 DET = {
     "ddet": ("dense", (30, 30, 30), 3, 1e-2, 8),
     "sdet": ("sparse", (40, 40, 40), 3000, 9),
