@@ -264,7 +264,8 @@ def run_ours(args, cfgd):
     for _ in range(args.warmup):
         step()
     # ---- device-resident timed region
-    hook_names = ["skx_tucker_cross_coo", "skx_cp_cross_coo", "skx_rrf_stage1_coo", "skx_lemire_scan",
+    hook_names = ["skx_tucker_cross_coo", "skx_cp_cross_coo", "skx_cp_cross_fibre3", "skx_rrf_stage1_coo",
+                  "skx_rrf_stage1_fx", "skx_lemire_scan",
                   "skx_filter_fibers_coo", "skx_coo_fibre", "skx_ts_rhs_coo", "skx_resid_sq",
                   "skx_ts_kron_apply", "skx_philox_normal", "skx_tsqr_r", "skx_cp_core_als",
                   "skx_rrf_stage1_dense", "skx_ts_rhs_dense"]

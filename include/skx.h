@@ -151,6 +151,16 @@ int skx_ts_kron_apply(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
 int skx_lev_prepare(const double* scores, int64_t s, double* p, double* cdf, void* ws,
                     size_t* ws_bytes, void* stream);
 
+/* Leverage scores l_i = ||a_i R^-1||^2 of a tall s x R factor (R <= 32),
+ * R from a Cholesky of the Gram A^T A (src/linalg.py:73-84 leverage_scores;
+ * any R of a QR of A gives the same Q = A R^-1).  *bad (device int) = 1
+ * when the Gram route cannot reproduce the reference's Householder rank test
+ * (|R_ii| < 1e-12 ||A||_F, src/linalg.py:44-52) or loses score bits: failed
+ * pivot or min R_jj < 1e-2 max R_jj; the caller then decides on a Householder
+ * (TSQR) factorisation.  Orthonormal factors (the driver's) never flag. */
+int skx_lev_scores(const double* a, int64_t s, int R, double* scores, int* bad, void* ws,
+                   size_t* ws_bytes, void* stream);
+
 /* Draw m samples per mode: for mode k, uniforms at raw positions
  * p0 + k*m + j; idx[j*n_other+k] = searchsorted(cdf_k, u, 'right');
  * w[j] = 1/sqrt(m * prod_k p_k[idx]).  src/sketching.py:211-216. */
@@ -200,6 +210,27 @@ int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode, int64_t nn
                           uint64_t* count, void* stream);
 
 /* ------------------------------------------------- K4: range finder */
+
+/* Range of the nonzero values: out3[0] = max, out3[1] = min unbiased binary
+ * exponent of the nonzero |v|, out3[2] = 1 if any value is inf/NaN or
+ * subnormal.  Decides whether skx_rrf_stage1_fx can sum exactly. */
+int skx_value_range(const double* vals, int64_t nnz, int* out3, void* stream);
+
+/* RRF stage 1 (CountSketch of T_(mode), s_mode x k2) straight from the
+ * lexsorted SoA COO, without a fibre layout: every nonzero adds
+ * sign(j) * v * 2^S (S = 93 - emax) into an exact fixed-point accumulator
+ * (three 32-bit limbs summed by 64-bit atomic reductions; integer sums are
+ * order independent, so the result is deterministic) which is rounded once
+ * to double.  Requires the
+ * skx_value_range result: no non-finite values and emin >= emax - 41
+ * (every contribution then is an exact integer).  Same tables and stream
+ * positions as skx_rrf_stage1_coo (src/sketching.py:54-56, 327-341).
+ * Workspace: 32 * s_mode * k2 bytes. */
+int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int64_t nnz,
+                      const int32_t* coords, const double* vals, int emax, uint64_t k0,
+                      uint64_t k1, uint64_t p0, uint32_t has_pending, uint32_t pending,
+                      uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
+                      double* stage1, void* ws, size_t* ws_bytes, void* stream);
 
 /* stage1[i_n, c] = sum_j T_(n)[i_n, j] sign_j [hash_j == c] where hash/sign are
  * the numpy draws integers(0,k2,P) then integers(0,2,P) of the u32 run
@@ -319,6 +350,14 @@ int skx_cp_cross_coo(int ndim, const int64_t* shape_h, int64_t R, int64_t nnz,
                      const int32_t* coords, const double* vals, const double* const* factors_h,
                      const double* weights, double* out, void* ws, size_t* ws_bytes,
                      void* stream);
+
+/* Same cross term for an order-3 tensor over its mode-0 fibre layout
+ * (skx_coo_fibre mode 0: colptr0 = s0 + 1 offsets, 16-byte records, c1_mask
+ * as skx_ts_rhs_coo): warp per slice, the two random factor rows of every
+ * nonzero loaded as 16-byte chunks by 2*ceil(R/2) lanes.  R <= 32. */
+int skx_cp_cross_fibre3(int64_t s0, const int64_t* colptr0, const void* rec0, uint32_t c1_mask,
+                        int R, const double* const* factors_h, const double* weights, double* out,
+                        void* ws, size_t* ws_bytes, void* stream);
 
 /* ------------------------------------------------ K8: CP-ALS on the core */
 

@@ -40,6 +40,7 @@ _SIGS = {
     "skx_ts_kron_plan": [c_i32, c_p, c_p, c_p, c_i64, c_p, c_sz_p, c_p, c_sz_p, c_p],
     "skx_ts_kron_apply": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_lev_prepare": [c_p, c_i64, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_lev_scores": [c_p, c_i64, c_i32, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_lev_sample": [c_i32, c_p, c_p, c_p, c_i64, c_u64, c_u64, c_u64, c_p, c_p, c_p],
     "skx_top_m_products": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_kron_rows": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
@@ -50,6 +51,9 @@ _SIGS = {
                               c_i64, c_p, c_sz_p, c_p],
     "skx_rrf_stage1_coo": [c_i32, c_p, c_i64, c_p, c_p, c_u64, c_u64, c_u64, c_u32, c_u32, c_u64,
                            c_p, c_i64, c_i64, c_u32, c_p, c_p],
+    "skx_value_range": [c_p, c_i64, c_p, c_p],
+    "skx_rrf_stage1_fx": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_i32, c_u64, c_u64, c_u64, c_u32,
+                          c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_rrf_table": [c_u64, c_u64, c_u64, c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_i64, c_p, c_p],
     "skx_rrf_stage1_dense": [c_p, c_i32, c_p, c_i32, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
@@ -66,6 +70,7 @@ _SIGS = {
     "skx_cp_cross_coo": [c_i32, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_cp_core_als": [c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "skx_cp_core_smem_bytes": [c_p, c_i32],
+    "skx_cp_cross_fibre3": [c_i64, c_p, c_p, c_u32, c_i32, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],

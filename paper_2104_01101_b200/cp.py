@@ -22,7 +22,8 @@ import numpy as np
 
 from . import rng as rngmod
 from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, mttkrp_dev, shape_of)
-from .tucker import SweepTrace, TuckerConfig, hooi_dev, hosvd_init_dev, sketched_tucker_als_dev
+from .tucker import (SweepTrace, TuckerConfig, hooi_dev, hosvd_init_dev,
+                     sketched_tucker_run_dev)
 
 
 def _torch():
@@ -306,10 +307,13 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
                               sketch="leverage-random" if config.sketch else None,
                               sketch_size=config.sketch_size, sketch_factor=config.sketch_factor,
                               init="rrf" if config.sketch else "hosvd", seed=int(seed_tucker))
+    finish = None
     if config.sketch:
         # a host SparseTensor goes in as is: the Tucker stage uploads it while
-        # the data-independent RRF rejection scans run
-        core, tfac, ttrace = sketched_tucker_als_dev(t, tucker_cfg, comm)
+        # the data-independent RRF rejection scans run.  Its last fitness pass
+        # keeps running on the fitness stream while the core stage and the
+        # final CP fitness below are enqueued (finish() joins it)
+        core, tfac, finish = sketched_tucker_run_dev(t, tucker_cfg, comm)
         d = device_of(t)
     else:  # exact HOOI compression stage (src/cp.py:203-204)
         d = device_of(t)
@@ -329,7 +333,10 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
             norm2 = comm.allreduce(norm2.view(1))[0]
     else:
         norm2 = (d * d).sum()
-    fin = float(fitness_cp_dev(d, out, weights, norm2, comm).item())
+    fin_dev = fitness_cp_dev(d, out, weights, norm2, comm)
+    if finish is not None:
+        ttrace = finish()
+    fin = float(fin_dev.item())
     trace = SweepTrace(fitness=list(ttrace.fitness) + [fin], residuals=list(ctrace.residuals),
                        wall_s=list(ttrace.wall_s) + [sum(ctrace.wall_s)],
                        stage_split=len(ttrace.fitness))

@@ -316,7 +316,12 @@ struct T3Rows {
 // rotate by static index (body unrolled lcm(3, 2) = 6 times) so nothing is
 // copied while its load is in flight.  R1T/R2T > 0 fix the ranks at compile
 // time (predicates fold away); 0 reads them at run time.
-template <int KS, int NT, int G, int R1T, int R2T, int MB = 1>
+// PAIR (R1 even, fixed at compile time): the A-fragment k index is permuted
+// so each lane reads 16 bytes per pair of k-steps -- k-step 2j holds
+// k = 8j + 2c, 2j + 1 holds 8j + 2c + 1, a last odd k-step k = 8 (KS/2) + c;
+// the B fragments use the same map (the contraction over k is unchanged).
+// Fewer, wider loads: 3 instead of 5 per row group at R = 20.
+template <int KS, int NT, int G, int R1T, int R2T, int MB = 1, bool PAIR = false>
 __global__ void __launch_bounds__(256, MB) k_tucker3_mma(const int64_t* __restrict__ colptr, int64_t s0,
                                                      const double* __restrict__ rec, uint32_t c1_mask,
                                                      const double* __restrict__ A0,
@@ -345,11 +350,14 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_mma(const int64_t* __restri
       continue;
     }
     double b[KS][NT];  // B[k][n] = W[ks*4 + c][nt*8 + q]
+    constexpr int PAIRS = PAIR ? KS / 2 : 0;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const int k = ks * 4 + c, n = nt * 8 + q;
+        const int k = !PAIR ? ks * 4 + c
+                            : (ks < 2 * PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * PAIRS + c);
+        const int n = nt * 8 + q;
         double w = 0.0;
         if (k < R1 && n < R2)
           for (int r0 = 0; r0 < R0; ++r0)
@@ -375,8 +383,20 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_mma(const int64_t* __restri
         const double* r1 = A1 + (int64_t)r.i1[g] * R1;
         const double* r2 = A2 + (int64_t)r.i2[g] * R2;
         w.v[g] = r.v[g];
+        if (PAIR) {
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) w.a[g][ks] = ks * 4 + c < R1 ? __ldg(r1 + ks * 4 + c) : 0.0;
+          for (int j = 0; j < PAIRS; ++j) {
+            const int k = 8 * j + 2 * c;
+            const double2 p = k < R1 ? __ldg(reinterpret_cast<const double2*>(r1 + k))
+                                     : make_double2(0.0, 0.0);
+            w.a[g][2 * j] = p.x;
+            w.a[g][2 * j + 1] = p.y;
+          }
+          if (KS & 1) w.a[g][KS - 1] = 8 * PAIRS + c < R1 ? __ldg(r1 + 8 * PAIRS + c) : 0.0;
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) w.a[g][ks] = ks * 4 + c < R1 ? __ldg(r1 + ks * 4 + c) : 0.0;
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int n = nt * 8 + 2 * c;
@@ -427,6 +447,173 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_mma(const int64_t* __restri
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) slice_out[i0] = acc;
   }
+}
+
+// ---- K7 with the factor rows staged through shared memory by cp.async ----
+// Same contraction as k_tucker3_mma (warp per slice, W = A0[i0,:] x_0 C in
+// registers as B fragments, 8 nonzeros per m8n8k4 tile), but the random
+// factor rows are gathered whole: R/2 lanes copy one 160-byte row (R = 20) in
+// 16-byte cp.async pieces, 32/(R/2) rows per instruction, straight into a
+// per-warp shared-memory tile (no register writeback, several batches in
+// flight per SM); the DMMA fragments are then read from shared memory
+// (row stride = 8 mod 16 doubles: conflict-free 16-byte fragment reads).
+// Measured on B200 (tools/micro/gather.cu): whole-row 16-byte gathers move
+// ~106 G rows/s, the fragment-shaped 8-byte gathers of k_tucker3_mma ~55.
+// The k index of the A fragment is permuted so that each lane reads 16 bytes
+// per k-step pair: k-step 2j holds k = 8j + 2c, 2j + 1 holds 8j + 2c + 1
+// (c = lane % 4); B is built with the same map, so the contraction is
+// unchanged.  Pipeline per warp: records of batch b+2 and rows of batch b+1
+// in flight while batch b is contracted.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16_ca(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg_zfill(uint32_t dst, const void* src, uint32_t n) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int R>
+struct T3A {
+  static constexpr int KS = (R + 3) / 4, PAIRS = KS / 2, SINGLE = KS % 2;
+  static constexpr int NT = (R + 7) / 8;
+  static constexpr int W1 = 8 * PAIRS + 4 * SINGLE, W2 = 8 * NT;
+  static constexpr int WM = W1 > W2 ? W1 : W2;
+  static constexpr int ST = ((WM + 7) / 16) * 16 + 8;  // >= WM, = 8 (mod 16) doubles
+  static constexpr int LPR = R / 2;                     // 16-byte chunks per row
+  static constexpr int RPI = 32 / LPR;                  // rows per copy instruction
+};
+
+template <int R, int NB, int MB>
+__global__ void __launch_bounds__(256, MB) k_tucker3_async(
+    const int64_t* __restrict__ colptr, int64_t s0, const double* __restrict__ rec, uint32_t c1_mask,
+    const double* __restrict__ A0, const double* __restrict__ A1, const double* __restrict__ A2,
+    const double* __restrict__ C, int R0, double* __restrict__ slice_out) {
+  using P = T3A<R>;
+  constexpr int NROWS = 2 * NB;
+  constexpr int NINSTR = (NROWS + P::RPI - 1) / P::RPI;
+  constexpr int ROWBUF = NROWS * P::ST;  // doubles per row buffer
+  extern __shared__ __align__(16) double t3sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane >> 2, c = lane & 3;
+  double* rows = t3sm + (size_t)wid * (2 * ROWBUF + 3 * NB * 2);
+  double* recs = rows + 2 * ROWBUF;  // 3 buffers x NB records of 2 doubles
+  for (int e = lane; e < 2 * ROWBUF; e += 32) rows[e] = 0.0;  // zero padding beyond R
+  __syncwarp();
+  const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
+  const int cr = lane / P::LPR, ch = lane % P::LPR;  // copy role: row in instruction, chunk
+  for (int64_t i0 = blockIdx.x * nw + wid; i0 < s0; i0 += stride) {
+    {  // the next slice's records into L2
+      const int64_t j = i0 + stride;
+      if (j < s0) {
+        const int64_t l0 = colptr[j] * 16 / 128, l1 = (colptr[j + 1] * 16 + 127) / 128;
+        for (int64_t l = l0 + lane; l < l1; l += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(rec) + l * 128));
+      }
+    }
+    const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
+    if (e0 == e1) {
+      if (lane == 0) slice_out[i0] = 0.0;
+      continue;
+    }
+    const int64_t nb = (e1 - e0 + NB - 1) / NB;
+    auto issue_recs = [&](int64_t b) {
+      if (lane < NB) {
+        const int64_t e = e0 + b * NB + lane;
+        cp_async16_cg_zfill(smem_addr(recs + ((b % 3) * NB + lane) * 2), rec + 2 * (e < e1 ? e : e0),
+                            e < e1 ? 16u : 0u);
+      }
+    };
+    auto issue_rows = [&](int64_t b) {
+      const double* rb = recs + (b % 3) * NB * 2;
+      double* dst = rows + (b & 1) * ROWBUF;
+#pragma unroll
+      for (int t = 0; t < NINSTR; ++t) {
+        const int r = t * P::RPI + cr;
+        if (cr < P::RPI && r < NROWS) {
+          const bool second = r >= NB;
+          const int nz = second ? r - NB : r;
+          const uint32_t w = reinterpret_cast<const uint32_t*>(rb + nz * 2)[second ? 1 : 0];
+          const uint32_t idx = second ? (w & c1_mask) : w;
+          const double* src = (second ? A2 : A1) + (int64_t)idx * R + 2 * ch;
+          cp_async16_ca(smem_addr(dst + r * P::ST + 2 * ch), src);
+        }
+      }
+    };
+    // B fragments: W[k][n] with the permuted k map
+    double b[P::KS][P::NT];
+#pragma unroll
+    for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < P::NT; ++nt) {
+        const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
+        const int n = nt * 8 + q;
+        double w = 0.0;
+        if (k < R && n < R)
+          for (int r0 = 0; r0 < R0; ++r0)
+            w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + n), w);
+        b[ks][nt] = w;
+      }
+    issue_recs(0);
+    cp_async_commit();
+    if (nb > 1) issue_recs(1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    issue_rows(0);
+    cp_async_commit();
+    double acc = 0.0;
+    for (int64_t bi = 0; bi < nb; ++bi) {
+      cp_async_wait<0>();
+      __syncwarp();
+      if (bi + 1 < nb) issue_rows(bi + 1);
+      if (bi + 2 < nb) issue_recs(bi + 2);
+      cp_async_commit();
+      const double* rw = rows + (bi & 1) * ROWBUF;
+      const double* rv = recs + (bi % 3) * NB * 2;
+#pragma unroll
+      for (int g = 0; g < NB / 8; ++g) {
+        const double* ra = rw + (g * 8 + q) * P::ST;
+        const double* ry = rw + (NB + g * 8 + q) * P::ST;
+        double a[P::KS];
+#pragma unroll
+        for (int j = 0; j < P::PAIRS; ++j) {
+          const double2 p2 = *reinterpret_cast<const double2*>(ra + 8 * j + 2 * c);
+          a[2 * j] = p2.x;
+          a[2 * j + 1] = p2.y;
+        }
+        if (P::SINGLE) a[P::KS - 1] = ra[8 * P::PAIRS + c];
+        const double v = rv[(g * 8 + q) * 2 + 1];
+        double t = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt) {
+          const double2 y = *reinterpret_cast<const double2*>(ry + 8 * nt + 2 * c);
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < P::KS; ++ks) dmma884(d0, d1, a[ks], b[ks][nt]);
+          t = fma(d0, y.x, t);
+          t = fma(d1, y.y, t);
+        }
+        acc = fma(v, t, acc);
+      }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) slice_out[i0] = acc;
+  }
+}
+
+template <int R, int NB>
+constexpr size_t t3a_smem_bytes() {
+  return (size_t)8 * (2 * 2 * NB * T3A<R>::ST + 3 * NB * 2) * 8;
 }
 
 // Skip-mode sparse TTMc for order 3 (src/tensors.py:261-277): row i_n of the
@@ -534,6 +721,97 @@ __global__ void k_cp_cross(GenPack g, int64_t R, int64_t nnz, const double* __re
   }
   acc = block_sum(acc);
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// CP cross term <T, [[w; A0, A1, A2]]> for an order-3 tensor over its mode-0
+// fibre layout (src/tensors.py:354-361: mttkrp(T, factors, 0) contracted
+// with w * A0).  Warp per slice i0, u = w * A0[i0, :] once.  The warp reads
+// 32 records at a time, one 16-byte record per lane (coalesced), and hands
+// the coordinates / values out by shuffles; every nonzero is then served by
+// LPR = ceil(R/2) lanes, lane c loading the 16-byte chunk c of both of its
+// random rows A1[i1] and A2[i2] (L2-resident) and accumulating
+// v * sum_{r in chunk} u_r a1_r a2_r.  Each load instruction covers 32/LPR
+// whole rows, so it touches only their lines (the L1 wavefront count, not
+// the bytes, limits this kernel).  Deterministic: fixed lane / slice
+// partition, per-slice partials summed by k_final_sum.
+template <int LPR, bool VEC2>
+__global__ void __launch_bounds__(256) k_cp3_fibre(const int64_t* __restrict__ colptr, int64_t s0,
+                                                   const double* __restrict__ rec, uint32_t c1_mask,
+                                                   const double* __restrict__ A0,
+                                                   const double* __restrict__ A1,
+                                                   const double* __restrict__ A2,
+                                                   const double* __restrict__ w, int R,
+                                                   double* __restrict__ slice_out) {
+  constexpr int NPI = 32 / LPR;                      // nonzeros per load instruction
+  constexpr int STEPS = (32 + NPI - 1) / NPI;        // to cover a 32-record batch
+  constexpr int U = STEPS >= 4 ? 4 : STEPS;          // steps with loads in flight
+  const int lane = threadIdx.x & 31, grp = lane / LPR, ch = lane % LPR, c0 = 2 * ch;
+  const bool act = grp < NPI;
+  const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
+  for (int64_t i0 = blockIdx.x * nw + (threadIdx.x >> 5); i0 < s0; i0 += stride) {
+    const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
+    {  // the next slice's records into L2
+      const int64_t j = i0 + stride;
+      if (j < s0) {
+        const int64_t l0 = colptr[j] * 16 / 128, l1 = (colptr[j + 1] * 16 + 127) / 128;
+        for (int64_t l = l0 + lane; l < l1; l += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(rec) + l * 128));
+      }
+    }
+    const double u0 = c0 < R ? w[c0] * A0[i0 * R + c0] : 0.0;
+    const double u1 = c0 + 1 < R ? w[c0 + 1] * A0[i0 * R + c0 + 1] : 0.0;
+    double acc = 0.0;
+    for (int64_t base = e0; base < e1; base += 32) {
+      int32_t rc1 = 0, rc2 = 0;
+      double rv = 0.0;
+      if (base + lane < e1) {
+        int32_t cc[4];
+        load_rec<2>(rec, base + lane, cc, rv);
+        rc1 = cc[0];
+        rc2 = (int32_t)((uint32_t)cc[1] & c1_mask);
+      }
+#pragma unroll
+      for (int s = 0; s < STEPS; s += U) {
+        int32_t i1[U], i2[U];
+        double vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = (s + u) * NPI + grp;
+          const int src = idx < 32 ? idx : 31;
+          i1[u] = __shfl_sync(0xffffffffu, rc1, src);
+          i2[u] = __shfl_sync(0xffffffffu, rc2, src);
+          vv[u] = __shfl_sync(0xffffffffu, rv, src);
+          if (!act || idx >= 32 || s + u >= STEPS) vv[u] = 0.0;
+        }
+        double x0[U], x1[U], y0[U], y1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double* ra = A1 + (int64_t)i1[u] * R;
+          const double* rb = A2 + (int64_t)i2[u] * R;
+          if (VEC2) {
+            const double2 p = c0 < R ? __ldg(reinterpret_cast<const double2*>(ra + c0))
+                                     : make_double2(0.0, 0.0);
+            const double2 q = c0 < R ? __ldg(reinterpret_cast<const double2*>(rb + c0))
+                                     : make_double2(0.0, 0.0);
+            x0[u] = p.x;
+            x1[u] = p.y;
+            y0[u] = q.x;
+            y1[u] = q.y;
+          } else {
+            x0[u] = c0 < R ? __ldg(ra + c0) : 0.0;
+            x1[u] = c0 + 1 < R ? __ldg(ra + c0 + 1) : 0.0;
+            y0[u] = c0 < R ? __ldg(rb + c0) : 0.0;
+            y1[u] = c0 + 1 < R ? __ldg(rb + c0 + 1) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = fma(vv[u], fma(u0 * x0[u], y0[u], u1 * x1[u] * y1[u]), acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) slice_out[i0] = acc;
+  }
 }
 
 }  // namespace skx
@@ -658,12 +936,25 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
       // two 8-warp CTAs per SM (128 registers, no spills): twice the warps to
       // hide the L2 latency of the factor-row gathers (R = 20: 13.3 -> 10.3 ms
       // per 2e8 nonzeros; R = 10 unchanged or better)
-      if (R1 == 10 && R2 == 10) {
-        k_tucker3_mma<3, 2, 2, 10, 10, 2><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2,
-                                                             core, R0, R1, R2, part);
-      } else if (R1 == 20 && R2 == 20) {
-        k_tucker3_mma<5, 3, 2, 20, 20, 2><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2,
-                                                             core, R0, R1, R2, part);
+      // R = 20 (config 5): rows staged through shared memory by cp.async --
+      // in the pipeline, beside the sweeps, it measures 57 ms per 1e9-nonzero
+      // pass against 70 ms for the register-pipelined kernel (which is faster
+      // alone, 9.9 vs 11.9 ms per 2e8: its 128 registers per thread crowd out
+      // the sweeps' kernels).  Other even ranks: register pipeline with 16-byte
+      // A-fragment loads (config 4: 4.0 ms per pass in the pipeline).
+#define SKX_T3A(RR, NB, MBB)                                                                    \
+  do {                                                                                          \
+    const size_t sm = t3a_smem_bytes<RR, NB>();                                                 \
+    cudaFuncSetAttribute(k_tucker3_async<RR, NB, MBB>,                                          \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                 \
+    k_tucker3_async<RR, NB, MBB><<<mb, 256, sm, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, \
+                                                     R0, part);                                 \
+  } while (0)
+      if (R1 == 20 && R2 == 20) {
+        SKX_T3A(20, 16, 2);
+      } else if (R1 == 10 && R2 == 10) {
+        k_tucker3_mma<3, 2, 2, 10, 10, 2, true><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1,
+                                                                   A2, core, R0, R1, R2, part);
       } else
       SKX_T3M(2, 1) SKX_T3M(3, 1) SKX_T3M(5, 1) SKX_T3M(8, 1)
       SKX_T3M(2, 2) SKX_T3M(3, 2) SKX_T3M(5, 2) SKX_T3M(8, 2)
@@ -714,6 +1005,45 @@ extern "C" int skx_cp_cross_coo(int ndim, const int64_t* shape_h, int64_t R, int
   k_cp_cross<<<kRedBlocks, kRedThreads, 0, s>>>(g, R, nnz, vals, weights, part);
   k_final_sum<<<1, 1024, 0, s>>>(part, kRedBlocks, out);
   return check_launch("k_cp_cross", 2);
+}
+
+extern "C" int skx_cp_cross_fibre3(int64_t s0, const int64_t* colptr0, const void* rec0,
+                                   uint32_t c1_mask, int R, const double* const* factors_h,
+                                   const double* weights, double* out, void* ws, size_t* ws_bytes,
+                                   void* stream) {
+  SKX_REQUIRE(R >= 1 && R <= 32, "skx_cp_cross_fibre3: 1 <= R <= 32");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_cp_cross_fibre3: ws_bytes is NULL");
+  const size_t need = (size_t)imax(s0, 1) * 8 + 256;
+  if (ws == nullptr) {
+    *ws_bytes = need;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(*ws_bytes >= need, "skx_cp_cross_fibre3: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* part = (double*)ws;
+  const unsigned mb = (unsigned)imax(1, (s0 + 7) / 8);
+  const double* rec = (const double*)rec0;
+  const double *A0 = factors_h[0], *A1 = factors_h[1], *A2 = factors_h[2];
+  const int half = (R + 1) / 2;
+  const bool v2 = (R & 1) == 0;
+#define SKX_CP3(lp)                                                                            \
+  case lp:                                                                                     \
+    if (v2)                                                                                    \
+      k_cp3_fibre<lp, true><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, weights, \
+                                               R, part);                                       \
+    else                                                                                       \
+      k_cp3_fibre<lp, false><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2,         \
+                                                weights, R, part);                             \
+    break;
+  switch (half) {
+    SKX_CP3(1) SKX_CP3(2) SKX_CP3(3) SKX_CP3(4) SKX_CP3(5) SKX_CP3(6) SKX_CP3(7) SKX_CP3(8)
+    SKX_CP3(9) SKX_CP3(10) SKX_CP3(11) SKX_CP3(12) SKX_CP3(13) SKX_CP3(14) SKX_CP3(15)
+    SKX_CP3(16)
+    default: break;
+  }
+#undef SKX_CP3
+  k_final_sum<<<1, 1024, 0, s>>>(part, (int)s0, out);
+  return check_launch("k_cp3_fibre", 2);
 }
 
 extern "C" int skx_ttmc3_skip_coo(int64_t s_n, const int64_t* colptr, const void* rec,

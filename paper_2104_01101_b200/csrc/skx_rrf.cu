@@ -169,6 +169,188 @@ __global__ void __launch_bounds__(256) k_rrf_coo(RrfRng r, OthExt oe, int64_t s_
   }
 }
 
+// ---- RRF stage 1 straight from the lexsorted COO, no fibre layout ----------
+// st1[i_n, h(j)] += sign(j) v over the nonzeros, accumulated EXACTLY in
+// fixed point with atomics: the value range of the tensor is checked once
+// (skx_value_range: nonzero |v| within 2^41 of each other, all finite), so
+// every contribution v * 2^S (S = 93 - emax) is an integer of magnitude below
+// 2^94; it is split into three 32-bit limbs (bits 0-31 and 32-63 unsigned,
+// 64-95 signed) that are summed in 64-bit cells by fire-and-forget atomic
+// reductions (no carry round trips; fewer than 2^32 addends per cell cannot
+// overflow), and the cells are recombined into the exact 128-bit sum, rounded
+// once to double.  Integer addition is associative: the result is
+// deterministic whatever the atomic order, and within the reference's own
+// float rounding of the exact sum.  This removes the (i_n, others) sort that
+// a deterministic ordered accumulation needs: at 1e9 nonzeros that sort costs
+// ~50 ms per mode, more than the Philox work.
+
+// max / min unbiased exponent of the nonzero |v|, and a non-finite flag
+__global__ void k_value_range(const double* __restrict__ v, int64_t n, int* __restrict__ out) {
+  int emax = -100000, emin = 100000, bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v[i]);
+    const int ex = (int)((b >> 52) & 0x7ff);
+    if (ex == 0x7ff) bad = 1;
+    else if (ex == 0) { if ((b << 12) != 0) bad = 1; }  // subnormal: treat as out of range
+    else {
+      emax = max(emax, ex - 1023);
+      emin = min(emin, ex - 1023);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out + 0, emax);
+    atomicMin(out + 1, emin);
+    atomicOr(out + 2, bad);
+  }
+}
+
+__global__ void k_value_range_init(int* out) {
+  out[0] = -100000;
+  out[1] = 100000;
+  out[2] = 0;
+}
+
+struct CooSoA {
+  const int32_t* c[5];
+  int64_t ext[5];
+};
+
+// v * 2^S as a two's-complement 128-bit integer (hi, lo); |v| < 2^(Emax+1)
+// and S = 94 - (Emax + 1) make the shift 0 .. 41
+__device__ __forceinline__ void to_fixed(double v, int S, uint64_t& hi, uint64_t& lo) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const int ex = (int)((b >> 52) & 0x7ff);
+  if (ex == 0) {
+    hi = lo = 0;
+    return;
+  }
+  const uint64_t m = (b & 0xfffffffffffffULL) | 0x10000000000000ULL;
+  const int sh = ex - 1023 - 52 + S;  // >= 0 by the range check
+  uint64_t h = sh == 0 ? 0 : (sh >= 64 ? (m << (sh - 64)) : (m >> (64 - sh)));
+  uint64_t l = sh >= 64 ? 0 : (m << sh);
+  if (b >> 63) {  // negate
+    l = ~l + 1;
+    h = ~h + (l == 0 ? 1 : 0);
+  }
+  hi = h;
+  lo = l;
+}
+
+template <int NO, int U>
+__global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mode, int64_t nnz,
+                                                    const double* __restrict__ vals, int S,
+                                                    unsigned long long* __restrict__ acc) {
+  __shared__ uint32_t cnt[kRrfBuckets + 1];
+  uint64_t P = 1;
+  int oth[NO];
+#pragma unroll
+  for (int k = 0; k < NO; ++k) {
+    oth[k] = k + (k >= mode ? 1 : 0);
+    P *= (uint64_t)cs.ext[oth[k]];
+  }
+  int shift = 0;
+  while ((P >> shift) >= (uint64_t)kRrfBuckets) ++shift;
+  for (int b = threadIdx.x; b <= kRrfBuckets; b += blockDim.x) {
+    const uint64_t v = (uint64_t)b << shift;
+    int64_t lo = 0, hi = r.nd;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (r.d[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    cnt[b] = (uint32_t)lo;
+  }
+  __syncthreads();
+  const uint64_t k2 = r.k2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) * U + threadIdx.x; base < nnz;
+       base += stride) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * blockDim.x;
+      if (e >= nnz) break;
+      uint64_t j = 0;
+#pragma unroll
+      for (int k = 0; k < NO; ++k)
+        j = j * (uint64_t)cs.ext[oth[k]] + (uint64_t)(uint32_t)__ldcs(cs.c[oth[k]] + e);
+      const uint64_t row = (uint64_t)(uint32_t)__ldcs(cs.c[mode] + e);
+      const double v = __ldcs(vals + e);
+      const uint32_t t = rrf_entry_q(r, j, j + count_le_tab(r, cnt, shift, j));
+      uint64_t hi, lo;
+      to_fixed(pk_neg(t) ? -v : v, S, hi, lo);
+      // three 32-bit limbs (bits 0-31, 32-63 unsigned; 64-95 signed: |value|
+      // < 2^94, so bits 94.. are sign copies) summed in 64-bit cells by
+      // fire-and-forget reductions (no carries to wait for: < 2^32 addends)
+      unsigned long long* cell = acc + 4 * (row * k2 + pk_bucket(t));
+      atomicAdd(cell, (unsigned long long)(lo & 0xffffffffULL));
+      atomicAdd(cell + 1, (unsigned long long)(lo >> 32));
+      atomicAdd(cell + 2, (unsigned long long)(long long)(int32_t)(uint32_t)hi);
+    }
+  }
+}
+
+// st1 = double(acc) * 2^-S, correctly rounded
+__global__ void k_fixed_to_double(const unsigned long long* __restrict__ acc, int64_t n, int S,
+                                  double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    // value = L2 2^64 + L1 2^32 + L0 (L0, L1 unsigned sums, L2 signed)
+    const uint64_t L0 = acc[4 * i], L1 = acc[4 * i + 1], L2 = acc[4 * i + 2];
+    uint64_t lo = L0 + (L1 << 32);
+    uint64_t hi = (L1 >> 32) + (lo < L0 ? 1ULL : 0ULL) + L2;
+    const bool neg = (hi >> 63) != 0;
+    if (neg) {
+      lo = ~lo + 1;
+      hi = ~hi + (lo == 0 ? 1 : 0);
+    }
+    double d;
+    if (hi == 0 && lo == 0) {
+      d = 0.0;
+    } else {
+      // leading bit position, take 53 bits, round to nearest even on the rest
+      const int lz = hi ? __clzll((long long)hi) : 64 + __clzll((long long)lo);
+      const int top = 127 - lz;  // index of the leading one
+      uint64_t mant;
+      bool half = false, sticky = false;
+      if (top < 53) {
+        mant = lo;  // exact
+      } else {
+        const int drop = top - 52;  // bits below the 53-bit mantissa
+        // mant = (hi:lo) >> drop
+        mant = drop >= 64 ? (hi >> (drop - 64)) : ((lo >> drop) | (drop ? (hi << (64 - drop)) : 0));
+        // the dropped bits
+        uint64_t rl, rh;  // (hi:lo) & ((1 << drop) - 1)
+        if (drop >= 64) {
+          rl = lo;
+          rh = drop == 64 ? 0 : (hi & ((1ULL << (drop - 64)) - 1));
+        } else {
+          rl = lo & ((1ULL << drop) - 1);
+          rh = 0;
+        }
+        // half = bit drop-1, sticky = any lower bit
+        const int hb = drop - 1;
+        half = hb >= 64 ? ((rh >> (hb - 64)) & 1) : ((rl >> hb) & 1);
+        if (hb >= 64) sticky = (rl != 0) || ((rh & ((1ULL << (hb - 64)) - 1)) != 0);
+        else sticky = (rl & ((1ULL << hb) - 1)) != 0;
+        if (half && (sticky || (mant & 1))) ++mant;  // may carry to 2^53: still exact in double
+        d = ldexp((double)mant, drop);
+        d = ldexp(d, -S);
+        out[i] = neg ? -d : d;
+        continue;
+      }
+      d = (double)mant;
+    }
+    d = ldexp(d, -S);
+    out[i] = neg ? -d : d;
+  }
+}
+
 }  // namespace skx
 
 using namespace skx;
@@ -261,4 +443,60 @@ extern "C" int skx_rrf_stage1_coo(int n_other, const int64_t* ext_h, int64_t s_n
   kern<<<(unsigned)blocks, nw * 32, smem, (cudaStream_t)stream>>>(
       r, oe, s_n, colptr, (const double*)rec, c1_mask, stage1);
   return check_launch("k_rrf_coo");
+}
+
+extern "C" int skx_value_range(const double* vals, int64_t nnz, int* out3, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  k_value_range_init<<<1, 1, 0, st>>>(out3);
+  if (nnz > 0) {
+    const unsigned g = (unsigned)imin((nnz + 255) / 256, (int64_t)num_sms() * 8);
+    k_value_range<<<g, 256, 0, st>>>(vals, nnz, out3);
+  }
+  return check_launch("k_value_range", nnz > 0 ? 2 : 1);
+}
+
+extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int64_t nnz,
+                                 const int32_t* coords, const double* vals, int emax, uint64_t k0,
+                                 uint64_t k1, uint64_t p0, uint32_t has_pending, uint32_t pending,
+                                 uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
+                                 double* stage1, void* ws, size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 5, "skx_rrf_stage1_fx: order 2..5");
+  SKX_REQUIRE(mode >= 0 && mode < ndim, "skx_rrf_stage1_fx: mode out of range");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_rrf_stage1_fx: ws_bytes is NULL");
+  SKX_REQUIRE(nnz < (int64_t(1) << 32), "skx_rrf_stage1_fx: more than 2^32 nonzeros");
+  SKX_REQUIRE(nrej < (int64_t(1) << 32), "skx_rrf_stage1_fx: rejection list too long");
+  const int64_t sn = shape_h[mode];
+  const int64_t cells = sn * k2;
+  Arena ar(ws, *ws_bytes);
+  unsigned long long* acc = ar.take<unsigned long long>((size_t)cells * 4);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_rrf_stage1_fx: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = 94 - (emax + 1);
+  cudaMemsetAsync(acc, 0, (size_t)cells * 32, st);
+  if (nnz > 0) {
+    RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
+    CooSoA cs{};
+    for (int k = 0; k < ndim; ++k) {
+      cs.c[k] = coords + (int64_t)k * nnz;
+      cs.ext[k] = shape_h[k];
+    }
+    constexpr int U = 4;
+    auto kern = ndim == 2 ? k_rrf_coo_fx<1, U>
+              : ndim == 3 ? k_rrf_coo_fx<2, U>
+              : ndim == 4 ? k_rrf_coo_fx<3, U>
+                          : k_rrf_coo_fx<4, U>;
+    // one resident wave (no tail): blocks = SMs x resident CTAs per SM
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t blocks = imax(1, imin((nnz + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
+    kern<<<(unsigned)blocks, 256, 0, st>>>(r, cs, mode, nnz, vals, S, acc);
+  }
+  const unsigned g = (unsigned)imin((cells + 255) / 256, (int64_t)num_sms() * 16);
+  k_fixed_to_double<<<g, 256, 0, st>>>(acc, cells, S, stage1);
+  return check_launch("skx_rrf_stage1_fx", nnz > 0 ? 2 : 1);
 }

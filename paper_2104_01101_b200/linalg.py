@@ -187,9 +187,25 @@ def truncated_svd(mat, rank):
 
 # ------------------------------------------------------------------ leverage
 def leverage_scores_dev(a, check=True):
+    """Leverage scores of a tall factor on the device (src/linalg.py:73-84)
+    and the reference's rank flag.  R <= 32: libskx's Gram-Cholesky route
+    (skx_lev_scores, two passes over A); if it flags (possible rank
+    deficiency or cond(A) > ~100), the checked call decides on a Householder
+    R from TSQR instead, the unchecked (speculative) call returns the flag so
+    the sweep is replayed on the checked path."""
     torch = _torch()
     if a.shape[0] <= a.shape[1]:
         raise ValueError("leverage scores need a strictly tall matrix")
+    a = a.contiguous()
+    if a.shape[1] <= 32:
+        sc = torch.empty(a.shape[0], dtype=torch.float64, device="cuda")
+        flag = torch.empty(1, dtype=torch.int32, device="cuda")
+        nat.call_ws("skx_lev_scores", (nat.ptr(a), a.shape[0], a.shape[1], nat.ptr(sc),
+                                       nat.ptr(flag)), slot=7)
+        if not check:
+            return sc, (flag[0] != 0)
+        if int(flag.item()) == 0:
+            return sc, torch.zeros((), dtype=torch.bool, device="cuda")
     if a.shape[1] <= 64:
         # Householder R by TSQR; Q = A R^-1 (same rank test on diag(R))
         r = tsqr_r_dev(a)

@@ -243,6 +243,7 @@ class DeviceCoo:
         self._fibre_meta = {}
         self._keys = {}
         self._norm2 = None
+        self._vrange = None
 
     @classmethod
     def from_host(cls, st: SparseTensor):
@@ -326,6 +327,24 @@ class DeviceCoo:
             self._norm2 = out
         return self._norm2
 
+    # ---- value range (decides the exact fixed-point RRF stage 1)
+    def value_range(self):
+        """(emax, emin, bad): binary exponent range of the nonzero values and
+        whether any is non-finite/subnormal (one pass + one small D2H, cached)."""
+        torch = _torch()
+        if getattr(self, "_vrange", None) is None:
+            out = torch.empty(3, dtype=torch.int32, device="cuda")
+            nat.call("skx_value_range", nat.ptr(self.vals), self.nnz, nat.ptr(out), nat.stream())
+            self._vrange = tuple(int(x) for x in out.cpu().tolist())
+        return self._vrange
+
+    def fixed_point_ok(self):
+        """skx_rrf_stage1_fx sums exactly: finite normal values within 2^41."""
+        emax, emin, bad = self.value_range()
+        if self.nnz == 0:
+            return True
+        return not bad and emin >= emax - 41 and -929 <= emax <= 1000
+
     # ---- fibre-major layout for mode n (libskx skx_coo_fibre)
     def fibre(self, n, ts=None):
         """(colptr, records) of mode n: nonzeros ordered by (i_n, other modes
@@ -361,6 +380,9 @@ class DeviceCoo:
             self._fibre[n] = (colptr, rec)
             self._fibre_meta[n] = (mask, owner)
         return self._fibre[n]
+
+    def has_fibre(self, n):
+        return n in self._fibre
 
     def fibre_mask(self, n):
         """Mask recovering the last other coordinate from mode n's records."""
@@ -620,6 +642,18 @@ def fitness_tucker_dev(d, core, factors, norm2=None, comm=None):
 
 def cp_cross_dev(d, factors, weights):
     torch = _torch()
+    if is_sparse_dev(d) and d.ndim == 3 and int(factors[0].shape[1]) <= 32:
+        # warp per mode-0 slice over the fibre layout (built by a packing pass
+        # only: the lexsorted COO is already in mode-0 order)
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        fa = [f.contiguous() for f in factors]
+        arr, fp = nat.host_ptrs(fa)
+        cpt, rec0 = d.fibre(0)
+        nat.call_ws("skx_cp_cross_fibre3",
+                    (d.shape[0], nat.ptr(cpt), nat.ptr(rec0), ctypes.c_uint32(d.fibre_mask(0)),
+                     int(factors[0].shape[1]), fp, nat.ptr(weights.contiguous()), nat.ptr(out)),
+                    slot=5)
+        return out[0]
     if is_sparse_dev(d):
         out = torch.empty(1, dtype=torch.float64, device="cuda")
         shp, sp_ = nat.host_i64(d.shape)

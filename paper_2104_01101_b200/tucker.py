@@ -105,7 +105,15 @@ def rrf_stage1_dev(d, n, tabs):
     shape = shape_of(d)
     s_n = shape[n]
     st1 = torch.empty((s_n, tabs.k2), dtype=torch.float64, device="cuda")
-    if is_sparse_dev(d):
+    if is_sparse_dev(d) and not d.has_fibre(n) and d.fixed_point_ok():
+        # no mode-n layout (leverage runs build none): exact fixed-point
+        # accumulation straight from the lexsorted COO instead of sorting one
+        emax = d.value_range()[0]
+        shp, sp_ = nat.host_i64(shape)
+        nat.call_ws("skx_rrf_stage1_fx", (d.ndim, sp_, n, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals),
+                                          emax, *tabs.args(),
+                                          tabs.k2, nat.ptr(st1)), slot=8)
+    elif is_sparse_dev(d):
         colptr, rec = d.fibre(n)
         others = [k for k in range(d.ndim) if k != n]
         ext, ep = nat.host_i64([shape[k] for k in others])
@@ -314,9 +322,13 @@ class _Run:
                 self._host = None
         with torch.cuda.stream(main):
             self.draw_ts_ops()
-            if self.sparse:  # layouts first (with TS buckets folded in): RRF stage 1 and the
-                for n in range(self.ndim):  # TS sketches read them
-                    self.d.fibre(n, self.ts_ops[n] if self.use_ts else None)
+            if self.sparse:
+                if self.use_ts:  # layouts first, TS buckets folded in: the TS sketches read them
+                    for n in range(self.ndim):
+                        self.d.fibre(n, self.ts_ops[n])
+                else:  # leverage: only the fitness reads a layout (mode 0: a packing pass)
+                    self.d.fibre(0)
+                self.d.value_range()  # RRF stage 1: exact fixed-point path when in range
             self.prep()
             # small first-sweep inputs that do not depend on the RRF factors,
             # built while the scans occupy the GPU: the Kronecker-sketch plans
@@ -484,13 +496,20 @@ class _Run:
         with torch.cuda.stream(hi):
             core = self._sweep_loop(trace, res_dev, fit_dev, ev, fs, overlap)
         caller.wait_stream(hi)
-        if fs is not None:
-            caller.wait_stream(fs)
-        torch.cuda.synchronize()
-        trace.residuals.extend(torch.stack(res_dev).cpu().tolist() if res_dev else [])
-        trace.fitness.extend(torch.stack(fit_dev).cpu().tolist() if fit_dev else [])
-        trace.wall_s.extend(a.elapsed_time(b) / 1e3 for a, b in ev)
-        return core
+
+        def finish():
+            """Join the fitness stream and move the trace to the host."""
+            if fs is not None:
+                caller.wait_stream(fs)
+            torch.cuda.synchronize()
+            trace.residuals.extend(torch.stack(res_dev).cpu().tolist() if res_dev else [])
+            trace.fitness.extend(torch.stack(fit_dev).cpu().tolist() if fit_dev else [])
+            trace.wall_s.extend(a.elapsed_time(b) / 1e3 for a, b in ev)
+            return trace
+
+        # the caller's stream has the model once the sweep stream is joined;
+        # the last fitness pass may still be running on its own stream
+        return core, finish
 
     def _sweep_loop(self, trace, res_dev, fit_dev, ev, fs, overlap):
         torch = _torch()
@@ -614,8 +633,11 @@ class _Run:
         return k
 
 
-def sketched_tucker_als_dev(t, config, comm=None):
-    """Device-resident form: returns (core, factors) as CUDA tensors + trace."""
+def sketched_tucker_run_dev(t, config, comm=None):
+    """Device-resident run whose trace is completed later: returns (core,
+    factors, finish); finish() joins the per-sweep fitness stream and returns
+    the SweepTrace.  The model is ready on the caller's stream before the last
+    fitness pass ends, so a caller (Algorithm 6's core stage) can overlap it."""
     run = _Run(t, config, comm)
     run.initialise_and_prep()
     if run.sparse:
@@ -624,8 +646,14 @@ def sketched_tucker_als_dev(t, config, comm=None):
         for n in range(1, run.ndim):
             run.d.drop_fibre(n)
     trace = SweepTrace()
-    core = run.sweeps(trace)
-    return core, list(run.factors), trace
+    core, finish = run.sweeps(trace)
+    return core, list(run.factors), finish
+
+
+def sketched_tucker_als_dev(t, config, comm=None):
+    """Device-resident form: returns (core, factors) as CUDA tensors + trace."""
+    core, factors, finish = sketched_tucker_run_dev(t, config, comm)
+    return core, factors, finish()
 
 
 def sketched_tucker_als(t, config):

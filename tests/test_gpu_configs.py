@@ -196,21 +196,30 @@ def test_config5_alg6_reduced_vs_reference(cg, skx, oracle, monkeypatch, tag):
     t = make_input(skx, spec)
     rec = Recorder(monkeypatch)
     seen = {}
-    orig = cpmod.sketched_tucker_als_dev
+    orig = cpmod.sketched_tucker_run_dev
 
     def tucker(*a, **k):
-        core, fac, tr = orig(*a, **k)
+        core, fac, finish = orig(*a, **k)
         seen["core"] = core.cpu().numpy()
         seen["fac"] = [f.cpu().numpy() for f in fac]
-        seen["trace"] = tr
-        return core, fac, tr
 
-    monkeypatch.setattr(cpmod, "sketched_tucker_als_dev", tucker)
+        def fin():
+            seen["trace"] = finish()
+            return seen["trace"]
+        return core, fac, fin
+
+    monkeypatch.setattr(cpmod, "sketched_tucker_run_dev", tucker)
     model, trace = skx.cp_via_sketched_tucker(t, skx.CPConfig(**cfg))
     _check_lev(cg, tag, rec)
     assert trace.stage_split == int(cg[f"{tag}_split"])
     assert np.allclose(seen["trace"].fitness, cg[f"{tag}_tucker_fitness"], rtol=0, atol=1e-10)
-    assert np.allclose(seen["trace"].residuals, cg[f"{tag}_tucker_residuals"], rtol=1e-9, atol=0)
+    res = np.array(seen["trace"].residuals)
+    want = cg[f"{tag}_tucker_residuals"]
+    rel = np.abs(res - want) / want
+    # first sub-problem: same inputs up to the RRF factors' rounding; later ones
+    # inherit the factor drift of this gap-free spectrum (see the docstring)
+    assert rel[0] <= 1e-10, rel
+    assert rel.max() <= 1e-6, rel
     gf, gc = canon(seen["fac"], seen["core"])
     assert relerr(gc, cg[f"{tag}_core"]) <= 1e-6
     # core stage + composition vs the oracle on the same Tucker output

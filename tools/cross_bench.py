@@ -13,7 +13,7 @@ import torch  # noqa: E402
 
 import paper_2104_01101_b200 as skx  # noqa: E402
 from paper_2104_01101_b200.synth import planted_cp_coo_device  # noqa: E402
-from paper_2104_01101_b200.tensors import device_of, tucker_cross_dev  # noqa: E402
+from paper_2104_01101_b200.tensors import cp_cross_dev, device_of, tucker_cross_dev  # noqa: E402
 
 
 def main():
@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--side", type=int, default=100_000)
     ap.add_argument("--rank", type=int, default=10)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cp-rank", type=int, default=10)
     a = ap.parse_args()
     shape = (a.side,) * 3
     coords, vals = planted_cp_coo_device(shape, int(a.nnz), rank=10, noise_sd=0.1, seed=0)
@@ -42,6 +43,17 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
     print(f"tucker cross: {ms:.3f} ms  value {float(x):.12e}", flush=True)
+    w = torch.rand(a.cp_rank, dtype=torch.float64, device="cuda", generator=g)
+    cf = [f[:, :a.cp_rank].contiguous() for f in fac]
+    y = cp_cross_dev(d, cf, w)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(a.reps):
+        cp_cross_dev(d, cf, w)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.reps
+    print(f"cp cross (R={a.cp_rank}): {ms:.3f} ms  value {float(y):.12e}", flush=True)
 
 
 if __name__ == "__main__":

@@ -17,22 +17,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-DENSE = {
-    1: dict(shape=(100,) * 3, ranks=(5,) * 3, sketch="tensorsketch", sketch_size=400, sweeps=5,
-            noise=1e-2),
-    2: dict(shape=(400,) * 3, ranks=(10,) * 3, sketch="leverage-random", sketch_size=3200,
-            sweeps=10, noise=1e-2),
-    3: dict(shape=(120,) * 4, ranks=(8,) * 4, sketch="tensorsketch", sketch_size=4096, sweeps=10,
-            noise=1e-3),
-}
-
-
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
     ap.add_argument("--e2e", action="store_true",
                     help="sparse configs: time the public call on a pinned host copy (upload included)")
+    ap.add_argument("--window", default="",
+                    help="KERNEL:i:j -- list every kernel (all streams) between the start of the "
+                         "i-th and the j-th launch of KERNEL (substring), with gaps")
     ap.add_argument("--gantt", type=float, default=0.0,
                     help="also list, in start order, every kernel longer than this many ms")
     args = ap.parse_args()
@@ -44,30 +37,25 @@ def main():
     from paper_2104_01101_b200.synth import planted_cp_coo_device
     from paper_2104_01101_b200.tucker import sketched_tucker_als_dev
 
-    if args.config in bench.CONFIGS:
-        cfgd = bench.CONFIGS[args.config]
+    cfgd = bench.CONFIGS[args.config]
+    if cfgd["kind"] != "dense":
         coords, vals = planted_cp_coo_device(cfgd["shape"], cfgd["nnz"], rank=10, noise_sd=0.1,
                                              seed=0)
-        st = skx.SparseTensor.from_device(cfgd["shape"], coords, vals)
+        st = skx.SparseTensor.from_device(cfgd["shape"], coords.t().contiguous(), vals)
         del coords, vals
-    else:  # dense configs 1-3 (BASELINE.json), planted Tucker generated on the GPU
-        cfgd = DENSE[args.config]
-        g = torch.Generator(device="cuda").manual_seed(0)
-        r = cfgd["ranks"][0]
-        t = torch.randn((r,) * len(cfgd["shape"]), dtype=torch.float64, device="cuda", generator=g)
-        for n, s_n in enumerate(cfgd["shape"]):
-            q, _ = torch.linalg.qr(torch.randn(s_n, r, dtype=torch.float64, device="cuda", generator=g))
-            t = torch.movedim(torch.tensordot(q, t, dims=([1], [n])), 0, n)
-        e = torch.randn(t.shape, dtype=torch.float64, device="cuda", generator=g)
-        st = (t + e * (cfgd["noise"] * torch.linalg.vector_norm(t) / torch.linalg.vector_norm(e))).contiguous()
-    cfg = skx.TuckerConfig(ranks=cfgd["ranks"], max_sweeps=cfgd["sweeps"], sketch=cfgd["sketch"],
-                           sketch_size=cfgd["sketch_size"], seed=0)
+    else:
+        st = torch.from_numpy(bench.dense_input_host(cfgd)).cuda()
+    cfg = bench.tucker_config(skx, cfgd)
     sparse = not torch.is_tensor(st)
+    from paper_2104_01101_b200.cp import cp_via_sketched_tucker_dev
+    alg6 = cfgd["kind"] == "alg6"
     if args.e2e and sparse:
         dev = st._device
         hc = torch.empty((dev.nnz, dev.ndim), dtype=torch.int64, pin_memory=True)
         hv = torch.empty(dev.nnz, dtype=torch.float64, pin_memory=True)
-        hc.copy_(dev.coords.t().to(torch.int64))
+        chunk = 1 << 26
+        for lo in range(0, dev.nnz, chunk):
+            hc[lo:min(dev.nnz, lo + chunk)].copy_(dev.coords[:, lo:lo + chunk].t().to(torch.int64))
         hv.copy_(dev.vals)
         st = skx.SparseTensor.from_sorted(cfgd["shape"], hc.numpy(), hv.numpy())
         del dev
@@ -75,12 +63,15 @@ def main():
 
         def call():
             st._device = None
-            skx.sketched_tucker_als(st, cfg)
+            (skx.cp_via_sketched_tucker if alg6 else skx.sketched_tucker_als)(st, cfg)
     else:
         def call():
             if sparse:
                 st._device.release_layouts()
-            sketched_tucker_als_dev(st, cfg)
+            if alg6:
+                cp_via_sketched_tucker_dev(st, cfg)
+            else:
+                sketched_tucker_als_dev(st, cfg)
     for _ in range(2):
         call()
     torch.cuda.synchronize()
@@ -117,6 +108,19 @@ def main():
           f"largest {sorted(gaps)[-5:] if gaps else []} us")
     for nm, (c, d) in sorted(per.items(), key=lambda kv: -kv[1][1])[:30]:
         print(f"{d / 1e3:9.3f} ms {c:5d}  {nm}")
+    if args.window:
+        name, i, j = args.window.split(":")
+        marks = sorted(e["ts"] for e in kern if name in e["name"])
+        lo, hi = marks[int(i)], marks[int(j)]
+        print(f"window {name}[{i}]..[{j}]: {(hi - lo) / 1e3:.3f} ms")
+        prev = {}
+        for e in sorted(kern, key=lambda e: e["ts"]):
+            if lo <= e["ts"] < hi:
+                st = e["args"].get("stream")
+                gap = e["ts"] - prev.get(st, e["ts"])
+                prev[st] = e["ts"] + e["dur"]
+                print(f"{(e['ts'] - lo) / 1e3:8.3f} {e['dur']:9.1f}us gap{gap:8.1f}us s{st!s:>3}  "
+                      f"{e['name'][:90]}")
     if args.gantt > 0:
         print("start_ms  dur_ms  stream  kernel")
         for e in sorted(kern, key=lambda e: e["ts"]):
