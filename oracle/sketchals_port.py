@@ -774,3 +774,66 @@ def cp_via_tucker(t, rank, tucker_sweeps=5, cp_sweeps=None, sketch_size=None,
                wall_s=list(ttr.wall_s) + [sum(ctr.wall_s)],
                stage_split=len(ttr.fitness))
     return out, weights, tr, (core, B)
+
+
+def _vec_col(t):
+    """vec(T) as a (prod shape, 1) column, sparse-aware (src/tucker.py:205-213)."""
+    if isinstance(t, Coo):
+        flat = np.ravel_multi_index(t.coords.T, t.shape)
+        return sp.csr_matrix((t.values, (flat, np.zeros(len(flat), dtype=np.int64))),
+                             shape=(int(np.prod(t.shape)), 1))
+    return np.asarray(t).reshape(-1, 1)
+
+
+def ref_tucker_ts(t, ranks, max_sweeps=5, sketch_size=None, sketch_factor=None, init=None,
+                  rrf_width=None, seed=0, tol=0.0):
+    """One-variable-at-a-time TensorSketch baseline (src/tucker.py:303-364):
+    RRF init of every mode, per-mode operators + right-hand sides and one
+    all-mode operator for the core, drawn once; per sweep N unconstrained
+    factor solves (core fixed, QR re-orthonormalised) and one core solve."""
+    import time
+
+    shape = tuple(t.shape)
+    nd = len(shape)
+    ranks = tuple(int(r) for r in ranks)
+    m = resolve_m(ranks, sketch_size, sketch_factor)
+    r_init, r_sketch = streams(seed, 2)
+    init = init or "rrf"
+    A = []
+    for n in range(nd):
+        if init == "rrf":
+            k1 = resolve_k1(ranks, ranks[n], rrf_width, sketch_size, sketch_factor)
+            A.append(init_rrf(unfold(t, n), ranks[n], k1, r_init))
+        else:
+            A.append(np.linalg.qr(r_init.standard_normal((shape[n], ranks[n])))[0][:, :ranks[n]])
+    tabs, rhs = [], []
+    for n in range(nd):
+        ext = tuple(shape[k] for k in _rest(nd, n))
+        tb = ts_tables(ext, m, r_sketch)
+        tabs.append((tb, ext))
+        rhs.append(ts_rhs(tb[0], tb[1], ext, m, unfold_t(t, n)))
+    ctab = ts_tables(shape, m, r_sketch)
+    crhs = ts_rhs(ctab[0], ctab[1], shape, m, _vec_col(t))
+
+    def core_solve():
+        z = ts_kron(ctab[0], ctab[1], shape, m, A)
+        sol = np.linalg.lstsq(z, crhs, rcond=None)[0]
+        return sol.reshape(ranks), float(np.linalg.norm(z @ sol - crhs))
+
+    core, _ = core_solve()
+    tr = Trace()
+    for _ in range(max_sweeps):
+        t0 = time.perf_counter()
+        for n in range(nd):
+            (hs, ss), ext = tabs[n]
+            z = ts_kron(hs, ss, ext, m, [A[k] for k in _rest(nd, n)]) @ unfold(core, n).T
+            sol = np.linalg.lstsq(z, rhs[n], rcond=None)[0]
+            tr.residuals.append(float(np.linalg.norm(z @ sol - rhs[n])))
+            A[n] = np.linalg.qr(sol.T)[0][:, :ranks[n]]
+        core, cres = core_solve()
+        tr.residuals.append(cres)
+        tr.wall_s.append(time.perf_counter() - t0)
+        tr.fitness.append(float(fitness_tucker(t, core, A)))
+        if len(tr.fitness) > 1 and abs(tr.fitness[-1] - tr.fitness[-2]) < tol:
+            break
+    return core, A, tr

@@ -14,8 +14,10 @@ from .linalg import (LeverageProfile, RankDeficientError, SvdResult, leverage_sc
 from .sketching import (CompositeSketchOp, CountSketchOp, LevSamplerOp, TensorSketchOp,
                         composite_apply, lev_apply, lev_apply_krp, lev_build, ts_apply_kron,
                         ts_apply_rhs)
-from .tucker import (SweepTrace, TuckerConfig, hooi, hosvd_init, init_rrf, sketched_tucker_als)
+from .tucker import (SweepTrace, TuckerConfig, hooi, hosvd_init, init_rrf, ref_tucker_ts,
+                     sketched_tucker_als)
 from .cp import CPConfig, cp_als, cp_via_sketched_tucker, sketched_cp_als
+from .formats import load_cp, load_tucker, read_tensor, save_cp, save_tucker, write_tensor
 from .rng import make_rng, split_rng
 
 __version__ = "0.1.0"

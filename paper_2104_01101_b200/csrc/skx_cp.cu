@@ -53,6 +53,13 @@ __device__ void cp_jacobi_eig(double* a, double* v, int n, double* cs, int* pq, 
   const int nn = n + (n & 1);
   const int npair = nn / 2;
   for (int e = tid; e < n * n; e += blockDim.x) v[e] = (e / n == e % n) ? 1.0 : 0.0;
+  // rotations keep ||a||_F; an off-diagonal entry below eps ||a||_F is at the
+  // backward-error level of a LAPACK SVD of a (absolute criterion: a relative
+  // one, |a_pq| < eps sqrt(a_pp a_qq), never settles under rounding when the
+  // spectrum spans orders of magnitude)
+  double fro2 = 0.0;
+  for (int e = 0; e < n * n; ++e) fro2 += a[e] * a[e];
+  const double tiny = 1e-16 * sqrt(fro2);
   __syncthreads();
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) *flag = 0;
@@ -76,8 +83,7 @@ __device__ void cp_jacobi_eig(double* a, double* v, int n, double* cs, int* pq, 
         if (q < n) {
           const double apq = a[p * n + q];
           const double app = a[p * n + p], aqq = a[q * n + q];
-          if (apq != 0.0 && fabs(apq) > 2.220446049250313e-16 * sqrt(fabs(app * aqq)) &&
-              fabs(apq) > 1e-300) {
+          if (fabs(apq) > tiny && fabs(apq) > 1e-300) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);

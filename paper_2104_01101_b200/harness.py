@@ -61,16 +61,16 @@ def adopt_config(cfg, cls):
 
 def run_single(tensor, algorithm, cfg):
     """One decomposition run; returns (model, trace, resolved sketch size) like
-    src/harness.py:115-138.  `ref-ts` (the unsketched-ALS baseline the paper
-    compares against, src/tucker.py:303-364) is not on the GPU path and raises."""
+    src/harness.py:115-138; `ref-ts` is the one-variable TensorSketch baseline
+    (src/tucker.py:303-364)."""
     if algorithm not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {algorithm!r}; choose from {ALGORITHMS}")
     t = adopt_tensor(tensor)
     if algorithm in TUCKER_ALGS:
         cfg = adopt_config(cfg, tucker_mod.TuckerConfig)
         if algorithm == "ref-ts":
-            raise NotImplementedError("ref-ts is the reference's own baseline; run it there")
-        if algorithm == "hooi":
+            model, trace = tucker_mod.ref_tucker_ts(t, cfg)
+        elif algorithm == "hooi":
             model, trace = tucker_mod.hooi(t, cfg)
         else:
             model, trace = tucker_mod.sketched_tucker_als(t, cfg)

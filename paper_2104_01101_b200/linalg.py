@@ -608,3 +608,38 @@ def rsvd_lrls(z, y, rank, rng, oversample=10):
     core_t, v, _ = rsvd_lrls_dev(z, y, rank, src, oversample)
     src.sync_host()
     return _np(core_t), _np(v)
+
+
+def qr_lapack_dev(a):
+    """Thin Householder QR with LAPACK's reflector convention (dgeqrf/dlarfg:
+    beta = -sign(alpha) ||x||, v(1) = 1, tau = (beta - alpha) / beta; Q from
+    the reflectors as dorgqr), so Q's column signs are numpy.linalg.qr's.
+    Needed where a factor's signs are not washed out downstream (ref_tucker_ts
+    re-orthonormalises a factor while the core stays fixed, src/tucker.py:
+    353-356).  Column loop of small device ops, no host sync; for narrow
+    matrices (k = rank columns)."""
+    torch = _torch()
+    A = a.to(torch.float64).clone()
+    m, k = A.shape
+    vs, taus = [], []
+    for j in range(min(m, k)):
+        x = A[j:, j]
+        alpha = x[0]
+        xnorm = torch.linalg.vector_norm(x[1:]) if m - j > 1 else torch.zeros((), dtype=A.dtype,
+                                                                              device=A.device)
+        beta = -torch.copysign(torch.hypot(alpha, xnorm), alpha)
+        trivial = xnorm == 0
+        tau = torch.where(trivial, torch.zeros_like(beta), (beta - alpha) / beta)
+        denom = torch.where(trivial, torch.ones_like(alpha), alpha - beta)
+        v = x / denom
+        v[0] = 1.0
+        w = v @ A[j:, j:]
+        A[j:, j:] -= tau * torch.outer(v, w)
+        A[j, j] = torch.where(trivial, alpha, beta)
+        vs.append(v)
+        taus.append(tau)
+    Q = torch.eye(m, k, dtype=A.dtype, device=A.device)
+    for j in reversed(range(len(vs))):
+        v = vs[j]
+        Q[j:, :] -= taus[j] * torch.outer(v, v @ Q[j:, :])
+    return Q, torch.triu(A[:k, :])

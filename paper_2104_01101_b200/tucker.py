@@ -19,7 +19,8 @@ import numpy as np
 
 from . import _native as nat
 from . import rng as rngmod
-from .linalg import (NormalSource, RankDeficientError, resid_dev, rsvd_lrls_dev, rsvd_lrls_hits_dev,
+from .linalg import (NormalSource, RankDeficientError, qr_lapack_dev, resid_dev, rsvd_lrls_dev,
+                     rsvd_lrls_hits_dev,
                      rsvd_lrls_rows_dev, top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, finish_rrf_scan,
                         gather_coo_dev, gather_dense_dev, hits_to_dense, kron_rows_dev, lev_det_dev,
@@ -178,9 +179,10 @@ def init_rrf(tn, rank, width, rng):
 
 
 def random_orthonormal_dev(n_rows, n_cols, gen):
+    """Q of a Gaussian matrix (src/tucker.py:107-109) with numpy's QR signs."""
     torch = _torch()
     g = torch.from_numpy(gen.standard_normal((n_rows, n_cols))).cuda()
-    q, _ = torch.linalg.qr(g, mode="reduced")
+    q, _ = qr_lapack_dev(g)
     return q[:, :n_cols].contiguous()
 
 
@@ -769,4 +771,108 @@ def hooi_dev(t, config):
 def hooi(t, config):
     """Exact Tucker-ALS (src/tucker.py:155-193)."""
     core, factors, trace = hooi_dev(t, config)
+    return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace
+
+
+# ------------------------------------------------------------------ ref-ts
+def _vec_sketch_dev(op, d):
+    """TensorSketch of vec(T) over every mode (src/tucker.py:205-213 +
+    ts_apply_rhs): the mode-0 right-hand side of T viewed as a
+    (1, s_1, ..., s_N) tensor; returns an (m,) device vector."""
+    torch = _torch()
+    if is_sparse_dev(d):
+        c = torch.cat([torch.zeros((1, d.nnz), dtype=torch.int32, device="cuda"), d.coords])
+        d1 = DeviceCoo((1,) + d.shape, c.contiguous(), d.vals)
+        return ts_rhs_mode_dev(op, d1, 0)[0]
+    return ts_rhs_dense_dev(op, d.reshape((1,) + tuple(d.shape)).contiguous(), 0)[0]
+
+
+def _lstsq_dev(z, b):
+    """Least squares min ||z x - b|| with numpy lstsq(rcond=None) semantics
+    (src/tucker.py:345, 353): the minimum-norm SVD solve for narrow systems,
+    QR with R^-1 for the full-rank core system."""
+    torch = _torch()
+    from .cp import _lstsq_min_norm_dev
+    if z.shape[1] <= 64:
+        return _lstsq_min_norm_dev(z, b)
+    q, r = torch.linalg.qr(z, mode="reduced")
+    return torch.linalg.solve_triangular(r, q.transpose(0, 1) @ b, upper=True)
+
+
+def ref_tucker_ts_dev(t, config):
+    """The reference's one-variable-at-a-time TensorSketch baseline
+    (src/tucker.py:303-364) on the device: RRF (or random) init of every
+    mode from the first of two seed streams; per mode a TensorSketch operator
+    and right-hand side, plus one over all modes for the core, drawn once;
+    each sweep solves N unconstrained sketched factor problems (core fixed;
+    factors re-orthonormalised by QR) and one core problem (factors fixed).
+    Returns (core, factors, trace)."""
+    import time
+    torch = _torch()
+    if config.sketch != "tensorsketch":
+        raise ValueError("the reference baseline is TensorSketch-based")
+    _validate_ranks(tuple(int(s) for s in t.shape), config.ranks)
+    d = device_of(t)
+    shape = shape_of(d)
+    ndim = len(shape)
+    ranks = config.ranks
+    _validate_ranks(shape, ranks)
+    m = config.resolved_sketch_size()
+    _check_sketch_size(m, ranks)
+    rng_init, rng_sketch = rngmod.split_rng(config.seed, 2)
+    init = config.init or "rrf"
+    factors = []
+    for n in range(ndim):
+        if init == "rrf":
+            factors.append(init_rrf_dev(d, n, ranks[n], config.resolved_rrf_width(ranks[n]),
+                                        rng_init))
+        elif init == "random":
+            factors.append(random_orthonormal_dev(shape[n], ranks[n], rng_init))
+        else:
+            raise ValueError(f"unknown init {init!r} for ref_tucker_ts")
+    ops, rhs = [], []
+    for n in range(ndim):
+        op = TensorSketchOp.build(tuple(shape[k] for k in range(ndim) if k != n), m, rng_sketch)
+        ops.append(op)
+        rhs.append((ts_rhs_mode_dev(op, d, n) if is_sparse_dev(d) else
+                    ts_rhs_dense_dev(op, d, n)).t())  # Y_n, m x s_n
+    core_op = TensorSketchOp.build(shape, m, rng_sketch)
+    core_rhs = _vec_sketch_dev(core_op, d).view(m, 1)
+    norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
+
+    def update_core():
+        z = ts_kron_dev(core_op, factors)
+        sol = _lstsq_dev(z, core_rhs)
+        return sol.reshape(ranks), torch.linalg.vector_norm(z @ sol - core_rhs)
+
+    core, _ = update_core()
+    trace = SweepTrace()
+    for _ in range(config.max_sweeps):
+        tic = time.perf_counter()
+        res = []
+        for n in range(ndim):
+            others = [factors[k] for k in range(ndim) if k != n]
+            cn = core.movedim(n, 0).reshape(ranks[n], -1)  # matricize(core, n)
+            z = ts_kron_dev(ops[n], others) @ cn.t()
+            sol = _lstsq_dev(z, rhs[n])
+            res.append(torch.linalg.vector_norm(z @ sol - rhs[n]))
+            q, _ = qr_lapack_dev(sol.t())  # numpy's signs: the core stays fixed
+            factors[n] = q[:, :ranks[n]].contiguous()
+        core, core_res = update_core()
+        res.append(core_res)
+        fit = fitness_tucker_dev(d, core.contiguous(), factors, norm2)
+        vals = torch.stack(res + [fit]).cpu().tolist()
+        trace.residuals.extend(vals[:-1])
+        trace.wall_s.append(time.perf_counter() - tic)
+        trace.fitness.append(float(vals[-1]))
+        if (len(trace.fitness) > 1
+                and abs(trace.fitness[-1] - trace.fitness[-2]) < config.convergence_tol):
+            break
+    return core, factors, trace
+
+
+def ref_tucker_ts(t, config):
+    """Reference sketched baseline, one variable per sub-problem
+    (src/tucker.py:303-364)."""
+    core, factors, trace = ref_tucker_ts_dev(t, config)
     return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace

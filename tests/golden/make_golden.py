@@ -306,6 +306,47 @@ def topm_cases():
     put("tm_count", np.array(len(cases)))
 
 
+def refts_and_format_cases():
+    """ref_tucker_ts (src/tucker.py:303-364) on a dense and a sparse input,
+    and the text formats (src/tensors.py:371-428) as written by the
+    reference."""
+    import tempfile
+    for tag, spec, cfg in (
+            ("rtsd", ("dense", (20, 18, 16), 3, 1e-2, 41),
+             dict(ranks=(3, 3, 3), max_sweeps=3, sketch="tensorsketch", sketch_size=200, seed=3)),
+            ("rtss", ("sparse", (30, 30, 30), 4000, 42),
+             dict(ranks=(3, 3, 3), max_sweeps=3, sketch="tensorsketch", sketch_size=200, seed=4)),
+            ("rtdr", ("dense", (20, 18, 16), 3, 1e-2, 41),
+             dict(ranks=(3, 3, 3), max_sweeps=3, sketch="tensorsketch", sketch_size=200, seed=3,
+                  init="random")),
+            ("rtsr", ("sparse", (30, 30, 30), 4000, 42),
+             dict(ranks=(3, 3, 3), max_sweeps=3, sketch="tensorsketch", sketch_size=200, seed=4,
+                  init="random"))):
+        model, trace = ref.ref_tucker_ts(make_input(spec), ref.TuckerConfig(**cfg))
+        store_run(tag, model, trace)
+    gen = np.random.default_rng(43)
+    dense = gen.standard_normal((2, 3, 4))
+    coords = np.array([[0, 1, 2], [1, 0, 0], [1, 2, 3], [0, 0, 1]])
+    st = ref.SparseTensor((2, 3, 4), coords, gen.standard_normal(4))
+    mat = gen.standard_normal((3, 2))
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, obj, fn in (("fmt_dense", dense, ref.write_tensor),
+                              ("fmt_sparse", st, ref.write_tensor),
+                              ("fmt_matrix", mat, None)):
+            path = os.path.join(tmp, name)
+            if fn is None:
+                from sketchals.tensors import write_matrix
+                write_matrix(path, obj)
+            else:
+                fn(path, obj)
+            with open(path) as fh:
+                put(name, np.array(fh.read()))
+    put("fmt_dense_arr", dense)
+    put("fmt_sparse_coords", st.coords)
+    put("fmt_sparse_values", st.values)
+    put("fmt_matrix_arr", mat)
+
+
 def cp_als_cases():
     """Exact CP-ALS on a sparse tensor (rrf init) and on a dense one."""
     c, v = planted_cp_coo_host((30, 30, 30), 3000, rank=3, seed=21)
@@ -320,10 +361,10 @@ def cp_als_cases():
 
 
 def main():
-    if sys.argv[1:] == ["topm"]:  # add just these cases to an existing file
+    if sys.argv[1:] in (["topm"], ["refts"]):  # add just these cases to an existing file
         path = os.path.join(HERE, "golden.npz")
         OUT.update(dict(np.load(path)))
-        topm_cases()
+        {"topm": topm_cases, "refts": refts_and_format_cases}[sys.argv[1]]()
         np.savez_compressed(path, **OUT)
         print("wrote", path, len(OUT), "arrays")
         return
@@ -336,6 +377,7 @@ def main():
     deterministic_cases()
     cp_als_cases()
     topm_cases()
+    refts_and_format_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print("wrote", path, len(OUT), "arrays", os.path.getsize(path), "bytes")

@@ -52,9 +52,10 @@ def test_adopt_config_and_tensor():
 def test_run_single_errors():
     with pytest.raises(ValueError):
         harness.run_single(np.zeros((2, 2, 2)), "nope", TuckerConfig((1, 1, 1)))
-    with pytest.raises(NotImplementedError):
+    # ref-ts validates like the reference (TensorSketch only) before any device work
+    with pytest.raises(ValueError):
         harness.run_single(np.zeros((2, 2, 2)), "ref-ts",
-                           TuckerConfig((1, 1, 1), sketch="tensorsketch", sketch_size=8))
+                           TuckerConfig((1, 1, 1), sketch="leverage-random", sketch_size=8))
 
 
 @pytest.mark.gpu

@@ -288,3 +288,21 @@ def test_sketched_tucker_deterministic(golden, oracle, tag):
         assert relerr(a, b) <= 1e-10
     assert relerr(got_c, ref_c) <= 1e-10
     assert np.allclose(tr.residuals, golden[f"{tag}_residuals"], rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("tag", ["rtsd", "rtss", "rtdr", "rtsr"])
+def test_ref_tucker_ts_vs_reference_golden(golden, oracle, tag):
+    dense = tag in ("rtsd", "rtdr")
+    spec = ("dense", (20, 18, 16), 3, 1e-2, 41) if dense else ("sparse", (30, 30, 30), 4000, 42)
+    seed = 3 if dense else 4
+    init = "random" if tag in ("rtdr", "rtsr") else None
+    t = make_input(oracle, spec)
+    core, fac, tr = oracle.ref_tucker_ts(t, (3, 3, 3), max_sweeps=3, sketch_size=200, seed=seed,
+                                         init=init)
+    got_f, got_c = canon(fac, core)
+    ref_f, ref_c = canon([golden[f"{tag}_a{k}"] for k in range(3)], golden[f"{tag}_core"])
+    for a, b in zip(got_f, ref_f):
+        assert relerr(a, b) <= 1e-10
+    assert relerr(got_c, ref_c) <= 1e-10
+    assert np.allclose(tr.residuals, golden[f"{tag}_residuals"], rtol=1e-10, atol=0)
+    assert np.allclose(tr.fitness, golden[f"{tag}_fitness"], rtol=0, atol=1e-12)
