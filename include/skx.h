@@ -278,7 +278,7 @@ int skx_resid_sq(const double* u, const double* vt, int64_t n_out, int64_t n_in,
                  void* stream);
 
 /* R factor (w x w, row-major, upper) of the n x w matrix A[i,j] = a[i*rs + j*cs]
- * by TSQR with Householder blocks (LAPACK dlarfg signs), w <= 64.  Replaces the
+ * by TSQR with Householder blocks (LAPACK dlarfg signs), w <= 96.  Replaces the
  * LAPACK QRs of tall-skinny operands: np.linalg.qr in src/linalg.py:45 (factor
  * leverage scores) and the SVDs of src/linalg.py:59 / src/tucker.py:141, which
  * are taken as SVD(R). */
@@ -290,7 +290,7 @@ int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t cs, double
  * factorisation of the sketched system (src/linalg.py:103). */
 int skx_chol_upper(const double* g, int n, double* r, int* info, void* stream);
 
-/* One-sided Jacobi SVD of the n x n matrix A[i,j] = a[i*rs + j*cs] (n <= 64):
+/* One-sided Jacobi SVD of the n x n matrix A[i,j] = a[i*rs + j*cs] (n <= 112):
  * A = U diag(s) V^T with s descending, U and V row-major.  Replaces the LAPACK
  * SVD of small R factors (src/linalg.py:59, src/tucker.py:141). */
 int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u, double* s,

@@ -224,9 +224,9 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(const double* __restrict__ A
     __syncthreads();  // everyone has read `changed` before thread 0 resets it
     if (!any) break;
   }
-  // singular values and descending order (n <= 64: one thread sorts)
-  __shared__ double sv[64];
-  __shared__ int ord[64];
+  // singular values and descending order (n <= 112: one thread sorts)
+  __shared__ double sv[112];
+  __shared__ int ord[112];
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     double s2 = 0.0;
     for (int i = 0; i < n; ++i) s2 = fma(A[j * n + i], A[j * n + i], s2);
@@ -474,7 +474,7 @@ extern "C" int skx_chol_upper(const double* g, int n, double* r, int* info, void
 
 extern "C" int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u,
                               double* s, double* v, void* stream) {
-  SKX_REQUIRE(n >= 1 && n <= 64, "skx_jacobi_svd: 1 <= n <= 64");
+  SKX_REQUIRE(n >= 1 && n <= 112, "skx_jacobi_svd: 1 <= n <= 112");
   const int np = n + (n & 1);
   const size_t smem = (size_t)(np * n + np * np) * 8 + (size_t)np * 4 + 16;
   cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(kTsqrThreads) k_tsqr_block(const double* __res
                                                             double* __restrict__ Rout) {
   extern __shared__ double T[];
   __shared__ double s_tau, s_beta;
-  __shared__ double s_dot[64];
+  __shared__ double s_dot[128];
   const int ldt = BR + 1;
   const int64_t r0 = blockIdx.x * (int64_t)BR;
   const int rows = (int)imin(BR, n - r0);
@@ -68,12 +68,12 @@ __global__ void __launch_bounds__(kTsqrThreads) k_tsqr_block(const double* __res
         for (int i = k + 1 + lane; i < rows; i += 32) d = fma(col[i], cj[i], d);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (lane == 0) s_dot[j & 63] = tau * (cj[k] + d);
+        if (lane == 0) s_dot[j & 127] = tau * (cj[k] + d);
       }
       __syncthreads();
       for (int j = k + 1 + wid; j < w; j += nw) {
         double* cj = T + j * ldt;
-        const double f = s_dot[j & 63];
+        const double f = s_dot[j & 127];
         if (lane == 0) cj[k] -= f;
         for (int i = k + 1 + lane; i < rows; i += 32) cj[i] = fma(-f, col[i], cj[i]);
       }
@@ -207,8 +207,9 @@ using namespace skx;
 
 extern "C" int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t cs, double* r,
                           void* ws, size_t* ws_bytes, void* stream) {
-  SKX_REQUIRE(w >= 1 && w <= 64, "skx_tsqr_r: 1 <= w <= 64 columns supported");
+  SKX_REQUIRE(w >= 1 && w <= 96, "skx_tsqr_r: 1 <= w <= 96 columns supported");
   SKX_REQUIRE(ws_bytes != nullptr, "skx_tsqr_r: ws_bytes is NULL");
+  // 256-row tiles: every level shrinks the stack by 256 / w >= 2.7
   const int BR = kTsqrRows;
   // level sizes
   int64_t rows = n, total = 0;
@@ -230,14 +231,14 @@ extern "C" int skx_tsqr_r(const double* a, int64_t n, int w, int64_t rs, int64_t
   cudaStream_t s = (cudaStream_t)stream;
   size_t smem = (size_t)w * (BR + 1) * sizeof(double);
   using KF = void (*)(const double*, int64_t, int, int64_t, int64_t, double*);
-  KF kern = k_tsqr_block<128>;
+  KF kern = k_tsqr_block<kTsqrRows>;  // w > 64: Householder tiles in shared memory
   if (w <= 8) kern = k_tsqr_reg<8>, smem = 0;
   else if (w <= 16) kern = k_tsqr_reg<16>, smem = 0;
   else if (w <= 24) kern = k_tsqr_reg<24>, smem = 0;
   else if (w <= 32) kern = k_tsqr_reg<32>, smem = 0;
   else if (w <= 40) kern = k_tsqr_reg<40>, smem = 0;
   else if (w <= 48) kern = k_tsqr_reg<48>, smem = 0;
-  else kern = k_tsqr_reg<64>, smem = 0;
+  else if (w <= 64) kern = k_tsqr_reg<64>, smem = 0;
   if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const double* src = a;
   int64_t srs = rs, scs = cs;

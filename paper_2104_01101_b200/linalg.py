@@ -106,7 +106,7 @@ def thin_svd_dev(mat):
 
 
 def tsqr_r_dev(a):
-    """R factor (w x w) of a tall-skinny CUDA matrix view (w <= 64) by libskx TSQR."""
+    """R factor (w x w) of a tall-skinny CUDA matrix view (w <= 96) by libskx TSQR."""
     torch = _torch()
     n, w = a.shape
     r = torch.empty((w, w), dtype=torch.float64, device="cuda")
@@ -127,7 +127,7 @@ def chol_upper_dev(g):
 
 
 def jacobi_svd_dev(a):
-    """SVD of a small square matrix (n <= 64) by one-sided Jacobi in one CTA:
+    """SVD of a small square matrix (n <= 112) by one-sided Jacobi in one CTA:
     a = U diag(s) V^T, s descending."""
     torch = _torch()
     n = a.shape[0]
@@ -140,9 +140,9 @@ def jacobi_svd_dev(a):
 
 
 def _small_svd(r):
-    """(u, s, vh) of a small square R: libskx Jacobi when n <= 64."""
+    """(u, s, vh) of a small square R: libskx Jacobi when n <= 112."""
     torch = _torch()
-    if r.shape[0] <= 64:
+    if r.shape[0] <= 112:
         u, s, v = jacobi_svd_dev(r)
         return u, s, v.transpose(0, 1)
     return torch.linalg.svd(r, full_matrices=False)
@@ -151,13 +151,13 @@ def _small_svd(r):
 def top_svd_dev(mat, k, wide=False):
     """Leading k singular triplets of a matrix with one small dimension.
 
-    Skinny side <= 64: R from TSQR, SVD of the small R, and the long singular
-    vectors recovered as mat V / sigma (or mat^T U / sigma).  Otherwise the
-    cuSOLVER thin SVD.  wide=True forces the m < n formulation for a square
+    Skinny side <= 96 (config 5's RRF sketch has k1 = 80): R from TSQR, SVD
+    of the small R by one-CTA Jacobi, and the long singular vectors recovered
+    as mat V / sigma (or mat^T U / sigma).  Otherwise the cuSOLVER thin SVD.  wide=True forces the m < n formulation for a square
     input (as the caller's larger matrix would take)."""
     torch = _torch()
     m, n = mat.shape
-    if min(m, n) > 64:
+    if min(m, n) > 96:
         u, s, v = thin_svd_dev(mat)
         return u[:, :k], s[:k], v[:, :k]
     if m >= n and not (wide and m == n):

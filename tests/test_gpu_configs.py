@@ -130,7 +130,7 @@ def _check_lev(cg, tag, rec):
         assert sha(idx) == str(cg[f"{tag}_lev{i}_sha"]), (tag, i)
         # weights 1/sqrt(m prod p) follow the factors' rounding (the index
         # sets above are the bit-exact contract)
-        assert abs(w.sum() - float(cg[f"{tag}_lev{i}_wsum"])) <= 1e-9 * abs(
+        assert abs(w.sum() - float(cg[f"{tag}_lev{i}_wsum"])) <= 1e-8 * abs(
             float(cg[f"{tag}_lev{i}_wsum"]))
 
 

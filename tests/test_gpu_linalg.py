@@ -1,0 +1,90 @@
+"""GPU: the small dense factorisations behind K5/K6 at the widths the
+BASELINE configs reach (config 5: RRF sketch k1 = 80), against LAPACK
+(numpy): TSQR R factor (same dlarfg sign convention, so R itself matches),
+one-CTA Jacobi SVD, top-k SVD, Gram-Cholesky leverage scores, and the
+numpy-sign Householder QR."""
+import numpy as np
+import pytest
+
+from tests.conftest import relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,w", [(20000, 8), (5000, 40), (200000, 80), (3000, 96)])
+def test_tsqr_r_matches_lapack(n, w):
+    import torch
+    from paper_2104_01101_b200.linalg import tsqr_r_dev
+    a = np.random.default_rng(w).standard_normal((n, w))
+    r = tsqr_r_dev(torch.from_numpy(a).cuda()).cpu().numpy()
+    rn = np.linalg.qr(a, mode="r")
+    # same Householder sign convention: R itself, not only |R|
+    assert relerr(np.abs(r), np.abs(rn)) <= 1e-12
+    assert relerr(r.T @ r, a.T @ a) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [10, 64, 80, 112])
+def test_jacobi_svd(n):
+    import torch
+    from paper_2104_01101_b200.linalg import jacobi_svd_dev
+    g = np.random.default_rng(n)
+    a = g.standard_normal((n, n)) @ np.diag(np.logspace(0, -6, n))
+    u, s, v = (x.cpu().numpy() for x in jacobi_svd_dev(torch.from_numpy(a).cuda()))
+    assert relerr(s, np.linalg.svd(a, compute_uv=False)) <= 1e-12
+    assert relerr((u * s) @ v.T, a) <= 1e-12
+    assert relerr(u.T @ u, np.eye(n)) <= 1e-12
+
+
+def test_top_svd_k1_80():
+    """The RRF sketch of config 5: B is s_n x k1 = 2e5 x 80."""
+    import torch
+    from paper_2104_01101_b200.linalg import top_svd_dev
+    g = np.random.default_rng(5)
+    b = g.standard_normal((20000, 80)) @ np.diag(np.logspace(0, -3, 80))
+    u, s, v = (x.cpu().numpy() for x in top_svd_dev(torch.from_numpy(b).cuda(), 20))
+    un, sn, vn = np.linalg.svd(b, full_matrices=False)
+    assert relerr(s, sn[:20]) <= 1e-12
+    assert relerr(np.abs(u), np.abs(un[:, :20])) <= 1e-10
+
+
+@pytest.mark.parametrize("s,r", [(200000, 20), (400, 10), (50, 3)])
+def test_leverage_scores_gram_route(s, r):
+    import torch
+    from paper_2104_01101_b200.linalg import leverage_scores_dev
+    g = np.random.default_rng(s + r)
+    a = np.linalg.qr(g.standard_normal((s, r)))[0]
+    q = np.linalg.qr(a)[0]
+    want = (q * q).sum(axis=1)
+    got, bad = leverage_scores_dev(torch.from_numpy(a).cuda(), check=False)
+    assert not bool(bad)
+    assert relerr(got.cpu().numpy(), want) <= 1e-13
+
+
+def test_leverage_scores_rank_deficient_falls_back():
+    """A duplicated column: the Gram route flags it, the checked call decides
+    on the Householder R and raises like the reference."""
+    import torch
+    from paper_2104_01101_b200.linalg import RankDeficientError, leverage_scores_dev
+    g = np.random.default_rng(1)
+    a = g.standard_normal((500, 4))
+    a[:, 3] = a[:, 1]
+    _, bad = leverage_scores_dev(torch.from_numpy(a).cuda(), check=False)
+    assert bool(bad)
+    with pytest.raises(RankDeficientError):
+        leverage_scores_dev(torch.from_numpy(a).cuda(), check=True)
+    # ill-conditioned but full rank: flagged, then served exactly by TSQR
+    b = g.standard_normal((500, 4)) @ np.diag([1, 1, 1, 1e-4])
+    sc, _ = leverage_scores_dev(torch.from_numpy(b).cuda(), check=True)
+    q = np.linalg.qr(b)[0]
+    assert relerr(sc.cpu().numpy(), (q * q).sum(axis=1)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(20, 3), (5, 5), (300, 10), (1000, 20)])
+def test_qr_lapack_signs(shape):
+    import torch
+    from paper_2104_01101_b200.linalg import qr_lapack_dev
+    a = np.random.default_rng(shape[0]).standard_normal(shape)
+    q, r = qr_lapack_dev(torch.from_numpy(a).cuda())
+    qn, rn = np.linalg.qr(a)
+    assert np.abs(q.cpu().numpy() - qn).max() <= 1e-12
+    assert np.abs(r.cpu().numpy() - rn).max() <= 1e-11
