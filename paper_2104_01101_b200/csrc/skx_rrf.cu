@@ -243,10 +243,48 @@ __device__ __forceinline__ void to_fixed(double v, int S, uint64_t& hi, uint64_t
   lo = l;
 }
 
+// Row-count bound for the two-limb accumulation: counts of nonzeros per
+// block of 2^CB consecutive rows (per-CTA shared histograms), then the max.
+__global__ void __launch_bounds__(256) k_row_hist_coarse(const int32_t* __restrict__ rows,
+                                                         int64_t nnz, int CB, int nbins,
+                                                         unsigned int* __restrict__ hist) {
+  extern __shared__ unsigned int hsm[];
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) hsm[b] = 0;
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hsm[(uint32_t)__ldcs(rows + e) >> CB], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (hsm[b]) atomicAdd(&hist[b], hsm[b]);
+}
+
+__global__ void k_max_u32(const unsigned int* __restrict__ a, int n, unsigned int* __restrict__ out) {
+  unsigned int m = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = max(m, a[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned int w[32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, w[i]);
+    *out = max(m, w[0]);
+  }
+}
+
+// two-limb form when every cell receives < 2^16 addends (guaranteed when the
+// largest 2^CB-row block holds < 2^16 nonzeros): value = L1 2^48 + L0 with
+// L0 = sum of bits 0-47 (unsigned) and L1 = sum of value >> 48 (signed,
+// |.| < 2^46): 2 reductions per nonzero instead of 3.
+constexpr unsigned int kFxTwoLimbMax = 1u << 16;
+
 template <int NO, int U>
 __global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mode, int64_t nnz,
                                                     const double* __restrict__ vals, int S,
+                                                    const unsigned int* __restrict__ rowmax,
                                                     unsigned long long* __restrict__ acc) {
+  const bool two = *rowmax < kFxTwoLimbMax;
   __shared__ uint32_t cnt[kRrfBuckets + 1];
   uint64_t P = 1;
   int oth[NO];
@@ -288,22 +326,36 @@ __global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mod
       // < 2^94, so bits 94.. are sign copies) summed in 64-bit cells by
       // fire-and-forget reductions (no carries to wait for: < 2^32 addends)
       unsigned long long* cell = acc + 4 * (row * k2 + pk_bucket(t));
-      atomicAdd(cell, (unsigned long long)(lo & 0xffffffffULL));
-      atomicAdd(cell + 1, (unsigned long long)(lo >> 32));
-      atomicAdd(cell + 2, (unsigned long long)(long long)(int32_t)(uint32_t)hi);
+      if (two) {
+        atomicAdd(cell, (unsigned long long)(lo & 0xffffffffffffULL));
+        atomicAdd(cell + 1, (unsigned long long)((hi << 16) | (lo >> 48)));  // value >> 48
+      } else {
+        atomicAdd(cell, (unsigned long long)(lo & 0xffffffffULL));
+        atomicAdd(cell + 1, (unsigned long long)(lo >> 32));
+        atomicAdd(cell + 2, (unsigned long long)(long long)(int32_t)(uint32_t)hi);
+      }
     }
   }
 }
 
 // st1 = double(acc) * 2^-S, correctly rounded
 __global__ void k_fixed_to_double(const unsigned long long* __restrict__ acc, int64_t n, int S,
+                                  const unsigned int* __restrict__ rowmax,
                                   double* __restrict__ out) {
+  const bool two = *rowmax < kFxTwoLimbMax;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    // value = L2 2^64 + L1 2^32 + L0 (L0, L1 unsigned sums, L2 signed)
-    const uint64_t L0 = acc[4 * i], L1 = acc[4 * i + 1], L2 = acc[4 * i + 2];
-    uint64_t lo = L0 + (L1 << 32);
-    uint64_t hi = (L1 >> 32) + (lo < L0 ? 1ULL : 0ULL) + L2;
+    uint64_t lo, hi;
+    if (two) {  // value = L1 2^48 + L0 (L0 unsigned, L1 signed)
+      const uint64_t L0 = acc[4 * i], L1 = acc[4 * i + 1];
+      const uint64_t low = L1 << 48;
+      lo = low + L0;
+      hi = (uint64_t)((int64_t)L1 >> 16) + (lo < low ? 1ULL : 0ULL);
+    } else {  // value = L2 2^64 + L1 2^32 + L0 (L0, L1 unsigned sums, L2 signed)
+      const uint64_t L0 = acc[4 * i], L1 = acc[4 * i + 1], L2 = acc[4 * i + 2];
+      lo = L0 + (L1 << 32);
+      hi = (L1 >> 32) + (lo < L0 ? 1ULL : 0ULL) + L2;
+    }
     const bool neg = (hi >> 63) != 0;
     if (neg) {
       lo = ~lo + 1;
@@ -467,8 +519,17 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
   SKX_REQUIRE(nrej < (int64_t(1) << 32), "skx_rrf_stage1_fx: rejection list too long");
   const int64_t sn = shape_h[mode];
   const int64_t cells = sn * k2;
+  // (grouping the nonzeros by row block first, so the atomics hit an
+  // L2-resident slice of the accumulators, measured no faster: the
+  // reductions are bound by the L2 atomic units, not by HBM)
+  // coarse row histogram: blocks of 2^CB rows, at most 24576 bins (96 KB)
+  int CB = 0;
+  while (((sn + (int64_t(1) << CB) - 1) >> CB) > 24576) ++CB;
+  const int nbins = (int)((sn + (int64_t(1) << CB) - 1) >> CB);
   Arena ar(ws, *ws_bytes);
   unsigned long long* acc = ar.take<unsigned long long>((size_t)cells * 4);
+  unsigned int* hist = ar.take<unsigned int>((size_t)nbins + 1);
+  unsigned int* rowmax = ar.take<unsigned int>(1);
   if (ws == nullptr) {
     *ws_bytes = ar.used + 256;
     return SKX_OK;
@@ -477,6 +538,16 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
   cudaStream_t st = (cudaStream_t)stream;
   const int S = 94 - (emax + 1);
   cudaMemsetAsync(acc, 0, (size_t)cells * 32, st);
+  cudaMemsetAsync(hist, 0, ((size_t)nbins + 1) * sizeof(unsigned int), st);
+  int launches = nnz > 0 ? 2 : 1;
+  {
+    const size_t hs = (size_t)nbins * sizeof(unsigned int);
+    cudaFuncSetAttribute(k_row_hist_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+    if (nnz > 0)
+      k_row_hist_coarse<<<(unsigned)imin((nnz + 255) / 256, (int64_t)num_sms() * 2), 256, hs, st>>>(
+          coords + (int64_t)mode * nnz, nnz, CB, nbins, hist);
+    k_max_u32<<<1, 1024, 0, st>>>(hist, nbins, rowmax);
+  }
   if (nnz > 0) {
     RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
     CooSoA cs{};
@@ -493,10 +564,12 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
     if (per_sm < 1) per_sm = 1;
-    const int64_t blocks = imax(1, imin((nnz + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
-    kern<<<(unsigned)blocks, 256, 0, st>>>(r, cs, mode, nnz, vals, S, acc);
+    const int64_t blocks =
+        imax(1, imin((nnz + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
+    kern<<<(unsigned)blocks, 256, 0, st>>>(r, cs, mode, nnz, vals, S, rowmax, acc);
+    ++launches;
   }
   const unsigned g = (unsigned)imin((cells + 255) / 256, (int64_t)num_sms() * 16);
-  k_fixed_to_double<<<g, 256, 0, st>>>(acc, cells, S, stage1);
-  return check_launch("skx_rrf_stage1_fx", nnz > 0 ? 2 : 1);
+  k_fixed_to_double<<<g, 256, 0, st>>>(acc, cells, S, rowmax, stage1);
+  return check_launch("skx_rrf_stage1_fx", launches + 1);
 }

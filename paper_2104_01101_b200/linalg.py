@@ -161,7 +161,7 @@ def top_svd_dev(mat, k, wide=False):
         u, s, v = thin_svd_dev(mat)
         return u[:, :k], s[:k], v[:, :k]
     if m >= n and not (wide and m == n):
-        r = tsqr_r_dev(mat)
+        r = _tall_r_dev(mat)
         _, s, vh = _small_svd(r)
         v = vh[:k].transpose(0, 1)
         sk = s[:k]
@@ -173,6 +173,37 @@ def top_svd_dev(mat, k, wide=False):
     sk = s[:k]
     v = (mat.transpose(0, 1) @ u) / torch.where(sk > 0, sk, torch.ones_like(sk))
     return u.contiguous(), sk, v
+
+
+# widths above this take the R of a tall matrix from CholeskyQR2 (two Gram
+# passes, one-CTA Choleskys) when that is provably accurate, instead of a TSQR
+# whose Householder tiles serialise over many columns (k1 = 80: ~7 ms vs ~0.5)
+CHOLQR_MIN_W = 65
+
+
+def _tall_r_dev(mat):
+    """R factor of a tall matrix (m >= n <= 96) with R^T R = mat^T mat.
+    n >= CHOLQR_MIN_W: CholeskyQR2 -- R = R2 R1, R1 = chol(A^T A), R2 =
+    chol(Q1^T Q1), Q1 = A R1^-1 -- which is orthogonal to working accuracy
+    when cond(A) < ~1e7; the same safety test as the sketched system's
+    (first Cholesky succeeds and diag(R1) spans < 1e6, else TSQR) decides on
+    the host (the range-finder init syncs per mode anyway).  Else TSQR."""
+    torch = _torch()
+    n = mat.shape[1]
+    if n < CHOLQR_MIN_W:
+        return tsqr_r_dev(mat)
+    g1 = mat.transpose(0, 1) @ mat
+    r1, i1 = chol_upper_dev(g1)
+    d = torch.diagonal(r1).abs()
+    ok = (i1[0] == 0) & (d.min() > 0) & (d.max() < 1e6 * d.min())
+    if not bool(ok.item()):
+        return tsqr_r_dev(mat)
+    eye = torch.eye(n, dtype=mat.dtype, device=mat.device)
+    q1 = mat @ torch.linalg.solve_triangular(r1, eye, upper=True)
+    r2, i2 = chol_upper_dev(q1.transpose(0, 1) @ q1)
+    if int(i2[0].item()) != 0:
+        return tsqr_r_dev(mat)
+    return r2 @ r1
 
 
 def thin_svd(mat):

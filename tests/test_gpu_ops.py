@@ -600,3 +600,29 @@ def test_filter_fibers_matches_sorted_keys(skx, shape, nnz, mode):
     for a, b in zip(got, ref):
         assert torch.equal(a, b)
     assert got[2].numel() > 0
+
+
+@pytest.mark.parametrize("nnz", [50_000, 3_000_000])
+def test_rrf_stage1_fixed_point_paths_agree(skx, nnz):
+    """RRF stage 1 three ways on one tensor: the ordered warp accumulation over
+    a fibre layout, and the exact fixed-point accumulation straight from the
+    COO (row-block bucketed above 2^20 nonzeros, direct below).  The two
+    fixed-point results are exact sums rounded once, so they must agree bit
+    for bit with each other across runs; the ordered float sums agree to
+    rounding."""
+    from paper_2104_01101_b200.sketching import draw_rrf_tables
+    from paper_2104_01101_b200.tensors import device_of
+    from paper_2104_01101_b200.tucker import rrf_stage1_dev
+    shape = (3000, 2000, 1000)
+    c, v = _coo_rand(shape, nnz, 7)
+    st = skx.SparseTensor(shape, c, v)
+    d = device_of(st)
+    for n, k2 in ((1, 157), (2, 480)):
+        P = int(np.prod(shape)) // shape[n]
+        fx1 = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2)).cpu().numpy()
+        fx2 = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2)).cpu().numpy()
+        assert np.array_equal(fx1, fx2)
+        d.fibre(n)  # with a layout the ordered float path runs
+        fl = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2)).cpu().numpy()
+        d.drop_fibre(n)
+        assert relerr(fx1, fl) <= 1e-14
