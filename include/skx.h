@@ -359,6 +359,13 @@ int skx_cp_cross_fibre3(int64_t s0, const int64_t* colptr0, const void* rec0, ui
                         int R, const double* const* factors_h, const double* weights, double* out,
                         void* ws, size_t* ws_bytes, void* stream);
 
+/* Dense mode product with a factor's transpose, the building block of the
+ * dense Tucker fitness (src/tensors.py:217-247, 349-353): for T viewed as
+ * (B, s, P) in C order, out[b, r, p] = sum_i a[i*R + r] T[b, i, p]
+ * (out is B x R x P).  R <= 32. */
+int skx_ttm_lead(const double* t, int64_t B, int64_t s, int64_t P, const double* a, int R,
+                 double* out, void* stream);
+
 /* ------------------------------------------------ K8: CP-ALS on the core */
 
 /* CP-ALS of a dense order-3 core (dims_h = I, J, K; C-order) in one CTA:

@@ -71,6 +71,7 @@ _SIGS = {
     "skx_cp_core_als": [c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "skx_cp_core_smem_bytes": [c_p, c_i32],
     "skx_cp_cross_fibre3": [c_i64, c_p, c_p, c_u32, c_i32, c_p, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_ttm_lead": [c_p, c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],

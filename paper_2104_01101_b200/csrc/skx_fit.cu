@@ -1067,3 +1067,68 @@ extern "C" int skx_ttmc3_skip_coo(int64_t s_n, const int64_t* colptr, const void
 #undef SKX_TT
   return check_launch("k_ttmc3_skip");
 }
+
+// ---- dense TTM chain for the Tucker fitness of a dense tensor -------------
+// out[b, r, p] = sum_i A[i, r] T[b, i, p] for T viewed as (B, s, P) in C
+// order: the mode-n product with A^T of a tensor whose modes before n are
+// folded into B and after n into P (src/tensors.py:217-247, ttmc with every
+// mode, as the fitness needs: src/tensors.py:349-353).  Applied mode after
+// mode, the first pass streams the whole tensor once (HBM-bound: R FMAs per
+// 8-byte element on the FP64 pipe) and the later ones touch tensors smaller
+// by R_n / s_n.  Thread per output column p; A's rows are staged through
+// shared memory in tiles of 64; the R accumulators live in registers.
+namespace skx {
+template <int RT>
+__global__ void __launch_bounds__(256) k_ttm_lead(const double* __restrict__ T, int64_t B, int64_t s,
+                                                  int64_t P, const double* __restrict__ A, int R,
+                                                  double* __restrict__ out) {
+  __shared__ double At[64 * RT];
+  const int64_t nblk_p = (P + blockDim.x - 1) / blockDim.x;
+  for (int64_t blk = blockIdx.x; blk < B * nblk_p; blk += gridDim.x) {
+    const int64_t b = blk / nblk_p;
+    const int64_t p = (blk - b * nblk_p) * blockDim.x + threadIdx.x;
+    double acc[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) acc[r] = 0.0;
+    const double* tb = T + b * s * P;
+    for (int64_t i0 = 0; i0 < s; i0 += 64) {
+      const int ni = (int)imin(64, s - i0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < ni * RT; e += blockDim.x) {
+        const int ii = e / RT, r = e - ii * RT;
+        At[e] = r < R ? A[(i0 + ii) * R + r] : 0.0;
+      }
+      __syncthreads();
+      if (p < P) {
+        for (int ii = 0; ii < ni; ++ii) {
+          const double x = __ldcs(tb + (i0 + ii) * P + p);
+#pragma unroll
+          for (int r = 0; r < RT; ++r) acc[r] = fma(At[ii * RT + r], x, acc[r]);
+        }
+      }
+    }
+    if (p < P) {
+      double* ob = out + b * (int64_t)R * P + p;
+      for (int r = 0; r < R; ++r) ob[(int64_t)r * P] = acc[r < RT ? r : 0];
+    }
+  }
+}
+}  // namespace skx
+
+extern "C" int skx_ttm_lead(const double* t, int64_t B, int64_t s, int64_t P, const double* a,
+                            int R, double* out, void* stream) {
+  SKX_REQUIRE(R >= 1 && R <= 32, "skx_ttm_lead: 1 <= R <= 32");
+  SKX_REQUIRE(B >= 1 && s >= 1 && P >= 1, "skx_ttm_lead: empty operand");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t work = B * ((P + 255) / 256);
+  const unsigned g = (unsigned)imin(work, (int64_t)num_sms() * 8);
+#define SKX_TL(rt) k_ttm_lead<rt><<<g, 256, 0, st>>>(t, B, s, P, a, R, out)
+  if (R <= 4) SKX_TL(4);
+  else if (R <= 8) SKX_TL(8);
+  else if (R <= 12) SKX_TL(12);
+  else if (R <= 16) SKX_TL(16);
+  else if (R <= 24) SKX_TL(24);
+  else SKX_TL(32);
+#undef SKX_TL
+  return check_launch("k_ttm_lead");
+}

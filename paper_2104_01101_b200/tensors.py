@@ -559,11 +559,7 @@ def ttmc_dev(d, factors, skip=None):
     torch = _torch()
     nd = d.ndim
     if not is_sparse_dev(d):
-        out = d
-        for k in range(nd):
-            if k != skip:
-                out = ttm_dev(out, factors[k].t(), k)
-        return out
+        return ttmc_all_dense_dev(d, factors, skip)
     if skip is not None:
         y = _ttmc_skip_sparse_dev(d, factors, skip)
         shp = [d.shape[k] if k == skip else factors[k].shape[1] for k in range(nd)]
@@ -622,10 +618,34 @@ def tucker_cross_dev(d, core, factors):
                      nat.ptr(core.contiguous()), nat.ptr(cpt), nat.ptr(rec0),
                      ctypes.c_uint32(d.fibre_mask(0)), nat.ptr(out)), slot=5)
         return out[0]
-    proj = d
-    for k, a in enumerate(factors):
-        proj = ttm_dev(proj, a.t(), k)
-    return (proj * core).sum()
+    return (ttmc_all_dense_dev(d, factors) * core).sum()
+
+
+def ttmc_all_dense_dev(d, factors, skip=None):
+    """ttmc(T, factors, skip) of a dense C-order CUDA tensor by libskx mode
+    products in ascending mode order (skx_ttm_lead; the first streams the
+    tensor once).  Ranks > 32 use torch tensordot."""
+    torch = _torch()
+    modes = [k for k in range(len(factors)) if k != skip]
+    if any(int(factors[k].shape[1]) > 32 for k in modes):
+        proj = d
+        for k in modes:
+            proj = ttm_dev(proj, factors[k].t(), k)
+        return proj
+    cur = d.contiguous()
+    shape = list(cur.shape)
+    for k in modes:
+        a = factors[k]
+        B = int(np.prod(shape[:k])) if k else 1
+        s = shape[k]
+        P = int(np.prod(shape[k + 1:])) if k + 1 < len(shape) else 1
+        R = int(a.shape[1])
+        out = torch.empty(B * R * P, dtype=torch.float64, device="cuda")
+        nat.call("skx_ttm_lead", nat.ptr(cur), B, s, P, nat.ptr(a.contiguous()), R, nat.ptr(out),
+                 nat.stream())
+        shape[k] = R
+        cur = out.view(shape)
+    return cur
 
 
 def fitness_tucker_dev(d, core, factors, norm2=None, comm=None):
