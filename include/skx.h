@@ -146,6 +146,18 @@ int skx_ts_kron_apply(int n_other, const int64_t* ext_h, const int64_t* ranks_h,
 
 /* ------------------------------------------------------ K3: leverage */
 
+/* Leverage gather of an order-3 COO tensor for a mode-1 or mode-2
+ * sub-problem straight from its mode-0 fibre layout (skx_coo_fibre mode 0;
+ * c1_mask as skx_ts_rhs_coo): sample j's fibre (idx[2j] = i0, idx[2j+1] =
+ * the other index) lies in slice i0.  Call twice: with hit_col == NULL to
+ * write hit_off (m + 1 offsets, hit_off[m] = total), then with outputs of
+ * `cap` entries: per sample, ascending column, value scaled by w[j].
+ * Replaces _fetch_rows on the CSR of T_(n)^T (src/sketching.py:262-267). */
+int skx_slice_hits(int mode, int64_t s0, const int64_t* colptr0, const void* rec0,
+                   uint32_t c1_mask, const int64_t* idx, const double* w, int64_t m,
+                   int64_t* hit_off, int64_t* hit_col, double* hit_val, int64_t cap, void* ws,
+                   size_t* ws_bytes, void* stream);
+
 /* p = max(scores,0)/sum, cdf = cumsum(p)/cdf[-1] (src/sketching.py:207-210 and
  * numpy Generator.choice).  */
 int skx_lev_prepare(const double* scores, int64_t s, double* p, double* cdf, void* ws,
@@ -365,6 +377,19 @@ int skx_cp_cross_fibre3(int64_t s0, const int64_t* colptr0, const void* rec0, ui
  * (out is B x R x P).  R <= 32. */
 int skx_ttm_lead(const double* t, int64_t B, int64_t s, int64_t P, const double* a, int R,
                  double* out, void* stream);
+
+/* K5: the passes over the sketched right-hand side Y in rsvd_lrls
+ * (src/linalg.py:103-112, associated form: Y G and W^T Y with w <= 32
+ * columns), on FP64 tensor cores.  Row-major operands with leading
+ * dimensions; N <= 32.
+ *   skx_gemm_ab:  C (M x N) = A (M x K) B (K x N), A streamed by rows;
+ *   skx_gemm_atb: C (M x N) = A^T B with A (K x M), B (K x N): split-K over
+ *                 CTAs, partials summed in a fixed order (workspace query
+ *                 with ws = NULL).  Deterministic. */
+int skx_gemm_ab(int64_t M, int N, int64_t K, const double* A, int64_t lda, const double* B,
+                int64_t ldb, double* C, int64_t ldc, void* stream);
+int skx_gemm_atb(int64_t M, int N, int64_t K, const double* A, int64_t lda, const double* B,
+                 int64_t ldb, double* C, int64_t ldc, void* ws, size_t* ws_bytes, void* stream);
 
 /* ------------------------------------------------ K8: CP-ALS on the core */
 

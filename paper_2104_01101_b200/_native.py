@@ -41,6 +41,8 @@ _SIGS = {
     "skx_ts_kron_apply": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_lev_prepare": [c_p, c_i64, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_lev_scores": [c_p, c_i64, c_i32, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_slice_hits": [c_i32, c_i64, c_p, c_p, c_u32, c_p, c_p, c_i64, c_p, c_p, c_p, c_i64, c_p,
+                       c_sz_p, c_p],
     "skx_lev_sample": [c_i32, c_p, c_p, c_p, c_i64, c_u64, c_u64, c_u64, c_p, c_p, c_p],
     "skx_top_m_products": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_kron_rows": [c_i32, c_p, c_p, c_p, c_p, c_i64, c_p, c_p],
@@ -72,6 +74,8 @@ _SIGS = {
     "skx_cp_core_smem_bytes": [c_p, c_i32],
     "skx_cp_cross_fibre3": [c_i64, c_p, c_p, c_u32, c_i32, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_ttm_lead": [c_p, c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p],
+    "skx_gemm_ab": [c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p],
+    "skx_gemm_atb": [c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_sz_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],

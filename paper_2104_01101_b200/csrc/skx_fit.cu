@@ -1,6 +1,8 @@
 // K5 residual and K7 fitness passes (src/tucker.py:274; src/tensors.py:
 // 339-368).  All reductions use a fixed grid and a fixed combination order,
 // so results are bitwise reproducible.
+#include <stdlib.h>
+
 #include "skx_common.cuh"
 
 namespace skx {
@@ -491,7 +493,10 @@ struct T3A {
   static constexpr int RPI = 32 / LPR;                  // rows per copy instruction
 };
 
-template <int R, int NB, int MB>
+// D = row lookahead (batches): rows of batch b+D and records of batch b+D+2
+// are in flight while batch b is contracted (D+1 row buffers, D+3 record
+// buffers per warp).
+template <int R, int NB, int MB, int D>
 __global__ void __launch_bounds__(256, MB) k_tucker3_async(
     const int64_t* __restrict__ colptr, int64_t s0, const double* __restrict__ rec, uint32_t c1_mask,
     const double* __restrict__ A0, const double* __restrict__ A1, const double* __restrict__ A2,
@@ -500,11 +505,12 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
   constexpr int NROWS = 2 * NB;
   constexpr int NINSTR = (NROWS + P::RPI - 1) / P::RPI;
   constexpr int ROWBUF = NROWS * P::ST;  // doubles per row buffer
+  constexpr int NRB = D + 1, NRC = D + 3;
   extern __shared__ __align__(16) double t3sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane >> 2, c = lane & 3;
-  double* rows = t3sm + (size_t)wid * (2 * ROWBUF + 3 * NB * 2);
-  double* recs = rows + 2 * ROWBUF;  // 3 buffers x NB records of 2 doubles
-  for (int e = lane; e < 2 * ROWBUF; e += 32) rows[e] = 0.0;  // zero padding beyond R
+  double* rows = t3sm + (size_t)wid * (NRB * ROWBUF + NRC * NB * 2);
+  double* recs = rows + NRB * ROWBUF;  // NRC buffers x NB records of 2 doubles
+  for (int e = lane; e < NRB * ROWBUF; e += 32) rows[e] = 0.0;  // zero padding beyond R
   __syncwarp();
   const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
   const int cr = lane / P::LPR, ch = lane % P::LPR;  // copy role: row in instruction, chunk
@@ -526,13 +532,13 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
     auto issue_recs = [&](int64_t b) {
       if (lane < NB) {
         const int64_t e = e0 + b * NB + lane;
-        cp_async16_cg_zfill(smem_addr(recs + ((b % 3) * NB + lane) * 2), rec + 2 * (e < e1 ? e : e0),
-                            e < e1 ? 16u : 0u);
+        cp_async16_cg_zfill(smem_addr(recs + ((b % NRC) * NB + lane) * 2),
+                            rec + 2 * (e < e1 ? e : e0), e < e1 ? 16u : 0u);
       }
     };
     auto issue_rows = [&](int64_t b) {
-      const double* rb = recs + (b % 3) * NB * 2;
-      double* dst = rows + (b & 1) * ROWBUF;
+      const double* rb = recs + (b % NRC) * NB * 2;
+      double* dst = rows + (b % NRB) * ROWBUF;
 #pragma unroll
       for (int t = 0; t < NINSTR; ++t) {
         const int r = t * P::RPI + cr;
@@ -560,23 +566,25 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
             w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + n), w);
         b[ks][nt] = w;
       }
-    issue_recs(0);
+    // prologue: records of batches 0..D+1, then rows of batches 0..D-1
+    for (int64_t b2 = 0; b2 < D + 2 && b2 < nb; ++b2) issue_recs(b2);
     cp_async_commit();
-    if (nb > 1) issue_recs(1);
-    cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<0>();
     __syncwarp();
-    issue_rows(0);
+    for (int64_t b2 = 0; b2 < D && b2 < nb; ++b2) issue_rows(b2);
     cp_async_commit();
     double acc = 0.0;
     for (int64_t bi = 0; bi < nb; ++bi) {
-      cp_async_wait<0>();
+      // rows(bi) and records(bi + D) were committed >= 2 groups ago (the
+      // prologue group at bi = 0): only the newest group may stay in flight
+      if (bi == 0) cp_async_wait<0>();
+      else cp_async_wait<1>();
       __syncwarp();
-      if (bi + 1 < nb) issue_rows(bi + 1);
-      if (bi + 2 < nb) issue_recs(bi + 2);
+      if (bi + D < nb) issue_rows(bi + D);
+      if (bi + D + 2 < nb) issue_recs(bi + D + 2);
       cp_async_commit();
-      const double* rw = rows + (bi & 1) * ROWBUF;
-      const double* rv = recs + (bi % 3) * NB * 2;
+      const double* rw = rows + (bi % NRB) * ROWBUF;
+      const double* rv = recs + (bi % NRC) * NB * 2;
 #pragma unroll
       for (int g = 0; g < NB / 8; ++g) {
         const double* ra = rw + (g * 8 + q) * P::ST;
@@ -611,9 +619,9 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
   }
 }
 
-template <int R, int NB>
+template <int R, int NB, int D>
 constexpr size_t t3a_smem_bytes() {
-  return (size_t)8 * (2 * 2 * NB * T3A<R>::ST + 3 * NB * 2) * 8;
+  return (size_t)8 * ((D + 1) * 2 * NB * T3A<R>::ST + (D + 3) * NB * 2) * 8;
 }
 
 // Skip-mode sparse TTMc for order 3 (src/tensors.py:261-277): row i_n of the
@@ -942,16 +950,24 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
       // alone, 9.9 vs 11.9 ms per 2e8: its 128 registers per thread crowd out
       // the sweeps' kernels).  Other even ranks: register pipeline with 16-byte
       // A-fragment loads (config 4: 4.0 ms per pass in the pipeline).
-#define SKX_T3A(RR, NB, MBB)                                                                    \
+#define SKX_T3A(RR, NB, MBB, DD)                                                                \
   do {                                                                                          \
-    const size_t sm = t3a_smem_bytes<RR, NB>();                                                 \
-    cudaFuncSetAttribute(k_tucker3_async<RR, NB, MBB>,                                          \
+    const size_t sm = t3a_smem_bytes<RR, NB, DD>();                                             \
+    cudaFuncSetAttribute(k_tucker3_async<RR, NB, MBB, DD>,                                      \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                 \
-    k_tucker3_async<RR, NB, MBB><<<mb, 256, sm, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, core, \
-                                                     R0, part);                                 \
+    k_tucker3_async<RR, NB, MBB, DD><<<mb, 256, sm, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, \
+                                                         core, R0, part);                       \
   } while (0)
-      if (R1 == 20 && R2 == 20) {
-        SKX_T3A(20, 16, 2);
+      static const int t3v = [] {
+        const char* e = getenv("SKX_T3_VARIANT");
+        return e ? atoi(e) : 0;
+      }();
+      if (R1 == 20 && R2 == 20 && t3v == 1) {
+        SKX_T3A(20, 8, 2, 2);
+      } else if (R1 == 20 && R2 == 20 && t3v == 2) {
+        SKX_T3A(20, 16, 1, 2);
+      } else if (R1 == 20 && R2 == 20) {
+        SKX_T3A(20, 16, 2, 1);
       } else if (R1 == 10 && R2 == 10) {
         k_tucker3_mma<3, 2, 2, 10, 10, 2, true><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1,
                                                                    A2, core, R0, R1, R2, part);

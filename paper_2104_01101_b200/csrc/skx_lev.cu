@@ -263,6 +263,77 @@ __global__ void __launch_bounds__(256) k_filter_fibers(int ndim, int mode, Coord
   }
 }
 
+// ---- sampled fibres of an order-3 tensor from its mode-0 fibre layout ----
+// Modes 1 and 2 of a leverage sub-problem sample fibres (i0, i_b): every
+// hit lies in slice i0 of the mode-0 layout (records {i1, i2 | sketch bits,
+// v} sorted by (i1, i2)).  Mode 2 (fibre (i0, i1)): the hits are the
+// records of slice i0 with c1 == i1, a contiguous run found by binary
+// search.  Mode 1 (fibre (i0, i2)): a warp scans the slice (~nnz/s0 records)
+// for c2 == i2.  Hits come out per sample in ascending column order, as the
+// key-sorted gather gives them.  Replaces the full pass over the coordinates
+// (12 B/nnz per sub-problem) for these modes.
+template <bool WRITE>
+__global__ void __launch_bounds__(256) k_slice_hits(int mode, const int64_t* __restrict__ colptr0,
+                                                    const int4* __restrict__ rec0, uint32_t c1_mask,
+                                                    const int64_t* __restrict__ idx,
+                                                    const double* __restrict__ w, int64_t m,
+                                                    int64_t* __restrict__ cnt,
+                                                    const int64_t* __restrict__ off,
+                                                    int64_t* __restrict__ hit_col,
+                                                    double* __restrict__ hit_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (j >= m) return;
+  const int64_t i0 = idx[2 * j];
+  const int32_t tgt = (int32_t)idx[2 * j + 1];
+  int64_t a = colptr0[i0], b = colptr0[i0 + 1];
+  const double wj = WRITE ? w[j] : 0.0;
+  int64_t o = WRITE ? off[j] : 0;
+  if (mode == 2) {
+    // run of records with c1 == tgt (c1 = record.x, sorted ascending)
+    int64_t lo = a, hi = b;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(&rec0[mid].x) < tgt) lo = mid + 1; else hi = mid;
+    }
+    int64_t lo2 = lo;
+    hi = b;
+    while (lo2 < hi) {
+      const int64_t mid = (lo2 + hi) >> 1;
+      if (__ldg(&rec0[mid].x) <= tgt) lo2 = mid + 1; else hi = mid;
+    }
+    if (!WRITE) {
+      if (lane == 0) cnt[j] = lo2 - lo;
+      return;
+    }
+    for (int64_t e = lo + lane; e < lo2; e += 32) {
+      const int4 r = __ldg(&rec0[e]);
+      hit_col[o + (e - lo)] = (int64_t)((uint32_t)r.y & c1_mask);
+      hit_val[o + (e - lo)] = wj * __hiloint2double(r.w, r.z);
+    }
+    return;
+  }
+  // mode 1: scan the slice for c2 == tgt
+  int64_t found = 0;
+  for (int64_t base = a; base < b; base += 32) {
+    const int64_t e = base + lane;
+    int4 r = make_int4(0, -1, 0, 0);
+    bool hit = false;
+    if (e < b) {
+      r = __ldg(&rec0[e]);
+      hit = (int32_t)((uint32_t)r.y & c1_mask) == tgt;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (WRITE && hit) {
+      const int64_t at = o + found + __popc(bal & ((1u << lane) - 1u));
+      hit_col[at] = (int64_t)r.x;
+      hit_val[at] = wj * __hiloint2double(r.w, r.z);
+    }
+    found += __popc(bal);
+  }
+  if (!WRITE && lane == 0) cnt[j] = found;
+}
+
 }  // namespace skx
 
 using namespace skx;
@@ -393,4 +464,37 @@ extern "C" int skx_gather_fibers_coo(int n_other, const int64_t* ext_h, int64_t 
   k_gather_coo_write<<<g, 256, 0, s>>>(keys, vals, s_n, lo, cnt, hit_off, w, m, cap, hit_col,
                                        hit_val);
   return check_launch("gather_fibers_coo", 3);
+}
+
+extern "C" int skx_slice_hits(int mode, int64_t s0, const int64_t* colptr0, const void* rec0,
+                              uint32_t c1_mask, const int64_t* idx, const double* w, int64_t m,
+                              int64_t* hit_off, int64_t* hit_col, double* hit_val, int64_t cap,
+                              void* ws, size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(mode == 1 || mode == 2, "skx_slice_hits: mode 1 or 2 of an order-3 tensor");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_slice_hits: ws_bytes is NULL");
+  (void)s0;
+  Arena ar(ws, *ws_bytes);
+  int64_t* cnt = ar.take<int64_t>(m + 1);
+  size_t cb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cb, cnt, hit_off, (int)(m + 1));
+  void* tmp = ar.take<char>(cb);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_slice_hits: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned g = (unsigned)((m * 32 + 255) / 256);
+  const int4* r = (const int4*)rec0;
+  if (hit_col == nullptr) {  // count pass: hit_off[m] = total
+    cudaMemsetAsync(cnt + m, 0, sizeof(int64_t), st);
+    k_slice_hits<false><<<g, 256, 0, st>>>(mode, colptr0, r, c1_mask, idx, w, m, cnt, nullptr,
+                                           nullptr, nullptr);
+    cub::DeviceScan::ExclusiveSum(tmp, cb, cnt, hit_off, (int)(m + 1), st);
+    return check_launch("k_slice_hits(count)", 2);
+  }
+  SKX_REQUIRE(cap >= 0, "skx_slice_hits: negative capacity");
+  k_slice_hits<true><<<g, 256, 0, st>>>(mode, colptr0, r, c1_mask, idx, w, m, nullptr, hit_off,
+                                        hit_col, hit_val);
+  return check_launch("k_slice_hits(write)");
 }

@@ -46,6 +46,18 @@ class Comm:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self._sibling = None
+
+    def sibling(self):
+        """A second communicator over the same ranks (created once, by every
+        rank at the same point of the program) for collectives issued from
+        another CUDA stream -- the per-sweep fitness all-reduce runs beside the
+        next sweep's collectives, and operations of one NCCL communicator must
+        not run concurrently on two streams."""
+        if self._sibling is None:
+            self._sibling = Comm(self.dist.new_group(ranks=list(range(self.world)))) \
+                if self.world > 1 else self
+        return self._sibling
 
     def allreduce(self, t):
         if self.world > 1:

@@ -376,6 +376,55 @@ class NormalSource:
 
 
 # ------------------------------------------------------------------ rsvd_lrls
+def _row_major(t):
+    """(tensor, leading dim) of a 2-D view whose rows are contiguous."""
+    if t.stride(1) == 1 and t.stride(0) >= t.shape[1]:
+        return t, int(t.stride(0))
+    t = t.contiguous()
+    return t, int(t.shape[1])
+
+
+def y_times_dev(y, g):
+    """Y G (m x w) for the m x s right-hand side Y -- stored row-major or as
+    the transpose of a row-major s x m Y^T -- and a narrow s x w G (w <= 32):
+    libskx FP64 tensor-core streaming kernels (skx_gemm_ab / skx_gemm_atb)."""
+    torch = _torch()
+    m, s = y.shape
+    w = int(g.shape[1])
+    if w > 32:
+        return y @ g
+    gm, ldg = _row_major(g)
+    out = torch.empty((m, w), dtype=torch.float64, device="cuda")
+    if y.stride(0) == 1 and y.stride(1) >= m:  # Y^T storage: Y G = (Y^T)^T G
+        nat.call_ws("skx_gemm_atb", (m, w, s, nat.ptr(y), int(y.stride(1)), nat.ptr(gm), ldg,
+                                     nat.ptr(out), w), slot=10)
+    else:
+        ym, ldy = _row_major(y)
+        nat.call("skx_gemm_ab", m, w, s, nat.ptr(ym), ldy, nat.ptr(gm), ldg, nat.ptr(out), w,
+                 nat.stream())
+    return out
+
+
+def ty_times_dev(wm, y):
+    """W^T Y (w x s) for the m x s right-hand side Y (either storage) and a
+    narrow m x w W, returned as the transpose of a contiguous s x w array."""
+    torch = _torch()
+    m, s = y.shape
+    w = int(wm.shape[1])
+    if w > 32:
+        return wm.transpose(0, 1) @ y
+    wmm, ldw = _row_major(wm)
+    out = torch.empty((s, w), dtype=torch.float64, device="cuda")  # (W^T Y)^T = Y^T W
+    if y.stride(0) == 1 and y.stride(1) >= m:  # Y^T row-major s x m: Y^T W streams its rows
+        nat.call("skx_gemm_ab", s, w, m, nat.ptr(y), int(y.stride(1)), nat.ptr(wmm), ldw,
+                 nat.ptr(out), w, nat.stream())
+    else:
+        ym, ldy = _row_major(y)
+        nat.call_ws("skx_gemm_atb", (s, w, m, nat.ptr(ym), ldy, nat.ptr(wmm), ldw, nat.ptr(out), w),
+                    slot=10)
+    return out.transpose(0, 1)
+
+
 def resid_dev(z, core_t, a, y):
     """|| Z core_t a^T - Y ||_F as a device scalar (src/tucker.py:274); one
     fused pass over Y in its storage order."""
@@ -512,8 +561,8 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None, pr
         # Same algebra, associated so that Y (m x s, the big operand) only meets
         # width-column matrices: X_ls G = R^-1 Q_z^T (Y G) and
         # Q^T X_ls = (Q_z R^-T Q)^T Y.  2.5x fewer flops at configs 2/4/5.
-        q, wm = assoc_mid_dev(qz, rz, y @ g if yg is None else yg)
-        d = wm.transpose(0, 1) @ y
+        q, wm = assoc_mid_dev(qz, rz, y_times_dev(y, g) if yg is None else yg)
+        d = ty_times_dev(wm, y)
     else:
         x = torch.linalg.solve_triangular(rz, qz.transpose(0, 1) @ y, upper=True)
         q, _ = torch.linalg.qr(x @ g, mode="reduced")
@@ -523,7 +572,8 @@ def rsvd_lrls_dev(z, y, rank, normals, oversample=10, check=True, defer=None, pr
     return core_t, v.contiguous(), bad
 
 
-def rsvd_lrls_rows_dev(z, yt_loc, row_lo, s, rank, normals, comm, oversample=10, check=True):
+def rsvd_lrls_rows_dev(z, yt_loc, row_lo, s, rank, normals, comm, oversample=10, check=True,
+                       defer=None):
     """rsvd_lrls_dev + residual with the right-hand side split by columns over
     ranks: this rank holds Y^T rows [row_lo, row_lo + rows) as
     yt_loc.  Column-separable steps run on the local block -- Y G (all-reduced,
@@ -537,8 +587,8 @@ def rsvd_lrls_rows_dev(z, yt_loc, row_lo, s, rank, normals, comm, oversample=10,
         raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
     if rank > min(r, s):
         raise ValueError(f"rank {rank} exceeds min({r}, {s})")
-    qz, rz, bad = sketch_qr_dev(z)
-    if check and bool(bad.item()):
+    qz, rz, bad = sketch_qr_dev(z, defer)
+    if check and defer is None and bool(bad.item()):
         raise RankDeficientError("rank-deficient sketched system")
     width = min(rank + oversample, s)
     g = normals.normal((s, width))  # the whole stream is drawn on every rank

@@ -466,6 +466,25 @@ def gather_coo_dev(keys, vals, ext_others, s_n, idx, w):
     return hit_off, hit_col[:total], hit_val[:total]
 
 
+def gather_slices_dev(d, n, idx, w):
+    """(hit_off, hit_col, hit_val) of the sampled mode-n fibres of an order-3
+    DeviceCoo, n in (1, 2), from slices of its mode-0 layout (skx_slice_hits):
+    same result as filter_fibers_dev + gather_coo_dev without a pass over
+    every nonzero."""
+    torch = _torch()
+    colptr, rec = d.fibre(0)
+    m = idx.shape[0]
+    hit_off = torch.empty(m + 1, dtype=torch.int64, device="cuda")
+    args = (n, d.shape[0], nat.ptr(colptr), nat.ptr(rec), ctypes.c_uint32(d.fibre_mask(0)),
+            nat.ptr(idx.contiguous()), nat.ptr(w), m, nat.ptr(hit_off))
+    nat.call_ws("skx_slice_hits", args + (None, None, 0), slot=9)
+    total = int(hit_off[m].item())
+    hit_col = torch.empty(max(total, 1), dtype=torch.int64, device="cuda")
+    hit_val = torch.empty(max(total, 1), dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_slice_hits", args + (nat.ptr(hit_col), nat.ptr(hit_val), total), slot=9)
+    return hit_off, hit_col[:total], hit_val[:total]
+
+
 FILTER_CAP0 = 1 << 16
 
 

@@ -20,13 +20,13 @@ import numpy as np
 from . import _native as nat
 from . import rng as rngmod
 from .linalg import (NormalSource, RankDeficientError, qr_lapack_dev, resid_dev, rsvd_lrls_dev,
-                     rsvd_lrls_hits_dev,
+                     rsvd_lrls_hits_dev, y_times_dev,
                      rsvd_lrls_rows_dev, top_svd_dev)
 from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, finish_rrf_scan,
-                        gather_coo_dev, gather_dense_dev, hits_to_dense, kron_rows_dev, lev_det_dev,
-                        lev_sample_dev, mode_last_dev,
-                        plan_rrf_scans, rrf_table_dev, ts_kron_dev, ts_kron_plan_dev,
-                        ts_rhs_dense_dev, ts_rhs_mode_dev)
+                        gather_coo_dev, gather_dense_dev, gather_slices_dev, hits_to_dense,
+                        kron_rows_dev, lev_det_dev, lev_sample_dev, mode_last_dev, plan_rrf_scans,
+                        rrf_table_dev, ts_kron_dev, ts_kron_plan_dev, ts_rhs_dense_dev,
+                        ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
                       matricize, shape_of, ttm_dev, ttmc_dev)
 
@@ -389,7 +389,8 @@ class _Run:
                 s_n = self.shape[n]
                 lo, _ = self.comm.row_slab(s_n)
                 core_t, a_loc, _, res = rsvd_lrls_rows_dev(z, self.ts_rhs[n], lo, s_n,
-                                                           self.ranks[n], self.normals, self.comm)
+                                                           self.ranks[n], self.normals, self.comm,
+                                                           defer=defer)
                 return core_t, self.comm.allgather_rows(a_loc.contiguous(), s_n), res
             y = self.ts_rhs[n].t()
             return self._finish_dense(z, y, n, defer, pre)
@@ -404,9 +405,13 @@ class _Run:
                                 lev_sample_dev(others, self.m, self.rng_sketch))
             z = kron_rows_dev(others, idx, w)
             if self.sparse:
-                keys, vals = filter_fibers_dev(self.d, n, idx)
-                ext = [self.shape[k] for k in self.others(n)]
-                off, col, val = gather_coo_dev(keys, vals, ext, self.shape[n], idx, w)
+                if self.ndim == 3 and n >= 1:
+                    # the sampled fibres lie in slices of the mode-0 layout
+                    off, col, val = gather_slices_dev(self.d, n, idx, w)
+                else:
+                    keys, vals = filter_fibers_dev(self.d, n, idx)
+                    ext = [self.shape[k] for k in self.others(n)]
+                    off, col, val = gather_coo_dev(keys, vals, ext, self.shape[n], idx, w)
                 row = None
                 total = col.numel()
                 if self.comm is not None:
@@ -453,7 +458,7 @@ class _Run:
         cur = torch.cuda.current_stream()
         side.wait_stream(cur)
         with torch.cuda.stream(side):
-            yg = self.ts_rhs[n].t() @ g
+            yg = y_times_dev(self.ts_rhs[n].t(), g)
             ev = torch.cuda.Event()
             ev.record(side)
         g.record_stream(side)
@@ -490,13 +495,14 @@ class _Run:
         # needs its value first (or collectives would interleave across streams):
         # the sub-problems run on the high-priority stream, the fitness on a
         # low-priority one, so the block scheduler serves the solves first
-        overlap = self.cfg.convergence_tol <= 0 and self.comm is None and self.sparse
+        overlap = self.cfg.convergence_tol <= 0 and self.sparse
+        fit_comm = self.comm.sibling() if (self.comm is not None and overlap) else self.comm
         fs = _fit_stream() if overlap else None
         caller = torch.cuda.current_stream()
         hi = _init_streams()[1] if overlap else caller
         hi.wait_stream(caller)
         with torch.cuda.stream(hi):
-            core = self._sweep_loop(trace, res_dev, fit_dev, ev, fs, overlap)
+            core = self._sweep_loop(trace, res_dev, fit_dev, ev, fs, overlap, fit_comm)
         caller.wait_stream(hi)
 
         def finish():
@@ -513,7 +519,7 @@ class _Run:
         # the last fitness pass may still be running on its own stream
         return core, finish
 
-    def _sweep_loop(self, trace, res_dev, fit_dev, ev, fs, overlap):
+    def _sweep_loop(self, trace, res_dev, fit_dev, ev, fs, overlap, fit_comm=None):
         torch = _torch()
         core = None
         # TensorSketch sweeps run speculatively: every sub-problem takes the
@@ -525,7 +531,9 @@ class _Run:
         # state on the checked path (second QR pass / Householder /
         # rank-deficiency redraw) and everything enqueued after it is
         # discarded, so the results are those of the checked path either way.
-        speculate = self.comm is None
+        # multi-rank too: every flag is a function of replicated data (Z, the
+        # factors), so all ranks take the same replay decisions
+        speculate = True
         pipeline = speculate and self.cfg.convergence_tol <= 0
         nsw = self.cfg.max_sweeps
         pending = None  # (sweep, start state, host flag, event) awaiting its check
@@ -585,7 +593,7 @@ class _Run:
                 # factors that are replaced (not overwritten) by later solves
                 fs.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(fs):
-                    f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, self.comm)
+                    f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, fit_comm)
                 for t in [core] + list(self.factors):
                     t.record_stream(fs)
             else:

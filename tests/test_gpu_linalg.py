@@ -88,3 +88,21 @@ def test_qr_lapack_signs(shape):
     qn, rn = np.linalg.qr(a)
     assert np.abs(q.cpu().numpy() - qn).max() <= 1e-12
     assert np.abs(r.cpu().numpy() - rn).max() <= 1e-11
+
+
+@pytest.mark.parametrize("m,s,w,storage", [(1600, 100000, 20, "t"), (3200, 400, 20, "r"),
+                                           (400, 120, 18, "t"), (37, 1001, 5, "r"),
+                                           (100, 33, 32, "t"), (77, 9, 1, "r")])
+def test_y_passes_vs_torch(m, s, w, storage):
+    """Y G and W^T Y of rsvd_lrls on libskx's FP64 tensor-core kernels, for
+    Y stored row-major (dense / leverage) or as Y^T (TensorSketch)."""
+    import torch
+    from paper_2104_01101_b200.linalg import ty_times_dev, y_times_dev
+    g = np.random.default_rng(m + s)
+    yh = g.standard_normal((m, s))
+    y = (torch.from_numpy(np.ascontiguousarray(yh.T)).cuda().t() if storage == "t"
+         else torch.from_numpy(yh).cuda())
+    G = torch.from_numpy(g.standard_normal((s, w))).cuda()
+    W = torch.from_numpy(g.standard_normal((m, w))).cuda()
+    assert relerr(y_times_dev(y, G).cpu().numpy(), yh @ G.cpu().numpy()) <= 1e-13
+    assert relerr(ty_times_dev(W, y).cpu().numpy(), W.cpu().numpy().T @ yh) <= 1e-13

@@ -626,3 +626,33 @@ def test_rrf_stage1_fixed_point_paths_agree(skx, nnz):
         fl = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2)).cpu().numpy()
         d.drop_fibre(n)
         assert relerr(fx1, fl) <= 1e-14
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_slice_hits_match_filter_gather(skx, packed):
+    """Leverage gather of modes 1 / 2 from slices of the mode-0 layout equals
+    the full-scan filter + key gather (repeated samples, empty fibres, a
+    mode-0 layout carrying TensorSketch bits)."""
+    import torch
+    from paper_2104_01101_b200.sketching import (filter_fibers_dev, gather_coo_dev,
+                                                 gather_slices_dev)
+    from paper_2104_01101_b200.tensors import device_of
+    shape = (60, 50, 40)
+    c, v = _coo_rand(shape, 30000, 11)
+    d = device_of(skx.SparseTensor(shape, c, v))
+    if packed:
+        op = skx.TensorSketchOp.build((50, 40), 64, skx.make_rng(3))
+        d.fibre(0, op)
+    g = np.random.default_rng(5)
+    for n in (1, 2):
+        ext = [shape[k] for k in range(3) if k != n]
+        idx = np.stack([g.integers(0, ext[0], 500), g.integers(0, ext[1], 500)], axis=1)
+        idx[7] = idx[3]  # a repeated sample
+        idx_t = torch.from_numpy(idx).cuda()
+        w = torch.from_numpy(g.uniform(size=500)).cuda()
+        keys, vals = filter_fibers_dev(d, n, idx_t)
+        o1, c1, v1 = gather_coo_dev(keys, vals, ext, shape[n], idx_t, w)
+        o2, c2, v2 = gather_slices_dev(d, n, idx_t, w)
+        assert torch.equal(o1, o2)
+        assert torch.equal(c1, c2)
+        assert torch.equal(v1, v2)
