@@ -223,6 +223,19 @@ int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode, int64_t nn
 
 /* ------------------------------------------------- K4: range finder */
 
+/* Chunk-wise skx_rrf_stage1_fx for a tensor arriving in pieces: the caller
+ * zeroes `acc` (s_mode * k2 cells of 32 bytes), calls _acc per chunk (coords
+ * = the chunk's first entry of SoA row 0, rows ld apart; three-limb sums,
+ * *limb_flag is set accordingly) and _convert once.  Same exact sums. */
+int skx_rrf_stage1_fx_acc(int ndim, const int64_t* shape_h, int mode, int64_t n,
+                          const int32_t* coords, int64_t ld, const double* vals, int emax,
+                          uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
+                          uint32_t pending, uint64_t sign_q0, const uint64_t* rej, int64_t nrej,
+                          int64_t k2, unsigned long long* acc, unsigned int* limb_flag,
+                          void* stream);
+int skx_rrf_stage1_fx_convert(const unsigned long long* acc, int64_t cells, int emax,
+                              const unsigned int* limb_flag, double* stage1, void* stream);
+
 /* Range of the nonzero values: out3[0] = max, out3[1] = min unbiased binary
  * exponent of the nonzero |v|, out3[2] = 1 if any value is inf/NaN or
  * subnormal.  Decides whether skx_rrf_stage1_fx can sum exactly. */

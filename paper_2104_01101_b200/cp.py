@@ -320,20 +320,31 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
         core, tfac, ttrace = hooi_dev(d, tucker_cfg)
     core_cfg = replace(config, sketch=None, sketch_size=None, sketch_factor=None,
                        init="hosvd-of-core", seed=int(seed_cp))
-    cfac, cw, ctrace = cp_als_dev(core, core_cfg, on_core=True)
-    weights = cw.clone()
-    out = []
-    for b, a in zip(tfac, cfac):
-        unit, nrm = _normalize_columns_dev(b @ a)
-        out.append(unit)
-        weights = weights * nrm
-    if is_sparse_dev(d):
-        norm2 = d.norm2()[0].clone()
-        if comm is not None:
-            norm2 = comm.allreduce(norm2.view(1))[0]
-    else:
-        norm2 = (d * d).sum()
-    fin_dev = fitness_cp_dev(d, out, weights, norm2, comm)
+    # the core stage and the final CP fitness go to the high-priority stream:
+    # they run beside the Tucker stage's last fitness pass (low priority)
+    # instead of queueing behind its CTAs
+    from .tucker import _init_streams
+    caller = torch.cuda.current_stream()
+    hi = _init_streams()[1]
+    hi.wait_stream(caller)
+    with torch.cuda.stream(hi):
+        cfac, cw, ctrace = cp_als_dev(core, core_cfg, on_core=True)
+        weights = cw.clone()
+        out = []
+        for b, a in zip(tfac, cfac):
+            unit, nrm = _normalize_columns_dev(b @ a)
+            out.append(unit)
+            weights = weights * nrm
+        if is_sparse_dev(d):
+            norm2 = d.norm2()[0].clone()
+            if comm is not None:
+                norm2 = comm.allreduce(norm2.view(1))[0]
+        else:
+            norm2 = (d * d).sum()
+        fin_dev = fitness_cp_dev(d, out, weights, norm2, comm)
+    caller.wait_stream(hi)
+    for t in [fin_dev, weights] + out:
+        t.record_stream(caller)
     if finish is not None:
         ttrace = finish()
     fin = float(fin_dev.item())

@@ -522,9 +522,11 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
   // (grouping the nonzeros by row block first, so the atomics hit an
   // L2-resident slice of the accumulators, measured no faster: the
   // reductions are bound by the L2 atomic units, not by HBM)
-  // coarse row histogram: blocks of 2^CB rows, at most 24576 bins (96 KB)
+  // coarse row histogram: blocks of 2^CB rows, at most 32768 bins (128 KB of
+  // shared memory): 8-row blocks up to s_n = 262144 (config 5: ~40000
+  // nonzeros per block, under the 2^16 two-limb bound)
   int CB = 0;
-  while (((sn + (int64_t(1) << CB) - 1) >> CB) > 24576) ++CB;
+  while (((sn + (int64_t(1) << CB) - 1) >> CB) > 32768) ++CB;
   const int nbins = (int)((sn + (int64_t(1) << CB) - 1) >> CB);
   Arena ar(ws, *ws_bytes);
   unsigned long long* acc = ar.take<unsigned long long>((size_t)cells * 4);
@@ -572,4 +574,54 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
   const unsigned g = (unsigned)imin((cells + 255) / 256, (int64_t)num_sms() * 16);
   k_fixed_to_double<<<g, 256, 0, st>>>(acc, cells, S, rowmax, stage1);
   return check_launch("skx_rrf_stage1_fx", launches + 1);
+}
+
+// Chunk-wise form of skx_rrf_stage1_fx for a COO tensor that arrives in
+// pieces (host upload pipelined with the sketch): the caller owns the
+// accumulator (s_mode x k2 cells of 32 bytes, zeroed), adds chunk after chunk
+// (coords = first nonzero of the chunk in each of the ndim SoA rows, rows ld
+// apart) with three-limb reductions -- no row histogram of the whole tensor
+// exists yet -- and finally converts.  Same sums as the one-shot call.
+__global__ void k_u32_max_sentinel(unsigned int* p) { *p = 0xffffffffu; }
+
+extern "C" int skx_rrf_stage1_fx_acc(int ndim, const int64_t* shape_h, int mode, int64_t n,
+                                     const int32_t* coords, int64_t ld, const double* vals,
+                                     int emax, uint64_t k0, uint64_t k1, uint64_t p0,
+                                     uint32_t has_pending, uint32_t pending, uint64_t sign_q0,
+                                     const uint64_t* rej, int64_t nrej, int64_t k2,
+                                     unsigned long long* acc, unsigned int* limb_flag,
+                                     void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 5, "skx_rrf_stage1_fx_acc: order 2..5");
+  SKX_REQUIRE(mode >= 0 && mode < ndim, "skx_rrf_stage1_fx_acc: mode out of range");
+  SKX_REQUIRE(nrej < (int64_t(1) << 32), "skx_rrf_stage1_fx_acc: rejection list too long");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_u32_max_sentinel<<<1, 1, 0, st>>>(limb_flag);  // three limbs
+  if (n <= 0) return check_launch("skx_rrf_stage1_fx_acc", 1);
+  RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
+  CooSoA cs{};
+  for (int k = 0; k < ndim; ++k) {
+    cs.c[k] = coords + (int64_t)k * ld;
+    cs.ext[k] = shape_h[k];
+  }
+  constexpr int U = 4;
+  auto kern = ndim == 2 ? k_rrf_coo_fx<1, U>
+            : ndim == 3 ? k_rrf_coo_fx<2, U>
+            : ndim == 4 ? k_rrf_coo_fx<3, U>
+                        : k_rrf_coo_fx<4, U>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t blocks = imax(1, imin((n + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
+  kern<<<(unsigned)blocks, 256, 0, st>>>(r, cs, mode, n, vals, 94 - (emax + 1), limb_flag, acc);
+  return check_launch("skx_rrf_stage1_fx_acc", 2);
+}
+
+extern "C" int skx_rrf_stage1_fx_convert(const unsigned long long* acc, int64_t cells, int emax,
+                                         const unsigned int* limb_flag, double* stage1,
+                                         void* stream) {
+  if (cells <= 0) return SKX_OK;
+  const unsigned g = (unsigned)imin((cells + 255) / 256, (int64_t)num_sms() * 16);
+  k_fixed_to_double<<<g, 256, 0, (cudaStream_t)stream>>>(acc, cells, 94 - (emax + 1), limb_flag,
+                                                         stage1);
+  return check_launch("k_fixed_to_double");
 }

@@ -132,8 +132,11 @@ def rrf_stage1_dev(d, n, tabs):
 
 def _rrf_finish(d, n, rank, tabs, gauss, comm=None):
     """Composite sketch B = (T_(n) T_cs) G and its leading left singular vectors."""
+    return _rrf_from_stage1(rrf_stage1_dev(d, n, tabs), rank, gauss, comm)
+
+
+def _rrf_from_stage1(st1, rank, gauss, comm=None):
     torch = _torch()
-    st1 = rrf_stage1_dev(d, n, tabs)
     b = st1 @ torch.from_numpy(gauss).cuda()
     if comm is not None:
         # the Gaussian stage is linear: reduce the s_n x k1 product of each
@@ -204,6 +207,22 @@ def _init_streams():
         lo, hi = torch.cuda.Stream.priority_range()
         _STREAMS[dev] = (torch.cuda.Stream(priority=lo), torch.cuda.Stream(priority=hi))
     return _STREAMS[dev]
+
+
+# host COO inputs of at least this many nonzeros are uploaded in chunks of
+# this many rows (leverage runs; the TensorSketch layouts need the whole tensor)
+UPLOAD_CHUNK = 1 << 26
+
+_UP_STREAMS = {}
+
+
+def _upload_streams():
+    """(copy, convert) streams for the chunked host upload, one pair per device."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _UP_STREAMS:
+        _UP_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return _UP_STREAMS[dev]
 
 
 _YG_STREAMS = {}
@@ -316,6 +335,14 @@ class _Run:
         # RRF stage 1 of mode n (high priority) overlaps scan n+1.
         scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
                                self.comm)
+        if self._host is not None and not self.use_ts and self._host.nnz >= UPLOAD_CHUNK:
+            # leverage run on a host COO: upload in chunks and sketch them as
+            # they land, under the remaining upload
+            with torch.cuda.stream(main):
+                self._init_from_host_chunked(modes, scans, dims, main)
+            caller.wait_stream(main)
+            caller.wait_stream(side)
+            return
         if self._host is not None:
             with torch.cuda.stream(main):
                 self.draw_ts_ops()
@@ -345,6 +372,97 @@ class _Run:
                 self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm)
         caller.wait_stream(main)
         caller.wait_stream(side)
+
+    def _init_from_host_chunked(self, modes, scans, dims, main):
+        """Host COO -> device in UPLOAD_CHUNK-row pieces on a copy stream
+        (double-buffered int64 staging, converted to the int32 SoA layout on a
+        second stream), values first.  RRF stage 1 of every mode accumulates
+        each chunk as soon as it is converted (exact fixed-point sums, three
+        limbs: the sums do not depend on the chunking), so the range-finder
+        sketches finish with the upload instead of after it; the rejection
+        scans run meanwhile.  Falls back to the whole-tensor path when the
+        values do not admit exact fixed-point sums."""
+        torch = _torch()
+        st = self._host
+        nd, nnz = self.ndim, st.nnz
+        copy, conv = _upload_streams()
+        copy.wait_stream(main)
+        conv.wait_stream(main)
+        import warnings
+        with warnings.catch_warnings():  # read-only host arrays are only read
+            warnings.simplefilter("ignore", UserWarning)
+            hc = torch.from_numpy(np.ascontiguousarray(st.coords))
+            hv = torch.from_numpy(np.ascontiguousarray(st.values))
+        vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        coords = torch.empty((nd, nnz), dtype=torch.int32, device="cuda")
+        with torch.cuda.stream(copy):
+            vals.copy_(hv, non_blocking=True)
+            ev_v = torch.cuda.Event()
+            ev_v.record(copy)
+        chunk = UPLOAD_CHUNK
+        staging = [torch.empty((chunk, nd), dtype=torch.int64, device="cuda") for _ in range(2)]
+        conv_ev, bounds = [], []
+        for i, lo in enumerate(range(0, nnz, chunk)):
+            hi = min(nnz, lo + chunk)
+            buf = staging[i % 2]
+            with torch.cuda.stream(copy):
+                if i >= 2:
+                    copy.wait_event(conv_ev[i - 2])  # staging buffer drained
+                buf[:hi - lo].copy_(hc[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            with torch.cuda.stream(conv):
+                conv.wait_event(ev)
+                coords[:, lo:hi].copy_(buf[:hi - lo].t())
+                cev = torch.cuda.Event()
+                cev.record(conv)
+            buf.record_stream(conv)
+            buf.record_stream(copy)
+            conv_ev.append(cev)
+            bounds.append((lo, hi))
+        main.wait_event(ev_v)
+        vals.record_stream(copy)
+        d = DeviceCoo(self.shape, coords, vals)
+        st._device = d
+        self._host = None
+        self._attach(d)
+        fx = d.fixed_point_ok()  # one small D2H once the values are in
+        self.normals.prefetch()
+        # the RRF tables of every mode, in the reference's draw order
+        tabs_all = []
+        for n, scan, (P, k2, width) in zip(modes, scans, dims):
+            tabs = finish_rrf_scan(scan, self.rng_init, P)
+            gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
+            tabs_all.append((n, tabs, gauss))
+        if not fx:
+            for ev in conv_ev:
+                main.wait_event(ev)
+            self.d.fibre(0)
+            for n, tabs, gauss in tabs_all:
+                self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm)
+            return
+        emax = d.value_range()[0]
+        shp, sp_ = nat.host_i64(self.shape)
+        accs = {}
+        for n, tabs, _ in tabs_all:
+            accs[n] = (torch.zeros(self.shape[n] * tabs.k2 * 4, dtype=torch.int64, device="cuda"),
+                       torch.empty(1, dtype=torch.int32, device="cuda"))
+        for (lo, hi), ev in zip(bounds, conv_ev):
+            main.wait_event(ev)
+            cptr = ctypes.c_void_p(coords.data_ptr() + lo * 4)
+            vptr = ctypes.c_void_p(vals.data_ptr() + lo * 8)
+            for n, tabs, _ in tabs_all:
+                acc, flag = accs[n]
+                nat.call("skx_rrf_stage1_fx_acc", nd, sp_, n, hi - lo, cptr, nnz, vptr, emax,
+                         *tabs.args(), tabs.k2, nat.ptr(acc), nat.ptr(flag), nat.stream())
+        coords.record_stream(main)
+        self.d.fibre(0)  # the fitness layout (a packing pass)
+        for n, tabs, gauss in tabs_all:
+            acc, flag = accs[n]
+            st1 = torch.empty((self.shape[n], tabs.k2), dtype=torch.float64, device="cuda")
+            nat.call("skx_rrf_stage1_fx_convert", nat.ptr(acc), self.shape[n] * tabs.k2, emax,
+                     nat.ptr(flag), nat.ptr(st1), nat.stream())
+            self.factors[n] = _rrf_from_stage1(st1, self.ranks[n], gauss, self.comm)
 
     def _draw_ts(self, n):
         ext = tuple(self.shape[k] for k in self.others(n))

@@ -236,3 +236,27 @@ def test_config5_alg6_reduced_vs_reference(cg, skx, oracle, monkeypatch, tag):
     assert np.allclose(trace.fitness, cg[f"{tag}_fitness"], rtol=0, atol=1e-9)
     assert np.allclose(trace.residuals, cg[f"{tag}_residuals"], rtol=1e-5, atol=0)
     assert relerr(model.weights, cg[f"{tag}_cp_w"]) <= 1e-4
+
+
+def test_config5_chunked_host_upload_is_exact(cg, skx, monkeypatch):
+    """Algorithm 6 from a HOST COO (the public-API path the e2e bench times):
+    the tensor is uploaded in chunks and the range-finder sketches accumulate
+    each chunk as it lands.  Exact fixed-point sums make the result bitwise
+    identical to the device-resident run, and the leverage index sets match
+    the reference."""
+    from paper_2104_01101_b200 import tucker
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    spec, cfg = CASES["c5b"]
+    _, shape, nnz, seed = spec
+    c, v = planted_cp_coo_host(shape, nnz, rank=10, seed=seed)
+    monkeypatch.setattr(tucker, "UPLOAD_CHUNK", 1 << 21)  # 5 chunks
+    rec = Recorder(monkeypatch)
+    host = skx.SparseTensor.from_sorted(shape, c, v)
+    m1, t1 = skx.cp_via_sketched_tucker(host, skx.CPConfig(**cfg))
+    _check_lev(cg, "c5b", rec)
+    dev = skx.SparseTensor(shape, c, v)  # device ingest: one-shot path
+    m2, t2 = skx.cp_via_sketched_tucker(dev, skx.CPConfig(**cfg))
+    assert t1.fitness == t2.fitness and t1.residuals == t2.residuals
+    assert np.array_equal(m1.weights, m2.weights)
+    for a, b in zip(m1.factors, m2.factors):
+        assert np.array_equal(a, b)
