@@ -370,7 +370,7 @@ def run_ours(args, cfgd):
         "metric": METRIC,
         "value": round(value, 4), "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; sparse generated on the GPU)",
         "config": {"workload": cfgd["workload"], "config_id": args.config,

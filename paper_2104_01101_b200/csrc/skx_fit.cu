@@ -1,8 +1,6 @@
 // K5 residual and K7 fitness passes (src/tucker.py:274; src/tensors.py:
 // 339-368).  All reductions use a fixed grid and a fixed combination order,
 // so results are bitwise reproducible.
-#include <stdlib.h>
-
 #include "skx_common.cuh"
 
 namespace skx {
@@ -575,9 +573,10 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
     cp_async_commit();
     double acc = 0.0;
     for (int64_t bi = 0; bi < nb; ++bi) {
-      // rows(bi) and records(bi + D) were committed >= 2 groups ago (the
-      // prologue group at bi = 0): only the newest group may stay in flight
-      if (bi == 0) cp_async_wait<0>();
+      // rows(bi) were committed D groups ago and records(bi + D) two groups
+      // ago (or in the prologue): with D >= 2 only the newest group may stay
+      // in flight; with D = 1 rows(bi) are the newest group themselves
+      if (bi == 0 || D < 2) cp_async_wait<0>();
       else cp_async_wait<1>();
       __syncwarp();
       if (bi + D < nb) issue_rows(bi + D);
@@ -585,30 +584,43 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
       cp_async_commit();
       const double* rw = rows + (bi % NRB) * ROWBUF;
       const double* rv = recs + (bi % NRC) * NB * 2;
+      constexpr int NG = NB / 8;
+      // fragments of every group first, then the DMMAs k-step by k-step over
+      // all (group, n-tile) accumulators: NG * NT independent chains
+      double a[NG][P::KS], d[NG][P::NT][2];
 #pragma unroll
-      for (int g = 0; g < NB / 8; ++g) {
+      for (int g = 0; g < NG; ++g) {
         const double* ra = rw + (g * 8 + q) * P::ST;
-        const double* ry = rw + (NB + g * 8 + q) * P::ST;
-        double a[P::KS];
 #pragma unroll
         for (int j = 0; j < P::PAIRS; ++j) {
           const double2 p2 = *reinterpret_cast<const double2*>(ra + 8 * j + 2 * c);
-          a[2 * j] = p2.x;
-          a[2 * j + 1] = p2.y;
+          a[g][2 * j] = p2.x;
+          a[g][2 * j + 1] = p2.y;
         }
-        if (P::SINGLE) a[P::KS - 1] = ra[8 * P::PAIRS + c];
-        const double v = rv[(g * 8 + q) * 2 + 1];
+        if (P::SINGLE) a[g][P::KS - 1] = ra[8 * P::PAIRS + c];
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+          for (int nt = 0; nt < P::NT; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const double* ry = rw + (NB + g * 8 + q) * P::ST;
         double t = 0.0;
 #pragma unroll
         for (int nt = 0; nt < P::NT; ++nt) {
-          const double2 y = *reinterpret_cast<const double2*>(ry + 8 * nt + 2 * c);
-          double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < P::KS; ++ks) dmma884(d0, d1, a[ks], b[ks][nt]);
-          t = fma(d0, y.x, t);
-          t = fma(d1, y.y, t);
+          // the last n-tile of R = 20 holds 4 real columns: lanes c >= 2 read padding
+          const bool live = nt * 8 + 2 * c < R;
+          const double2 y = live ? *reinterpret_cast<const double2*>(ry + 8 * nt + 2 * c)
+                                 : make_double2(0.0, 0.0);
+          t = fma(d[g][nt][0], y.x, t);
+          t = fma(d[g][nt][1], y.y, t);
         }
-        acc = fma(v, t, acc);
+        acc = fma(rv[(g * 8 + q) * 2 + 1], t, acc);
       }
     }
     cp_async_wait<0>();
@@ -958,15 +970,9 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
     k_tucker3_async<RR, NB, MBB, DD><<<mb, 256, sm, s>>>(colptr0, s0, rec, c1_mask, A0, A1, A2, \
                                                          core, R0, part);                       \
   } while (0)
-      static const int t3v = [] {
-        const char* e = getenv("SKX_T3_VARIANT");
-        return e ? atoi(e) : 0;
-      }();
-      if (R1 == 20 && R2 == 20 && t3v == 1) {
-        SKX_T3A(20, 8, 2, 2);
-      } else if (R1 == 20 && R2 == 20 && t3v == 2) {
-        SKX_T3A(20, 16, 1, 2);
-      } else if (R1 == 20 && R2 == 20) {
+      // (row lookahead D = 2 with NB = 8 or one CTA per SM measured slower
+      // in the pipeline: 592 / 610 vs 538 ms per config-5 call)
+      if (R1 == 20 && R2 == 20) {
         SKX_T3A(20, 16, 2, 1);
       } else if (R1 == 10 && R2 == 10) {
         k_tucker3_mma<3, 2, 2, 10, 10, 2, true><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1,

@@ -279,6 +279,20 @@ __global__ void k_max_u32(const unsigned int* __restrict__ a, int n, unsigned in
 // |.| < 2^46): 2 reductions per nonzero instead of 3.
 constexpr unsigned int kFxTwoLimbMax = 1u << 16;
 
+// d-array entries held in shared memory by the FX kernel (the rejection
+// lists of configs 4-5 hold ~1e2-2.4e3 entries); larger lists read global memory
+constexpr int kFxSmemD = 3072;
+
+__device__ __forceinline__ uint64_t count_le_tab_s(const uint64_t* dsm, int64_t nd_s,
+                                                   const uint64_t* dg, const uint32_t* cnt,
+                                                   int shift, uint64_t j) {
+  const uint64_t b = j >> shift;
+  uint32_t i = cnt[b];
+  const uint32_t e = cnt[b + 1];
+  while (i < e && (i < nd_s ? dsm[i] : dg[i]) <= j) ++i;
+  return i;
+}
+
 template <int NO, int U>
 __global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mode, int64_t nnz,
                                                     const double* __restrict__ vals, int S,
@@ -286,6 +300,7 @@ __global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mod
                                                     unsigned long long* __restrict__ acc) {
   const bool two = *rowmax < kFxTwoLimbMax;
   __shared__ uint32_t cnt[kRrfBuckets + 1];
+  __shared__ uint64_t dsm[kFxSmemD];
   uint64_t P = 1;
   int oth[NO];
 #pragma unroll
@@ -304,28 +319,39 @@ __global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mod
     }
     cnt[b] = (uint32_t)lo;
   }
+  const int64_t nd_s = imin(r.nd, kFxSmemD);
+  for (int64_t i = threadIdx.x; i < nd_s; i += blockDim.x) dsm[i] = r.d[i];
   __syncthreads();
   const uint64_t k2 = r.k2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) * U + threadIdx.x; base < nnz;
        base += stride) {
+    // all loads of the U elements first (no early exit between them), then
+    // the Philox work and the reductions
+    uint32_t cc[U][NO], rw[U];
+    double vv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e = base + (int64_t)u * blockDim.x;
-      if (e >= nnz) break;
+      const int64_t ee = e < nnz ? e : base;
+#pragma unroll
+      for (int k = 0; k < NO; ++k) cc[u][k] = (uint32_t)__ldcs(cs.c[oth[k]] + ee);
+      rw[u] = (uint32_t)__ldcs(cs.c[mode] + ee);
+      vv[u] = e < nnz ? __ldcs(vals + ee) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + (int64_t)u * blockDim.x >= nnz) continue;
       uint64_t j = 0;
 #pragma unroll
-      for (int k = 0; k < NO; ++k)
-        j = j * (uint64_t)cs.ext[oth[k]] + (uint64_t)(uint32_t)__ldcs(cs.c[oth[k]] + e);
-      const uint64_t row = (uint64_t)(uint32_t)__ldcs(cs.c[mode] + e);
-      const double v = __ldcs(vals + e);
-      const uint32_t t = rrf_entry_q(r, j, j + count_le_tab(r, cnt, shift, j));
+      for (int k = 0; k < NO; ++k) j = j * (uint64_t)cs.ext[oth[k]] + (uint64_t)cc[u][k];
+      const uint32_t t = rrf_entry_q(r, j, j + count_le_tab_s(dsm, nd_s, r.d, cnt, shift, j));
       uint64_t hi, lo;
-      to_fixed(pk_neg(t) ? -v : v, S, hi, lo);
+      to_fixed(pk_neg(t) ? -vv[u] : vv[u], S, hi, lo);
       // three 32-bit limbs (bits 0-31, 32-63 unsigned; 64-95 signed: |value|
       // < 2^94, so bits 94.. are sign copies) summed in 64-bit cells by
       // fire-and-forget reductions (no carries to wait for: < 2^32 addends)
-      unsigned long long* cell = acc + 4 * (row * k2 + pk_bucket(t));
+      unsigned long long* cell = acc + 4 * ((uint64_t)rw[u] * k2 + pk_bucket(t));
       if (two) {
         atomicAdd(cell, (unsigned long long)(lo & 0xffffffffffffULL));
         atomicAdd(cell + 1, (unsigned long long)((hi << 16) | (lo >> 48)));  // value >> 48

@@ -656,3 +656,35 @@ def test_slice_hits_match_filter_gather(skx, packed):
         assert torch.equal(o1, o2)
         assert torch.equal(c1, c2)
         assert torch.equal(v1, v2)
+
+
+@pytest.mark.parametrize("shape,nnz,R", [((2000, 4000, 3000), 2_000_000, 20),
+                                         ((50, 20000, 20000), 2_000_000, 20),
+                                         ((200000, 200000, 200000), 20_000_000, 20),
+                                         ((100000, 100000, 100000), 10_000_000, 10),
+                                         ((3000, 500, 700), 300_000, 7)])
+def test_tucker_cross_kernels_vs_einsum(skx, shape, nnz, R):
+    """The sparse fitness cross term (K7: cp.async-staged at R = 20, register
+    pipeline at R = 10, generic otherwise) against a chunked einsum, including
+    many short slices (config-5-like: ~100 nonzeros per slice, several
+    pipelined batches each) and long ones."""
+    import torch
+    from paper_2104_01101_b200.synth import planted_cp_coo_device
+    from paper_2104_01101_b200.tensors import device_of, tucker_cross_dev
+    coords, vals = planted_cp_coo_device(shape, nnz, rank=10, noise_sd=0.1, seed=1)
+    d = device_of(skx.SparseTensor.from_device(shape, coords, vals, validate=False))
+    g = torch.Generator(device="cuda").manual_seed(1)
+    fac = [torch.linalg.qr(torch.randn(s, R, dtype=torch.float64, device="cuda", generator=g))[0]
+           for s in shape]
+    core = torch.randn(R, R, R, dtype=torch.float64, device="cuda", generator=g)
+    got = float(tucker_cross_dev(d, core, fac))
+    c, v = d.coords.long(), d.vals
+    ref, mag = 0.0, 0.0
+    for lo in range(0, d.nnz, 1 << 20):
+        hi = min(d.nnz, lo + (1 << 20))
+        t = torch.einsum("ea,abc->ebc", fac[0][c[0, lo:hi]], core)
+        t = torch.einsum("ebc,eb->ec", t, fac[1][c[1, lo:hi]])
+        per = v[lo:hi] * (t * fac[2][c[2, lo:hi]]).sum(1)
+        ref += float(per.sum())
+        mag += float(per.abs().sum())
+    assert abs(got - ref) <= 1e-12 * mag, (got, ref, mag)

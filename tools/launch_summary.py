@@ -7,6 +7,7 @@ boundary is the first k_lemire_scan launch of each call).
 """
 import collections
 import csv
+import gzip
 import sys
 
 
@@ -14,7 +15,8 @@ def main():
     path = sys.argv[1]
     tail = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     rows = []
-    with open(path) as fh:
+    opener = gzip.open if path.endswith(".gz") else open
+    with opener(path, "rt") as fh:
         lines = [ln for ln in fh if ln.startswith('"')]
     for r in csv.DictReader(lines):
         if r["Metric Name"] != "gpu__time_duration.sum":
