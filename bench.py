@@ -246,13 +246,17 @@ def run_ours(args, cfgd):
         del coords, vals
         local_nnz = inp._device.nnz
 
+    traces = []
+
     def step():
         if cfgd["kind"] != "dense":
             inp._device.release_layouts()  # each step rebuilds its per-mode layouts
         if cfgd["kind"] == "alg6":
             _, _, tr = cp_via_sketched_tucker_dev(inp, cfg, comm)
+            traces.append((tuple(tr.fitness), tuple(tr.residuals)))
             return tr.wall_s[:tr.stage_split], tr.wall_s[tr.stage_split]
         _, _, tr = sketched_tucker_als_dev(inp, cfg, comm)
+        traces.append((tuple(tr.fitness), tuple(tr.residuals)))
         return tr.wall_s, 0.0
 
     def barrier():
@@ -389,6 +393,10 @@ def run_ours(args, cfgd):
         "dominant_kernel": dom,
         "fp64_peak_tflops": round(peak_fp64, 2) if peak_fp64 else None,
         "gpu_launches": int(launches),
+        # every step's trace bitwise equal to the first (deterministic kernels:
+        # a race or an order-dependent reduction would show up here)
+        "deterministic": all(t == traces[0] for t in traces),
+        "final_fitness": traces[-1][0][-1] if traces else None,
         "clocks": clk,
         "e2e": e2e,
     }

@@ -330,3 +330,22 @@ def test_ref_tucker_ts_vs_reference_golden(golden, oracle, skx, tag):
     else:
         assert np.allclose(trace.fitness, golden[f"{tag}_fitness"], rtol=0, atol=0.1)
         assert len(trace.residuals) == len(golden[f"{tag}_residuals"])
+
+
+def test_config5_shape_run_bitwise_deterministic(skx):
+    """A config-5-shaped run (5e4^3, R = 20, leverage m = 6400, short
+    fitness slices, fixed-point RRF) twice: bitwise identical model and
+    trace (no race in the cp.async-staged fitness or the atomics)."""
+    from paper_2104_01101_b200.synth import planted_cp_coo_device
+    shape = (50_000,) * 3  # ~50 sampled-fibre hits per sub-problem: rank 20 is reachable
+    coords, vals = planted_cp_coo_device(shape, 20_000_000, rank=10, noise_sd=0.1, seed=2)
+    st = skx.SparseTensor.from_device(shape, coords, vals, validate=False)
+    cfg = skx.CPConfig(rank=10, tucker_rank=20, sketch="leverage-random", sketch_factor=16,
+                       tucker_sweeps=2, max_sweeps=10, seed=0)
+    m1, t1 = skx.cp_via_sketched_tucker(st, cfg)
+    st._device.release_layouts()
+    m2, t2 = skx.cp_via_sketched_tucker(st, cfg)
+    assert t1.fitness == t2.fitness and t1.residuals == t2.residuals
+    assert np.array_equal(m1.weights, m2.weights)
+    for a, b in zip(m1.factors, m2.factors):
+        assert np.array_equal(a, b)
