@@ -194,31 +194,23 @@ def host_ptrs(tensors):
 
 
 class Workspace:
-    """Grow-only per-device scratch buffers (slots) shared by stream-ordered
-    calls.  Each slot remembers the streams it was handed to; when a slot
-    grows, the old buffer is marked used on those streams (record_stream), so
-    the caching allocator cannot hand it out again before their queued work
-    has finished."""
+    """Grow-only per-device scratch buffers, one per (slot, stream).  A slot's
+    buffer is only ever handed to calls on one stream, so two streams running
+    the same entry point concurrently (the per-sweep fitness on its side
+    stream next to Algorithm 6's final CP fitness) never share scratch, and a
+    grown buffer's predecessor is released in that stream's order."""
 
     def __init__(self):
         self._buf = {}
-        self._streams = {}
 
     def get(self, nbytes, slot=0):
         import torch
-        dev = torch.cuda.current_device()
-        key = (dev, slot)
         cur = torch.cuda.current_stream()
+        key = (torch.cuda.current_device(), slot, cur.cuda_stream)
         buf = self._buf.get(key)
-        users = self._streams.setdefault(key, {})
         if buf is None or buf.numel() < nbytes:
-            if buf is not None:
-                for st in users.values():
-                    buf.record_stream(st)
-                users.clear()
             buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
             self._buf[key] = buf
-        users[cur.cuda_stream] = cur
         return buf
 
 

@@ -688,3 +688,40 @@ def test_tucker_cross_kernels_vs_einsum(skx, shape, nnz, R):
         ref += float(per.sum())
         mag += float(per.abs().sum())
     assert abs(got - ref) <= 1e-12 * mag, (got, ref, mag)
+
+
+@pytest.mark.gpu
+def test_fitness_kernels_concurrent_streams_bitwise(skx):
+    """The per-sweep Tucker fitness (side stream) and Algorithm 6's final CP
+    fitness (another stream) run concurrently in a config-5 call and share
+    the entry points' scratch slot: each stream must get its own scratch, so
+    the concurrent results equal the serial ones bit for bit."""
+    import torch
+    from paper_2104_01101_b200.synth import planted_cp_coo_device
+    from paper_2104_01101_b200.tensors import cp_cross_dev, device_of, tucker_cross_dev
+    shape = (100_000,) * 3
+    coords, vals = planted_cp_coo_device(shape, 20_000_000, rank=10, noise_sd=0.1, seed=3)
+    d = device_of(skx.SparseTensor.from_device(shape, coords, vals, validate=False))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    fac = [torch.linalg.qr(torch.randn(s, 20, dtype=torch.float64, device="cuda", generator=g))[0]
+           for s in shape]
+    core = torch.randn(20, 20, 20, dtype=torch.float64, device="cuda", generator=g)
+    cfac = [torch.randn(s, 10, dtype=torch.float64, device="cuda", generator=g) for s in shape]
+    w = torch.rand(10, dtype=torch.float64, device="cuda", generator=g)
+    t_ser = tucker_cross_dev(d, core, fac).clone()
+    c_ser = cp_cross_dev(d, cfac, w).clone()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        s1.wait_stream(torch.cuda.current_stream())
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s1):
+            t_con = tucker_cross_dev(d, core, fac)
+        with torch.cuda.stream(s2):
+            c_con = cp_cross_dev(d, cfac, w)
+        torch.cuda.synchronize()
+        outs.append((t_con.clone(), c_con.clone()))
+    for t_con, c_con in outs:
+        assert torch.equal(t_con, t_ser)
+        assert torch.equal(c_con, c_ser)
