@@ -83,6 +83,7 @@ class SparseTensor:
         self._unfoldings = {}
         self._mode_sort = {}
         self._device = None
+        self._soa = None  # pinned int32 (N, nnz) staging copy (from_sorted)
 
     @classmethod
     def from_sorted(cls, shape, coords, values):
@@ -113,7 +114,25 @@ class SparseTensor:
                 raise ValueError("coordinates must be lexsorted and duplicate-free")
         obj = cls.__new__(cls)
         obj._init(shape, coords, values)
+        if coords.shape[0] >= DEVICE_INGEST_NNZ and max(shape) < 2 ** 31:
+            obj._stage_soa()
         return obj
+
+    def _stage_soa(self):
+        """Stage the coordinates in the device layout -- int32, one row per
+        mode (N x nnz) -- in pinned host memory, once, at construction: every
+        later upload then moves 4 B per coordinate instead of the API's 8 and
+        needs no conversion pass on either side."""
+        torch = _torch()
+        import warnings
+        with warnings.catch_warnings():  # read-only host arrays are only read
+            warnings.simplefilter("ignore", UserWarning)
+            c64 = torch.from_numpy(self._coords)
+        soa = torch.empty((self.ndim, c64.shape[0]), dtype=torch.int32, pin_memory=True)
+        chunk = 1 << 24
+        for lo in range(0, c64.shape[0], chunk):
+            soa[:, lo:lo + chunk].copy_(c64[lo:lo + chunk].t())
+        self._soa = soa
 
     @classmethod
     def from_device(cls, shape, coords, values, validate=True):
@@ -253,11 +272,13 @@ class DeviceCoo:
         import warnings
         with warnings.catch_warnings():  # read-only host arrays are only read
             warnings.simplefilter("ignore", UserWarning)
-            c64 = torch.from_numpy(np.ascontiguousarray(st.coords))
             v = torch.from_numpy(np.ascontiguousarray(st.values))
+            vd = v.to("cuda", non_blocking=True)
+            if getattr(st, "_soa", None) is not None:  # staged int32 SoA: one H2D
+                return cls(st.shape, st._soa.to("cuda", non_blocking=True), vd)
+            c64 = torch.from_numpy(np.ascontiguousarray(st.coords))
         # one H2D of the caller's arrays, then int64 AoS -> int32 SoA on device
         cd = c64.to("cuda", non_blocking=True)
-        vd = v.to("cuda", non_blocking=True)
         return cls(st.shape, cd.t().to(torch.int32).contiguous(), vd)
 
     @classmethod

@@ -335,7 +335,8 @@ class _Run:
         # RRF stage 1 of mode n (high priority) overlaps scan n+1.
         scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
                                self.comm)
-        if self._host is not None and not self.use_ts and self._host.nnz >= UPLOAD_CHUNK:
+        if (self._host is not None and not self.use_ts and self._host.nnz >= UPLOAD_CHUNK
+                and self._host._soa is not None):
             # leverage run on a host COO: upload in chunks and sketch them as
             # they land, under the remaining upload
             with torch.cuda.stream(main):
@@ -374,24 +375,22 @@ class _Run:
         caller.wait_stream(side)
 
     def _init_from_host_chunked(self, modes, scans, dims, main):
-        """Host COO -> device in UPLOAD_CHUNK-row pieces on a copy stream
-        (double-buffered int64 staging, converted to the int32 SoA layout on a
-        second stream), values first.  RRF stage 1 of every mode accumulates
-        each chunk as soon as it is converted (exact fixed-point sums, three
-        limbs: the sums do not depend on the chunking), so the range-finder
+        """Host COO (staged as pinned int32 SoA by SparseTensor.from_sorted)
+        -> device in UPLOAD_CHUNK-column pieces on a copy stream, values
+        first.  RRF stage 1 of every mode accumulates each chunk as soon as it
+        has landed (exact fixed-point sums, three limbs: the sums do not
+        depend on the chunking), so the range-finder
         sketches finish with the upload instead of after it; the rejection
         scans run meanwhile.  Falls back to the whole-tensor path when the
         values do not admit exact fixed-point sums."""
         torch = _torch()
         st = self._host
         nd, nnz = self.ndim, st.nnz
-        copy, conv = _upload_streams()
+        copy, _ = _upload_streams()
         copy.wait_stream(main)
-        conv.wait_stream(main)
         import warnings
         with warnings.catch_warnings():  # read-only host arrays are only read
             warnings.simplefilter("ignore", UserWarning)
-            hc = torch.from_numpy(np.ascontiguousarray(st.coords))
             hv = torch.from_numpy(np.ascontiguousarray(st.values))
         vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
         coords = torch.empty((nd, nnz), dtype=torch.int32, device="cuda")
@@ -400,24 +399,15 @@ class _Run:
             ev_v = torch.cuda.Event()
             ev_v.record(copy)
         chunk = UPLOAD_CHUNK
-        staging = [torch.empty((chunk, nd), dtype=torch.int64, device="cuda") for _ in range(2)]
+        soa = st._soa  # coordinates staged as pinned int32 SoA: straight into place
         conv_ev, bounds = [], []
-        for i, lo in enumerate(range(0, nnz, chunk)):
+        for lo in range(0, nnz, chunk):
             hi = min(nnz, lo + chunk)
-            buf = staging[i % 2]
             with torch.cuda.stream(copy):
-                if i >= 2:
-                    copy.wait_event(conv_ev[i - 2])  # staging buffer drained
-                buf[:hi - lo].copy_(hc[lo:hi], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            with torch.cuda.stream(conv):
-                conv.wait_event(ev)
-                coords[:, lo:hi].copy_(buf[:hi - lo].t())
+                for k in range(nd):
+                    coords[k, lo:hi].copy_(soa[k, lo:hi], non_blocking=True)
                 cev = torch.cuda.Event()
-                cev.record(conv)
-            buf.record_stream(conv)
-            buf.record_stream(copy)
+                cev.record(copy)
             conv_ev.append(cev)
             bounds.append((lo, hi))
         main.wait_event(ev_v)
