@@ -1,6 +1,9 @@
 // K5 residual and K7 fitness passes (src/tucker.py:274; src/tensors.py:
 // 339-368).  All reductions use a fixed grid and a fixed combination order,
 // so results are bitwise reproducible.
+#include <cuda.h>
+#include <cstdlib>
+
 #include "skx_common.cuh"
 
 namespace skx {
@@ -631,6 +634,228 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_async(
   }
 }
 
+// R = 20 with the mode-2 factor rows brought in by the TMA unit
+// (cp.async.bulk.tensor tile::gather4, four rows per instruction) while the
+// mode-1 rows keep the 16-byte cp.async path: the two gathers then load
+// different units (TMA engine vs the LSU/L1 data pipe, which the cp.async
+// row copies plus the fragment reads saturate in k_tucker3_async).  The
+// tensor map's box is 24 columns wide over a 20-column factor, so the four
+// padding columns arrive as TMA out-of-bounds zeros: rows land at the
+// conflict-free stride of 24 doubles and the last n-tile needs no masking.
+// Completion of a batch's TMA rows is tracked by one mbarrier per row
+// buffer (expect_tx = NB rows x 192 bytes).
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm, uint64_t* bar,
+                                            int32_t col, int32_t r0, int32_t r1, int32_t r2,
+                                            int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(tm), "r"(smem_addr(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
+constexpr int kT3tR = 20, kT3tST = 24;  // rank, smem row stride (doubles)
+
+template <int NB, int MB, int D>
+__global__ void __launch_bounds__(256, MB) k_tucker3_tma(
+    const __grid_constant__ CUtensorMap tmC, const int64_t* __restrict__ colptr, int64_t s0,
+    const double* __restrict__ rec, uint32_t c1_mask, const double* __restrict__ A0,
+    const double* __restrict__ A1, const double* __restrict__ C, int R0,
+    double* __restrict__ slice_out) {
+  constexpr int R = kT3tR, ST = kT3tST;
+  using P = T3A<R>;
+  static_assert(P::ST == ST, "row stride");
+  constexpr int NINSTR = (NB + P::RPI - 1) / P::RPI;
+  constexpr int ROWBUF = NB * ST;  // doubles per row buffer (one operand)
+  constexpr int NRB = D + 1, NRC = D + 3;
+  constexpr uint32_t TX = NB * ST * 8;
+  extern __shared__ __align__(128) double t3sm[];
+  __shared__ __align__(8) uint64_t bars[8][NRB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane >> 2, c = lane & 3;
+  // per warp: [NRB][NB][ST] TMA rows (C), [NRB][NB][ST] cp.async rows (A1), [NRC][NB][2] records
+  double* rowsC = t3sm + (size_t)wid * (2 * NRB * ROWBUF + NRC * NB * 2);
+  double* rowsA = rowsC + NRB * ROWBUF;
+  double* recs = rowsA + NRB * ROWBUF;
+  for (int e = lane; e < NRB * ROWBUF; e += 32) rowsA[e] = 0.0;  // zero padding beyond R
+  if (lane == 0)
+    for (int b = 0; b < NRB; ++b) mbar_init(&bars[wid][b], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t phase = 0;  // bit b: parity of row buffer b's next completion
+  const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
+  const int cr = lane / P::LPR, ch = lane % P::LPR;
+  for (int64_t i0 = blockIdx.x * nw + wid; i0 < s0; i0 += stride) {
+    {  // the next slice's records into L2
+      const int64_t j = i0 + stride;
+      if (j < s0) {
+        const int64_t l0 = colptr[j] * 16 / 128, l1 = (colptr[j + 1] * 16 + 127) / 128;
+        for (int64_t l = l0 + lane; l < l1; l += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(rec) + l * 128));
+      }
+    }
+    const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
+    if (e0 == e1) {
+      if (lane == 0) slice_out[i0] = 0.0;
+      continue;
+    }
+    const int64_t nb = (e1 - e0 + NB - 1) / NB;
+    auto issue_recs = [&](int64_t b) {
+      if (lane < NB) {
+        const int64_t e = e0 + b * NB + lane;
+        cp_async16_cg_zfill(smem_addr(recs + ((b % NRC) * NB + lane) * 2),
+                            rec + 2 * (e < e1 ? e : e0), e < e1 ? 16u : 0u);
+      }
+    };
+    auto issue_rows = [&](int64_t b) {
+      const int slot = (int)(b % NRB);
+      const uint32_t* rb = reinterpret_cast<const uint32_t*>(recs + (b % NRC) * NB * 2);
+      // mode-2 rows: one gather4 per four records (padding records are zero:
+      // row 0, contributing nothing)
+      // order this warp's earlier generic reads of the buffer before the
+      // async-proxy writes into it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0) mbar_expect_tx(&bars[wid][slot], TX);
+      __syncwarp();
+      if (lane < NB / 4) {
+        const int32_t i0_ = (int32_t)(rb[(4 * lane + 0) * 4 + 1] & c1_mask);
+        const int32_t i1_ = (int32_t)(rb[(4 * lane + 1) * 4 + 1] & c1_mask);
+        const int32_t i2_ = (int32_t)(rb[(4 * lane + 2) * 4 + 1] & c1_mask);
+        const int32_t i3_ = (int32_t)(rb[(4 * lane + 3) * 4 + 1] & c1_mask);
+        tma_gather4(smem_addr(rowsC + slot * ROWBUF + 4 * lane * ST), &tmC, &bars[wid][slot], 0,
+                    i0_, i1_, i2_, i3_);
+      }
+      // mode-1 rows: R/2 lanes per row, 16-byte cp.async pieces
+      double* dst = rowsA + slot * ROWBUF;
+#pragma unroll
+      for (int t = 0; t < NINSTR; ++t) {
+        const int r = t * P::RPI + cr;
+        if (cr < P::RPI && r < NB) {
+          const uint32_t idx = rb[r * 4];
+          cp_async16_ca(smem_addr(dst + r * ST + 2 * ch), A1 + (int64_t)idx * R + 2 * ch);
+        }
+      }
+    };
+    double b[P::KS][P::NT];
+#pragma unroll
+    for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < P::NT; ++nt) {
+        const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
+        const int n = nt * 8 + q;
+        double w = 0.0;
+        if (k < R && n < R)
+          for (int r0 = 0; r0 < R0; ++r0)
+            w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + n), w);
+        b[ks][nt] = w;
+      }
+    for (int64_t b2 = 0; b2 < D + 2 && b2 < nb; ++b2) issue_recs(b2);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int64_t b2 = 0; b2 < D && b2 < nb; ++b2) issue_rows(b2);
+    cp_async_commit();
+    double acc = 0.0;
+    for (int64_t bi = 0; bi < nb; ++bi) {
+      if (bi == 0 || D < 2) cp_async_wait<0>();
+      else cp_async_wait<1>();
+      const int slot = (int)(bi % NRB);
+      mbar_wait(&bars[wid][slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      __syncwarp();
+      if (bi + D < nb) issue_rows(bi + D);
+      if (bi + D + 2 < nb) issue_recs(bi + D + 2);
+      cp_async_commit();
+      const double* ra0 = rowsA + slot * ROWBUF;
+      const double* ry0 = rowsC + slot * ROWBUF;
+      const double* rv = recs + (bi % NRC) * NB * 2;
+      constexpr int NG = NB / 8;
+      double a[NG][P::KS], d[NG][P::NT][2];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const double* ra = ra0 + (g * 8 + q) * ST;
+#pragma unroll
+        for (int j = 0; j < P::PAIRS; ++j) {
+          const double2 p2 = *reinterpret_cast<const double2*>(ra + 8 * j + 2 * c);
+          a[g][2 * j] = p2.x;
+          a[g][2 * j + 1] = p2.y;
+        }
+        if (P::SINGLE) a[g][P::KS - 1] = ra[8 * P::PAIRS + c];
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+          for (int nt = 0; nt < P::NT; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const double* ry = ry0 + (g * 8 + q) * ST;
+        double t = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt) {  // columns 20..23 are TMA zero fill
+          const double2 y = *reinterpret_cast<const double2*>(ry + 8 * nt + 2 * c);
+          t = fma(d[g][nt][0], y.x, t);
+          t = fma(d[g][nt][1], y.y, t);
+        }
+        acc = fma(rv[(g * 8 + q) * 2 + 1], t, acc);
+      }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) slice_out[i0] = acc;
+  }
+}
+
+template <int NB, int D>
+constexpr size_t t3t_smem_bytes() {
+  return (size_t)8 * (2 * (D + 1) * NB * kT3tST + (D + 3) * NB * 2) * 8;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*SkxEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool skx_factor_tmap(CUtensorMap* tm, const double* A, int64_t rows, int R, int box_cols) {
+  static SkxEncodeTiled enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      enc = nullptr;
+    if (enc == nullptr) return false;
+  }
+  if (rows >= (int64_t(1) << 31) || ((uintptr_t)A % 16) != 0 || (R * 8) % 16 != 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)R, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)R * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int R, int NB, int D>
 constexpr size_t t3a_smem_bytes() {
   return (size_t)8 * ((D + 1) * 2 * NB * T3A<R>::ST + (D + 3) * NB * 2) * 8;
@@ -972,7 +1197,21 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
   } while (0)
       // (row lookahead D = 2 with NB = 8 or one CTA per SM measured slower
       // in the pipeline: 592 / 610 vs 538 ms per config-5 call)
-      if (R1 == 20 && R2 == 20) {
+      CUtensorMap tmC;
+      // SKX_K7_ASYNC set: the all-cp.async kernel (A/B and test hook; read per call)
+      const bool force_async = getenv("SKX_K7_ASYNC") != nullptr;
+      if (R1 == 20 && R2 == 20 && !force_async &&
+          skx_factor_tmap(&tmC, A2, shape_h[2], 20, kT3tST)) {
+        // (variants measured at config 5, alone: NB = 16 / 2 CTAs per SM /
+        // lookahead 1 = 45.0 ms; NB = 8 with 3 or 4 CTAs 46.5 / 51.2; lookahead
+        // 2 59-67; epilogue of batch b-1 deferred behind batch b's DMMAs 56-82
+        // (register spills))
+        const size_t sm = t3t_smem_bytes<16, 1>();
+        cudaFuncSetAttribute(k_tucker3_tma<16, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm);
+        k_tucker3_tma<16, 2, 1><<<mb, 256, sm, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A1, core,
+                                                     R0, part);
+      } else if (R1 == 20 && R2 == 20) {
         SKX_T3A(20, 16, 2, 1);
       } else if (R1 == 10 && R2 == 10) {
         k_tucker3_mma<3, 2, 2, 10, 10, 2, true><<<mb, 256, 0, s>>>(colptr0, s0, rec, c1_mask, A0, A1,

@@ -660,17 +660,25 @@ def test_slice_hits_match_filter_gather(skx, packed):
 
 @pytest.mark.parametrize("shape,nnz,R", [((2000, 4000, 3000), 2_000_000, 20),
                                          ((50, 20000, 20000), 2_000_000, 20),
+                                         ((3000, 2000, 20), 1_000_000, 20),
                                          ((200000, 200000, 200000), 20_000_000, 20),
                                          ((100000, 100000, 100000), 10_000_000, 10),
                                          ((3000, 500, 700), 300_000, 7)])
-def test_tucker_cross_kernels_vs_einsum(skx, shape, nnz, R):
-    """The sparse fitness cross term (K7: cp.async-staged at R = 20, register
-    pipeline at R = 10, generic otherwise) against a chunked einsum, including
+@pytest.mark.parametrize("k7_async", [False, True])
+def test_tucker_cross_kernels_vs_einsum(skx, shape, nnz, R, k7_async, monkeypatch):
+    """The sparse fitness cross term (K7 at R = 20: mode-1 rows by cp.async and
+    mode-2 rows by TMA gather4 with zero-filled padding columns, or both by
+    cp.async; register pipeline at R = 10; generic otherwise) against a
+    chunked einsum, including a 20-row mode-2 factor (the whole TMA tensor),
     many short slices (config-5-like: ~100 nonzeros per slice, several
     pipelined batches each) and long ones."""
     import torch
     from paper_2104_01101_b200.synth import planted_cp_coo_device
     from paper_2104_01101_b200.tensors import device_of, tucker_cross_dev
+    if k7_async:
+        if R != 20:
+            pytest.skip("the cp.async / TMA choice exists at R = 20 only")
+        monkeypatch.setenv("SKX_K7_ASYNC", "1")  # mode-2 rows by cp.async instead of TMA
     coords, vals = planted_cp_coo_device(shape, nnz, rank=10, noise_sd=0.1, seed=1)
     d = device_of(skx.SparseTensor.from_device(shape, coords, vals, validate=False))
     g = torch.Generator(device="cuda").manual_seed(1)
