@@ -329,6 +329,21 @@ int skx_jacobi_svd(const double* a, int n, int64_t rs, int64_t cs, double* u, do
 int skx_lrls_mid(const double* rz, const double* b, int r, int w, double* q, double* x,
                  void* stream);
 
+/* Upper Cholesky factor R (R^T R = g) AND its inverse R^-1 of an SPD n x n
+ * Gram (row-major; n <= 512) in one CTA: blocked left-looking Cholesky and
+ * blocked bottom-up inverse on FP64 tensor cores.  *info = 0, or k+1 when
+ * pivot k is not positive (r and rinv are then zero).  The wide-system
+ * (r = prod of the other ranks > 128: configs 3 and 5) step of the Cholesky
+ * QR that stands in for reduced_qr(z) (src/linalg.py:38-52, called at
+ * src/linalg.py:103); replaces cuSOLVER potrf + a TRSM against I. */
+int skx_chol_inv_upper(const double* g, int n, double* r, double* rinv, int* info, void* stream);
+
+/* Thin Q (r x w row-major, w <= 32, w <= r) of the r x w row-major matrix c by
+ * Householder reflections with LAPACK's geqr2/org2r conventions, one CTA
+ * (2 r w doubles of shared memory).  The QR of X_ls G in rsvd_lrls
+ * (src/linalg.py:109) for wide systems (r > 128). */
+int skx_house_q(const double* c, int r, int w, double* q, void* stream);
+
 /* Skip-mode sparse TTMc of an order-3 COO tensor (ttmc(t, factors, skip=n),
  * src/tensors.py:261-277): from mode n's fibre-major layout (skx_coo_fibre /
  * skx_coo_fibre_ts with c1_mask), out (s_n x R1*R2, row-major; column

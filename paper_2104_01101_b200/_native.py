@@ -65,6 +65,8 @@ _SIGS = {
     "skx_sumsq": [c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_tsqr_r": [c_p, c_i64, c_i32, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_chol_upper": [c_p, c_i32, c_p, c_p, c_p],
+    "skx_chol_inv_upper": [c_p, c_i32, c_p, c_p, c_p, c_p],
+    "skx_house_q": [c_p, c_i32, c_i32, c_p, c_p],
     "skx_jacobi_svd": [c_p, c_i32, c_i64, c_i64, c_p, c_p, c_p, c_p],
     "skx_ttmc3_skip_coo": [c_i64, c_p, c_p, c_u32, c_p, c_i32, c_p, c_i32, c_p, c_p],
     "skx_cholqr_flags": [c_p, c_p, c_p, c_p, c_i32, c_p, c_p],

@@ -2,6 +2,8 @@
 // gather (src/sketching.py:193-217, 262-287; src/linalg.py:73-84).
 #include <cub/cub.cuh>
 
+#include <stdlib.h>
+
 #include "skx_common.cuh"
 
 namespace skx {
@@ -75,6 +77,73 @@ __global__ void k_lev_final(int64_t s, const double* __restrict__ part,
   lev_chunk(s, t, lo, hi);
   const double offs = part[t], L = tot[1];
   for (int64_t i = lo; i < hi; ++i) cdf[i] = (cdf[i] + offs) / L;
+}
+
+// The same five steps in ONE CTA (kLevFusedThreads threads, each owning the
+// chunks t, t + kLevFusedThreads, ...): identical arithmetic and order, so
+// identical bits; one launch and one SM instead of five launches over 32 SMs
+// (the leverage path runs beside the fitness pass, where every extra launch
+// waits for a free SM slot).
+constexpr int kLevFusedThreads = 512;
+constexpr int kLevPer = kLevChunks / kLevFusedThreads;
+
+__global__ void __launch_bounds__(kLevFusedThreads) k_lev_prepare1(const double* __restrict__ sc,
+                                                                  int64_t s, double* __restrict__ p,
+                                                                  double* __restrict__ cdf) {
+  __shared__ double part[kLevChunks];
+  __shared__ double tot[2];
+  const int t0 = threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kLevPer; ++u) {
+    int64_t lo, hi;
+    lev_chunk(s, t0 + u * kLevFusedThreads, lo, hi);
+    double acc = 0.0;
+    for (int64_t i = lo; i < hi; ++i) acc += fmax(sc[i], 0.0);
+    part[t0 + u * kLevFusedThreads] = acc;
+  }
+  __syncthreads();
+  if (t0 == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kLevChunks; ++i) t += part[i];
+    tot[0] = t;
+  }
+  __syncthreads();
+  const double total = tot[0];
+#pragma unroll
+  for (int u = 0; u < kLevPer; ++u) {
+    int64_t lo, hi;
+    lev_chunk(s, t0 + u * kLevFusedThreads, lo, hi);
+    double run = 0.0;
+    for (int64_t i = lo; i < hi; ++i) {
+      const double pi = fmax(sc[i], 0.0) / total;
+      p[i] = pi;
+      run += pi;
+      cdf[i] = run;
+    }
+    part[t0 + u * kLevFusedThreads] = run;
+  }
+  __syncthreads();
+  if (t0 == 0) {
+    const int64_t per = (s + kLevChunks - 1) / kLevChunks;
+    const int c_last = (int)((s - 1) / per);
+    double t = 0.0, last = 0.0;
+    for (int i = 0; i < kLevChunks; ++i) {
+      const double v = part[i];
+      part[i] = t;
+      if (i == c_last) last = v + t;
+      t += v;
+    }
+    tot[1] = last;
+  }
+  __syncthreads();
+  const double L = tot[1];
+#pragma unroll
+  for (int u = 0; u < kLevPer; ++u) {
+    int64_t lo, hi;
+    lev_chunk(s, t0 + u * kLevFusedThreads, lo, hi);
+    const double offs = part[t0 + u * kLevFusedThreads];
+    for (int64_t i = lo; i < hi; ++i) cdf[i] = (cdf[i] + offs) / L;
+  }
 }
 
 struct PtrPack {
@@ -373,6 +442,10 @@ extern "C" int skx_lev_prepare(const double* scores, int64_t s, double* p, doubl
   }
   SKX_REQUIRE(ar.ok(), "skx_lev_prepare: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  if (getenv("SKX_LEV_5K") == nullptr) {  // (the five-launch form stays for A/B runs)
+    k_lev_prepare1<<<1, kLevFusedThreads, 0, st>>>(scores, s, p, cdf);
+    return check_launch("k_lev_prepare1");
+  }
   const unsigned g = kLevChunks / 32;
   k_lev_sums<<<g, 32, 0, st>>>(scores, s, part);
   k_lev_total<<<1, 32, 0, st>>>(part, tot);

@@ -126,6 +126,34 @@ def chol_upper_dev(g):
     return r, info
 
 
+def chol_inv_upper_dev(g):
+    """Upper Cholesky factor R of an SPD n x n Gram (n <= 512) and R^-1, one
+    libskx CTA (blocked, FP64 tensor cores); returns (R, R^-1, info) with info
+    a device int (0 = success)."""
+    torch = _torch()
+    n = g.shape[0]
+    r = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    rinv = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    nat.call("skx_chol_inv_upper", nat.ptr(g.contiguous()), n, nat.ptr(r), nat.ptr(rinv),
+             nat.ptr(info), nat.stream())
+    return r, rinv, info
+
+
+def house_q_dev(c):
+    """Thin Householder Q (LAPACK sign convention) of a tall r x w matrix with
+    w <= 32, one libskx CTA."""
+    torch = _torch()
+    r, w = c.shape
+    q = torch.empty((r, w), dtype=torch.float64, device="cuda")
+    nat.call("skx_house_q", nat.ptr(c.contiguous()), r, w, nat.ptr(q), nat.stream())
+    return q
+
+
+CHOL_INV_MAX = 512
+HOUSE_Q_SMEM = 227 * 1024
+
+
 def jacobi_svd_dev(a):
     """SVD of a small square matrix (n <= 112) by one-sided Jacobi in one CTA:
     a = U diag(s) V^T, s descending."""
@@ -465,21 +493,32 @@ def sketch_qr_dev(z, defer=None):
     if m < r:
         return qr_flag_dev(z)
 
-    def chol(g):  # one-CTA libskx kernel up to 128; cuSOLVER potrf beyond (no host sync)
+    def chol(g):
+        """(R, R^-1 or None, info): one-CTA libskx kernels -- register Cholesky
+        up to 128, blocked Cholesky + inverse up to 512; cuSOLVER potrf beyond
+        (no host sync either way)."""
         if r <= 128:
-            return chol_upper_dev(g)
+            u, info = chol_upper_dev(g)
+            return u, None, info
+        if r <= CHOL_INV_MAX:
+            return chol_inv_upper_dev(g)
         u, info = torch.linalg.cholesky_ex(g, upper=True)
-        return u, info.view(1)
+        return u, None, info.view(1)
+
+    def inverse(u, uinv):
+        if uinv is None:
+            uinv = torch.linalg.solve_triangular(u, torch.eye(r, dtype=z.dtype, device=z.device),
+                                                 upper=True)
+        return uinv
 
     g1 = z.transpose(0, 1) @ z
-    r1, i1 = chol(g1)
+    r1, r1inv, i1 = chol(g1)
     if r <= 128:
         z1 = torch.linalg.solve_triangular(r1, z, upper=True, left=False)
     else:
-        # large r: one TRSM for R^-1 (r right-hand sides, parallel) and a GEMM,
-        # instead of a latency-bound TRSM with the m x r operand
-        eye = torch.eye(r, dtype=z.dtype, device=z.device)
-        r1inv = torch.linalg.solve_triangular(r1, eye, upper=True)
+        # large r: R^-1 (from the Cholesky kernel itself up to r = 512) and one
+        # GEMM, instead of a latency-bound TRSM with the m x r operand
+        r1inv = inverse(r1, r1inv)
         z1 = z @ r1inv
         r1._skx_inv = r1inv  # reused by assoc_mid_dev when the one-pass R is kept
     g2 = z1.transpose(0, 1) @ z1
@@ -495,9 +534,15 @@ def sketch_qr_dev(z, defer=None):
         return qr_flag_dev(z)
     if bool(flags[1]):
         return z1, r1, flags[2]
-    r2, i2 = chol(g2)
-    q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
+    r2, r2inv, i2 = chol(g2)
+    if r <= 128:
+        q = torch.linalg.solve_triangular(r2, z1, upper=True, left=False)
+    else:
+        r2inv = inverse(r2, r2inv)
+        q = z1 @ r2inv
     rz = r2 @ r1
+    if r > 128:
+        rz._skx_inv = r1inv @ r2inv  # (R2 R1)^-1
     tol = 1e-12 * torch.sqrt(torch.trace(g1))  # ||Z||_F
     bad = (torch.diagonal(rz).abs() < tol).any()
     flags2 = torch.stack([i2[0] != 0, bad]).cpu()
@@ -526,7 +571,9 @@ def assoc_mid_dev(qz, rz, yg):
     if rinv is None:
         rinv = torch.linalg.solve_triangular(rz, torch.eye(r, dtype=rz.dtype, device=rz.device),
                                              upper=True)
-    q, _ = torch.linalg.qr(rinv @ b, mode="reduced")
+    c = rinv @ b
+    q = house_q_dev(c) if w <= 32 and 2 * r * w * 8 <= HOUSE_Q_SMEM else \
+        torch.linalg.qr(c, mode="reduced")[0]
     return q, qz @ (rinv.transpose(0, 1) @ q)
 
 

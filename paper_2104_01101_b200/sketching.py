@@ -326,6 +326,27 @@ class LevSamplerOp:
         return np.ravel_multi_index(self.indices.T, self.extents)
 
 
+def _lev_profile(f, check):
+    """(scores, rank flag, p, cdf) of a factor, cached on the tensor: within a
+    sweep each factor serves two sub-problems (mode n samples the factors of
+    the other modes, and a factor is replaced -- not modified -- when its own
+    mode is solved), so the second use needs no recomputation.  The cache is
+    keyed by the check mode and the tensor's version counter."""
+    torch = _torch()
+    key = (bool(check), f._version)
+    ent = getattr(f, "_skx_lev", None)
+    if ent is not None and ent[0] == key:
+        return ent[1]
+    sc, bad = leverage_scores_dev(f, check=check)
+    p = torch.empty_like(sc)
+    cdf = torch.empty_like(sc)
+    nat.call_ws("skx_lev_prepare", (nat.ptr(sc), int(sc.numel()), nat.ptr(p), nat.ptr(cdf)),
+                slot=6)
+    val = (sc, bad, p, cdf)
+    f._skx_lev = (key, val)
+    return val
+
+
 def lev_sample_dev(factors, m, gen, check=True):
     """Random leverage sampler on device.  Computes every factor's scores
     first (QR rank check before any draw, as src/sketching.py:204-211), then
@@ -334,17 +355,11 @@ def lev_sample_dev(factors, m, gen, check=True):
     torch = _torch()
     if m < 1:
         raise ValueError("sample count must be positive")
-    scores, bads = [], []
+    scores, bads, ps, cdfs = [], [], [], []
     for f in factors:
-        sc, bad = leverage_scores_dev(f, check=check)
+        sc, bad, p, cdf = _lev_profile(f, check)
         scores.append(sc)
         bads.append(bad)
-    ps, cdfs = [], []
-    for sc in scores:
-        p = torch.empty_like(sc)
-        cdf = torch.empty_like(sc)
-        nat.call_ws("skx_lev_prepare", (nat.ptr(sc), int(sc.numel()), nat.ptr(p), nat.ptr(cdf)),
-                    slot=6)
         ps.append(p)
         cdfs.append(cdf)
     k = len(factors)

@@ -106,3 +106,46 @@ def test_y_passes_vs_torch(m, s, w, storage):
     W = torch.from_numpy(g.standard_normal((m, w))).cuda()
     assert relerr(y_times_dev(y, G).cpu().numpy(), yh @ G.cpu().numpy()) <= 1e-13
     assert relerr(ty_times_dev(W, y).cpu().numpy(), W.cpu().numpy().T @ yh) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [1, 31, 33, 129, 400, 512])
+def test_chol_inv_upper(n):
+    """One-CTA blocked Cholesky + inverse (r > 128: configs 3 and 5) vs LAPACK."""
+    import torch
+    from paper_2104_01101_b200.linalg import chol_inv_upper_dev
+    g = np.random.default_rng(n)
+    z = g.standard_normal((2 * n + 8, n)) @ np.diag(np.logspace(0, -2, n))
+    gram = z.T @ z
+    r, rinv, info = (x.cpu().numpy() for x in chol_inv_upper_dev(torch.from_numpy(gram).cuda()))
+    assert int(info[0]) == 0
+    rn = np.linalg.cholesky(gram).T
+    assert np.all(np.tril(r, -1) == 0) and np.all(np.tril(rinv, -1) == 0)
+    assert relerr(r, rn) <= 1e-12
+    assert relerr(rinv, np.linalg.inv(rn)) <= 1e-11
+    assert relerr(r @ rinv, np.eye(n)) <= 1e-12
+
+
+def test_chol_inv_upper_not_spd():
+    import torch
+    from paper_2104_01101_b200.linalg import chol_inv_upper_dev
+    g = np.random.default_rng(1)
+    a = g.standard_normal((300, 300))
+    gram = a @ a.T
+    gram[100, 100] = -1.0  # pivot 100 (or earlier) fails
+    r, rinv, info = (x.cpu().numpy() for x in chol_inv_upper_dev(torch.from_numpy(gram).cuda()))
+    assert 1 <= int(info[0]) <= 101
+    assert not r.any() and not rinv.any()
+
+
+@pytest.mark.parametrize("r,w", [(400, 30), (512, 18), (130, 32), (40, 7)])
+def test_house_q(r, w):
+    """Thin Householder Q of the associated middle step (r > 128) vs LAPACK:
+    same reflector convention, so Q itself matches numpy's."""
+    import torch
+    from paper_2104_01101_b200.linalg import house_q_dev
+    g = np.random.default_rng(r + w)
+    c = g.standard_normal((r, w)) @ np.diag(np.logspace(0, -8, w))
+    q = house_q_dev(torch.from_numpy(c).cuda()).cpu().numpy()
+    qn = np.linalg.qr(c)[0]
+    assert relerr(q, qn) <= 1e-10
+    assert relerr(q.T @ q, np.eye(w)) <= 1e-13
