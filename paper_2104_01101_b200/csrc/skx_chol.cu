@@ -22,6 +22,7 @@ namespace {
 constexpr int kCiThreads = 512;  // 16 warps
 constexpr int kCiWarps = kCiThreads / 32;
 constexpr int kCiMaxN = 512;
+constexpr int kCiTiles = 4;  // 8 x 8 output tiles per warp step (their C loads in flight together)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -33,135 +34,200 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // kernel by other warps of this CTA, so the non-coherent __ldg path is unsafe.
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
-constexpr int kSaLd = 36;  // SA row stride (doubles): = 4 mod 16, conflict-free fragment reads
-
-// acc[mt] += sum_k SA[k][8 mt + q] * B[k][col], k in [0, k_hi) (k_hi a multiple
-// of 4), for one 8-column tile starting at global column `col0` of row-major B
-// (leading dim ld); columns >= ncol and rows >= k_valid read as zero.
-// SA: shared, [k][kSaLd].
-__device__ __forceinline__ void panel_gemm_tile(const double* __restrict__ SA, const double* B,
-                                                int64_t ld, int col0, int ncol, int k_hi,
-                                                int k_valid, double (&acc)[4][2], int q, int c) {
-  const int col = col0 + q;
-  const bool live = col < ncol;
-  int k = 0;
-  // four B loads in flight per lane
-  for (; k + 16 <= k_hi; k += 16) {
-    double b[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int kk = k + 4 * u + c;
-      b[u] = (live && kk < k_valid) ? ldcg(B + (int64_t)kk * ld + col) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double* sa = SA + (k + 4 * u + c) * kSaLd + q;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) dmma(acc[mt][0], acc[mt][1], sa[8 * mt], b[u]);
-    }
-  }
-  for (; k < k_hi; k += 4) {
-    const int kk = k + c;
-    const double b = (live && kk < k_valid) ? ldcg(B + (int64_t)kk * ld + col) : 0.0;
-    const double* sa = SA + (k + c) * kSaLd + q;
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) dmma(acc[mt][0], acc[mt][1], sa[8 * mt], b);
-  }
-}
-
 }  // namespace
 
+// Leading dimension (doubles) of a shared [32][*] operand block holding
+// `cols` columns: >= cols and = 4 mod 16, so that the m8n8k4 fragment reads
+// (lane (q, c) -> row c, column q) of a half-warp hit 16 distinct 8-byte banks.
+// (cols is first rounded up to whole 8-column tiles and to the 32-wide diagonal
+// block, which every panel touches)
+__host__ __device__ __forceinline__ int ci_ld(int cols) {
+  const int x = 8 * ((max(cols, 32) + 7) / 8);
+  return x + (x % 16 == 0 ? 4 : 12);
+}
+
+// The 528 entries (i, j), i <= j, of a 32 x 32 upper triangle, two per thread
+// of the CTA (e = t and t + 512): the diagonal-block steps below touch one
+// entry per thread per step, with one barrier per step.
+__device__ __forceinline__ void ut_entry(int e, int& i, int& j) {
+  // row i holds 32 - i entries, starting at e_i = 32 i - i (i - 1) / 2
+  i = 0;
+  while (i < 31 && 32 * (i + 1) - (i + 1) * i / 2 <= e) ++i;
+  j = i + (e - (32 * i - i * (i - 1) / 2));
+}
+
+// Factor the SPD 32 x 32 block D (shared, leading dim ld; upper triangle
+// read) in place into upper R (R^T R = D) -- right-looking with the unscaled
+// update a_ij -= a_ki a_kj / a_kk, rows scaled at the end -- then X = R^-1
+// into Xo (leading dim 36) using V (36) as scratch.  Returns 0 or k+1 for the
+// first failing pivot.  All threads of the CTA call it.
+__device__ int cta_chol_inv32(double* D, int ld, double* V, double* Xo, int tid) {
+  int ei[2], ej[2];
+  bool own[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = tid + u * kCiThreads;
+    own[u] = e < 528;
+    ut_entry(own[u] ? e : 0, ei[u], ej[u]);
+  }
+  int bad = 0;
+  for (int k = 0; k < 32; ++k) {
+    const double akk = D[k * ld + k];
+    if (!(akk > 0.0)) {  // uniform (every thread reads the same pivot); NaN fails too
+      bad = k + 1;
+      break;
+    }
+    const double rp = 1.0 / akk;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (own[u] && ei[u] > k)
+        D[ei[u] * ld + ej[u]] = fma(-D[k * ld + ei[u]] * D[k * ld + ej[u]], rp, D[ei[u] * ld + ej[u]]);
+    __syncthreads();
+  }
+  if (bad) return bad;
+  // row k of R = row k / sqrt(a_kk); V = I
+  double rv[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    rv[u] = own[u] ? D[ei[u] * ld + ej[u]] / sqrt(D[ei[u] * ld + ei[u]]) : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (own[u]) {
+      const int i = ei[u], j = ej[u];
+      V[i * 36 + j] = i == j ? 1.0 : 0.0;
+      if (i != j) V[j * 36 + i] = 0.0;
+      Xo[j * 36 + i] = 0.0;  // lower part of the inverse (diagonal rewritten below)
+      D[i * ld + j] = rv[u];
+    }
+  __syncthreads();
+  // back substitution for all columns at once: step i finalises row i of X and
+  // removes it from the rows above
+  for (int i = 31; i >= 0; --i) {
+    const double rii = D[i * ld + i];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (own[u]) {
+        const int k = ei[u], j = ej[u];
+        if (j < i) continue;
+        const double xij = V[i * 36 + j] / rii;
+        if (k == i) Xo[i * 36 + j] = xij;
+        else if (k < i) V[k * 36 + j] = fma(-D[k * ld + i], xij, V[k * 36 + j]);
+      }
+    __syncthreads();
+  }
+  return 0;
+}
+
 // G: n x n SPD (row-major, symmetric; the upper triangle is read).  R, Rinv:
-// n x n row-major outputs (upper; zero below the diagonal); the block row being
-// formed is kept in place in R (resp. Rinv) between the GEMM and the solve.
-// info: 0, or k+1 for the first non-positive (or NaN) pivot k -- R and Rinv
-// are then zero.
+// n x n row-major outputs (upper; zero below the diagonal).  info: 0, or k+1
+// for the first non-positive (or NaN) pivot k -- R and Rinv are then zero.
+//
+// Right-looking blocked algorithms with 32-row panels, every GEMM operand in
+// shared memory (m8n8k4 FP64 tensor-core tiles, 8 x 8 outputs per warp item,
+// C tiles read and written once per panel in L2):
+//  Cholesky, panel p (rows P = [c0, c0 + 32) of R):  the block row of the
+//   trailing matrix (kept in R's own rows) -> shared; warp 0 factors the
+//   diagonal block and inverts it; the rest of the row is R_pp^-T times it (a
+//   32 x 32 x (n - c0 - 32) tile GEMM); the trailing upper triangle is
+//   updated A[i][j] -= sum_k R[c0+k][i] R[c0+k][j].
+//  Inverse X = R^-1, block rows bottom-up: W[Q] = I_Q + (the updates already
+//   subtracted), X[Q] = R_qq^-1 W[Q]; then every block row above takes its
+//   rank-32 update W[0:c0, c0:] -= R[0:c0, Q] X[Q, c0:].
 __global__ void __launch_bounds__(kCiThreads, 1) k_chol_inv(const double* __restrict__ G, int n,
                                                            double* R, double* Rinv,
                                                            int* __restrict__ info) {
-  extern __shared__ __align__(16) double SA[];  // [K][kSaLd] panel operand
-  __shared__ double Rpp[32][33];  // current diagonal block (factor, then inverse)
-  __shared__ double rdiag[32];
+  extern __shared__ __align__(16) double cism[];
+  __shared__ double Dinv[32][36];  // R_pp^-1 of the current panel
+  __shared__ double Vs[32 * 36];     // scratch of the diagonal-block inverse
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, q = lane >> 2, c = lane & 3;
   const int np = (n + 31) / 32;
   if (tid == 0) s_bad = 0;
+  // the trailing matrix lives in R's own rows; panel 0 reads G directly
   __syncthreads();
 
-  // ---------------- Cholesky, panel p: R rows [c0, c0 + w)
+  // ---------------- Cholesky
   for (int p = 0; p < np; ++p) {
-    const int c0 = 32 * p, w = min(32, n - c0), nc = n - c0;
-    for (int e = tid; e < c0 * 32; e += kCiThreads) {
-      const int k = e >> 5, m = e & 31;
-      SA[k * kSaLd + m] = m < w ? ldcg(R + (int64_t)k * n + c0 + m) : 0.0;
-    }
+    const int c0 = 32 * p, w = min(32, n - c0), nc = n - c0, ld = ci_ld(nc);
+    double* BR = cism;  // [32][ld]: block row, columns c0 .. n-1 (zero beyond)
+    const double* src = p == 0 ? G : R;  // first touch of the trailing matrix: G
+    for (int k = wid; k < 32; k += kCiWarps)
+      for (int j = lane; j < ld; j += 32)
+        BR[k * ld + j] = (k < w && j < nc && j >= k) ? ldcg(src + (int64_t)(c0 + k) * n + c0 + j) : 0.0;
     __syncthreads();
-    // block row: R[c0 + m][c0 + j] <- G[c0 + m][c0 + j] - sum_{k < c0} R[k][c0 + m] R[k][c0 + j]
-    const int ntile = (nc + 7) / 8;
-    for (int jt = wid; jt < ntile; jt += kCiWarps) {
-      double acc[4][2] = {};
-      if (c0 > 0) panel_gemm_tile(SA, R, n, c0 + 8 * jt, n, c0, c0, acc, q, c);
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int m = 8 * mt + q, j = 8 * jt + 2 * c + h;
-          if (m < w && j < nc)
-            R[(int64_t)(c0 + m) * n + c0 + j] = G[(int64_t)(c0 + m) * n + c0 + j] - acc[mt][h];
-        }
-    }
+    // partial last panel: identity beyond w in the diagonal block
+    for (int k = w + tid; k < 32; k += kCiThreads) BR[k * ld + k] = 1.0;
     __syncthreads();
-    // diagonal block: one warp, lane j holds column j of the upper triangle
-    if (wid == 0) {
-      double t[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        t[i] = (i <= lane && lane < w) ? ldcg(R + (int64_t)(c0 + i) * n + c0 + lane)
-                                       : (i == lane ? 1.0 : 0.0);
-      int bad = 0;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double piv = __shfl_sync(0xffffffffu, t[k], k);
-        if (!(piv > 0.0)) {  // warp-uniform; also catches NaN
-          bad = k + 1;
-          break;
-        }
-        const double d = sqrt(piv), rd = 1.0 / d;
-        if (lane == k) t[k] = d;
-        else if (lane > k) t[k] *= rd;  // r_kj
-        const double rkj = t[k];
-#pragma unroll
-        for (int i = k + 1; i < 32; ++i) {
-          const double rki = __shfl_sync(0xffffffffu, rkj, i);
-          if (lane >= i) t[i] = fma(-rki, rkj, t[i]);
-        }
-      }
-      if (bad && lane == 0) s_bad = c0 + bad;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) Rpp[i][lane] = i <= lane ? t[i] : 0.0;
-      if (!bad) rdiag[lane] = 1.0 / t[lane];
+    {
+      const int bad = cta_chol_inv32(BR, ld, Vs, &Dinv[0][0], tid);
+      if (bad && tid == 0) s_bad = c0 + bad;
+    }
+    // zero the padding rows of R_pp again (identity beyond w)
+    for (int e = tid; e < 32 * 32; e += kCiThreads) {
+      const int i = e >> 5, j = e & 31;
+      if (i >= w || j >= w || j < i) BR[i * ld + j] = 0.0;
     }
     __syncthreads();
     if (s_bad) break;
-    // the rest of the block row: R_pp^T X = T[:, 32:], one column per thread, in place
-    for (int j = 32 + tid; j < nc; j += kCiThreads) {
-      double* col = R + (int64_t)c0 * n + c0 + j;
-      double x[32];
+    // rest of the block row: R[P][c0+32+j] = (R_pp^-T B)[.][j], column tiles in place
+    const int rest = max(nc - 32, 0), rt = (rest + 7) / 8;
+    for (int jt = wid; jt < rt; jt += kCiWarps) {
+      double acc[4][2] = {};
+      const int j0 = 32 + 8 * jt;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        double v = ldcg(col + (int64_t)k * n);  // w = 32 whenever nc > 32
+      for (int ks = 0; ks < 8; ++ks) {
+        const double b = BR[(4 * ks + c) * ld + j0 + q];
 #pragma unroll
-        for (int i = 0; i < k; ++i) v = fma(-Rpp[i][k], x[i], v);
-        x[k] = v * rdiag[k];
+        for (int mt = 0; mt < 4; ++mt) dmma(acc[mt][0], acc[mt][1], Dinv[4 * ks + c][8 * mt + q], b);
       }
+      __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 32; ++k) col[(int64_t)k * n] = x[k];
+      for (int mt = 0; mt < 4; ++mt) {
+        BR[(8 * mt + q) * ld + j0 + 2 * c] = acc[mt][0];
+        BR[(8 * mt + q) * ld + j0 + 2 * c + 1] = acc[mt][1];
+      }
     }
-    // the diagonal block and the zero lower part of the block row
-    for (int e = tid; e < w * c0; e += kCiThreads) R[(int64_t)(c0 + e / c0) * n + e % c0] = 0.0;
-    for (int e = tid; e < w * w; e += kCiThreads) {
-      const int m = e / w, j = e % w;
-      R[(int64_t)(c0 + m) * n + c0 + j] = Rpp[m][j];
+    // Dinv -> the diagonal block of Rinv (read back by the inverse phase)
+    for (int i = wid; i < w; i += kCiWarps)
+      if (lane < w) Rinv[(int64_t)(c0 + i) * n + c0 + lane] = Dinv[i][lane];
+    __syncthreads();
+    // final R block row to global (zero left of the diagonal block)
+    for (int k = wid; k < w; k += kCiWarps)
+      for (int j = lane; j < n; j += 32) R[(int64_t)(c0 + k) * n + j] = j < c0 ? 0.0 : BR[k * ld + j - c0];
+    // trailing update of the upper triangle: rows / cols r0.., 8 x 8 tiles;
+    // warp per tile row (its A fragments in registers), four tiles in flight
+    const int r0 = c0 + 32;
+    for (int ti = wid; ti < rt; ti += kCiWarps) {
+      double a[8];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) a[ks] = -BR[(4 * ks + c) * ld + 32 + 8 * ti + q];
+      const int i = 8 * ti + q;
+      for (int tj = ti; tj < rt; tj += kCiTiles) {
+        double acc[kCiTiles][2];
+#pragma unroll
+        for (int v = 0; v < kCiTiles; ++v)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 8 * (tj + v) + 2 * c + h;
+            acc[v][h] = (tj + v < rt && i < rest && j < rest)
+                            ? ldcg(src + (int64_t)(r0 + i) * n + r0 + j) : 0.0;
+          }
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int v = 0; v < kCiTiles; ++v) {
+            const double b = tj + v < rt ? BR[(4 * ks + c) * ld + 32 + 8 * (tj + v) + q] : 0.0;
+            dmma(acc[v][0], acc[v][1], a[ks], b);
+          }
+#pragma unroll
+        for (int v = 0; v < kCiTiles; ++v)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 8 * (tj + v) + 2 * c + h;
+            if (tj + v < rt && i < rest && j < rest) R[(int64_t)(r0 + i) * n + r0 + j] = acc[v][h];
+          }
+      }
     }
     __syncthreads();
   }
@@ -174,71 +240,78 @@ __global__ void __launch_bounds__(kCiThreads, 1) k_chol_inv(const double* __rest
     return;
   }
 
-  // ---------------- inverse X = R^-1, block rows bottom-up:
-  // X[P, P] = R_pp^-1;  X[P, rest] = -R_pp^-1 (R[P, rest] X[rest, rest])
-  for (int p = np - 1; p >= 0; --p) {
-    const int c0 = 32 * p, w = min(32, n - c0), r0 = c0 + w, rest = n - r0;
-    const int rest4 = (rest + 3) & ~3;
-    for (int e = tid; e < rest4 * 32; e += kCiThreads) {  // SA[k][m] = R[c0 + m][r0 + k]
-      const int k = e >> 5, m = e & 31;
-      SA[k * kSaLd + m] = (m < w && k < rest) ? ldcg(R + (int64_t)(c0 + m) * n + r0 + k) : 0.0;
-    }
-    // diagonal block inverse: lane j back-substitutes R_pp x = e_j
-    if (wid == 0) {
-      double rp[32];  // rp[i] = R_pp[i][lane] (this lane's column)
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        rp[i] = (i < w && lane < w) ? ldcg(R + (int64_t)(c0 + i) * n + c0 + lane)
-                                    : (i == lane ? 1.0 : 0.0);
-      double x[32];
-#pragma unroll
-      for (int i = 31; i >= 0; --i) {
-        double v = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = i + 1; k < 32; ++k) v = fma(-__shfl_sync(0xffffffffu, rp[i], k), x[k], v);
-        const double rii = __shfl_sync(0xffffffffu, rp[i], i);
-        x[i] = (i <= lane) ? v / rii : 0.0;
+  // ---------------- inverse, block rows bottom-up
+  for (int Q = np - 1; Q >= 0; --Q) {
+    const int c0 = 32 * Q, w = min(32, n - c0), nq = n - c0, ld = ci_ld(nq);
+    double* BX = cism;             // [32][ld]: W then X block row, columns c0 ..
+    double* RC = cism + 32 * ld;   // [c0][36]: R[m][c0 + k]
+    // W[Q] = I_Q beside the updates accumulated in Rinv's block row (the
+    // bottom block row has none)
+    for (int k = wid; k < 32; k += kCiWarps)
+      for (int j = lane; j < ld; j += 32) {
+        double v = 0.0;
+        if (k < w && j < nq)
+          v = j < 32 ? (j == k ? 1.0 : 0.0) : ldcg(Rinv + (int64_t)(c0 + k) * n + c0 + j);
+        BX[k * ld + j] = v;
       }
+    for (int i = wid; i < 32; i += kCiWarps)
+      Dinv[i][lane] = (i < w && lane < w) ? ldcg(Rinv + (int64_t)(c0 + i) * n + c0 + lane) : 0.0;
+    for (int m = wid; m < c0; m += kCiWarps)
+      RC[m * 36 + lane] = lane < w ? ldcg(R + (int64_t)m * n + c0 + lane) : 0.0;
+    __syncthreads();
+    // X[Q] = R_qq^-1 W[Q], column tiles in place
+    const int nt = (nq + 7) / 8;
+    for (int jt = wid; jt < nt; jt += kCiWarps) {
+      double acc[4][2] = {};
+      const int j0 = 8 * jt;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) Rpp[i][lane] = x[i];
+      for (int ks = 0; ks < 8; ++ks) {
+        const double b = BX[(4 * ks + c) * ld + j0 + q];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma(acc[mt][0], acc[mt][1], Dinv[8 * mt + q][4 * ks + c], b);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        BX[(8 * mt + q) * ld + j0 + 2 * c] = acc[mt][0];
+        BX[(8 * mt + q) * ld + j0 + 2 * c + 1] = acc[mt][1];
+      }
     }
     __syncthreads();
-    if (rest > 0) {
-      // Y = R[P, rest] X[rest, rest] into X's own block row (X upper
-      // triangular: output column j needs rows k <= j only)
-      const int ntile = (rest + 7) / 8;
-      for (int jt = wid; jt < ntile; jt += kCiWarps) {
-        double acc[4][2] = {};
-        const int khi = min(rest4, (8 * jt + 8 + 3) & ~3);
-        panel_gemm_tile(SA, Rinv + (int64_t)r0 * n, n, r0 + 8 * jt, n, khi, rest, acc, q, c);
+    for (int k = wid; k < w; k += kCiWarps)
+      for (int j = lane; j < n; j += 32) Rinv[(int64_t)(c0 + k) * n + j] = j < c0 ? 0.0 : BX[k * ld + j - c0];
+    // W[0:c0, c0:] -= R[0:c0, Q] X[Q, c0:]: warp per tile row, four tiles in flight
+    const int mtile = c0 / 8;
+    for (int ti = wid; ti < mtile; ti += kCiWarps) {
+      double a[8];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
+      for (int ks = 0; ks < 8; ++ks) a[ks] = -RC[(8 * ti + q) * 36 + 4 * ks + c];
+      const int i = 8 * ti + q;
+      for (int tj = 0; tj < nt; tj += kCiTiles) {
+        double acc[kCiTiles][2];
+#pragma unroll
+        for (int v = 0; v < kCiTiles; ++v)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int m = 8 * mt + q, j = 8 * jt + 2 * c + h;
-            if (m < w && j < rest) Rinv[(int64_t)(c0 + m) * n + r0 + j] = acc[mt][h];
+            const int j = 8 * (tj + v) + 2 * c + h;
+            // first touch (the block's own 32 columns): the update starts from 0
+            acc[v][h] = (tj + v < nt && j < nq && j >= 32) ? ldcg(Rinv + (int64_t)i * n + c0 + j) : 0.0;
+          }
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+          for (int v = 0; v < kCiTiles; ++v) {
+            const double b = tj + v < nt ? BX[(4 * ks + c) * ld + 8 * (tj + v) + q] : 0.0;
+            dmma(acc[v][0], acc[v][1], a[ks], b);
+          }
+#pragma unroll
+        for (int v = 0; v < kCiTiles; ++v)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = 8 * (tj + v) + 2 * c + h;
+            if (tj + v < nt && j < nq) Rinv[(int64_t)i * n + c0 + j] = acc[v][h];
           }
       }
-      __syncthreads();
-      // X[P, rest] = -R_pp^-1 Y, one column per thread, in place
-      for (int j = tid; j < rest; j += kCiThreads) {
-        double* col = Rinv + (int64_t)c0 * n + r0 + j;
-        double y[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) y[k] = k < w ? ldcg(col + (int64_t)k * n) : 0.0;
-#pragma unroll
-        for (int m = 0; m < 32; ++m) {
-          double v = 0.0;
-#pragma unroll
-          for (int k = m; k < 32; ++k) v = fma(Rpp[m][k], y[k], v);
-          if (m < w) col[(int64_t)m * n] = -v;
-        }
-      }
-    }
-    for (int e = tid; e < w * c0; e += kCiThreads) Rinv[(int64_t)(c0 + e / c0) * n + e % c0] = 0.0;
-    for (int e = tid; e < w * w; e += kCiThreads) {
-      const int m = e / w, j = e % w;
-      Rinv[(int64_t)(c0 + m) * n + c0 + j] = Rpp[m][j];
     }
     __syncthreads();
   }
@@ -330,8 +403,9 @@ using namespace skx;
 extern "C" int skx_chol_inv_upper(const double* g, int n, double* r, double* rinv, int* info,
                                   void* stream) {
   SKX_REQUIRE(n >= 1 && n <= kCiMaxN, "skx_chol_inv_upper: 1 <= n <= %d", kCiMaxN);
-  // the staged panel operand: at most n rows of kSaLd doubles
-  const size_t smem = (size_t)((n + 3) & ~3) * kSaLd * 8;
+  // Cholesky: a 32-row block row; inverse: that plus the 32-column block of R
+  size_t smem = (size_t)32 * ci_ld(n) * 8;
+  for (int c0 = 0; c0 < n; c0 += 32) smem = std::max(smem, (size_t)(32 * ci_ld(n - c0) + 36 * c0) * 8);
   SKX_REQUIRE(smem <= (size_t)max_smem_optin(), "skx_chol_inv_upper: n = %d needs %zu B of shared memory",
               n, smem);
   cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

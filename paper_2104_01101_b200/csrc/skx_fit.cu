@@ -672,7 +672,14 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm,
 
 constexpr int kT3tR = 20, kT3tST = 24;  // rank, smem row stride (doubles)
 
-template <int NB, int MB, int D>
+// LEFT: the fourth-from-last n columns of W (16..19, which a third 8-wide
+// n-tile would pad to 24) go to the FP64 FMA pipe instead: each lane forms the
+// partial products of its own five A-fragment k values with W[k][16..19] and
+// dots them with a1[16..19]; the per-lane partials sum to the full term in
+// the warp reduction at the end of the slice.  The FP64 pipe (shared by DMMA
+// and DFMA) then does 10 DMMA + 29 DFMA per 8 nonzeros instead of 15 + 7:
+// ~14% fewer issue slots, no padded work.
+template <int NB, int MB, int D, bool LEFT = false>
 __global__ void __launch_bounds__(256, MB) k_tucker3_tma(
     const __grid_constant__ CUtensorMap tmC, const int64_t* __restrict__ colptr, int64_t s0,
     const double* __restrict__ rec, uint32_t c1_mask, const double* __restrict__ A0,
@@ -751,11 +758,12 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma(
         }
       }
     };
-    double b[P::KS][P::NT];
+    constexpr int NTD = LEFT ? 2 : P::NT;  // n-tiles on the tensor cores
+    double b[P::KS][NTD];
 #pragma unroll
     for (int ks = 0; ks < P::KS; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < P::NT; ++nt) {
+      for (int nt = 0; nt < NTD; ++nt) {
         const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
         const int n = nt * 8 + q;
         double w = 0.0;
@@ -764,6 +772,19 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma(
             w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + n), w);
         b[ks][nt] = w;
       }
+    double wl[LEFT ? P::KS : 1][4];  // W[k(ks, c)][16 + j]
+    if (LEFT) {
+#pragma unroll
+      for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
+          double w = 0.0;
+          for (int r0 = 0; r0 < R0; ++r0)
+            w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + 16 + j), w);
+          wl[LEFT ? ks : 0][j] = w;
+        }
+    }
     for (int64_t b2 = 0; b2 < D + 2 && b2 < nb; ++b2) issue_recs(b2);
     cp_async_commit();
     cp_async_wait<0>();
@@ -785,7 +806,7 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma(
       const double* ry0 = rowsC + slot * ROWBUF;
       const double* rv = recs + (bi % NRC) * NB * 2;
       constexpr int NG = NB / 8;
-      double a[NG][P::KS], d[NG][P::NT][2];
+      double a[NG][P::KS], d[NG][NTD][2];
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         const double* ra = ra0 + (g * 8 + q) * ST;
@@ -797,20 +818,36 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma(
         }
         if (P::SINGLE) a[g][P::KS - 1] = ra[8 * P::PAIRS + c];
 #pragma unroll
-        for (int nt = 0; nt < P::NT; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
+        for (int nt = 0; nt < NTD; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
       }
 #pragma unroll
       for (int ks = 0; ks < P::KS; ++ks)
 #pragma unroll
         for (int g = 0; g < NG; ++g)
 #pragma unroll
-          for (int nt = 0; nt < P::NT; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
+          for (int nt = 0; nt < NTD; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         const double* ry = ry0 + (g * 8 + q) * ST;
         double t = 0.0;
+        if (LEFT) {  // columns 16..19 on the FMA pipe: this lane's k values only
+          double pl[4];
 #pragma unroll
-        for (int nt = 0; nt < P::NT; ++nt) {  // columns 20..23 are TMA zero fill
+          for (int j = 0; j < 4; ++j) {
+            double v = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < P::KS; ++ks) v = fma(a[g][ks], wl[LEFT ? ks : 0][j], v);
+            pl[j] = v;
+          }
+          const double2 y0 = *reinterpret_cast<const double2*>(ry + 16);
+          const double2 y1 = *reinterpret_cast<const double2*>(ry + 18);
+          t = fma(pl[0], y0.x, t);
+          t = fma(pl[1], y0.y, t);
+          t = fma(pl[2], y1.x, t);
+          t = fma(pl[3], y1.y, t);
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTD; ++nt) {  // (without LEFT: columns 20..23 are TMA zero fill)
           const double2 y = *reinterpret_cast<const double2*>(ry + 8 * nt + 2 * c);
           t = fma(d[g][nt][0], y.x, t);
           t = fma(d[g][nt][1], y.y, t);
@@ -829,6 +866,169 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma(
 template <int NB, int D>
 constexpr size_t t3t_smem_bytes() {
   return (size_t)8 * (2 * (D + 1) * NB * kT3tST + (D + 3) * NB * 2) * 8;
+}
+
+// R = 20, variant 2: the mode-2 rows (the DMMA A operand) by TMA gather4 into
+// shared memory as in k_tucker3_tma, but the mode-1 rows -- needed only in
+// the epilogue dot t = sum_n T[e][n] a1_e[n] -- go straight from L2 into
+// registers in the D-fragment layout (lane (q, c): a1_q[8 nt + 2c, +1], three
+// 16-byte loads, the last for c < 2 only), issued one batch ahead.  No
+// cp.async row copies and no shared-memory reads of those rows: the L1 data
+// pipe (the binding unit of k_tucker3_tma: ~4.6e9 cp.async + 1e9 fragment
+// wavefronts per 1e9 nonzeros) only serves the TMA rows' fragments and the
+// records.  tools/micro/gather.cu: register-fragment 16-byte gathers run at
+// ~72 G rows/s against ~106 for whole-row copies, but they skip the
+// shared-memory write and read entirely.
+template <int NB, int MB, int D>
+__global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
+    const __grid_constant__ CUtensorMap tmC, const int64_t* __restrict__ colptr, int64_t s0,
+    const double* __restrict__ rec, uint32_t c1_mask, const double* __restrict__ A0,
+    const double* __restrict__ A2, const double* __restrict__ C, int R0,
+    double* __restrict__ slice_out) {
+  constexpr int R = kT3tR, ST = kT3tST;
+  using P = T3A<R>;
+  constexpr int ROWBUF = NB * ST;  // doubles per row buffer
+  constexpr int NRB = D + 1, NRC = D + 3;
+  constexpr uint32_t TX = NB * ST * 8;
+  constexpr int NG = NB / 8;
+  extern __shared__ __align__(128) double t3sm[];
+  __shared__ __align__(8) uint64_t bars[8][NRB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane >> 2, c = lane & 3;
+  double* rowsC = t3sm + (size_t)wid * (NRB * ROWBUF + NRC * NB * 2);
+  double* recs = rowsC + NRB * ROWBUF;
+  if (lane == 0)
+    for (int b = 0; b < NRB; ++b) mbar_init(&bars[wid][b], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t phase = 0;
+  const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
+  for (int64_t i0 = blockIdx.x * nw + wid; i0 < s0; i0 += stride) {
+    {  // the next slice's records into L2
+      const int64_t j = i0 + stride;
+      if (j < s0) {
+        const int64_t l0 = colptr[j] * 16 / 128, l1 = (colptr[j + 1] * 16 + 127) / 128;
+        for (int64_t l = l0 + lane; l < l1; l += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(rec) + l * 128));
+      }
+    }
+    const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
+    if (e0 == e1) {
+      if (lane == 0) slice_out[i0] = 0.0;
+      continue;
+    }
+    const int64_t nb = (e1 - e0 + NB - 1) / NB;
+    auto issue_recs = [&](int64_t b) {
+      if (lane < NB) {
+        const int64_t e = e0 + b * NB + lane;
+        cp_async16_cg_zfill(smem_addr(recs + ((b % NRC) * NB + lane) * 2),
+                            rec + 2 * (e < e1 ? e : e0), e < e1 ? 16u : 0u);
+      }
+    };
+    auto issue_rows = [&](int64_t b) {  // mode-1 rows (tmC maps A1): TMA, one gather4 per four records
+      const int slot = (int)(b % NRB);
+      const uint32_t* rb = reinterpret_cast<const uint32_t*>(recs + (b % NRC) * NB * 2);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0) mbar_expect_tx(&bars[wid][slot], TX);
+      __syncwarp();
+      if (lane < NB / 4) {
+        const int32_t i0_ = (int32_t)rb[(4 * lane + 0) * 4];
+        const int32_t i1_ = (int32_t)rb[(4 * lane + 1) * 4];
+        const int32_t i2_ = (int32_t)rb[(4 * lane + 2) * 4];
+        const int32_t i3_ = (int32_t)rb[(4 * lane + 3) * 4];
+        tma_gather4(smem_addr(rowsC + slot * ROWBUF + 4 * lane * ST), &tmC, &bars[wid][slot], 0,
+                    i0_, i1_, i2_, i3_);
+      }
+    };
+    // mode-2 rows of batch b straight into D-fragment registers
+    double2 y[NG][P::NT];
+    auto load_y = [&](int64_t b) {
+      const uint32_t* rb = reinterpret_cast<const uint32_t*>(recs + (b % NRC) * NB * 2);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const double2* row =
+            reinterpret_cast<const double2*>(A2 + (int64_t)(rb[(g * 8 + q) * 4 + 1] & c1_mask) * R);
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt)
+          y[g][nt] = (nt * 8 + 2 * c < R) ? __ldg(row + nt * 4 + c) : make_double2(0.0, 0.0);
+      }
+    };
+    double b[P::KS][P::NT];
+#pragma unroll
+    for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < P::NT; ++nt) {
+        const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
+        const int n = nt * 8 + q;
+        double w = 0.0;
+        if (k < R && n < R)
+          for (int r0 = 0; r0 < R0; ++r0)
+            w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + n), w);
+        b[ks][nt] = w;
+      }
+    for (int64_t b2 = 0; b2 < D + 2 && b2 < nb; ++b2) issue_recs(b2);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int64_t b2 = 0; b2 < D && b2 < nb; ++b2) issue_rows(b2);
+    load_y(0);
+    double acc = 0.0;
+    for (int64_t bi = 0; bi < nb; ++bi) {
+      cp_async_wait<0>();  // records of bi + 1 .. bi + D + 1
+      const int slot = (int)(bi % NRB);
+      mbar_wait(&bars[wid][slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      __syncwarp();
+      if (bi + D < nb) issue_rows(bi + D);
+      if (bi + D + 2 < nb) issue_recs(bi + D + 2);
+      cp_async_commit();
+      const double* ra0 = rowsC + slot * ROWBUF;
+      const double* rv = recs + (bi % NRC) * NB * 2;
+      double a[NG][P::KS], d[NG][P::NT][2];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        const double* ra = ra0 + (g * 8 + q) * ST;
+#pragma unroll
+        for (int j = 0; j < P::PAIRS; ++j) {
+          const double2 p2 = *reinterpret_cast<const double2*>(ra + 8 * j + 2 * c);
+          a[g][2 * j] = p2.x;
+          a[g][2 * j + 1] = p2.y;
+        }
+        if (P::SINGLE) a[g][P::KS - 1] = ra[8 * P::PAIRS + c];
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
+      }
+      double vq[NG];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) vq[g] = rv[(g * 8 + q) * 2 + 1];
+#pragma unroll
+      for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+          for (int nt = 0; nt < P::NT; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        double t = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < P::NT; ++nt) {
+          t = fma(d[g][nt][0], y[g][nt].x, t);
+          t = fma(d[g][nt][1], y[g][nt].y, t);
+        }
+        acc = fma(vq[g], t, acc);
+      }
+      if (bi + 1 < nb) load_y(bi + 1);  // consumed at the end of the next batch
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) slice_out[i0] = acc;
+  }
+}
+
+template <int NB, int D>
+constexpr size_t t3t2_smem_bytes() {
+  return (size_t)8 * ((D + 1) * NB * kT3tST + (D + 3) * NB * 2) * 8;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -1207,10 +1407,40 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
         // 2 59-67; epilogue of batch b-1 deferred behind batch b's DMMAs 56-82
         // (register spills))
         const size_t sm = t3t_smem_bytes<16, 1>();
-        cudaFuncSetAttribute(k_tucker3_tma<16, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm);
-        k_tucker3_tma<16, 2, 1><<<mb, 256, sm, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A1, core,
-                                                     R0, part);
+        // default: k_tucker3_tma2 (mode-1 rows by TMA, mode-2 rows into
+        // registers; config 5 alone: 36.9 ms per 1e9-nonzero pass against 43.4
+        // for k_tucker3_tma with the FMA-pipe tail and 45.1 padded).
+        // SKX_K7=1: k_tucker3_tma (A/B); SKX_K7=2[D][MB]: tma2 variants
+        const char* k7v = getenv("SKX_K7");
+        if ((k7v == nullptr || k7v[0] == '2') &&
+            skx_factor_tmap(&tmC, A1, shape_h[1], 20, kT3tST)) {  // mode-2 rows into registers
+          const int dd = (k7v != nullptr && k7v[1] == '2') ? 2 : 1;
+          const int mbb = (k7v != nullptr && k7v[1] != 0 && k7v[2] == '3') ? 3 : 2;
+#define SKX_T3T2(MBB, DD)                                                                     \
+  do {                                                                                        \
+    const size_t sm2 = t3t2_smem_bytes<16, DD>();                                             \
+    cudaFuncSetAttribute(k_tucker3_tma2<16, MBB, DD>,                                         \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);              \
+    k_tucker3_tma2<16, MBB, DD><<<mb, 256, sm2, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A2,  \
+                                                     core, R0, part);                         \
+  } while (0)
+          if (dd == 1 && mbb == 2) SKX_T3T2(2, 1);
+          else if (dd == 2 && mbb == 2) SKX_T3T2(2, 2);
+          else if (dd == 1) SKX_T3T2(3, 1);
+          else SKX_T3T2(3, 2);
+#undef SKX_T3T2
+        } else if (getenv("SKX_K7_PAD") == nullptr &&
+                   skx_factor_tmap(&tmC, A2, shape_h[2], 20, kT3tST)) {  // 16..19 on the FMA pipe
+          cudaFuncSetAttribute(k_tucker3_tma<16, 2, 1, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          k_tucker3_tma<16, 2, 1, true><<<mb, 256, sm, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A1,
+                                                             core, R0, part);
+        } else {  // (A/B: padded third n-tile on the tensor cores)
+          cudaFuncSetAttribute(k_tucker3_tma<16, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm);
+          k_tucker3_tma<16, 2, 1><<<mb, 256, sm, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A1, core,
+                                                       R0, part);
+        }
       } else if (R1 == 20 && R2 == 20) {
         SKX_T3A(20, 16, 2, 1);
       } else if (R1 == 10 && R2 == 10) {

@@ -10,6 +10,7 @@ the drivers (the *_dev functions).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -500,7 +501,7 @@ def sketch_qr_dev(z, defer=None):
         if r <= 128:
             u, info = chol_upper_dev(g)
             return u, None, info
-        if r <= CHOL_INV_MAX:
+        if r <= CHOL_INV_MAX and not os.environ.get("SKX_CHOL_CUSOLVER"):  # (env: A/B runs)
             return chol_inv_upper_dev(g)
         u, info = torch.linalg.cholesky_ex(g, upper=True)
         return u, None, info.view(1)

@@ -111,6 +111,58 @@ __global__ void __launch_bounds__(256) k_ldg4(const double* __restrict__ A, cons
   if (acc == 12345.678) out[0] = acc;
 }
 
+
+__global__ void __launch_bounds__(256) k_ldgf16(const double* __restrict__ A, const int* __restrict__ idx,
+                                                int64_t n, double* out) {
+  // register fragments for the K7 dot, 16-byte loads: lane (q, c) of a group of
+  // 8 rows loads cols {2c, 2c+1} and {8+2c, 9+2c} of row q plus cols 16..19
+  // (the same 32 bytes for the 4 lanes of a quad)
+  const int lane = threadIdx.x & 31, q = lane >> 2, c = lane & 3;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int64_t base = gw * 16; base + 16 <= n; base += tw * 16) {
+    double2 v[2][4];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const double2* row = reinterpret_cast<const double2*>(A + (int64_t)idx[base + g * 8 + q] * R);
+      v[g][0] = __ldg(row + c);
+      v[g][1] = __ldg(row + 4 + c);
+      v[g][2] = __ldg(row + 8);
+      v[g][3] = __ldg(row + 9);
+    }
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += v[g][u].x + v[g][u].y;
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_ldgf16b(const double* __restrict__ A, const int* __restrict__ idx,
+                                                 int64_t n, double* out) {
+  // as k_ldgf16 but cols 16..19 one per lane (LDG.64): 2 LDG.128 + 1 LDG.64
+  const int lane = threadIdx.x & 31, q = lane >> 2, c = lane & 3;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int64_t base = gw * 16; base + 16 <= n; base += tw * 16) {
+    double2 v[2][2];
+    double t[2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const double* rp = A + (int64_t)idx[base + g * 8 + q] * R;
+      const double2* row = reinterpret_cast<const double2*>(rp);
+      v[g][0] = __ldg(row + c);
+      v[g][1] = __ldg(row + 4 + c);
+      t[g] = __ldg(rp + 16 + c);
+    }
+#pragma unroll
+    for (int g = 0; g < 2; ++g) acc += v[g][0].x + v[g][0].y + v[g][1].x + v[g][1].y + t[g];
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
 int main() {
   const int64_t rows = 200000, n = 1 << 26;
   double* A;
@@ -134,14 +186,16 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int which = 0; which < 3; ++which) {
+  for (int which = 0; which < 5; ++which) {
     for (int ctas_per_sm = 1; ctas_per_sm <= 4; ctas_per_sm *= 2) {
       const int grid = sms * ctas_per_sm * (which == 0 ? 1 : 4);
       for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
         if (which == 0) k_tma<<<grid, WARPS * 32, smem>>>(A, idx, n, out);
         else if (which == 1) k_ldg10<<<grid, 256>>>(A, idx, n, out);
-        else k_ldg4<<<grid, 256>>>(A, idx, n, out);
+        else if (which == 2) k_ldg4<<<grid, 256>>>(A, idx, n, out);
+        else if (which == 3) k_ldgf16<<<grid, 256>>>(A, idx, n, out);
+        else k_ldgf16b<<<grid, 256>>>(A, idx, n, out);
         cudaEventRecord(e1);
         CK(cudaEventSynchronize(e1));
         CK(cudaGetLastError());
@@ -149,7 +203,7 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         if (rep == 2)
           printf("%-8s grid %6d: %.3f ms  %.2f Grows/s  %.2f TB/s rows\n",
-                 which == 0 ? "tma" : which == 1 ? "ldg10" : "ldg4(K7)", grid, ms, n / ms / 1e6,
+                 which == 0 ? "tma" : which == 1 ? "ldg10" : which == 2 ? "ldg4(K7)" : which == 3 ? "ldgf16" : "ldgf16b", grid, ms, n / ms / 1e6,
                  n * (double)ROWB / ms / 1e9);
       }
     }
