@@ -192,6 +192,8 @@ def kernel_work(cfgd, nnz, s0):
         w["skx_ts_rhs_coo"] = dict(bound="hbm", unit="GB/s",
                                    bytes=rec + s0 * cfgd.get("sketch_size", 0) * 8)
         w["skx_rrf_stage1_coo"] = dict(bound="hbm", unit="GB/s", bytes=rec)
+        # partition: coords (3 x 4 B) + value read, two 16-byte records written
+        w["skx_rrf_partition"] = dict(bound="hbm", unit="GB/s", bytes=nnz * (20 + 32))
     return w
 
 
@@ -272,7 +274,8 @@ def run_ours(args, cfgd):
                   "skx_rrf_stage1_fx", "skx_lemire_scan",
                   "skx_filter_fibers_coo", "skx_coo_fibre", "skx_ts_rhs_coo", "skx_resid_sq",
                   "skx_ts_kron_apply", "skx_philox_normal", "skx_tsqr_r", "skx_cp_core_als",
-                  "skx_rrf_stage1_dense", "skx_ts_rhs_dense"]
+                  "skx_rrf_stage1_dense", "skx_ts_rhs_dense", "skx_rrf_stage1_rec",
+                  "skx_rrf_partition", "skx_chol_inv_upper"]
     sinks = {nm: [] for nm in hook_names}
     for nm in hook_names:
         nat.set_event_hook(nm, sinks[nm])

@@ -344,6 +344,29 @@ int skx_chol_inv_upper(const double* g, int n, double* r, double* rinv, int* inf
  * (src/linalg.py:109) for wide systems (r > 128). */
 int skx_house_q(const double* c, int r, int w, double* q, void* stream);
 
+/* RRF stage 1 with L2-resident accumulators (leverage runs, config 5): the
+ * nonzeros of the lexsorted order-ndim COO (int32 SoA coords, ndim rows of
+ * nnz) partitioned by output row block for up to two RRF modes (modes_h[0..
+ * nmode-1]) into records key = i_n << 40 | j (j = flat other-mode index,
+ * others ascending, first slowest -- the unfolding column of
+ * src/tensors.py:151-166), value.  RNG-independent: runs while the rejection
+ * scans occupy the SMs.  Workspace queried with ws = NULL. */
+int skx_rrf_partition(int ndim, const int64_t* shape_h, int64_t nnz, const int32_t* coords,
+                      const double* vals, int nmode, const int* modes_h, uint64_t* key0,
+                      double* val0, uint64_t* key1, double* val1, void* ws, size_t* ws_bytes,
+                      void* stream);
+
+/* Stage 1 of the RRF composite sketch (src/sketching.py:327-341 with the
+ * tables of :305-324) of one mode from its partitioned records: exact
+ * fixed-point sums as skx_rrf_stage1_fx (bitwise the same result), with the
+ * accumulator rows of the current row block resident in L2.  rows = the
+ * mode's coordinate row of the COO (row-count bound for the limb count). */
+int skx_rrf_stage1_rec(int64_t s_n, uint64_t P, int64_t nnz, const int32_t* rows,
+                       const uint64_t* keys, const double* vals, int emax, uint64_t k0,
+                       uint64_t k1, uint64_t p0, uint32_t has_pending, uint32_t pending,
+                       uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
+                       double* stage1, void* ws, size_t* ws_bytes, void* stream);
+
 /* Skip-mode sparse TTMc of an order-3 COO tensor (ttmc(t, factors, skip=n),
  * src/tensors.py:261-277): from mode n's fibre-major layout (skx_coo_fibre /
  * skx_coo_fibre_ts with c1_mask), out (s_n x R1*R2, row-major; column

@@ -59,6 +59,10 @@ _SIGS = {
     "skx_rrf_stage1_fx_acc": [c_i32, c_p, c_i32, c_i64, c_p, c_i64, c_p, c_i32, c_u64, c_u64, c_u64,
                               c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p, c_p],
     "skx_rrf_stage1_fx_convert": [c_p, c_i64, c_i32, c_p, c_p, c_p],
+    "skx_rrf_partition": [c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p,
+                          c_p],
+    "skx_rrf_stage1_rec": [c_i64, c_u64, c_i64, c_p, c_p, c_p, c_i32, c_u64, c_u64, c_u64, c_u32,
+                           c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_rrf_table": [c_u64, c_u64, c_u64, c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_i64, c_p, c_p],
     "skx_rrf_stage1_dense": [c_p, c_i32, c_p, c_i32, c_p, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_resid_sq": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_sz_p, c_p],

@@ -19,8 +19,12 @@ namespace skx {
 
 namespace {
 
-constexpr int kCiThreads = 512;  // 16 warps
+// 8 warps x 128 registers = 32K registers: the CTA fits beside one CTA of
+// the fitness kernel it runs next to in the sweep pipeline (a 64K-register CTA
+// has to wait until a whole SM drains)
+constexpr int kCiThreads = 256;
 constexpr int kCiWarps = kCiThreads / 32;
+constexpr int kCiEpt = (528 + kCiThreads - 1) / kCiThreads;
 constexpr int kCiMaxN = 512;
 constexpr int kCiTiles = 4;  // 8 x 8 output tiles per warp step (their C loads in flight together)
 
@@ -46,9 +50,9 @@ __host__ __device__ __forceinline__ int ci_ld(int cols) {
   return x + (x % 16 == 0 ? 4 : 12);
 }
 
-// The 528 entries (i, j), i <= j, of a 32 x 32 upper triangle, two per thread
-// of the CTA (e = t and t + 512): the diagonal-block steps below touch one
-// entry per thread per step, with one barrier per step.
+// The 528 entries (i, j), i <= j, of a 32 x 32 upper triangle, kCiEpt per
+// thread of the CTA (e = t, t + kCiThreads, ...): the diagonal-block steps
+// below touch one entry per thread per step, with one barrier per step.
 __device__ __forceinline__ void ut_entry(int e, int& i, int& j) {
   // row i holds 32 - i entries, starting at e_i = 32 i - i (i - 1) / 2
   i = 0;
@@ -62,10 +66,10 @@ __device__ __forceinline__ void ut_entry(int e, int& i, int& j) {
 // into Xo (leading dim 36) using V (36) as scratch.  Returns 0 or k+1 for the
 // first failing pivot.  All threads of the CTA call it.
 __device__ int cta_chol_inv32(double* D, int ld, double* V, double* Xo, int tid) {
-  int ei[2], ej[2];
-  bool own[2];
+  int ei[kCiEpt], ej[kCiEpt];
+  bool own[kCiEpt];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < kCiEpt; ++u) {
     const int e = tid + u * kCiThreads;
     own[u] = e < 528;
     ut_entry(own[u] ? e : 0, ei[u], ej[u]);
@@ -79,20 +83,20 @@ __device__ int cta_chol_inv32(double* D, int ld, double* V, double* Xo, int tid)
     }
     const double rp = 1.0 / akk;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < kCiEpt; ++u)
       if (own[u] && ei[u] > k)
         D[ei[u] * ld + ej[u]] = fma(-D[k * ld + ei[u]] * D[k * ld + ej[u]], rp, D[ei[u] * ld + ej[u]]);
     __syncthreads();
   }
   if (bad) return bad;
   // row k of R = row k / sqrt(a_kk); V = I
-  double rv[2];
+  double rv[kCiEpt];
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < kCiEpt; ++u)
     rv[u] = own[u] ? D[ei[u] * ld + ej[u]] / sqrt(D[ei[u] * ld + ei[u]]) : 0.0;
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < kCiEpt; ++u)
     if (own[u]) {
       const int i = ei[u], j = ej[u];
       V[i * 36 + j] = i == j ? 1.0 : 0.0;
@@ -106,7 +110,7 @@ __device__ int cta_chol_inv32(double* D, int ld, double* V, double* Xo, int tid)
   for (int i = 31; i >= 0; --i) {
     const double rii = D[i * ld + i];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < kCiEpt; ++u)
       if (own[u]) {
         const int k = ei[u], j = ej[u];
         if (j < i) continue;
@@ -134,7 +138,7 @@ __device__ int cta_chol_inv32(double* D, int ld, double* V, double* Xo, int tid)
 //  Inverse X = R^-1, block rows bottom-up: W[Q] = I_Q + (the updates already
 //   subtracted), X[Q] = R_qq^-1 W[Q]; then every block row above takes its
 //   rank-32 update W[0:c0, c0:] -= R[0:c0, Q] X[Q, c0:].
-__global__ void __launch_bounds__(kCiThreads, 1) k_chol_inv(const double* __restrict__ G, int n,
+__global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __restrict__ G, int n,
                                                            double* R, double* Rinv,
                                                            int* __restrict__ info) {
   extern __shared__ __align__(16) double cism[];
@@ -322,20 +326,20 @@ __global__ void __launch_bounds__(kCiThreads, 1) k_chol_inv(const double* __rest
 // (LAPACK geqr2 + org2r conventions), one CTA: C in shared memory column-major,
 // warp k owning column k.  Replaces torch.linalg.qr (cuSOLVER geqrf/orgqr,
 // ~10 launches) in the r > 128 associated middle step of rsvd_lrls.
-__global__ void __launch_bounds__(1024, 1) k_house_q(const double* __restrict__ Cg, int r, int w,
+__global__ void __launch_bounds__(512) k_house_q(const double* __restrict__ Cg, int r, int w,
                                                      double* __restrict__ Qg) {
   extern __shared__ __align__(16) double hq[];
   double* C = hq;          // column-major, ld r
   double* Q = C + r * w;   // column-major, ld r
   __shared__ double tau[32];
-  const int tid = threadIdx.x, lane = tid & 31, k = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wk = tid >> 5, nwk = blockDim.x >> 5;
   for (int e = tid; e < r * w; e += blockDim.x) {
     const int i = e / w, j = e % w;
     C[j * r + i] = Cg[e];
   }
   __syncthreads();
   for (int j = 0; j < w; ++j) {
-    if (k == j) {
+    if (wk == j % nwk) {
       double* cj = C + j * r;
       double ss = 0.0;
       for (int i = j + 1 + lane; i < r; i += 32) ss = fma(cj[i], cj[i], ss);
@@ -356,7 +360,8 @@ __global__ void __launch_bounds__(1024, 1) k_house_q(const double* __restrict__ 
       }
     }
     __syncthreads();
-    if (k > j && k < w) {
+    for (int k = wk; k < w; k += nwk) {
+      if (k <= j) continue;
       const double tj = tau[j];
       const double* v = C + j * r;
       double* ck = C + k * r;
@@ -368,10 +373,11 @@ __global__ void __launch_bounds__(1024, 1) k_house_q(const double* __restrict__ 
       __syncwarp();
       if (lane == 0) ck[j] -= d;
       for (int i = j + 1 + lane; i < r; i += 32) ck[i] = fma(-d, v[i], ck[i]);
+      __syncwarp();
     }
     __syncthreads();
   }
-  if (k < w) {
+  for (int k = wk; k < w; k += nwk) {
     double* qk = Q + k * r;
     for (int i = lane; i < r; i += 32) qk[i] = i == k ? 1.0 : 0.0;
     __syncwarp();
@@ -418,6 +424,8 @@ extern "C" int skx_house_q(const double* c, int r, int w, double* q, void* strea
   const size_t smem = (size_t)2 * r * w * 8;
   SKX_REQUIRE(smem <= (size_t)max_smem_optin(), "skx_house_q: %d x %d too large", r, w);
   cudaFuncSetAttribute(k_house_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_house_q<<<1, 32 * w, smem, (cudaStream_t)stream>>>(c, r, w, q);
+  // at most 16 warps (warp k owns columns k, k + 16): 512 x 61 registers, so the
+  // CTA fits beside one CTA of the fitness kernel
+  k_house_q<<<1, 32 * (w < 16 ? w : 16), smem, (cudaStream_t)stream>>>(c, r, w, q);
   return check_launch("k_house_q");
 }

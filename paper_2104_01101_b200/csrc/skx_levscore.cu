@@ -133,8 +133,12 @@ __global__ void __launch_bounds__(kLsThreads) k_ls_chol(const double* __restrict
 
 // RP = R rounded up to a multiple of 8 (X zero padded), so the row and the
 // triangular product stay in registers
+// (128 threads: at up to 255 registers the CTA still fits beside one CTA of
+// the fitness kernel that runs next to the leverage path)
+constexpr int kLsRowThreads = 128;
+
 template <int RP>
-__global__ void __launch_bounds__(kLsThreads) k_ls_rows(const double* __restrict__ a, int64_t s,
+__global__ void __launch_bounds__(kLsRowThreads) k_ls_rows(const double* __restrict__ a, int64_t s,
                                                         int R, const double* __restrict__ rinv,
                                                         double* __restrict__ scores) {
   __shared__ double X[RP * RP];
@@ -182,10 +186,10 @@ extern "C" int skx_lev_scores(const double* a, int64_t s, int R, double* scores,
   cudaStream_t st = (cudaStream_t)stream;
   k_ls_gram<<<nparts, kLsThreads, 0, st>>>(a, s, R, part);
   k_ls_chol<<<1, kLsThreads, 0, st>>>(part, nparts, R, rinv, bad);
-  const unsigned g = (unsigned)imin((s + kLsThreads - 1) / kLsThreads, (int64_t)num_sms() * 8);
-  if (R <= 8) k_ls_rows<8><<<g, kLsThreads, 0, st>>>(a, s, R, rinv, scores);
-  else if (R <= 16) k_ls_rows<16><<<g, kLsThreads, 0, st>>>(a, s, R, rinv, scores);
-  else if (R <= 24) k_ls_rows<24><<<g, kLsThreads, 0, st>>>(a, s, R, rinv, scores);
-  else k_ls_rows<32><<<g, kLsThreads, 0, st>>>(a, s, R, rinv, scores);
+  const unsigned g = (unsigned)imin((s + kLsRowThreads - 1) / kLsRowThreads, (int64_t)num_sms() * 16);
+  if (R <= 8) k_ls_rows<8><<<g, kLsRowThreads, 0, st>>>(a, s, R, rinv, scores);
+  else if (R <= 16) k_ls_rows<16><<<g, kLsRowThreads, 0, st>>>(a, s, R, rinv, scores);
+  else if (R <= 24) k_ls_rows<24><<<g, kLsRowThreads, 0, st>>>(a, s, R, rinv, scores);
+  else k_ls_rows<32><<<g, kLsRowThreads, 0, st>>>(a, s, R, rinv, scores);
   return check_launch("skx_lev_scores", 3);
 }

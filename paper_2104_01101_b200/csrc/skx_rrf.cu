@@ -364,6 +364,150 @@ __global__ void __launch_bounds__(256) k_rrf_coo_fx(RrfRng r, CooSoA cs, int mod
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// RRF stage 1 with L2-resident accumulators (order-3 leverage runs, config 5).
+// The fixed-point accumulation above scatters 2 atomics per nonzero over the
+// whole s_n x k2 accumulator (3 GB at config 5): every atomic misses L2 and
+// costs a DRAM read-modify-write (ncu: ~130 GB of DRAM traffic for 20 GB of
+// input, long-scoreboard bound).  Here the nonzeros are first partitioned by
+// output row block -- a counting sort that needs no random numbers, so it runs
+// while the compute-bound rejection scans still occupy the SMs -- into
+// records {key = i_n << 40 | flat other index, value}; the stage-1 pass then
+// walks the records in row-block order with all CTAs in the same region, so
+// the live accumulator rows (a few MB) stay in L2.  Same integer sums, so
+// the result is bitwise that of skx_rrf_stage1_fx.
+constexpr int kPartTile = 65536;  // nonzeros per partition tile (256 threads x 256)
+constexpr int kPartMaxBk = 256;   // row blocks per mode
+
+struct PartPlan {
+  int nmode;
+  int mode[2];
+  int shift[2];  // row block = i_n >> shift
+  int nbk[2];
+};
+
+__global__ void __launch_bounds__(256) k_part_count(CooSoA cs, int64_t nnz, PartPlan pp,
+                                                    int64_t ntile, unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned int h[2][kPartMaxBk];
+  for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    for (int i = threadIdx.x; i < 2 * kPartMaxBk; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t e0 = (int64_t)t * kPartTile, e1 = imin(e0 + kPartTile, nnz);
+    for (int md = 0; md < pp.nmode; ++md) {
+      const int32_t* rows = cs.c[pp.mode[md]];
+      for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+        atomicAdd(&h[md][(uint32_t)__ldcs(rows + e) >> pp.shift[md]], 1u);
+    }
+    __syncthreads();
+    // bucket-major layout [mode][bucket][tile]: one exclusive scan per mode
+    // gives every (bucket, tile) its first output slot
+    for (int md = 0; md < pp.nmode; ++md)
+      for (int b = threadIdx.x; b < pp.nbk[md]; b += blockDim.x)
+        cnt[((int64_t)md * kPartMaxBk + b) * ntile + t] = h[md][b];
+    __syncthreads();
+  }
+}
+
+template <int NO>
+__global__ void __launch_bounds__(256) k_part_scatter(CooSoA cs, int64_t nnz,
+                                                      const double* __restrict__ vals, PartPlan pp,
+                                                      int64_t ntile, const unsigned long long* off,
+                                                      uint64_t* __restrict__ key0, double* __restrict__ val0,
+                                                      uint64_t* __restrict__ key1, double* __restrict__ val1) {
+  __shared__ unsigned long long pos[2][kPartMaxBk];
+  for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    for (int md = 0; md < pp.nmode; ++md)
+      for (int b = threadIdx.x; b < pp.nbk[md]; b += blockDim.x)
+        pos[md][b] = off[((int64_t)md * kPartMaxBk + b) * ntile + t];
+    __syncthreads();
+    const int64_t e0 = (int64_t)t * kPartTile, e1 = imin(e0 + kPartTile, nnz);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      uint32_t c[NO + 1];
+#pragma unroll
+      for (int k = 0; k <= NO; ++k) c[k] = (uint32_t)__ldcs(cs.c[k] + e);
+      const double v = __ldcs(vals + e);
+#pragma unroll
+      for (int md = 0; md < 2; ++md) {
+        if (md >= pp.nmode) break;
+        const int mode = pp.mode[md];
+        uint64_t j = 0;
+#pragma unroll
+        for (int k = 0; k <= NO; ++k)
+          if (k != mode) j = j * (uint64_t)cs.ext[k] + c[k];
+        const unsigned long long p = atomicAdd(&pos[md][c[mode] >> pp.shift[md]], 1ull);
+        const uint64_t key = ((uint64_t)c[mode] << 40) | j;
+        if (md == 0) {
+          __stcs(reinterpret_cast<unsigned long long*>(key0) + p, key);
+          __stcs(val0 + p, v);
+        } else {
+          __stcs(reinterpret_cast<unsigned long long*>(key1) + p, key);
+          __stcs(val1 + p, v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// k_rrf_coo_fx over partitioned records (key = i_n << 40 | j, value)
+template <int U>
+__global__ void __launch_bounds__(256) k_rrf_rec_fx(RrfRng r, uint64_t P, int64_t nnz,
+                                                    const uint64_t* __restrict__ keys,
+                                                    const double* __restrict__ vals, int S,
+                                                    const unsigned int* __restrict__ rowmax,
+                                                    unsigned long long* __restrict__ acc) {
+  const bool two = *rowmax < kFxTwoLimbMax;
+  __shared__ uint32_t cnt[kRrfBuckets + 1];
+  __shared__ uint64_t dsm[kFxSmemD];
+  int shift = 0;
+  while ((P >> shift) >= (uint64_t)kRrfBuckets) ++shift;
+  for (int b = threadIdx.x; b <= kRrfBuckets; b += blockDim.x) {
+    const uint64_t v = (uint64_t)b << shift;
+    int64_t lo = 0, hi = r.nd;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (r.d[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    cnt[b] = (uint32_t)lo;
+  }
+  const int64_t nd_s = imin(r.nd, kFxSmemD);
+  for (int64_t i = threadIdx.x; i < nd_s; i += blockDim.x) dsm[i] = r.d[i];
+  __syncthreads();
+  const uint64_t k2 = r.k2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) * U + threadIdx.x; base < nnz;
+       base += stride) {
+    uint64_t kk[U];
+    double vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = base + (int64_t)u * blockDim.x;
+      const int64_t ee = e < nnz ? e : base;
+      kk[u] = __ldcs(reinterpret_cast<const unsigned long long*>(keys) + ee);
+      vv[u] = e < nnz ? __ldcs(vals + ee) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + (int64_t)u * blockDim.x >= nnz) continue;
+      const uint64_t j = kk[u] & ((uint64_t(1) << 40) - 1);
+      const uint32_t row = (uint32_t)(kk[u] >> 40);
+      const uint32_t t = rrf_entry_q(r, j, j + count_le_tab_s(dsm, nd_s, r.d, cnt, shift, j));
+      uint64_t hi, lo;
+      to_fixed(pk_neg(t) ? -vv[u] : vv[u], S, hi, lo);
+      unsigned long long* cell = acc + 4 * ((uint64_t)row * k2 + pk_bucket(t));
+      if (two) {
+        atomicAdd(cell, (unsigned long long)(lo & 0xffffffffffffULL));
+        atomicAdd(cell + 1, (unsigned long long)((hi << 16) | (lo >> 48)));
+      } else {
+        atomicAdd(cell, (unsigned long long)(lo & 0xffffffffULL));
+        atomicAdd(cell + 1, (unsigned long long)(lo >> 32));
+        atomicAdd(cell + 2, (unsigned long long)(long long)(int32_t)(uint32_t)hi);
+      }
+    }
+  }
+}
+
 // st1 = double(acc) * 2^-S, correctly rounded
 __global__ void k_fixed_to_double(const unsigned long long* __restrict__ acc, int64_t n, int S,
                                   const unsigned int* __restrict__ rowmax,
@@ -650,4 +794,121 @@ extern "C" int skx_rrf_stage1_fx_convert(const unsigned long long* acc, int64_t 
   k_fixed_to_double<<<g, 256, 0, (cudaStream_t)stream>>>(acc, cells, 94 - (emax + 1), limb_flag,
                                                          stage1);
   return check_launch("k_fixed_to_double");
+}
+
+// Partition of an order-3..5 COO by output row block for up to two modes
+// (the RRF modes of a leverage run): records {key = i_n << 40 | j, value},
+// j the flat other-mode index (others ascending, first slowest), grouped by
+// row block i_n >> shift (order inside a block is not fixed -- stage 1's
+// integer sums do not depend on it).
+extern "C" int skx_rrf_partition(int ndim, const int64_t* shape_h, int64_t nnz,
+                                 const int32_t* coords, const double* vals, int nmode,
+                                 const int* modes_h, uint64_t* key0, double* val0, uint64_t* key1,
+                                 double* val1, void* ws, size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 5, "skx_rrf_partition: order 2..5");
+  SKX_REQUIRE(nmode >= 1 && nmode <= 2, "skx_rrf_partition: one or two modes");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_rrf_partition: ws_bytes is NULL");
+  PartPlan pp{};
+  pp.nmode = nmode;
+  uint64_t P[2] = {1, 1};
+  for (int md = 0; md < nmode; ++md) {
+    const int mode = modes_h[md];
+    SKX_REQUIRE(mode >= 0 && mode < ndim, "skx_rrf_partition: mode out of range");
+    pp.mode[md] = mode;
+    int sh = 0;
+    while (((shape_h[mode] + (int64_t(1) << sh) - 1) >> sh) > kPartMaxBk) ++sh;
+    pp.shift[md] = sh;
+    pp.nbk[md] = (int)((shape_h[mode] + (int64_t(1) << sh) - 1) >> sh);
+    SKX_REQUIRE(shape_h[mode] < (int64_t(1) << 24), "skx_rrf_partition: extent too large");
+    for (int k = 0; k < ndim; ++k)
+      if (k != mode) P[md] *= (uint64_t)shape_h[k];
+    SKX_REQUIRE(P[md] < (uint64_t(1) << 40), "skx_rrf_partition: other-mode index beyond 2^40");
+  }
+  const int64_t ntile = (nnz + kPartTile - 1) / kPartTile;
+  const size_t ncnt = (size_t)2 * kPartMaxBk * (size_t)imax(ntile, 1);
+  Arena ar(ws, *ws_bytes);
+  unsigned long long* cnt = ar.take<unsigned long long>(ncnt);
+  unsigned long long* off = ar.take<unsigned long long>(ncnt);
+  size_t cb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cb, cnt, off, (int)(kPartMaxBk * imax(ntile, 1)));
+  void* tmp = ar.take<char>(cb);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_rrf_partition: workspace too small");
+  if (nnz == 0) return SKX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CooSoA cs{};
+  for (int k = 0; k < ndim; ++k) {
+    cs.c[k] = coords + (int64_t)k * nnz;
+    cs.ext[k] = shape_h[k];
+  }
+  const unsigned g = (unsigned)imin(ntile, (int64_t)num_sms() * 8);
+  k_part_count<<<g, 256, 0, st>>>(cs, nnz, pp, ntile, cnt);
+  for (int md = 0; md < nmode; ++md) {
+    const size_t o = (size_t)md * kPartMaxBk * ntile;
+    size_t cb2 = cb;
+    cub::DeviceScan::ExclusiveSum(tmp, cb2, cnt + o, off + o, (int)(pp.nbk[md] * ntile), st);
+  }
+  auto kern = ndim == 2 ? k_part_scatter<1>
+            : ndim == 3 ? k_part_scatter<2>
+            : ndim == 4 ? k_part_scatter<3>
+                        : k_part_scatter<4>;
+  kern<<<g, 256, 0, st>>>(cs, nnz, vals, pp, ntile, off, key0, val0, key1, val1);
+  return check_launch("skx_rrf_partition", 2 + 2 * nmode);
+}
+
+// RRF stage 1 of one mode from its partitioned records (skx_rrf_partition):
+// same exact fixed-point sums as skx_rrf_stage1_fx, accumulators hit in L2.
+// rows: the mode's coordinate row of the COO (for the limb-count bound).
+extern "C" int skx_rrf_stage1_rec(int64_t sn, uint64_t P, int64_t nnz, const int32_t* rows,
+                                  const uint64_t* keys, const double* vals, int emax, uint64_t k0,
+                                  uint64_t k1, uint64_t p0, uint32_t has_pending, uint32_t pending,
+                                  uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
+                                  double* stage1, void* ws, size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_rrf_stage1_rec: ws_bytes is NULL");
+  SKX_REQUIRE(nrej < (int64_t(1) << 32), "skx_rrf_stage1_rec: rejection list too long");
+  const int64_t cells = sn * k2;
+  int CB = 0;
+  while (((sn + (int64_t(1) << CB) - 1) >> CB) > 32768) ++CB;
+  const int nbins = (int)((sn + (int64_t(1) << CB) - 1) >> CB);
+  Arena ar(ws, *ws_bytes);
+  unsigned long long* acc = ar.take<unsigned long long>((size_t)cells * 4);
+  unsigned int* hist = ar.take<unsigned int>((size_t)nbins + 1);
+  unsigned int* rowmax = ar.take<unsigned int>(1);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_rrf_stage1_rec: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = 94 - (emax + 1);
+  cudaMemsetAsync(acc, 0, (size_t)cells * 32, st);
+  cudaMemsetAsync(hist, 0, ((size_t)nbins + 1) * sizeof(unsigned int), st);
+  int launches = 1;
+  {
+    const size_t hs = (size_t)nbins * sizeof(unsigned int);
+    cudaFuncSetAttribute(k_row_hist_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+    if (nnz > 0) {
+      k_row_hist_coarse<<<(unsigned)imin((nnz + 255) / 256, (int64_t)num_sms() * 2), 256, hs, st>>>(
+          rows, nnz, CB, nbins, hist);
+      ++launches;
+    }
+    k_max_u32<<<1, 1024, 0, st>>>(hist, nbins, rowmax);
+  }
+  if (nnz > 0) {
+    RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
+    constexpr int U = 4;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rrf_rec_fx<U>, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t blocks =
+        imax(1, imin((nnz + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
+    k_rrf_rec_fx<U><<<(unsigned)blocks, 256, 0, st>>>(r, P, nnz, keys, vals, S, rowmax, acc);
+    ++launches;
+  }
+  const unsigned g = (unsigned)imin((cells + 255) / 256, (int64_t)num_sms() * 16);
+  k_fixed_to_double<<<g, 256, 0, st>>>(acc, cells, S, rowmax, stage1);
+  return check_launch("skx_rrf_stage1_rec", launches + 1);
 }

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(1024, 1) k_lrls_mid(const double* __restrict__
 // out[2] = rank-deficient (some |R_ii| < 1e-12 ||Z||_F), out[3] = the
 // speculative sweep must be replayed (out[0] | !out[1] | out[2]).  NaNs count
 // as failures, as the comparisons in torch do.
-__global__ void __launch_bounds__(1024) k_cholqr_flags(const double* __restrict__ g1,
+__global__ void __launch_bounds__(512) k_cholqr_flags(const double* __restrict__ g1,
                                                       const double* __restrict__ r1,
                                                       const int* __restrict__ info,
                                                       const double* __restrict__ g2, int r,
@@ -497,6 +497,6 @@ extern "C" int skx_lrls_mid(const double* rz, const double* b, int r, int w, dou
 extern "C" int skx_cholqr_flags(const double* g1, const double* r1, const int* info,
                                 const double* g2, int r, int* out, void* stream) {
   SKX_REQUIRE(r >= 1, "skx_cholqr_flags: empty system");
-  k_cholqr_flags<<<1, r > 128 ? 1024 : 256, 0, (cudaStream_t)stream>>>(g1, r1, info, g2, r, out);
+  k_cholqr_flags<<<1, r > 128 ? 512 : 256, 0, (cudaStream_t)stream>>>(g1, r1, info, g2, r, out);
   return check_launch("k_cholqr_flags");
 }

@@ -12,6 +12,7 @@ are outside this build's path.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -100,13 +101,45 @@ def _check_sketch_size(m, ranks):
 
 
 # ------------------------------------------------------------------ RRF init
-def rrf_stage1_dev(d, n, tabs):
-    """CountSketch stage of the composite sketch of T_(n): s_n x k2."""
+def rrf_partition_dev(d, modes):
+    """Records {i_n << 40 | j, value} of a DeviceCoo grouped by output row
+    block for the RRF modes (up to two), for skx_rrf_stage1_rec; None when
+    the fixed-point stage-1 path does not apply.  Returns {mode: (keys, vals)}."""
+    torch = _torch()
+    modes = [n for n in modes if not d.has_fibre(n)][:2]
+    if not modes or not d.fixed_point_ok() or d.nnz == 0:
+        return None
+    shape = d.shape
+    for n in modes:
+        if shape[n] >= (1 << 24) or int(np.prod([shape[k] for k in range(d.ndim) if k != n])) >= (1 << 40):
+            return None
+    recs = [(torch.empty(d.nnz, dtype=torch.int64, device="cuda"),
+             torch.empty(d.nnz, dtype=torch.float64, device="cuda")) for _ in modes]
+    shp, sp_ = nat.host_i64(shape)
+    marr = (ctypes.c_int * len(modes))(*modes)
+    k1, v1 = recs[1] if len(recs) > 1 else (None, None)
+    nat.call_ws("skx_rrf_partition", (d.ndim, sp_, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals),
+                                      len(modes), ctypes.cast(marr, ctypes.c_void_p),
+                                      nat.ptr(recs[0][0]), nat.ptr(recs[0][1]),
+                                      nat.ptr(k1) if k1 is not None else None,
+                                      nat.ptr(v1) if v1 is not None else None), slot=11)
+    return dict(zip(modes, recs))
+
+
+def rrf_stage1_dev(d, n, tabs, part=None):
+    """CountSketch stage of the composite sketch of T_(n): s_n x k2.  part:
+    this mode's partitioned records (rrf_partition_dev), if built."""
     torch = _torch()
     shape = shape_of(d)
     s_n = shape[n]
     st1 = torch.empty((s_n, tabs.k2), dtype=torch.float64, device="cuda")
-    if is_sparse_dev(d) and not d.has_fibre(n) and d.fixed_point_ok():
+    if part is not None:
+        keys, vals = part
+        emax = d.value_range()[0]
+        nat.call_ws("skx_rrf_stage1_rec", (s_n, ctypes.c_uint64(tabs.P), d.nnz,
+                                           nat.ptr(d.coords[n]), nat.ptr(keys), nat.ptr(vals), emax,
+                                           *tabs.args(), tabs.k2, nat.ptr(st1)), slot=8)
+    elif is_sparse_dev(d) and not d.has_fibre(n) and d.fixed_point_ok():
         # no mode-n layout (leverage runs build none): exact fixed-point
         # accumulation straight from the lexsorted COO instead of sorting one
         emax = d.value_range()[0]
@@ -130,9 +163,9 @@ def rrf_stage1_dev(d, n, tabs):
     return st1
 
 
-def _rrf_finish(d, n, rank, tabs, gauss, comm=None):
+def _rrf_finish(d, n, rank, tabs, gauss, comm=None, part=None):
     """Composite sketch B = (T_(n) T_cs) G and its leading left singular vectors."""
-    return _rrf_from_stage1(rrf_stage1_dev(d, n, tabs), rank, gauss, comm)
+    return _rrf_from_stage1(rrf_stage1_dev(d, n, tabs, part), rank, gauss, comm)
 
 
 def _rrf_from_stage1(st1, rank, gauss, comm=None):
@@ -350,6 +383,7 @@ class _Run:
                 self._host._device = DeviceCoo.from_host(self._host)
                 self._attach(self._host._device)
                 self._host = None
+        part = {}
         with torch.cuda.stream(main):
             self.draw_ts_ops()
             if self.sparse:
@@ -359,6 +393,14 @@ class _Run:
                 else:  # leverage: only the fitness reads a layout (mode 0: a packing pass)
                     self.d.fibre(0)
                 self.d.value_range()  # RRF stage 1: exact fixed-point path when in range
+                if not self.use_ts and self.d.ndim >= 3 and os.environ.get("SKX_RRF_PART") == "1":
+                    # (opt-in) the nonzeros partitioned by RRF output row block
+                    # while the scans run, so each stage 1 accumulates in L2.
+                    # Measured at config 5: stage 1 53/59 -> 45/44 ms per mode,
+                    # but the partition (64 ms, scattered 16-byte records) slows
+                    # the first scan 64 -> 117 ms: 477 -> 509 ms per call.  The
+                    # L2 atomic rate (~4.4e10/s), not DRAM, bounds both forms.
+                    part = rrf_partition_dev(self.d, modes) or {}
             self.prep()
             # small first-sweep inputs that do not depend on the RRF factors,
             # built while the scans occupy the GPU: the Kronecker-sketch plans
@@ -370,7 +412,8 @@ class _Run:
             for n, scan, (P, k2, width) in zip(modes, scans, dims):
                 tabs = finish_rrf_scan(scan, self.rng_init, P)
                 gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
-                self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm)
+                self.factors[n] = _rrf_finish(self.d, n, self.ranks[n], tabs, gauss, self.comm,
+                                              part.pop(n, None))
         caller.wait_stream(main)
         caller.wait_stream(side)
 

@@ -733,3 +733,30 @@ def test_fitness_kernels_concurrent_streams_bitwise(skx):
     for t_con, c_con in outs:
         assert torch.equal(t_con, t_ser)
         assert torch.equal(c_con, c_ser)
+
+
+@pytest.mark.parametrize("nnz", [50_000, 3_000_000])
+def test_rrf_stage1_partitioned_bitwise(skx, nnz):
+    """RRF stage 1 from row-block-partitioned records (skx_rrf_partition +
+    skx_rrf_stage1_rec, the L2-resident form the leverage driver uses) is
+    bitwise the direct fixed-point accumulation from the COO: the same
+    integer sums, rounded once."""
+    from paper_2104_01101_b200.sketching import draw_rrf_tables
+    from paper_2104_01101_b200.tensors import device_of
+    from paper_2104_01101_b200.tucker import rrf_partition_dev, rrf_stage1_dev
+    shape = (3000, 2000, 1000)
+    c, v = _coo_rand(shape, nnz, 11)
+    d = device_of(skx.SparseTensor(shape, c, v))
+    part = rrf_partition_dev(d, [1, 2])
+    assert part is not None and sorted(part) == [1, 2]
+    for n, k2 in ((1, 157), (2, 480)):
+        P = int(np.prod(shape)) // shape[n]
+        keys, vals = part[n]
+        # every nonzero exactly once, grouped by row block
+        rows = (keys >> 40).cpu().numpy()
+        assert len(rows) == nnz and np.array_equal(np.bincount(rows, minlength=shape[n]),
+                                                   np.bincount(c[:, n], minlength=shape[n]))
+        direct = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2)).cpu().numpy()
+        viapart = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2),
+                                 part[n]).cpu().numpy()
+        assert np.array_equal(direct, viapart)
