@@ -445,10 +445,15 @@ def run_e2e(args, cfgd, skx, torch, cfg, inp, host_dense):
         inp._device = None
         del dev
         torch.cuda.empty_cache()
-        # from_sorted staged the coordinates as pinned int32 SoA (the device
-        # layout): that copy and the values are what every call uploads
-        soa = host_st._soa
-        h2d = (soa.numel() * 4 if soa is not None else hc.numel() * 8) + hv.numel() * 8
+        # from_sorted staged the coordinates in pinned memory (order 3: slice
+        # pointers + one packed word per nonzero, else int32 SoA): that copy
+        # and the values are what every call uploads
+        soa, c3 = host_st._soa, host_st._c3
+        if c3 is not None:  # compact order-3 staging: slice pointers + one word per nonzero
+            h2d = (c3["packed"].numel() * 4 + c3["ptr0"].numel() * 8 + c3["exc_idx"].numel() * 12
+                   + hv.numel() * 8)
+        else:
+            h2d = (soa.numel() * 4 if soa is not None else hc.numel() * 8) + hv.numel() * 8
         del hc
         fn = skx.cp_via_sketched_tucker if cfgd["kind"] == "alg6" else skx.sketched_tucker_als
 

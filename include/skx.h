@@ -225,14 +225,16 @@ int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode, int64_t nn
 
 /* Chunk-wise skx_rrf_stage1_fx for a tensor arriving in pieces: the caller
  * zeroes `acc` (s_mode * k2 cells of 32 bytes), calls _acc per chunk (coords
- * = the chunk's first entry of SoA row 0, rows ld apart; three-limb sums,
- * *limb_flag is set accordingly) and _convert once.  Same exact sums. */
+ * = the chunk's first entry of SoA row 0, rows ld apart) and _convert once.
+ * Same exact sums.  max_per_cell: a bound on the nonzeros in any block of
+ * 2^CB mode-n rows (skx_stage_compact3's rowmax; CB as skx_rrf_stage1_fx
+ * chooses it), or -1 if unknown; *limb_flag records the limb count used. */
 int skx_rrf_stage1_fx_acc(int ndim, const int64_t* shape_h, int mode, int64_t n,
                           const int32_t* coords, int64_t ld, const double* vals, int emax,
                           uint64_t k0, uint64_t k1, uint64_t p0, uint32_t has_pending,
                           uint32_t pending, uint64_t sign_q0, const uint64_t* rej, int64_t nrej,
                           int64_t k2, unsigned long long* acc, unsigned int* limb_flag,
-                          void* stream);
+                          int64_t max_per_cell, void* stream);
 int skx_rrf_stage1_fx_convert(const unsigned long long* acc, int64_t cells, int emax,
                               const unsigned int* limb_flag, double* stage1, void* stream);
 
@@ -366,6 +368,36 @@ int skx_rrf_stage1_rec(int64_t s_n, uint64_t P, int64_t nnz, const int32_t* rows
                        uint64_t k1, uint64_t p0, uint32_t has_pending, uint32_t pending,
                        uint64_t sign_q0, const uint64_t* rej, int64_t nrej, int64_t k2,
                        double* stage1, void* ws, size_t* ws_bytes, void* stream);
+
+/* Host function (no GPU): the compact order-3 staging of an int64 (nnz, 3)
+ * COO, built once at SparseTensor.from_sorted -- validated on the way
+ * (*status: 0 ok, 1 coordinate out of range, 2 not strictly lexsorted;
+ * src/tensors.py:35-60) -- slice pointers ptr0[s0 + 1], packed[e] = (d << b2)
+ * | i2 (d = i1 increment inside the slice, absolute at a slice start; d >=
+ * 2^(32-b2) - 1 escapes to exc_idx/exc_val of capacity cap, *n_exc = the
+ * number needed). */
+int skx_stage_compact3(const int64_t* coords, int64_t nnz, int64_t s0, int64_t s1, int64_t s2,
+                       int b2, int64_t* ptr0, uint32_t* packed, int64_t* exc_idx,
+                       int32_t* exc_val, int64_t cap, int64_t* n_exc, int* status);
+
+/* Host function (no GPU), also at staging: what the device would otherwise
+ * compute with a full pass and a host round trip before any RRF stage-1 sum
+ * can start -- the value range as skx_value_range (vrange3) and, for modes 1
+ * and 2, the largest nonzero count of any block of 2^CB rows, CB the smallest
+ * with ceil(s_n / 2^CB) <= 32768 (rowmax2: the limb bound of skx_rrf_stage1_*). */
+int skx_stage_stats3(const int64_t* coords, const double* vals, int64_t nnz, int64_t s1, int64_t s2,
+                     int* vrange3, int64_t* rowmax2);
+
+/* Restore the int32 SoA device layout (3 rows of ld) of the lexsorted
+ * order-3 COO for slices [s_lo, s_hi) from its compact host staging (the
+ * tensor object's pinned upload form, SparseTensor.from_sorted): ptr0 = the
+ * mode-0 slice pointers (device, s_0 + 1), packed[e] = (d << b2) | i2 with d
+ * the i1 increment inside the slice (absolute for a slice's first nonzero;
+ * d = 2^(32-b2) - 1 escapes to exc_val at the sorted index exc_idx).  The
+ * layout the reference keeps in SparseTensor.coords (src/tensors.py:26-60). */
+int skx_coo_unpack3(const int64_t* ptr0, int64_t s_lo, int64_t s_hi, const uint32_t* packed,
+                    int b2, const int64_t* exc_idx, const int32_t* exc_val, int64_t n_exc,
+                    int32_t* coords, int64_t ld, void* stream);
 
 /* Skip-mode sparse TTMc of an order-3 COO tensor (ttmc(t, factors, skip=n),
  * src/tensors.py:261-277): from mode n's fibre-major layout (skx_coo_fibre /

@@ -57,8 +57,12 @@ _SIGS = {
     "skx_rrf_stage1_fx": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_i32, c_u64, c_u64, c_u64, c_u32,
                           c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p, c_sz_p, c_p],
     "skx_rrf_stage1_fx_acc": [c_i32, c_p, c_i32, c_i64, c_p, c_i64, c_p, c_i32, c_u64, c_u64, c_u64,
-                              c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p, c_p],
+                              c_u32, c_u32, c_u64, c_p, c_i64, c_i64, c_p, c_p, c_i64, c_p],
     "skx_rrf_stage1_fx_convert": [c_p, c_i64, c_i32, c_p, c_p, c_p],
+    "skx_stage_compact3": [c_p, c_i64, c_i64, c_i64, c_i64, c_i32, c_p, c_p, c_p, c_p, c_i64, c_p,
+                           c_p],
+    "skx_stage_stats3": [c_p, c_p, c_i64, c_i64, c_i64, c_p, c_p],
+    "skx_coo_unpack3": [c_p, c_i64, c_i64, c_p, c_i32, c_p, c_p, c_i64, c_p, c_i64, c_p],
     "skx_rrf_partition": [c_i32, c_p, c_i64, c_p, c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p,
                           c_p],
     "skx_rrf_stage1_rec": [c_i64, c_u64, c_i64, c_p, c_p, c_p, c_i32, c_u64, c_u64, c_u64, c_u32,

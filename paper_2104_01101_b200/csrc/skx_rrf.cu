@@ -750,9 +750,11 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
 // pieces (host upload pipelined with the sketch): the caller owns the
 // accumulator (s_mode x k2 cells of 32 bytes, zeroed), adds chunk after chunk
 // (coords = first nonzero of the chunk in each of the ndim SoA rows, rows ld
-// apart) with three-limb reductions -- no row histogram of the whole tensor
-// exists yet -- and finally converts.  Same sums as the one-shot call.
-__global__ void k_u32_max_sentinel(unsigned int* p) { *p = 0xffffffffu; }
+// apart) and finally converts.  Same sums as the one-shot call.  max_per_cell:
+// the caller's bound on the nonzeros of any 2^CB-row block of the mode (from
+// the host staging), or -1 when unknown -- two-limb reductions when it is
+// below 2^16, else three.
+__global__ void k_u32_set(unsigned int* p, unsigned int v) { *p = v; }
 
 extern "C" int skx_rrf_stage1_fx_acc(int ndim, const int64_t* shape_h, int mode, int64_t n,
                                      const int32_t* coords, int64_t ld, const double* vals,
@@ -760,12 +762,13 @@ extern "C" int skx_rrf_stage1_fx_acc(int ndim, const int64_t* shape_h, int mode,
                                      uint32_t has_pending, uint32_t pending, uint64_t sign_q0,
                                      const uint64_t* rej, int64_t nrej, int64_t k2,
                                      unsigned long long* acc, unsigned int* limb_flag,
-                                     void* stream) {
+                                     int64_t max_per_cell, void* stream) {
   SKX_REQUIRE(ndim >= 2 && ndim <= 5, "skx_rrf_stage1_fx_acc: order 2..5");
   SKX_REQUIRE(mode >= 0 && mode < ndim, "skx_rrf_stage1_fx_acc: mode out of range");
   SKX_REQUIRE(nrej < (int64_t(1) << 32), "skx_rrf_stage1_fx_acc: rejection list too long");
   cudaStream_t st = (cudaStream_t)stream;
-  k_u32_max_sentinel<<<1, 1, 0, st>>>(limb_flag);  // three limbs
+  k_u32_set<<<1, 1, 0, st>>>(limb_flag, (max_per_cell >= 0 && max_per_cell < 0xffffffffLL)
+                                            ? (unsigned int)max_per_cell : 0xffffffffu);
   if (n <= 0) return check_launch("skx_rrf_stage1_fx_acc", 1);
   RrfRng r = make_rng(k0, k1, p0, has_pending, pending, sign_q0, rej, nrej, k2);
   CooSoA cs{};

@@ -84,6 +84,7 @@ class SparseTensor:
         self._mode_sort = {}
         self._device = None
         self._soa = None  # pinned int32 (N, nnz) staging copy (from_sorted)
+        self._c3 = None   # compact order-3 staging (from_sorted, _stage_compact3)
 
     @classmethod
     def from_sorted(cls, shape, coords, values):
@@ -97,6 +98,11 @@ class SparseTensor:
             raise ValueError("from_sorted needs int64 coords and float64 values")
         if coords.ndim != 2 or coords.shape[1] != len(shape) or coords.shape[0] != values.shape[0]:
             raise ValueError("coords must be (nnz, N) matching values")
+        obj = cls.__new__(cls)
+        obj._init(shape, coords, values)
+        if (coords.shape[0] >= DEVICE_INGEST_NNZ and max(shape) < 2 ** 31
+                and obj._stage_compact3()):
+            return obj  # validated (range, strict lexsort) by the native staging pass
         if coords.size and ((coords.min(axis=0) < 0).any() or (coords.max(axis=0) >= np.asarray(shape)).any()):
             raise ValueError("coordinate out of range")
         chunk = 1 << 24
@@ -112,11 +118,63 @@ class SparseTensor:
                 eq &= a[:, n] == b[:, n]
             if not lt.all():
                 raise ValueError("coordinates must be lexsorted and duplicate-free")
-        obj = cls.__new__(cls)
-        obj._init(shape, coords, values)
         if coords.shape[0] >= DEVICE_INGEST_NNZ and max(shape) < 2 ** 31:
             obj._stage_soa()
         return obj
+
+    def _stage_compact3(self):
+        """Order 3: stage the coordinates in the compact upload form that
+        skx_coo_unpack3 expands on the device -- mode-0 slice pointers and one
+        uint32 per nonzero, (i1 increment within the slice << b2) | i2, with
+        an exception list for increments that do not fit -- in pinned host
+        memory, once, at construction.  4 bytes of coordinates per nonzero
+        cross PCIe per call instead of 12 (int32 SoA) or 24 (the API's int64).
+        Lossless; returns False when the shape does not admit it."""
+        if self.ndim != 3 or self._coords is None:
+            return False
+        s0, s1, s2 = self.shape
+        b2 = max(1, int(s2 - 1).bit_length())
+        if b2 > 24 or s0 >= 2 ** 31 or s1 >= 2 ** 31:
+            return False
+        from . import _native as nat
+        torch = _torch()
+        c = np.ascontiguousarray(self._coords, dtype=np.int64)
+        nnz = c.shape[0]
+        pin = torch.cuda.is_available()
+        packed = torch.empty(nnz, dtype=torch.int32, pin_memory=pin)
+        ptr0 = torch.empty(s0 + 1, dtype=torch.int64, pin_memory=pin)
+        cap = max(1024, nnz // 256)
+        while True:
+            exc_idx = torch.empty(cap, dtype=torch.int64)
+            exc_val = torch.empty(cap, dtype=torch.int32)
+            nx = ctypes.c_int64(0)
+            status = ctypes.c_int(0)
+            rc = nat.load(require_cuda=False).skx_stage_compact3(
+                c.ctypes.data_as(ctypes.c_void_p), nnz, s0, s1, s2, b2,
+                ctypes.c_void_p(ptr0.data_ptr()), ctypes.c_void_p(packed.data_ptr()),
+                ctypes.c_void_p(exc_idx.data_ptr()), ctypes.c_void_p(exc_val.data_ptr()), cap,
+                ctypes.byref(nx), ctypes.byref(status))
+            if rc != 0:
+                return False
+            if status.value == 1:
+                raise ValueError("coordinate out of range")
+            if status.value == 2:
+                raise ValueError("coordinates must be lexsorted and duplicate-free")
+            if nx.value <= cap:
+                break
+            cap = nx.value
+        exc_idx = exc_idx[:nx.value].clone()
+        exc_val = exc_val[:nx.value].clone()
+        # value range and per-mode row-block counts, so the device side need
+        # not scan the whole tensor before its first RRF stage-1 sum
+        vr = (ctypes.c_int * 3)()
+        rm = (ctypes.c_int64 * 2)()
+        v = np.ascontiguousarray(self._values, dtype=np.float64)
+        nat.load(require_cuda=False).skx_stage_stats3(
+            c.ctypes.data_as(ctypes.c_void_p), v.ctypes.data_as(ctypes.c_void_p), nnz, s1, s2, vr, rm)
+        stats = dict(vrange=(int(vr[0]), int(vr[1]), int(vr[2])), rowmax={1: int(rm[0]), 2: int(rm[1])})
+        self._c3 = dict(ptr0=ptr0, packed=packed, b2=b2, exc_idx=exc_idx, exc_val=exc_val, **stats)
+        return True
 
     def _stage_soa(self):
         """Stage the coordinates in the device layout -- int32, one row per
@@ -249,6 +307,33 @@ def _torch():
     return torch
 
 
+def compact3_aux_to_device(c3):
+    """Per-call device copies of the small parts of the compact order-3
+    staging: slice pointers and the exception list."""
+    return (c3["ptr0"].to("cuda", non_blocking=True), c3["exc_idx"].to("cuda", non_blocking=True),
+            c3["exc_val"].to("cuda", non_blocking=True))
+
+
+def unpack_compact3(c3, nnz, coords=None, s_lo=0, s_hi=None, packed_dev=None, aux=None):
+    """Device int32 SoA coordinates (3, nnz) of slices [s_lo, s_hi) from the
+    compact order-3 staging (SparseTensor._stage_compact3): the packed words
+    cross PCIe (or are already on the device in packed_dev), skx_coo_unpack3
+    expands them.  Returns the coordinate array."""
+    from . import _native as nat
+    torch = _torch()
+    ptr0, exi, exv = aux if aux is not None else compact3_aux_to_device(c3)
+    s0 = int(c3["ptr0"].numel()) - 1
+    s_hi = s0 if s_hi is None else s_hi
+    if coords is None:
+        coords = torch.empty((3, nnz), dtype=torch.int32, device="cuda")
+    if packed_dev is None:
+        packed_dev = c3["packed"].to("cuda", non_blocking=True)
+    nat.call("skx_coo_unpack3", nat.ptr(ptr0), s_lo, s_hi, nat.ptr(packed_dev), c3["b2"],
+             nat.ptr(exi) if exi.numel() else None, nat.ptr(exv) if exv.numel() else None,
+             int(exi.numel()), nat.ptr(coords), nnz, nat.stream())
+    return coords
+
+
 class DeviceCoo:
     """HBM-resident COO tensor with cached per-mode layouts."""
 
@@ -274,6 +359,10 @@ class DeviceCoo:
             warnings.simplefilter("ignore", UserWarning)
             v = torch.from_numpy(np.ascontiguousarray(st.values))
             vd = v.to("cuda", non_blocking=True)
+            if getattr(st, "_c3", None) is not None:  # compact order-3 staging
+                d = cls(st.shape, unpack_compact3(st._c3, st.nnz), vd)
+                d._vrange = st._c3["vrange"]  # computed at staging: no device pass
+                return d
             if getattr(st, "_soa", None) is not None:  # staged int32 SoA: one H2D
                 return cls(st.shape, st._soa.to("cuda", non_blocking=True), vd)
             c64 = torch.from_numpy(np.ascontiguousarray(st.coords))

@@ -28,7 +28,8 @@ from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, fini
                         kron_rows_dev, lev_det_dev, lev_sample_dev, mode_last_dev, plan_rrf_scans,
                         rrf_table_dev, ts_kron_dev, ts_kron_plan_dev, ts_rhs_dense_dev,
                         ts_rhs_mode_dev)
-from .tensors import (DeviceCoo, SparseTensor, TuckerModel, device_of, fitness_tucker_dev, is_sparse_dev,
+from .tensors import (DeviceCoo, SparseTensor, TuckerModel, compact3_aux_to_device, device_of,
+                      fitness_tucker_dev, is_sparse_dev, unpack_compact3,
                       matricize, shape_of, ttm_dev, ttmc_dev)
 
 SKETCH_KINDS = (None, "tensorsketch", "leverage-random", "leverage-deterministic")
@@ -254,7 +255,11 @@ def _upload_streams():
     torch = _torch()
     dev = torch.cuda.current_device()
     if dev not in _UP_STREAMS:
-        _UP_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+        _, hi = torch.cuda.Stream.priority_range()
+        # the convert stream runs the on-device unpack of each uploaded chunk
+        # at high priority (its CTAs go ahead of the rejection scans), so the
+        # copy stream only ever holds copies and the PCIe pipe never idles
+        _UP_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream(priority=hi))
     return _UP_STREAMS[dev]
 
 
@@ -369,7 +374,7 @@ class _Run:
         scans = plan_rrf_scans(self.rng_init, [(P, k2, k2 * w) for P, k2, w in dims], side,
                                self.comm)
         if (self._host is not None and not self.use_ts and self._host.nnz >= UPLOAD_CHUNK
-                and self._host._soa is not None):
+                and (self._host._soa is not None or self._host._c3 is not None)):
             # leverage run on a host COO: upload in chunks and sketch them as
             # they land, under the remaining upload
             with torch.cuda.stream(main):
@@ -429,37 +434,91 @@ class _Run:
         torch = _torch()
         st = self._host
         nd, nnz = self.ndim, st.nnz
-        copy, _ = _upload_streams()
+        copy, conv = _upload_streams()
         copy.wait_stream(main)
+        conv.wait_stream(main)
         import warnings
         with warnings.catch_warnings():  # read-only host arrays are only read
             warnings.simplefilter("ignore", UserWarning)
             hv = torch.from_numpy(np.ascontiguousarray(st.values))
         vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
         coords = torch.empty((nd, nnz), dtype=torch.int32, device="cuda")
-        with torch.cuda.stream(copy):
-            vals.copy_(hv, non_blocking=True)
+        chunk = UPLOAD_CHUNK
+        conv_ev, bounds = [], []
+        c3 = st._c3
+        if c3 is not None:
+            # compact order-3 staging: per slice-aligned chunk, its values and
+            # packed coordinate words cross PCIe and skx_coo_unpack3 expands
+            # them on the device (4 instead of 12 bytes of coordinates per
+            # nonzero over PCIe); the chunks' stage-1 sums start as they land
+            ptr_h = c3["ptr0"]
+            s0 = int(ptr_h.numel()) - 1
+            packed = torch.empty(nnz, dtype=torch.int32, device="cuda")
+            with torch.cuda.stream(copy):
+                aux = compact3_aux_to_device(c3)
+            s_lo = 0
+            while s_lo < s0:
+                lo = int(ptr_h[s_lo])
+                s_hi = int(torch.searchsorted(ptr_h, torch.tensor(lo + chunk), right=True)) - 1
+                s_hi = min(max(s_hi, s_lo + 1), s0)
+                hi = int(ptr_h[s_hi])
+                with torch.cuda.stream(copy):
+                    # values and coordinate words of the chunk (the value
+                    # range and the limb bound came with the staging, so the
+                    # chunk's stage-1 sums start as soon as it has landed)
+                    vals[lo:hi].copy_(hv[lo:hi], non_blocking=True)
+                    packed[lo:hi].copy_(c3["packed"][lo:hi], non_blocking=True)
+                    lev = torch.cuda.Event()
+                    lev.record(copy)
+                conv.wait_event(lev)
+                with torch.cuda.stream(conv):
+                    unpack_compact3(c3, nnz, coords, s_lo, s_hi, packed, aux)
+                    cev = torch.cuda.Event()
+                    cev.record(conv)
+                conv_ev.append(cev)
+                bounds.append((lo, hi))
+                s_lo = s_hi
             ev_v = torch.cuda.Event()
             ev_v.record(copy)
-        chunk = UPLOAD_CHUNK
-        soa = st._soa  # coordinates staged as pinned int32 SoA: straight into place
-        conv_ev, bounds = [], []
-        for lo in range(0, nnz, chunk):
-            hi = min(nnz, lo + chunk)
+            packed.record_stream(copy)
+            packed.record_stream(conv)
+            coords.record_stream(conv)
+            for t in aux:
+                t.record_stream(copy)
+                t.record_stream(conv)
+        else:
             with torch.cuda.stream(copy):
-                for k in range(nd):
-                    coords[k, lo:hi].copy_(soa[k, lo:hi], non_blocking=True)
-                cev = torch.cuda.Event()
-                cev.record(copy)
-            conv_ev.append(cev)
-            bounds.append((lo, hi))
-        main.wait_event(ev_v)
+                vals.copy_(hv, non_blocking=True)
+                ev_v = torch.cuda.Event()
+                ev_v.record(copy)
+            soa = st._soa  # coordinates staged as pinned int32 SoA: straight into place
+            for lo in range(0, nnz, chunk):
+                hi = min(nnz, lo + chunk)
+                with torch.cuda.stream(copy):
+                    for k in range(nd):
+                        coords[k, lo:hi].copy_(soa[k, lo:hi], non_blocking=True)
+                    cev = torch.cuda.Event()
+                    cev.record(copy)
+                conv_ev.append(cev)
+                bounds.append((lo, hi))
+        if c3 is None:
+            main.wait_event(ev_v)
         vals.record_stream(copy)
+        coords.record_stream(copy)
         d = DeviceCoo(self.shape, coords, vals)
+        if c3 is not None:
+            d._vrange = c3["vrange"]  # from the staging pass: no device scan, no sync
         st._device = d
         self._host = None
-        self._attach(d)
-        fx = d.fixed_point_ok()  # one small D2H once the values are in
+        if c3 is not None:
+            # ||T||^2 on the convert stream behind the last chunk (it has
+            # waited for every copy); the main stream joins it below, before
+            # the first pass that needs the whole tensor
+            with torch.cuda.stream(conv):
+                self._attach(d)
+        else:
+            self._attach(d)
+        fx = d.fixed_point_ok()  # staging's value range, or one small D2H once the values are in
         self.normals.prefetch()
         # the RRF tables of every mode, in the reference's draw order
         tabs_all = []
@@ -468,6 +527,7 @@ class _Run:
             gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
             tabs_all.append((n, tabs, gauss))
         if not fx:
+            main.wait_stream(conv)
             for ev in conv_ev:
                 main.wait_event(ev)
             self.d.fibre(0)
@@ -486,9 +546,11 @@ class _Run:
             vptr = ctypes.c_void_p(vals.data_ptr() + lo * 8)
             for n, tabs, _ in tabs_all:
                 acc, flag = accs[n]
+                bound = c3["rowmax"].get(n, -1) if c3 is not None else -1
                 nat.call("skx_rrf_stage1_fx_acc", nd, sp_, n, hi - lo, cptr, nnz, vptr, emax,
-                         *tabs.args(), tabs.k2, nat.ptr(acc), nat.ptr(flag), nat.stream())
+                         *tabs.args(), tabs.k2, nat.ptr(acc), nat.ptr(flag), bound, nat.stream())
         coords.record_stream(main)
+        main.wait_stream(conv)  # every chunk unpacked, ||T||^2 done
         self.d.fibre(0)  # the fitness layout (a packing pass)
         for n, tabs, gauss in tabs_all:
             acc, flag = accs[n]

@@ -760,3 +760,31 @@ def test_rrf_stage1_partitioned_bitwise(skx, nnz):
         viapart = rrf_stage1_dev(d, n, draw_rrf_tables(skx.make_rng(n), P, k2),
                                  part[n]).cpu().numpy()
         assert np.array_equal(direct, viapart)
+
+
+@pytest.mark.parametrize("shape,nnz", [((100, 1 << 22, 1 << 24), 1_500_000), ((3000, 2000, 1000), 2_000_000)])
+def test_compact_staging_roundtrip(skx, shape, nnz):
+    """SparseTensor.from_sorted stages an order-3 COO as slice pointers plus
+    one packed word per nonzero (i1 increment << b2 | i2, escapes for large
+    increments: shape 1 has b2 = 24, so every increment >= 255 escapes); the
+    device unpack restores the coordinates exactly, whole and in the
+    slice-aligned chunks the leverage driver uploads."""
+    import torch
+    from paper_2104_01101_b200.tensors import DeviceCoo, compact3_aux_to_device, unpack_compact3
+    c, v = _coo_rand(shape, nnz, 5)
+    st = skx.SparseTensor.from_sorted(shape, c.astype(np.int64), v)
+    assert st._c3 is not None
+    if shape[2] == 1 << 24:
+        assert st._c3["exc_idx"].numel() > 1000
+    d = DeviceCoo.from_host(st)
+    assert np.array_equal(d.coords.cpu().numpy().T.astype(np.int64), c)
+    # slice-aligned pieces into one buffer
+    c3 = st._c3
+    aux = compact3_aux_to_device(c3)
+    packed = c3["packed"].cuda()
+    out = torch.full((3, nnz), -1, dtype=torch.int32, device="cuda")
+    s0 = shape[0]
+    cuts = [0, s0 // 3, s0 // 3 + 1, (2 * s0) // 3, s0]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        unpack_compact3(c3, nnz, out, a, b, packed, aux)
+    assert np.array_equal(out.cpu().numpy().T.astype(np.int64), c)
