@@ -879,7 +879,7 @@ constexpr size_t t3t_smem_bytes() {
 // records.  tools/micro/gather.cu: register-fragment 16-byte gathers run at
 // ~72 G rows/s against ~106 for whole-row copies, but they skip the
 // shared-memory write and read entirely.
-template <int NB, int MB, int D>
+template <int NB, int MB, int D, bool LEFT = false>
 __global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
     const __grid_constant__ CUtensorMap tmC, const int64_t* __restrict__ colptr, int64_t s0,
     const double* __restrict__ rec, uint32_t c1_mask, const double* __restrict__ A0,
@@ -940,23 +940,31 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
       }
     };
     // mode-2 rows of batch b straight into D-fragment registers
-    double2 y[NG][P::NT];
+    constexpr int NTD = LEFT ? 2 : P::NT;  // n-tiles on the tensor cores
+    double2 y[NG][LEFT ? 4 : P::NT];
     auto load_y = [&](int64_t b) {
       const uint32_t* rb = reinterpret_cast<const uint32_t*>(recs + (b % NRC) * NB * 2);
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         const double2* row =
             reinterpret_cast<const double2*>(A2 + (int64_t)(rb[(g * 8 + q) * 4 + 1] & c1_mask) * R);
+        if (LEFT) {  // D-fragment columns of the two DMMA n-tiles + all of cols 16..19
+          y[g][0] = __ldg(row + c);
+          y[g][1] = __ldg(row + 4 + c);
+          y[g][2] = __ldg(row + 8);
+          y[g][LEFT ? 3 : 0] = __ldg(row + 9);
+        } else {
 #pragma unroll
-        for (int nt = 0; nt < P::NT; ++nt)
-          y[g][nt] = (nt * 8 + 2 * c < R) ? __ldg(row + nt * 4 + c) : make_double2(0.0, 0.0);
+          for (int nt = 0; nt < P::NT; ++nt)
+            y[g][nt] = (nt * 8 + 2 * c < R) ? __ldg(row + nt * 4 + c) : make_double2(0.0, 0.0);
+        }
       }
     };
-    double b[P::KS][P::NT];
+    double b[P::KS][NTD];
 #pragma unroll
     for (int ks = 0; ks < P::KS; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < P::NT; ++nt) {
+      for (int nt = 0; nt < NTD; ++nt) {
         const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
         const int n = nt * 8 + q;
         double w = 0.0;
@@ -965,6 +973,19 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
             w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + n), w);
         b[ks][nt] = w;
       }
+    double wl[LEFT ? P::KS : 1][4];  // W[k(ks, c)][16 + j]
+    if (LEFT) {
+#pragma unroll
+      for (int ks = 0; ks < P::KS; ++ks)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = ks < 2 * P::PAIRS ? 8 * (ks >> 1) + 2 * c + (ks & 1) : 8 * P::PAIRS + c;
+          double w = 0.0;
+          for (int r0 = 0; r0 < R0; ++r0)
+            w = fma(__ldg(A0 + i0 * R0 + r0), __ldg(C + ((int64_t)r0 * R + k) * R + 16 + j), w);
+          wl[LEFT ? ks : 0][j] = w;
+        }
+    }
     for (int64_t b2 = 0; b2 < D + 2 && b2 < nb; ++b2) issue_recs(b2);
     cp_async_commit();
     cp_async_wait<0>();
@@ -983,7 +1004,7 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
       cp_async_commit();
       const double* ra0 = rowsC + slot * ROWBUF;
       const double* rv = recs + (bi % NRC) * NB * 2;
-      double a[NG][P::KS], d[NG][P::NT][2];
+      double a[NG][P::KS], d[NG][NTD][2];
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         const double* ra = ra0 + (g * 8 + q) * ST;
@@ -995,7 +1016,7 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
         }
         if (P::SINGLE) a[g][P::KS - 1] = ra[8 * P::PAIRS + c];
 #pragma unroll
-        for (int nt = 0; nt < P::NT; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
+        for (int nt = 0; nt < NTD; ++nt) d[g][nt][0] = d[g][nt][1] = 0.0;
       }
       double vq[NG];
 #pragma unroll
@@ -1005,12 +1026,23 @@ __global__ void __launch_bounds__(256, MB) k_tucker3_tma2(
 #pragma unroll
         for (int g = 0; g < NG; ++g)
 #pragma unroll
-          for (int nt = 0; nt < P::NT; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
+          for (int nt = 0; nt < NTD; ++nt) dmma884(d[g][nt][0], d[g][nt][1], a[g][ks], b[ks][nt]);
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
         double t = 0.0;
+        if (LEFT) {  // cols 16..19: this lane's five k values (partials sum in the warp reduction)
 #pragma unroll
-        for (int nt = 0; nt < P::NT; ++nt) {
+          for (int j = 0; j < 4; ++j) {
+            double v = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < P::KS; ++ks) v = fma(a[g][ks], wl[LEFT ? ks : 0][j], v);
+            const double yj = j == 0 ? y[g][2].x : j == 1 ? y[g][2].y : j == 2 ? y[g][LEFT ? 3 : 0].x
+                                                                                 : y[g][LEFT ? 3 : 0].y;
+            t = fma(v, yj, t);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTD; ++nt) {
           t = fma(d[g][nt][0], y[g][nt].x, t);
           t = fma(d[g][nt][1], y[g][nt].y, t);
         }
@@ -1424,7 +1456,22 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
     k_tucker3_tma2<16, MBB, DD><<<mb, 256, sm2, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A2,  \
                                                      core, R0, part);                         \
   } while (0)
-          if (dd == 1 && mbb == 2) SKX_T3T2(2, 1);
+          if (k7v != nullptr && k7v[1] == 'L') {  // (A/B) FMA-pipe tail, NB = 16 or 8
+            const bool nb8 = k7v[2] == '8';
+            if (nb8) {
+              const size_t sm2 = t3t2_smem_bytes<8, 1>();
+              cudaFuncSetAttribute(k_tucker3_tma2<8, 2, 1, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+              k_tucker3_tma2<8, 2, 1, true><<<mb, 256, sm2, s>>>(tmC, colptr0, s0, rec, c1_mask, A0,
+                                                                   A2, core, R0, part);
+            } else {
+              const size_t sm2 = t3t2_smem_bytes<16, 1>();
+              cudaFuncSetAttribute(k_tucker3_tma2<16, 2, 1, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+              k_tucker3_tma2<16, 2, 1, true><<<mb, 256, sm2, s>>>(tmC, colptr0, s0, rec, c1_mask, A0,
+                                                                    A2, core, R0, part);
+            }
+          } else if (dd == 1 && mbb == 2) SKX_T3T2(2, 1);
           else if (dd == 2 && mbb == 2) SKX_T3T2(2, 2);
           else if (dd == 1) SKX_T3T2(3, 1);
           else SKX_T3T2(3, 2);
