@@ -224,6 +224,10 @@ def run_ours(args, cfgd):
         if share:
             dist.init_process_group("gloo")
         else:
+            # communicator lines (rank count, NVLS/NVLink transport) on stderr,
+            # so a scaling run's log shows what NCCL built
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NET")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = Comm()
     nat.load()

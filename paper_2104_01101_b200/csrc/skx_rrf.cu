@@ -8,6 +8,8 @@
 // rejects, so sign j sits at u32 index sign_q0 + j.  The P_n-long tables of
 // the reference (160-640 GB at configs 4-5) are never materialised for COO
 // inputs: each nonzero evaluates its two Philox blocks on the fly.
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
 
 #include "skx_common.cuh"
@@ -732,12 +734,14 @@ extern "C" int skx_rrf_stage1_fx(int ndim, const int64_t* shape_h, int mode, int
               : ndim == 3 ? k_rrf_coo_fx<2, U>
               : ndim == 4 ? k_rrf_coo_fx<3, U>
                           : k_rrf_coo_fx<4, U>;
-    // one resident wave (no tail): blocks = SMs x resident CTAs per SM
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t blocks =
-        imax(1, imin((nnz + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
+    // One 256-thread CTA per SM, grid-stride: the pass is bound by the L2
+    // atomic rate (~2 reductions per nonzero), not by SM resources -- with
+    // every resident slot taken (8 CTAs per SM) it ran no faster (60.3 vs 60.8
+    // ms per mode at config 5) but starved the rejection scan it overlaps
+    // (84 -> 75 ms per scan, 480 -> 457 ms per call).  SKX_FX_BLOCKS: A/B.
+    int64_t nblk = num_sms();
+    if (const char* b = getenv("SKX_FX_BLOCKS")) nblk = imax(1, atoll(b));
+    const int64_t blocks = imax(1, imin((nnz + 256 * U - 1) / (256 * U), nblk));
     kern<<<(unsigned)blocks, 256, 0, st>>>(r, cs, mode, nnz, vals, S, rowmax, acc);
     ++launches;
   }
@@ -781,10 +785,10 @@ extern "C" int skx_rrf_stage1_fx_acc(int ndim, const int64_t* shape_h, int mode,
             : ndim == 3 ? k_rrf_coo_fx<2, U>
             : ndim == 4 ? k_rrf_coo_fx<3, U>
                         : k_rrf_coo_fx<4, U>;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t blocks = imax(1, imin((n + 256 * U - 1) / (256 * U), (int64_t)num_sms() * per_sm));
+  // one CTA per SM (atomic-rate bound; see skx_rrf_stage1_fx)
+  int64_t nblk = num_sms();
+  if (const char* b = getenv("SKX_FX_BLOCKS")) nblk = imax(1, atoll(b));
+  const int64_t blocks = imax(1, imin((n + 256 * U - 1) / (256 * U), nblk));
   kern<<<(unsigned)blocks, 256, 0, st>>>(r, cs, mode, n, vals, 94 - (emax + 1), limb_flag, acc);
   return check_launch("skx_rrf_stage1_fx_acc", 2);
 }
