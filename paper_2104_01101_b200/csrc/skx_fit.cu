@@ -1456,19 +1456,9 @@ extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int6
     k_tucker3_tma2<16, MBB, DD><<<mb, 256, sm2, s>>>(tmC, colptr0, s0, rec, c1_mask, A0, A2,  \
                                                      core, R0, part);                         \
   } while (0)
-          if (k7v != nullptr && k7v[1] == 'M') {  // (A/B) FMA-pipe tail, 1 CTA/SM (255 regs), D = 2/3
-#define SKX_T3T2L1(DD)                                                                        \
-  do {                                                                                        \
-    const size_t sm2 = t3t2_smem_bytes<16, DD>();                                             \
-    cudaFuncSetAttribute(k_tucker3_tma2<16, 1, DD, true>,                                     \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);              \
-    k_tucker3_tma2<16, 1, DD, true><<<mb, 256, sm2, s>>>(tmC, colptr0, s0, rec, c1_mask, A0,  \
-                                                         A2, core, R0, part);                 \
-  } while (0)
-            if (k7v[2] == '3') SKX_T3T2L1(3);
-            else SKX_T3T2L1(2);
-#undef SKX_T3T2L1
-          } else if (k7v != nullptr && k7v[1] == 'L') {  // (A/B) FMA-pipe tail, NB = 16 or 8
+          // (A/B) FMA-pipe tail, NB = 16 or 8: 43.5 ms (spills at 128 registers);
+          // with one 255-register CTA per SM instead: 60.5 ms (half the warps)
+          if (k7v != nullptr && k7v[1] == 'L') {
             const bool nb8 = k7v[2] == '8';
             if (nb8) {
               const size_t sm2 = t3t2_smem_bytes<8, 1>();

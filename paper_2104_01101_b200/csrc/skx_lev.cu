@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256) k_slice_hits(int mode, const int64_t* __r
                                                     int64_t* __restrict__ cnt,
                                                     const int64_t* __restrict__ off,
                                                     int64_t* __restrict__ hit_col,
-                                                    double* __restrict__ hit_val) {
+                                                    double* __restrict__ hit_val, int64_t cap) {
   const int lane = threadIdx.x & 31;
   const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (j >= m) return;
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(256) k_slice_hits(int mode, const int64_t* __r
       if (lane == 0) cnt[j] = lo2 - lo;
       return;
     }
-    for (int64_t e = lo + lane; e < lo2; e += 32) {
+    for (int64_t e = lo + lane; e < lo2 && o + (e - lo) < cap; e += 32) {
       const int4 r = __ldg(&rec0[e]);
       hit_col[o + (e - lo)] = (int64_t)((uint32_t)r.y & c1_mask);
       hit_val[o + (e - lo)] = wj * __hiloint2double(r.w, r.z);
@@ -395,8 +395,10 @@ __global__ void __launch_bounds__(256) k_slice_hits(int mode, const int64_t* __r
     const unsigned bal = __ballot_sync(0xffffffffu, hit);
     if (WRITE && hit) {
       const int64_t at = o + found + __popc(bal & ((1u << lane) - 1u));
-      hit_col[at] = (int64_t)r.x;
-      hit_val[at] = wj * __hiloint2double(r.w, r.z);
+      if (at < cap) {  // (a fixed-capacity caller checks the total on the device)
+        hit_col[at] = (int64_t)r.x;
+        hit_val[at] = wj * __hiloint2double(r.w, r.z);
+      }
     }
     found += __popc(bal);
   }
@@ -562,12 +564,12 @@ extern "C" int skx_slice_hits(int mode, int64_t s0, const int64_t* colptr0, cons
   if (hit_col == nullptr) {  // count pass: hit_off[m] = total
     cudaMemsetAsync(cnt + m, 0, sizeof(int64_t), st);
     k_slice_hits<false><<<g, 256, 0, st>>>(mode, colptr0, r, c1_mask, idx, w, m, cnt, nullptr,
-                                           nullptr, nullptr);
+                                           nullptr, nullptr, 0);
     cub::DeviceScan::ExclusiveSum(tmp, cb, cnt, hit_off, (int)(m + 1), st);
     return check_launch("k_slice_hits(count)", 2);
   }
   SKX_REQUIRE(cap >= 0, "skx_slice_hits: negative capacity");
   k_slice_hits<true><<<g, 256, 0, st>>>(mode, colptr0, r, c1_mask, idx, w, m, nullptr, hit_off,
-                                        hit_col, hit_val);
+                                        hit_col, hit_val, cap);
   return check_launch("k_slice_hits(write)");
 }

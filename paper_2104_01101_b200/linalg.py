@@ -729,6 +729,63 @@ def rsvd_lrls_hits_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversampl
     return core_t, a, bad, resid
 
 
+def rsvd_lrls_hits_fixed_dev(z, hit_off, hit_col, hit_val, s, rank, normals, oversample=10,
+                             defer=None):
+    """rsvd_lrls_hits_dev with no host synchronisation: the hit list has a
+    fixed capacity (entries past the device total carry column s and value
+    0, see sketching.gather_slices_fixed_dev), the distinct hit columns are
+    found by a stable sort with a device-side segment count, and every product
+    with Y_H is a deterministic segment sum over the hits -- nothing is sized
+    on the host.  Same algebra: Y G and W^T Y restricted to the hit columns,
+    D padded with zero columns (the SVD of D and the factor rows are unchanged:
+    rows outside the hit columns are exactly zero).  The residual
+    ||Z core_t a^T - Y||_F^2 is split into the hit entries, sum (e_k - v_k)^2,
+    and the model mass elsewhere, ||P a^T||_F^2 - sum e_k^2 with P = Z core_t.
+    Returns (core_t, a (s x rank), bad, resid)."""
+    torch = _torch()
+    m, r = z.shape
+    if m < r:
+        raise ValueError(f"need at least as many rows as columns in z ({m} < {r})")
+    if rank > min(r, s):
+        raise ValueError(f"rank {rank} exceeds min({r}, {s})")
+    qz, rz, bad = sketch_qr_dev(z, defer)
+    width = min(rank + oversample, s)
+    g = normals.normal((s, width))
+    cap = int(hit_col.numel())
+    offs = hit_off.clamp(max=cap)
+    k = torch.arange(cap, device="cuda")
+    row = (torch.searchsorted(hit_off, k, right=True) - 1).clamp(0, m - 1)
+    gpad = torch.cat([g, torch.zeros((1, width), dtype=g.dtype, device="cuda")])
+    # Y G (m x width): per row, its hits' v g[col] in hit order
+    yg = torch.segment_reduce(hit_val[:, None] * gpad[hit_col], "sum", offsets=offs, axis=0,
+                              unsafe=True)
+    q, wm = assoc_mid_dev(qz, rz, yg)
+    # distinct hit columns (ascending; the sentinel s sorts last)
+    scol, perm = torch.sort(hit_col, stable=True)
+    newseg = torch.ones(cap, dtype=torch.bool, device="cuda")
+    newseg[1:] = scol[1:] != scol[:-1]
+    uid = torch.cumsum(newseg, 0) - 1
+    first = torch.full((cap + 1,), cap, dtype=torch.int64, device="cuda")
+    first.scatter_reduce_(0, uid, k, reduce="amin")
+    ucol = torch.full((cap,), s, dtype=torch.int64, device="cuda")
+    ucol.scatter_(0, uid, scol)
+    # D^T (cap x width): per distinct column, its hits' v W[row] in sorted order
+    contrib = (hit_val[:, None] * wm[row])[perm]
+    dt = torch.segment_reduce(contrib, "sum", offsets=first, axis=0, unsafe=True)
+    u, sv, vh = top_svd_dev(dt.t(), rank, wide=True)
+    core_t = q @ (u * sv)
+    a = torch.zeros((s + 1, rank), dtype=torch.float64, device="cuda")
+    a.index_copy_(0, ucol, vh)  # padded slots (column s) carry zero rows
+    a = a[:s].contiguous()
+    p = z @ core_t
+    e = (p[row] * a.index_select(0, hit_col.clamp(max=s - 1))).sum(dim=1)
+    e = torch.where(hit_col < s, e, torch.zeros_like(e))
+    hit_part = ((e - hit_val) ** 2).sum()
+    model = ((p.transpose(0, 1) @ p) * (a.transpose(0, 1) @ a)).sum()
+    resid = torch.sqrt(torch.clamp(hit_part + model - (e * e).sum(), min=0.0))
+    return core_t, a, bad, resid
+
+
 def rsvd_lrls(z, y, rank, rng, oversample=10):
     """Rank-constrained least squares min ||z x - y|| via randomized SVD."""
     z = _dev(z)

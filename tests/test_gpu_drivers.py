@@ -349,3 +349,34 @@ def test_config5_shape_run_bitwise_deterministic(skx):
     assert np.array_equal(m1.weights, m2.weights)
     for a, b in zip(m1.factors, m2.factors):
         assert np.array_equal(a, b)
+
+
+def test_fixed_capacity_hits_path_matches(skx, monkeypatch):
+    """Speculative leverage sweeps on a sparse tensor take the sync-free
+    fixed-capacity hit lists (no host read of hit counts, distinct columns by
+    a device sort, segment sums) when the sampled right-hand side is large;
+    forced here on a small tensor, it must reproduce the host-sized path to
+    rounding, and a capacity overflow must fall back (replay) to it exactly."""
+    import numpy as np
+    from paper_2104_01101_b200 import sketching, tucker
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from tests.conftest import canon, relerr
+    shape = (150, 120, 90)
+    c, v = planted_cp_coo_host(shape, 60_000, rank=3, seed=2)
+    st = skx.SparseTensor(shape, c, v)
+    # ranks 5 x 5 x 5: r = 25 > R + 10 = 15, the associated rsvd form
+    cfg = skx.TuckerConfig(ranks=(5, 5, 5), max_sweeps=3, sketch="leverage-random",
+                           sketch_size=900, seed=8)
+    monkeypatch.setattr(tucker, "FORCE_FIXED_HITS", False)
+    m0, t0 = skx.sketched_tucker_als(st, cfg)
+    f0, c0 = canon(m0.factors, m0.core)
+    for cap in (1 << 12, 8):  # 8: every sub-problem overflows -> checked replay
+        monkeypatch.setattr(tucker, "FORCE_FIXED_HITS", True)
+        monkeypatch.setattr(sketching, "HITS_CAP", cap)
+        m1, t1 = skx.sketched_tucker_als(st, cfg)
+        f1, c1 = canon(m1.factors, m1.core)
+        for a, b in zip(f1, f0):
+            assert relerr(a, b) <= 1e-10
+        assert relerr(c1, c0) <= 1e-10
+        assert np.allclose(t1.fitness, t0.fitness, rtol=0, atol=1e-12)
+        assert np.allclose(t1.residuals, t0.residuals, rtol=1e-9)

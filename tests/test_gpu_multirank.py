@@ -22,10 +22,16 @@ CONFIGS = {
     "lev": dict(ranks=(4, 5, 3), max_sweeps=3, sketch="leverage-random", sketch_size=600, seed=4),
     "lev_dense": dict(ranks=(4, 5, 3), max_sweeps=2, sketch="leverage-random", sketch_size=500,
                       seed=5),
+    "lev_fixed": dict(ranks=(4, 5, 3), max_sweeps=3, sketch="leverage-random", sketch_size=700,
+                      seed=6),
 }
 # lev_dense forces the dense sampled right-hand side (all-reduced) instead of
-# the gathered-hits path
+# the gathered-hits path; lev_fixed the sync-free fixed-capacity hit lists of
+# speculative sweeps (all-gathered and regrouped by row on the device) -- in
+# the multi-rank run only, so it is checked against the single-process
+# default path
 DENSE_TAGS = ("lev_dense",)
+FIXED_TAGS = ("lev_fixed",)
 
 
 def _free_port():
@@ -58,6 +64,9 @@ def _worker(rank, world, port, q):
     out = {}
     for tag, cfg in CONFIGS.items():
         tucker.HITS_DENSITY = 0.0 if tag in DENSE_TAGS else 0.05
+        # the fixed path is the multi-rank default; other tags pin the
+        # host-sized path (the single-process reference below)
+        tucker.FIXED_HITS_OFF = tag not in FIXED_TAGS
         core, fac, tr = sketched_tucker_als_dev(st, skx.TuckerConfig(**cfg), comm)
         out[tag] = (core.cpu().numpy(), [a.cpu().numpy() for a in fac], tr.fitness, tr.residuals)
     q.put((rank, out))
