@@ -188,7 +188,8 @@ def kernel_work(cfgd, nnz, s0):
                                          work=nnz * (2 * R * R + 2 * R) + s0 * 2 * R ** 3,
                                          bytes=rec)
         w["skx_cp_cross_coo"] = dict(bound="hbm", unit="GB/s", bytes=nnz * 20 + 0)
-        w["skx_filter_fibers_coo"] = dict(bound="hbm", unit="GB/s", bytes=nnz * 12)
+        # the two other-mode coordinate rows (int32) of every nonzero
+        w["skx_filter_fibers_coo"] = dict(bound="hbm", unit="GB/s", bytes=nnz * 8)
         w["skx_ts_rhs_coo"] = dict(bound="hbm", unit="GB/s",
                                    bytes=rec + s0 * cfgd.get("sketch_size", 0) * 8)
         w["skx_rrf_stage1_coo"] = dict(bound="hbm", unit="GB/s", bytes=rec)

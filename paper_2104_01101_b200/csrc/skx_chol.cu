@@ -11,7 +11,9 @@
 // streamed from L2 (R and R^-1 are written and re-read by the same CTA);
 // the 32 x 32 diagonal blocks are factored / inverted by one warp in
 // registers.  Fixed order everywhere: deterministic.
+#include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "skx_common.cuh"
 
@@ -26,6 +28,11 @@ constexpr int kCiThreads = 256;
 constexpr int kCiWarps = kCiThreads / 32;
 constexpr int kCiEpt = (528 + kCiThreads - 1) / kCiThreads;
 constexpr int kCiMaxN = 512;
+// above this order the cooperative multi-CTA form runs (kCiCoopCtas CTAs);
+// up to it one CTA, which starts beside the fitness kernel of a leverage
+// sweep without waiting for a whole grid's worth of free SMs (config 5: r = 400)
+constexpr int kCiCoopMinN = 400;
+constexpr int kCiCoopCtas = 24;
 constexpr int kCiTiles = 4;  // 8 x 8 output tiles per warp step (their C loads in flight together)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -138,6 +145,13 @@ __device__ int cta_chol_inv32(double* D, int ld, double* V, double* Xo, int tid)
 //  Inverse X = R^-1, block rows bottom-up: W[Q] = I_Q + (the updates already
 //   subtracted), X[Q] = R_qq^-1 W[Q]; then every block row above takes its
 //   rank-32 update W[0:c0, c0:] -= R[0:c0, Q] X[Q, c0:].
+//
+// COOP: the same algorithm on a cooperative grid of several CTAs -- every CTA
+// forms the (small) block row itself, identically, and the O(n^3) tile
+// updates are split over all warps of all CTAs, one grid barrier per panel;
+// CTA 0 writes the block rows.  For large r with the GPU to itself (config 3,
+// r = 512): one CTA is FP64-compute bound on a single SM there.
+template <bool COOP>
 __global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __restrict__ G, int n,
                                                            double* R, double* Rinv,
                                                            int* __restrict__ info) {
@@ -147,6 +161,13 @@ __global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __rest
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, q = lane >> 2, c = lane & 3;
   const int np = (n + 31) / 32;
+  const bool lead = !COOP || blockIdx.x == 0;  // writes the block rows
+  const int gwid = COOP ? blockIdx.x * kCiWarps + wid : wid;
+  const int gwarps = COOP ? gridDim.x * kCiWarps : kCiWarps;
+  auto grid_sync = [&]() {
+    if (COOP) cooperative_groups::this_grid().sync();
+    else __syncthreads();
+  };
   if (tid == 0) s_bad = 0;
   // the trailing matrix lives in R's own rows; panel 0 reads G directly
   __syncthreads();
@@ -192,17 +213,11 @@ __global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __rest
         BR[(8 * mt + q) * ld + j0 + 2 * c + 1] = acc[mt][1];
       }
     }
-    // Dinv -> the diagonal block of Rinv (read back by the inverse phase)
-    for (int i = wid; i < w; i += kCiWarps)
-      if (lane < w) Rinv[(int64_t)(c0 + i) * n + c0 + lane] = Dinv[i][lane];
     __syncthreads();
-    // final R block row to global (zero left of the diagonal block)
-    for (int k = wid; k < w; k += kCiWarps)
-      for (int j = lane; j < n; j += 32) R[(int64_t)(c0 + k) * n + j] = j < c0 ? 0.0 : BR[k * ld + j - c0];
     // trailing update of the upper triangle: rows / cols r0.., 8 x 8 tiles;
     // warp per tile row (its A fragments in registers), four tiles in flight
     const int r0 = c0 + 32;
-    for (int ti = wid; ti < rt; ti += kCiWarps) {
+    for (int ti = gwid; ti < rt; ti += gwarps) {
       double a[8];
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) a[ks] = -BR[(4 * ks + c) * ld + 32 + 8 * ti + q];
@@ -233,14 +248,26 @@ __global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __rest
           }
       }
     }
-    __syncthreads();
-  }
-  if (s_bad) {
-    for (int64_t e = tid; e < (int64_t)n * n; e += kCiThreads) {
-      R[e] = 0.0;
-      Rinv[e] = 0.0;
+    grid_sync();
+    // the final block row and R_pp^-1 to global only now: with COOP, slower
+    // CTAs may read these rows' trailing values until the barrier above
+    if (lead) {
+      for (int i = wid; i < w; i += kCiWarps)
+        if (lane < w) Rinv[(int64_t)(c0 + i) * n + c0 + lane] = Dinv[i][lane];
+      for (int k = wid; k < w; k += kCiWarps)
+        for (int j = lane; j < n; j += 32) R[(int64_t)(c0 + k) * n + j] = j < c0 ? 0.0 : BR[k * ld + j - c0];
     }
-    if (tid == 0) *info = s_bad;
+    __syncthreads();  // BR and Dinv are overwritten by the next panel
+  }
+  grid_sync();
+  if (s_bad) {  // (every CTA saw the same pivot)
+    if (lead) {
+      for (int64_t e = tid; e < (int64_t)n * n; e += kCiThreads) {
+        R[e] = 0.0;
+        Rinv[e] = 0.0;
+      }
+      if (tid == 0) *info = s_bad;
+    }
     return;
   }
 
@@ -282,11 +309,10 @@ __global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __rest
       }
     }
     __syncthreads();
-    for (int k = wid; k < w; k += kCiWarps)
-      for (int j = lane; j < n; j += 32) Rinv[(int64_t)(c0 + k) * n + j] = j < c0 ? 0.0 : BX[k * ld + j - c0];
+
     // W[0:c0, c0:] -= R[0:c0, Q] X[Q, c0:]: warp per tile row, four tiles in flight
     const int mtile = c0 / 8;
-    for (int ti = wid; ti < mtile; ti += kCiWarps) {
+    for (int ti = gwid; ti < mtile; ti += gwarps) {
       double a[8];
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) a[ks] = -RC[(8 * ti + q) * 36 + 4 * ks + c];
@@ -317,9 +343,14 @@ __global__ void __launch_bounds__(kCiThreads, 2) k_chol_inv(const double* __rest
           }
       }
     }
-    __syncthreads();
+    grid_sync();
+    // X's block row replaces W's only now (slower CTAs may still be reading W)
+    if (lead)
+      for (int k = wid; k < w; k += kCiWarps)
+        for (int j = lane; j < n; j += 32) Rinv[(int64_t)(c0 + k) * n + j] = j < c0 ? 0.0 : BX[k * ld + j - c0];
+    __syncthreads();  // BX is overwritten by the next step
   }
-  if (tid == 0) *info = 0;
+  if (lead && tid == 0) *info = 0;
 }
 
 // Thin Q (r x w, w <= 32) of a tall matrix C by Householder reflections
@@ -414,8 +445,22 @@ extern "C" int skx_chol_inv_upper(const double* g, int n, double* r, double* rin
   for (int c0 = 0; c0 < n; c0 += 32) smem = std::max(smem, (size_t)(32 * ci_ld(n - c0) + 36 * c0) * 8);
   SKX_REQUIRE(smem <= (size_t)max_smem_optin(), "skx_chol_inv_upper: n = %d needs %zu B of shared memory",
               n, smem);
-  cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_chol_inv<<<1, kCiThreads, smem, (cudaStream_t)stream>>>(g, n, r, rinv, info);
+  if (n > kCiCoopMinN && getenv("SKX_CHOL_ONE_CTA") == nullptr) {
+    // cooperative grid: every CTA resident at once (one per SM at this smem)
+    cudaFuncSetAttribute(k_chol_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_inv<true>, kCiThreads, smem);
+    const int grid = (int)imin(kCiCoopCtas, (int64_t)imax(per_sm, 0) * num_sms());
+    if (grid >= 2) {
+      void* args[] = {(void*)&g, (void*)&n, (void*)&r, (void*)&rinv, (void*)&info};
+      if (cudaLaunchCooperativeKernel((const void*)k_chol_inv<true>, dim3(grid), dim3(kCiThreads),
+                                      args, smem, (cudaStream_t)stream) == cudaSuccess)
+        return check_launch("k_chol_inv<coop>");
+      cudaGetLastError();  // fall back to one CTA
+    }
+  }
+  cudaFuncSetAttribute(k_chol_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_chol_inv<false><<<1, kCiThreads, smem, (cudaStream_t)stream>>>(g, n, r, rinv, info);
   return check_launch("k_chol_inv");
 }
 

@@ -332,6 +332,80 @@ __global__ void __launch_bounds__(256) k_filter_fibers(int ndim, int mode, Coord
   }
 }
 
+// Order-3 form of k_filter_fibers: each thread takes four consecutive
+// nonzeros with one 16-byte load per other-mode coordinate row (the generic
+// kernel spends most of its issue slots on per-element 4-byte loads and 64-bit
+// index arithmetic: ALU 66%, 0.29 of HBM), a 2^19-bit Bloom filter in 64 KB of
+// shared memory (2 probes: ~0.06% false positives at m = 6400 instead of
+// ~0.23%, so fewer L2-latency binary searches), and a persistent grid (the
+// filter is built once per CTA, not once per 1024 nonzeros).  Same output set
+// (the slot order of the hits is not fixed; the caller sorts the keys).
+constexpr int kBloomBits3 = 19;
+
+__device__ __forceinline__ uint2 flat_hash2_b(uint64_t f, int bb) {
+  const uint64_t a = f * 0x9E3779B97F4A7C15ull, b = (f ^ (f >> 29)) * 0xBF58476D1CE4E5B9ull;
+  return make_uint2((uint32_t)(a >> (64 - bb)), (uint32_t)(b >> (64 - bb)));
+}
+
+__global__ void __launch_bounds__(256) k_filter_fibers3v(
+    const int32_t* __restrict__ ca, const int32_t* __restrict__ cb, int64_t ext_b,
+    const int32_t* __restrict__ cmode, int64_t s_n, int64_t nnz, const double* __restrict__ vals,
+    const int64_t* __restrict__ sflat, int64_t m, int64_t* __restrict__ out_key,
+    double* __restrict__ out_val, int64_t cap, unsigned long long* __restrict__ count) {
+  extern __shared__ uint32_t bits3[];
+  constexpr int NW = 1 << (kBloomBits3 - 5);
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) bits3[i] = 0u;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    const uint2 h = flat_hash2_b((uint64_t)sflat[j], kBloomBits3);
+    atomicOr(&bits3[h.x >> 5], 1u << (h.x & 31));
+    atomicOr(&bits3[h.y >> 5], 1u << (h.y & 31));
+  }
+  __syncthreads();
+  auto probe = [&](int64_t e, int64_t flat) {
+    const uint2 h = flat_hash2_b((uint64_t)flat, kBloomBits3);
+    if (!((bits3[h.x >> 5] >> (h.x & 31)) & (bits3[h.y >> 5] >> (h.y & 31)) & 1u)) return;
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sflat[mid] < flat) lo = mid + 1; else hi = mid;
+    }
+    if (lo < m && sflat[lo] == flat) {
+      const unsigned long long slot = atomicAdd(count, 1ull);
+      if ((int64_t)slot < cap) {
+        out_key[slot] = flat * s_n + cmode[e];
+        out_val[slot] = vals[e];
+      }
+    }
+  };
+  const int64_t n4 = nnz >> 2;
+  const int4* a4 = reinterpret_cast<const int4*>(ca);
+  const int4* b4 = reinterpret_cast<const int4*>(cb);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  constexpr int U = 2;  // 16-byte loads of U groups in flight per thread
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < n4; g0 += U * stride) {
+    int4 av[U], bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t g = g0 + u * stride;
+      av[u] = g < n4 ? __ldcs(a4 + g) : make_int4(0, 0, 0, 0);
+      bv[u] = g < n4 ? __ldcs(b4 + g) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t g = g0 + u * stride;
+      if (g >= n4) continue;
+      probe(4 * g + 0, (int64_t)av[u].x * ext_b + bv[u].x);
+      probe(4 * g + 1, (int64_t)av[u].y * ext_b + bv[u].y);
+      probe(4 * g + 2, (int64_t)av[u].z * ext_b + bv[u].z);
+      probe(4 * g + 3, (int64_t)av[u].w * ext_b + bv[u].w);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int64_t e = 4 * n4 + threadIdx.x; e < nnz; e += blockDim.x)
+      probe(e, (int64_t)ca[e] * ext_b + cb[e]);
+}
+
 // ---- sampled fibres of an order-3 tensor from its mode-0 fibre layout ----
 // Modes 1 and 2 of a leverage sub-problem sample fibres (i0, i_b): every
 // hit lies in slice i0 of the mode-0 layout (records {i1, i2 | sketch bits,
@@ -425,6 +499,21 @@ extern "C" int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode,
   }
   cudaMemsetAsync(count, 0, sizeof(uint64_t), s);
   if (nnz == 0) return check_launch("skx_filter_fibers_coo");
+  if (ndim == 3) {
+    int o[2], k2 = 0;
+    for (int k = 0; k < 3; ++k)
+      if (k != mode) o[k2++] = k;
+    const bool al = ((uintptr_t)cp.c[o[0]] % 16 == 0) && ((uintptr_t)cp.c[o[1]] % 16 == 0);
+    if (al) {
+      const size_t smem = (size_t)(1 << (kBloomBits3 - 5)) * 4;
+      cudaFuncSetAttribute(k_filter_fibers3v, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int64_t blocks = imax(1, imin((nnz + 2047) / 2048, (int64_t)num_sms() * 2));
+      k_filter_fibers3v<<<(unsigned)blocks, 256, smem, s>>>(
+          cp.c[o[0]], cp.c[o[1]], shape_h[o[1]], cp.c[mode], shape_h[mode], nnz, vals, sflat, m,
+          out_key, out_val, cap, (unsigned long long*)count);
+      return check_launch("k_filter_fibers3v");
+    }
+  }
   const int64_t blocks = imin((nnz + 1023) / 1024, (int64_t)num_sms() * 16);
   k_filter_fibers<<<(unsigned)blocks, 256, 0, s>>>(ndim, mode, cp, nnz, vals, sflat, m, out_key,
                                                    out_val, cap, (unsigned long long*)count);

@@ -108,7 +108,7 @@ def test_y_passes_vs_torch(m, s, w, storage):
     assert relerr(ty_times_dev(W, y).cpu().numpy(), W.cpu().numpy().T @ yh) <= 1e-13
 
 
-@pytest.mark.parametrize("n", [1, 31, 33, 129, 400, 512])
+@pytest.mark.parametrize("n", [1, 31, 33, 129, 400, 401, 450, 512])
 def test_chol_inv_upper(n):
     """One-CTA blocked Cholesky + inverse (r > 128: configs 3 and 5) vs LAPACK."""
     import torch
@@ -125,11 +125,12 @@ def test_chol_inv_upper(n):
     assert relerr(r @ rinv, np.eye(n)) <= 1e-12
 
 
-def test_chol_inv_upper_not_spd():
+@pytest.mark.parametrize("n", [300, 480])  # one CTA / cooperative grid
+def test_chol_inv_upper_not_spd(n):
     import torch
     from paper_2104_01101_b200.linalg import chol_inv_upper_dev
     g = np.random.default_rng(1)
-    a = g.standard_normal((300, 300))
+    a = g.standard_normal((n, n))
     gram = a @ a.T
     gram[100, 100] = -1.0  # pivot 100 (or earlier) fails
     r, rinv, info = (x.cpu().numpy() for x in chol_inv_upper_dev(torch.from_numpy(gram).cuda()))
