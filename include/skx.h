@@ -465,12 +465,14 @@ int skx_ttm_lead(const double* t, int64_t B, int64_t s, int64_t P, const double*
  * (src/linalg.py:103-112, associated form: Y G and W^T Y with w <= 32
  * columns), on FP64 tensor cores.  Row-major operands with leading
  * dimensions; N <= 32.
- *   skx_gemm_ab:  C (M x N) = A (M x K) B (K x N), A streamed by rows;
+ *   skx_gemm_ab:  C (M x N) = A (M x K) B (K x N), A streamed by rows (K
+ *                 split over CTAs when the row blocks alone fill the GPU's
+ *                 waves badly; workspace query with ws = NULL);
  *   skx_gemm_atb: C (M x N) = A^T B with A (K x M), B (K x N): split-K over
  *                 CTAs, partials summed in a fixed order (workspace query
  *                 with ws = NULL).  Deterministic. */
 int skx_gemm_ab(int64_t M, int N, int64_t K, const double* A, int64_t lda, const double* B,
-                int64_t ldb, double* C, int64_t ldc, void* stream);
+                int64_t ldb, double* C, int64_t ldc, void* ws, size_t* ws_bytes, void* stream);
 int skx_gemm_atb(int64_t M, int N, int64_t K, const double* A, int64_t lda, const double* B,
                  int64_t ldb, double* C, int64_t ldc, void* ws, size_t* ws_bytes, void* stream);
 

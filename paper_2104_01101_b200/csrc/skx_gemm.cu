@@ -12,6 +12,8 @@
 // in shared memory with the same k map, so one 64-byte row piece per four
 // lanes comes in per load instruction.  Deterministic: fixed tiles, fixed
 // split-K partition, fixed reduction order.
+#include <stdlib.h>
+
 #include "skx_common.cuh"
 
 namespace skx {
@@ -27,14 +29,20 @@ constexpr int kGRows = 128;   // rows (A B) or columns (A^T B) of C per CTA
 
 // C[M x N] = A[M x K] B[K x N]; A row-major (lda), B row-major (ldb), N <= 8 NT.
 // CTA = 8 warps x 16 rows; K streamed in chunks of 32 (B chunk in shared).
+// blockIdx.y = K split: k in [y kchunk, (y + 1) kchunk), written to
+// C + y cstride (partials, summed in order by k_gemm_atb_sum).
 template <int NT, bool VEC>
 __global__ void __launch_bounds__(256) k_gemm_ab(int64_t M, int N, int64_t K,
                                                  const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb,
-                                                 double* __restrict__ C, int64_t ldc) {
+                                                 double* __restrict__ C, int64_t ldc,
+                                                 int64_t kchunk, int64_t cstride) {
   __shared__ double Bs[kGKC][8 * NT + 2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, q = lane >> 2, c = lane & 3;
   const int64_t row0 = blockIdx.x * (int64_t)kGRows + wid * 16;
+  const int64_t kbeg = blockIdx.y * kchunk;
+  K = imin(K, kbeg + kchunk);
+  C += blockIdx.y * cstride;
   double acc[2][NT][2];
 #pragma unroll
   for (int t = 0; t < 2; ++t)
@@ -43,7 +51,7 @@ __global__ void __launch_bounds__(256) k_gemm_ab(int64_t M, int N, int64_t K,
   const int64_t r0 = row0 + q, r1 = row0 + 8 + q;
   const double* a0 = A + (r0 < M ? r0 : 0) * lda;
   const double* a1 = A + (r1 < M ? r1 : 0) * lda;
-  for (int64_t k0 = 0; k0 < K; k0 += kGKC) {
+  for (int64_t k0 = kbeg; k0 < K; k0 += kGKC) {
     __syncthreads();
     for (int e = threadIdx.x; e < kGKC * 8 * NT; e += blockDim.x) {
       const int kk = e / (8 * NT), n = e - kk * (8 * NT);
@@ -157,23 +165,77 @@ __global__ void k_gemm_atb_sum(const double* __restrict__ P, int64_t MN, int S, 
 
 using namespace skx;
 
+namespace {
+// K split of skx_gemm_ab: the row blocks alone can leave a last partial wave
+// (config 4: 782 blocks on 592 CTA slots = 0.66 of two waves); split K into
+// S <= 4 chunks (>= 256 each) when that fills the waves better, partials
+// summed in a fixed order (deterministic for given shapes).
+int gab_split(int64_t M, int64_t K, int NT) {
+  static int occ[5] = {0, 0, 0, 0, 0};
+  if (occ[NT] == 0) {
+    int o = 0;
+    switch (NT) {
+      case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gemm_ab<1, true>, 256, 0); break;
+      case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gemm_ab<2, true>, 256, 0); break;
+      case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gemm_ab<3, true>, 256, 0); break;
+      default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_gemm_ab<4, true>, 256, 0); break;
+    }
+    occ[NT] = o > 0 ? o : 1;
+  }
+  const int64_t slots = (int64_t)num_sms() * occ[NT];
+  const int64_t mb = (M + kGRows - 1) / kGRows;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int S = 1; S <= 4; ++S) {
+    if (S > 1 && K < 256 * (int64_t)S) break;
+    const int64_t tiles = mb * S, waves = (tiles + slots - 1) / slots;
+    const double eff = (double)tiles / (double)(waves * slots);
+    if (eff > best_eff + 0.02) {
+      best = S;
+      best_eff = eff;
+    }
+    if (S == 1 && eff >= 0.9) break;
+  }
+  return best;
+}
+}  // namespace
+
 extern "C" int skx_gemm_ab(int64_t M, int N, int64_t K, const double* A, int64_t lda,
-                           const double* B, int64_t ldb, double* C, int64_t ldc, void* stream) {
+                           const double* B, int64_t ldb, double* C, int64_t ldc, void* ws,
+                           size_t* ws_bytes, void* stream) {
   SKX_REQUIRE(N >= 1 && N <= 32, "skx_gemm_ab: 1 <= N <= 32");
   SKX_REQUIRE(M >= 0 && K >= 0, "skx_gemm_ab: negative extent");
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_gemm_ab: ws_bytes is NULL");
+  const int NT = (N + 7) / 8;
+  int S = (M > 0 && K > 0 && getenv("SKX_GAB_NOSPLIT") == nullptr) ? gab_split(M, K, NT) : 1;
+  const int64_t kchunk = S > 1 ? ((K + S - 1) / S + kGKC - 1) / kGKC * kGKC : K;
+  if (S > 1) S = (int)((K + kchunk - 1) / kchunk);
+  Arena ar(ws, *ws_bytes);
+  double* P = S > 1 ? ar.take<double>((size_t)S * M * N) : nullptr;
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_gemm_ab: workspace too small");
   if (M == 0) return SKX_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const bool vec = (lda % 2 == 0) && ((uintptr_t)A % 16 == 0);
-  const unsigned g = (unsigned)((M + kGRows - 1) / kGRows);
-  const int NT = (N + 7) / 8;
-#define SKX_GAB(nt)                                                                      \
-  if (NT == nt) {                                                                        \
-    if (vec) k_gemm_ab<nt, true><<<g, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc);    \
-    else k_gemm_ab<nt, false><<<g, 256, 0, st>>>(M, N, K, A, lda, B, ldb, C, ldc);       \
+  const dim3 g((unsigned)((M + kGRows - 1) / kGRows), (unsigned)S);
+  double* out = S > 1 ? P : C;
+  const int64_t ldo = S > 1 ? N : ldc, cs = S > 1 ? M * N : 0;
+#define SKX_GAB(nt)                                                                                \
+  if (NT == nt) {                                                                                  \
+    if (vec) k_gemm_ab<nt, true><<<g, 256, 0, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kchunk, cs); \
+    else k_gemm_ab<nt, false><<<g, 256, 0, st>>>(M, N, K, A, lda, B, ldb, out, ldo, kchunk, cs);    \
   }
   SKX_GAB(1) SKX_GAB(2) SKX_GAB(3) SKX_GAB(4)
 #undef SKX_GAB
-  return check_launch("k_gemm_ab");
+  if (S > 1) {
+    const int64_t MN = M * N;
+    k_gemm_atb_sum<<<(unsigned)imin((MN + 255) / 256, (int64_t)num_sms() * 8), 256, 0, st>>>(
+        P, MN, S, M, N, C, ldc);
+  }
+  return check_launch("k_gemm_ab", S > 1 ? 2 : 1);
 }
 
 extern "C" int skx_gemm_atb(int64_t M, int N, int64_t K, const double* A, int64_t lda,

@@ -429,8 +429,8 @@ def y_times_dev(y, g):
                                      nat.ptr(out), w), slot=10)
     else:
         ym, ldy = _row_major(y)
-        nat.call("skx_gemm_ab", m, w, s, nat.ptr(ym), ldy, nat.ptr(gm), ldg, nat.ptr(out), w,
-                 nat.stream())
+        nat.call_ws("skx_gemm_ab", (m, w, s, nat.ptr(ym), ldy, nat.ptr(gm), ldg, nat.ptr(out), w),
+                    slot=10)
     return out
 
 
@@ -445,8 +445,8 @@ def ty_times_dev(wm, y):
     wmm, ldw = _row_major(wm)
     out = torch.empty((s, w), dtype=torch.float64, device="cuda")  # (W^T Y)^T = Y^T W
     if y.stride(0) == 1 and y.stride(1) >= m:  # Y^T row-major s x m: Y^T W streams its rows
-        nat.call("skx_gemm_ab", s, w, m, nat.ptr(y), int(y.stride(1)), nat.ptr(wmm), ldw,
-                 nat.ptr(out), w, nat.stream())
+        nat.call_ws("skx_gemm_ab", (s, w, m, nat.ptr(y), int(y.stride(1)), nat.ptr(wmm), ldw,
+                                    nat.ptr(out), w), slot=10)
     else:
         ym, ldy = _row_major(y)
         nat.call_ws("skx_gemm_atb", (s, w, m, nat.ptr(ym), ldy, nat.ptr(wmm), ldw, nat.ptr(out), w),

@@ -139,6 +139,69 @@ def test_speculative_sweep_replay_is_exact(skx, sparse, sketch, monkeypatch):
     assert tr0.residuals == tr1.residuals and tr0.fitness == tr1.fitness
 
 
+@pytest.mark.parametrize("sketch", ["tensorsketch", "leverage-random"])
+@pytest.mark.parametrize("sparse", [False, True])
+def test_side_stream_residuals_bitwise(skx, sparse, sketch, monkeypatch):
+    """Sub-problem residuals computed on the low-priority side stream (beside
+    the next sub-problem) equal the inline ones bit for bit, with and without
+    forced replays of speculative sweeps; and at a config-4-like size where
+    the side stream is the default."""
+    import torch
+    from paper_2104_01101_b200 import linalg, tucker
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from paper_2104_01101_b200.tucker import sketched_tucker_als_dev
+    shape = (60, 50, 40)
+    if sparse:
+        c, v = planted_cp_coo_host(shape, 20_000, rank=3, seed=4)
+        t = skx.SparseTensor(shape, c, v)
+    else:
+        t = np.random.default_rng(4).standard_normal(shape)
+    cfg = skx.TuckerConfig(ranks=(4, 5, 3), max_sweeps=3, sketch=sketch, sketch_size=400, seed=5)
+
+    def run(env_inline, force):
+        if env_inline:
+            monkeypatch.setenv("SKX_RESID_INLINE", "1")
+        else:
+            monkeypatch.delenv("SKX_RESID_INLINE", raising=False)
+        monkeypatch.setattr(tucker, "RESID_SIDE_MIN", 0)
+        orig = linalg.sketch_qr_dev
+        seen = set()
+
+        def forcing(z, defer=None):
+            out = orig(z, defer)
+            if force and defer is not None and id(defer) not in seen:
+                seen.add(id(defer))
+                defer.append(torch.ones((), dtype=torch.bool, device="cuda"))
+            return out
+        monkeypatch.setattr(linalg, "sketch_qr_dev", forcing)
+        if sparse:
+            t._device = None
+        out = sketched_tucker_als_dev(t, cfg)
+        monkeypatch.setattr(linalg, "sketch_qr_dev", orig)
+        return out
+
+    core0, fac0, tr0 = run(True, False)
+    for force in (False, True):
+        core1, fac1, tr1 = run(False, force)
+        assert torch.equal(core0, core1)
+        for a, b in zip(fac0, fac1):
+            assert torch.equal(a, b)
+        assert tr0.residuals == tr1.residuals and tr0.fitness == tr1.fitness
+    if sparse and sketch == "tensorsketch":  # Y_n = 1600 x 4000 >= RESID_SIDE_MIN: default path
+        monkeypatch.undo()
+        shape = (4000, 4000, 4000)
+        c, v = planted_cp_coo_host(shape, 400_000, rank=10, seed=6)
+        st = skx.SparseTensor(shape, c, v)
+        cfg = skx.TuckerConfig(ranks=(10, 10, 10), max_sweeps=2, sketch="tensorsketch",
+                               sketch_size=1600, seed=6)
+        assert 1600 * 4000 >= tucker.RESID_SIDE_MIN
+        _, _, tr_side = sketched_tucker_als_dev(st, cfg)
+        monkeypatch.setenv("SKX_RESID_INLINE", "1")
+        st._device = None
+        _, _, tr_inl = sketched_tucker_als_dev(st, cfg)
+        assert tr_side.residuals == tr_inl.residuals
+
+
 # ---- ttmc and exact HOOI (SURVEY 8b operator list, 8f rank 2) vs the reference
 from tests.test_oracle_golden import HOOI, TTMC, ttmc_factors, ttmc_input  # noqa: E402
 

@@ -92,10 +92,13 @@ def test_qr_lapack_signs(shape):
 
 @pytest.mark.parametrize("m,s,w,storage", [(1600, 100000, 20, "t"), (3200, 400, 20, "r"),
                                            (400, 120, 18, "t"), (37, 1001, 5, "r"),
-                                           (100, 33, 32, "t"), (77, 9, 1, "r")])
+                                           (100, 33, 32, "t"), (77, 9, 1, "r"),
+                                           (12000, 2000, 24, "r"), (1024, 30000, 20, "t")])
 def test_y_passes_vs_torch(m, s, w, storage):
     """Y G and W^T Y of rsvd_lrls on libskx's FP64 tensor-core kernels, for
-    Y stored row-major (dense / leverage) or as Y^T (TensorSketch)."""
+    Y stored row-major (dense / leverage) or as Y^T (TensorSketch); the
+    streamed-rows kernel with and without its K split (e.g. 1e5 rows: 3
+    chunks; 12000 rows: 4)."""
     import torch
     from paper_2104_01101_b200.linalg import ty_times_dev, y_times_dev
     g = np.random.default_rng(m + s)
