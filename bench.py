@@ -528,6 +528,49 @@ def _cpu_measure(cfg_id, cfgd, threads, reps=1):
     return scaled, raw, best, desc
 
 
+def _cpu_operators(cfg_id, cfgd):
+    """CPU rate of the reference's two bandwidth-class sketch operators on the
+    sparse sample (oracle restatements of src/sketching.py:150-175 and
+    :327-341), mode 1's unfolding, with the GPU kernels' byte models: COO
+    input 20 B/nnz read once, the m x s_n (k2 x s_n) output written once."""
+    from oracle import sketchals_port as orc
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    sm = SAMPLE[cfg_id]
+    if sm is None or cfgd["kind"] == "dense":
+        return None
+    shape, nnz = sm["shape"], sm["nnz"]
+    c, v = planted_cp_coo_host(shape, nnz, rank=10, noise_sd=0.1, seed=0)
+    t = orc.Coo(shape, c, v, presorted=True)
+    n = 1
+    tn_t = orc.unfold_t(t, n)  # (P_n x s_n), built outside the timed region
+    tn = tn_t.T.tocsr()
+    ext = [shape[k] for k in range(3) if k != n]
+    rng = orc.generator(0)
+    out = {}
+    if cfgd["sketch"] == "tensorsketch":
+        m = cfgd["sketch_size"]
+        hs, ss = orc.ts_tables(ext, m, rng)
+        t0 = time.perf_counter()
+        orc.ts_rhs(hs, ss, ext, m, tn_t)
+        dt = time.perf_counter() - t0
+        by = nnz * 20 + 8 * m * shape[n]
+        out["ts_apply_rhs"] = {"seconds": round(dt, 4), "gb_per_s": round(by / dt / 1e9, 4),
+                               "nnz_per_s": round(nnz / dt, 1), "m": m}
+    r = cfgd["ranks"][n]
+    width = r + 10
+    k2 = r * r + width
+    h, sg, g = orc.rrf_tables(tn.shape[1], width, k2, rng)
+    t0 = time.perf_counter()
+    orc.rrf_apply(tn, h, sg, g, k2)
+    dt = time.perf_counter() - t0
+    by = nnz * 20 + 8 * k2 * shape[n]
+    out["composite_apply"] = {"seconds": round(dt, 4), "gb_per_s": round(by / dt / 1e9, 4),
+                              "nnz_per_s": round(nnz / dt, 1), "k2": k2}
+    out["sample"] = (f"{shape[0]}^3 with {nnz:.1e} nnz, mode 1; bytes = 20 B/nnz COO + the "
+                     f"output once (the GPU kernels' model); BLAS threads as the call")
+    return out
+
+
 def cpu_baseline(cfg_id, cfgd):
     n = _cpu_threads()
     scaled, raw, secs, desc = _cpu_measure(cfg_id, cfgd, n)
@@ -545,6 +588,12 @@ def cpu_baseline(cfg_id, cfgd):
     if s1 is not None:
         out["one_thread"] = {"value": s1, "sample_sweeps_per_s": r1, "seconds_per_call": sec1,
                              "cores": 1}
+    try:
+        ops = _cpu_operators(cfg_id, cfgd)
+    except Exception as exc:  # context only: never fail the bench line over it
+        ops = {"error": repr(exc)[:200]}
+    if ops is not None:
+        out["operators"] = ops
     return out
 
 
