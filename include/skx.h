@@ -493,6 +493,54 @@ int skx_cp_core_als(const int64_t* dims_h, int rank, int sweeps, const double* c
                     int* info, void* stream);
 size_t skx_cp_core_smem_bytes(const int64_t* dims_h, int rank);
 
+/* ------------------------------------------- K7: model fitness, one call each
+ * fitness(t, model) = 1 - ||T - model||_F / ||T||_F assembled from
+ * ||T||^2 - 2 <T, model> + ||model||^2, clamped at 0 (src/tensors.py:339-368);
+ * *fit (device scalar) receives it.  norm2: device scalar ||T||^2 if the
+ * caller has it, else NULL (computed).  No host synchronisation. */
+
+/* Tucker model, sparse: cross term by skx_tucker_cross_coo (same arguments:
+ * colptr0 / rec0 = the mode-0 fibre layout for the order-3 kernels, or NULL),
+ * ||model||^2 = ||C||^2 (orthonormal factors, src/tensors.py:351-353). */
+int skx_fitness_tucker_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h, int64_t nnz,
+                           const int32_t* coords, const double* vals,
+                           const double* const* factors_h, const double* core,
+                           const int64_t* colptr0, const void* rec0, uint32_t c1_mask,
+                           const double* norm2, double* fit, void* ws, size_t* ws_bytes,
+                           void* stream);
+/* Tucker model, dense C-order tensor t: ttmc(t, A) by skx_ttm_lead mode
+ * products in ascending mode order (src/tensors.py:217-247), ranks <= 32. */
+int skx_fitness_tucker_dense(int ndim, const int64_t* shape_h, const double* t,
+                             const int64_t* ranks_h, const double* const* factors_h,
+                             const double* core, const double* norm2, double* fit, void* ws,
+                             size_t* ws_bytes, void* stream);
+/* CP model (factors s_k x R, weights R, R <= 32), sparse: cross term by
+ * skx_cp_cross_fibre3 (order 3 with the mode-0 layout) or skx_cp_cross_coo;
+ * ||model||^2 from the Hadamard product of the factor Grams
+ * (src/tensors.py:354-361). */
+int skx_fitness_cp_coo(int ndim, const int64_t* shape_h, int R, int64_t nnz,
+                       const int32_t* coords, const double* vals, const double* const* factors_h,
+                       const double* weights, const int64_t* colptr0, const void* rec0,
+                       uint32_t c1_mask, const double* norm2, double* fit, void* ws,
+                       size_t* ws_bytes, void* stream);
+
+/* ---------------------------------- multi-GPU reductions, NCCL
+ * The data-path collectives of the nnz-sharded solve (dist.py: Y_n
+ * reduce-scattered by columns, fitness cross terms all-reduced, the sampled
+ * fibres all-gathered), for callers that drive libskx without
+ * torch.distributed.  libnccl.so.2 is opened at first use (no link
+ * dependency).  unique_id / id_out: 128-byte ncclUniqueId in HOST memory
+ * (rank 0 creates it, the caller broadcasts it); comm: opaque handle.  Sums
+ * are float64; counts are elements; recv of reduce-scatter holds recv_count
+ * elements per rank, of all-gather nranks * send_count. */
+int skx_nccl_unique_id(void* id_out);
+int skx_nccl_init(const void* unique_id, int rank, int nranks, void** comm_out);
+int skx_nccl_destroy(void* comm);
+int skx_allreduce_sum(void* comm, const double* send, double* recv, int64_t count, void* stream);
+int skx_reduce_scatter_sum(void* comm, const double* send, double* recv, int64_t recv_count,
+                           void* stream);
+int skx_allgather(void* comm, const double* send, double* recv, int64_t send_count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

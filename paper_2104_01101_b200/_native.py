@@ -87,8 +87,19 @@ _SIGS = {
     "skx_cp_core_smem_bytes": [c_p, c_i32],
     "skx_cp_cross_fibre3": [c_i64, c_p, c_p, c_u32, c_i32, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_ttm_lead": [c_p, c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p],
-    "skx_gemm_ab": [c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_p, c_p],
+    "skx_gemm_ab": [c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_sz_p, c_p],
     "skx_gemm_atb": [c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_sz_p, c_p],
+    "skx_fitness_tucker_coo": [c_i32, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_u32, c_p,
+                               c_p, c_p, c_sz_p, c_p],
+    "skx_fitness_tucker_dense": [c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
+    "skx_fitness_cp_coo": [c_i32, c_p, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_u32, c_p, c_p,
+                           c_p, c_sz_p, c_p],
+    "skx_nccl_unique_id": [c_p],
+    "skx_nccl_init": [c_p, c_i32, c_i32, c_p],
+    "skx_nccl_destroy": [c_p],
+    "skx_allreduce_sum": [c_p, c_p, c_p, c_i64, c_p],
+    "skx_reduce_scatter_sum": [c_p, c_p, c_p, c_i64, c_p],
+    "skx_allgather": [c_p, c_p, c_p, c_i64, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],

@@ -74,7 +74,7 @@ def build(verbose=False, force=False):
             if verbose and msg:
                 print(msg)
     if jobs or _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"]
         run(cmd)
     return LIB
 

@@ -100,3 +100,17 @@ def test_rngref_c_matches_numpy():
             o = np.zeros(30_001, dtype=np.int64)
             lib.rr_bounded_fill(key[0], key[1], ctypes.addressof(st), k, o.size, o.ctypes.data)
             assert np.array_equal(ref, o), k
+
+
+def test_nccl_entries_host_side(lib):
+    """The NCCL binding opens libnccl at first use: a unique id is made on the
+    host (no GPU needed); invalid ranks and NULL handles are rejected with the
+    invalid-argument code before any NCCL call."""
+    buf = ctypes.create_string_buffer(128)
+    assert lib.skx_nccl_unique_id(buf) == 0
+    assert any(buf.raw)
+    comm = ctypes.c_void_p()
+    assert lib.skx_nccl_init(buf, 2, 2, ctypes.byref(comm)) == 1
+    assert lib.skx_nccl_init(None, 0, 1, ctypes.byref(comm)) == 1
+    assert lib.skx_allreduce_sum(None, None, None, ctypes.c_int64(1), None) == 1
+    assert lib.skx_nccl_unique_id(None) == 1

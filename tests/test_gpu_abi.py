@@ -1,0 +1,144 @@
+"""The composite C-ABI entries of SURVEY 8(b)'s export list, called through
+ctypes the way a C caller would: model fitness in one call (Tucker sparse /
+dense, CP sparse) against the Python layer and the CPU oracle, and the NCCL
+binding on a one-rank communicator."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_2104_01101_b200 as skx
+    from paper_2104_01101_b200 import _native as nat
+    nat.load()
+    return torch, skx, nat
+
+
+def _orthonormal(rng, s, r):
+    return np.linalg.qr(rng.standard_normal((s, r)))[0]
+
+
+@pytest.mark.parametrize("shape,nnz,R", [((300, 400, 500), 200_000, 10),
+                                         ((2000, 1500, 1000), 1_000_000, 20),
+                                         ((40, 30, 20, 10), 20_000, 4)])
+def test_fitness_tucker_coo_entry(env, oracle, shape, nnz, R):
+    torch, skx, nat = env
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from paper_2104_01101_b200.tensors import device_of
+    c, v = planted_cp_coo_host(shape, nnz, rank=3, seed=5)
+    st = skx.SparseTensor(shape, c, v)
+    d = device_of(st)
+    rng = np.random.default_rng(5)
+    ranks = [min(R, s) for s in shape]
+    fac = [_orthonormal(rng, s, r) for s, r in zip(shape, ranks)]
+    core = rng.standard_normal(ranks)
+    fd = [torch.from_numpy(a).cuda() for a in fac]
+    cd = torch.from_numpy(core).cuda()
+    shp, sp_ = nat.host_i64(shape)
+    rk, rp = nat.host_i64(ranks)
+    arr, fp = nat.host_ptrs(fd)
+    cpt, rec0 = d.fibre(0) if d.ndim == 3 else (None, None)
+    fit = torch.empty(1, dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_fitness_tucker_coo",
+                (d.ndim, sp_, rp, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp, nat.ptr(cd),
+                 nat.ptr(cpt), nat.ptr(rec0), ctypes.c_uint32(d.fibre_mask(0) if d.ndim == 3 else 0),
+                 None, nat.ptr(fit)))
+    got = float(fit.cpu())
+    ref_py = skx.fitness(st, skx.TuckerModel(core, fac))
+    ref_orc = oracle.fitness_tucker(oracle.Coo(shape, c, v), core, fac)
+    assert abs(got - ref_py) <= 1e-13, (got, ref_py)
+    assert abs(got - ref_orc) <= 1e-12, (got, ref_orc)
+    # caller-supplied ||T||^2
+    n2 = torch.tensor([float(np.sum(v * v))], dtype=torch.float64, device="cuda")
+    fit2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_fitness_tucker_coo",
+                (d.ndim, sp_, rp, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp, nat.ptr(cd),
+                 nat.ptr(cpt), nat.ptr(rec0), ctypes.c_uint32(d.fibre_mask(0) if d.ndim == 3 else 0),
+                 nat.ptr(n2), nat.ptr(fit2)))
+    assert abs(float(fit2.cpu()) - got) <= 1e-14
+
+
+@pytest.mark.parametrize("shape,R", [((60, 50, 40), 5), ((20, 18, 16, 14), 4)])
+def test_fitness_tucker_dense_entry(env, oracle, shape, R):
+    torch, skx, nat = env
+    rng = np.random.default_rng(7)
+    t = rng.standard_normal(shape)
+    ranks = [R] * len(shape)
+    fac = [_orthonormal(rng, s, R) for s in shape]
+    core = rng.standard_normal(ranks)
+    td = torch.from_numpy(t).cuda()
+    fd = [torch.from_numpy(a).cuda() for a in fac]
+    cd = torch.from_numpy(core).cuda()
+    shp, sp_ = nat.host_i64(shape)
+    rk, rp = nat.host_i64(ranks)
+    arr, fp = nat.host_ptrs(fd)
+    fit = torch.empty(1, dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_fitness_tucker_dense",
+                (len(shape), sp_, nat.ptr(td), rp, fp, nat.ptr(cd), None, nat.ptr(fit)))
+    got = float(fit.cpu())
+    assert abs(got - skx.fitness(t, skx.TuckerModel(core, fac))) <= 1e-13
+    assert abs(got - oracle.fitness_tucker(t, core, fac)) <= 1e-12
+
+
+@pytest.mark.parametrize("shape,nnz,R,layout", [((300, 400, 500), 200_000, 10, True),
+                                                ((300, 400, 500), 200_000, 7, False),
+                                                ((40, 30, 20, 10), 20_000, 5, False)])
+def test_fitness_cp_coo_entry(env, oracle, shape, nnz, R, layout):
+    torch, skx, nat = env
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from paper_2104_01101_b200.tensors import device_of
+    c, v = planted_cp_coo_host(shape, nnz, rank=3, seed=8)
+    st = skx.SparseTensor(shape, c, v)
+    d = device_of(st)
+    rng = np.random.default_rng(8)
+    fac = [rng.standard_normal((s, R)) for s in shape]
+    w = rng.random(R) + 0.5
+    fd = [torch.from_numpy(a).cuda() for a in fac]
+    wd = torch.from_numpy(w).cuda()
+    shp, sp_ = nat.host_i64(shape)
+    arr, fp = nat.host_ptrs(fd)
+    cpt, rec0 = d.fibre(0) if layout else (None, None)
+    fit = torch.empty(1, dtype=torch.float64, device="cuda")
+    nat.call_ws("skx_fitness_cp_coo",
+                (d.ndim, sp_, R, d.nnz, nat.ptr(d.coords), nat.ptr(d.vals), fp, nat.ptr(wd),
+                 nat.ptr(cpt), nat.ptr(rec0), ctypes.c_uint32(d.fibre_mask(0) if layout else 0),
+                 None, nat.ptr(fit)))
+    got = float(fit.cpu())
+    ref_py = skx.fitness(st, skx.CPModel(fac, w))
+    ref_orc = oracle.fitness_cp(oracle.Coo(shape, c, v), fac, w)
+    assert abs(got - ref_py) <= 1e-12 * max(1.0, abs(ref_py)), (got, ref_py)
+    assert abs(got - ref_orc) <= 1e-11 * max(1.0, abs(ref_orc)), (got, ref_orc)
+
+
+def test_nccl_one_rank(env):
+    """A one-rank communicator: all-reduce, reduce-scatter and all-gather are
+    copies (a B200 box gives one GPU per call; several ranks of one device are
+    not a valid NCCL communicator)."""
+    torch, skx, nat = env
+    lib = nat.load()
+    uid = ctypes.create_string_buffer(128)
+    assert lib.skx_nccl_unique_id(uid) == 0
+    comm = ctypes.c_void_p()
+    assert lib.skx_nccl_init(uid, 0, 1, ctypes.byref(comm)) == 0
+    try:
+        x = torch.randn(1000, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        st = nat.stream()
+        assert lib.skx_allreduce_sum(comm, nat.ptr(x), nat.ptr(y), ctypes.c_int64(1000), st) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+        y.zero_()
+        assert lib.skx_reduce_scatter_sum(comm, nat.ptr(x), nat.ptr(y), ctypes.c_int64(1000), st) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+        y.zero_()
+        assert lib.skx_allgather(comm, nat.ptr(x), nat.ptr(y), ctypes.c_int64(1000), st) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+    finally:
+        assert lib.skx_nccl_destroy(comm) == 0
