@@ -347,6 +347,7 @@ __device__ __forceinline__ uint2 flat_hash2_b(uint64_t f, int bb) {
   return make_uint2((uint32_t)(a >> (64 - bb)), (uint32_t)(b >> (64 - bb)));
 }
 
+template <int U>
 __global__ void __launch_bounds__(256) k_filter_fibers3v(
     const int32_t* __restrict__ ca, const int32_t* __restrict__ cb, int64_t ext_b,
     const int32_t* __restrict__ cmode, int64_t s_n, int64_t nnz, const double* __restrict__ vals,
@@ -382,7 +383,6 @@ __global__ void __launch_bounds__(256) k_filter_fibers3v(
   const int4* a4 = reinterpret_cast<const int4*>(ca);
   const int4* b4 = reinterpret_cast<const int4*>(cb);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  constexpr int U = 2;  // 16-byte loads of U groups in flight per thread
   for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < n4; g0 += U * stride) {
     int4 av[U], bv[U];
 #pragma unroll
@@ -506,9 +506,13 @@ extern "C" int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode,
     const bool al = ((uintptr_t)cp.c[o[0]] % 16 == 0) && ((uintptr_t)cp.c[o[1]] % 16 == 0);
     if (al) {
       const size_t smem = (size_t)(1 << (kBloomBits3 - 5)) * 4;
-      cudaFuncSetAttribute(k_filter_fibers3v, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int64_t blocks = imax(1, imin((nnz + 2047) / 2048, (int64_t)num_sms() * 2));
-      k_filter_fibers3v<<<(unsigned)blocks, 256, smem, s>>>(
+      // four groups of four nonzeros (2 x 16-byte loads each) in flight per
+      // thread (config 5, beside K7: 3.93 ms with two, 3.11 with four, 5.63
+      // with eight per 1e9-nonzero pass)
+      cudaFuncSetAttribute(k_filter_fibers3v<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      k_filter_fibers3v<4><<<(unsigned)blocks, 256, smem, s>>>(
           cp.c[o[0]], cp.c[o[1]], shape_h[o[1]], cp.c[mode], shape_h[mode], nnz, vals, sflat, m,
           out_key, out_val, cap, (unsigned long long*)count);
       return check_launch("k_filter_fibers3v");
