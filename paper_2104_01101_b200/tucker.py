@@ -298,6 +298,20 @@ def _fit_stream():
     return _FIT_STREAMS[dev]
 
 
+_ST1_STREAMS = {}
+
+
+def _stage1_stream(i):
+    """High-priority stream for the chunked RRF stage-1 sums of the i-th
+    range-finder mode (i >= 1; the first runs on the init main stream)."""
+    torch = _torch()
+    key = (torch.cuda.current_device(), i)
+    if key not in _ST1_STREAMS:
+        _, hi = torch.cuda.Stream.priority_range()
+        _ST1_STREAMS[key] = torch.cuda.Stream(priority=hi)
+    return _ST1_STREAMS[key]
+
+
 _RES_STREAMS = {}
 # sub-problem residuals over a Y of at least this many entries run on a side
 # stream (config 4: 1.6e8, 83.8 -> 81.8 ms per call); below it the extra
@@ -548,13 +562,13 @@ class _Run:
             self._attach(d)
         fx = d.fixed_point_ok()  # staging's value range, or one small D2H once the values are in
         self.normals.prefetch()
-        # the RRF tables of every mode, in the reference's draw order
-        tabs_all = []
-        for n, scan, (P, k2, width) in zip(modes, scans, dims):
-            tabs = finish_rrf_scan(scan, self.rng_init, P)
-            gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
-            tabs_all.append((n, tabs, gauss))
         if not fx:
+            # the RRF tables of every mode, in the reference's draw order
+            tabs_all = []
+            for n, scan, (P, k2, width) in zip(modes, scans, dims):
+                tabs = finish_rrf_scan(scan, self.rng_init, P)
+                gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
+                tabs_all.append((n, tabs, gauss))
             main.wait_stream(conv)
             for ev in conv_ev:
                 main.wait_event(ev)
@@ -564,22 +578,47 @@ class _Run:
             return
         emax = d.value_range()[0]
         shp, sp_ = nat.host_i64(self.shape)
-        accs = {}
-        for n, tabs, _ in tabs_all:
-            accs[n] = (torch.zeros(self.shape[n] * tabs.k2 * 4, dtype=torch.int64, device="cuda"),
-                       torch.empty(1, dtype=torch.int32, device="cuda"))
-        for (lo, hi), ev in zip(bounds, conv_ev):
-            main.wait_event(ev)
-            cptr = ctypes.c_void_p(coords.data_ptr() + lo * 4)
-            vptr = ctypes.c_void_p(vals.data_ptr() + lo * 8)
-            for n, tabs, _ in tabs_all:
-                acc, flag = accs[n]
-                bound = c3["rowmax"].get(n, -1) if c3 is not None else -1
-                nat.call("skx_rrf_stage1_fx_acc", nd, sp_, n, hi - lo, cptr, nnz, vptr, emax,
-                         *tabs.args(), tabs.k2, nat.ptr(acc), nat.ptr(flag), bound, nat.stream())
+        # Each mode's chunk sums are enqueued as soon as its own rejection scan
+        # is resolved (tables in the reference's draw order), on a stream of
+        # its own: mode 1's run beside scan 2 as the chunks land instead of
+        # waiting for it, mode 2's catch up behind scan 2.
+        tabs_all, accs, side = [], {}, []
+        ev0 = torch.cuda.Event()
+        ev0.record(main)  # everything before the chunk sums (not mode 1's chunk loop)
+        for i, (n, scan, (P, k2, width)) in enumerate(zip(modes, scans, dims)):
+            sn = main if i == 0 else _stage1_stream(i)
+            if sn is not main:
+                sn.wait_event(ev0)
+                for t in (coords, vals):
+                    t.record_stream(sn)
+                side.append(sn)
+            with torch.cuda.stream(sn):
+                # the scan's finish and the accumulator on this mode's stream
+                tabs = finish_rrf_scan(scan, self.rng_init, P)
+                acc = torch.zeros(self.shape[n] * tabs.k2 * 4, dtype=torch.int64, device="cuda")
+                flag = torch.empty(1, dtype=torch.int32, device="cuda")
+            gauss = self.rng_init.standard_normal((k2, width)) / np.sqrt(width)
+            tabs_all.append((n, tabs, gauss))
+            accs[n] = (acc, flag)
+            if sn is not main:
+                for t in (acc, flag, tabs.d):
+                    t.record_stream(main)  # converted on the main stream below
+            bound = c3["rowmax"].get(n, -1) if c3 is not None else -1
+            with torch.cuda.stream(sn):
+                for (lo, hi), ev in zip(bounds, conv_ev):
+                    sn.wait_event(ev)
+                    cptr = ctypes.c_void_p(coords.data_ptr() + lo * 4)
+                    vptr = ctypes.c_void_p(vals.data_ptr() + lo * 8)
+                    nat.call("skx_rrf_stage1_fx_acc", nd, sp_, n, hi - lo, cptr, nnz, vptr, emax,
+                             *tabs.args(), tabs.k2, nat.ptr(acc), nat.ptr(flag), bound, nat.stream())
+        # the fitness layout (a packing pass) on the convert stream behind the
+        # last unpack, beside the last chunks' sums
+        with torch.cuda.stream(conv):
+            self.d.fibre(0)
+        for sn in side:
+            main.wait_stream(sn)
         coords.record_stream(main)
-        main.wait_stream(conv)  # every chunk unpacked, ||T||^2 done
-        self.d.fibre(0)  # the fitness layout (a packing pass)
+        main.wait_stream(conv)  # every chunk unpacked, ||T||^2 done, layout built
         for n, tabs, gauss in tabs_all:
             acc, flag = accs[n]
             st1 = torch.empty((self.shape[n], tabs.k2), dtype=torch.float64, device="cuda")
