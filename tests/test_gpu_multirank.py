@@ -104,3 +104,59 @@ def test_two_ranks_match_single_process():
             assert np.allclose(fit, tr.fitness, rtol=0, atol=1e-12)
             assert np.allclose(resid, tr.residuals, rtol=1e-10)
     tucker.HITS_DENSITY = 0.05
+
+
+ALG6 = dict(rank=3, tucker_rank=5, sketch="leverage-random", sketch_size=600, tucker_sweeps=3,
+            max_sweeps=10, seed=7)
+
+
+def _worker_alg6(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    import paper_2104_01101_b200 as skx
+    from paper_2104_01101_b200.cp import cp_via_sketched_tucker_dev
+    from paper_2104_01101_b200.dist import Comm, shard_device_coo
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Comm()
+    c, v = planted_cp_coo_host(SHAPE, NNZ, rank=3, seed=2)
+    coords = torch.from_numpy(c.T.astype(np.int32)).cuda()
+    vals = torch.from_numpy(v).cuda()
+    cs, vs, _ = shard_device_coo(coords, vals, SHAPE, world, rank)
+    st = skx.SparseTensor.from_device(SHAPE, cs, vs)
+    fac, w, tr = cp_via_sketched_tucker_dev(st, skx.CPConfig(**ALG6), comm)
+    q.put((rank, ([a.cpu().numpy() for a in fac], w.cpu().numpy(), tr.fitness, tr.residuals)))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_alg6_match_single_process():
+    """Algorithm 6 (the config-5 bench workload) with the nonzeros sharded over
+    two ranks -- sketched Tucker stage over the ranks, replicated CP-ALS on
+    the core, CP fitness cross term all-reduced -- against one process."""
+    import multiprocessing as mp
+    import paper_2104_01101_b200 as skx
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_alg6, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c, v = planted_cp_coo_host(SHAPE, NNZ, rank=3, seed=2)
+    model, tr = skx.cp_via_sketched_tucker(skx.SparseTensor(SHAPE, c, v), skx.CPConfig(**ALG6))
+    for r in (0, 1):
+        fac, w, fit, resid = res[r]
+        assert np.allclose(fit, tr.fitness, rtol=0, atol=1e-10), (fit, tr.fitness)
+        assert np.allclose(resid, tr.residuals, rtol=1e-8)
+        assert relerr(w, model.weights) <= 1e-8
+        for a, b in zip(fac, model.factors):
+            assert relerr(a, b) <= 1e-8
