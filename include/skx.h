@@ -101,6 +101,12 @@ int skx_coo_fibre_ts(const int64_t* shape_h, int mode, int64_t nnz, const int32_
                      const double* vals, const uint32_t* tab, const int64_t* tab_off_h,
                      int64_t m, void* rec_out, int64_t* colptr, uint32_t* c1_mask, void* ws,
                      size_t* ws_bytes, void* stream);
+/* Records [lo, hi) of the mode-0 fibre layout of a lexsorted COO (input order,
+ * the layout skx_coo_fibre builds for mode 0; its colptr is the mode-0 slice
+ * pointer array), coordinate rows of stride ld: the layout built chunk by
+ * chunk while a host COO is uploaded (src/tensors.py:89-95 mode_sort(0)). */
+int skx_coo_pack0_range(int ndim, int64_t ld, int64_t lo, int64_t hi, const int32_t* coords,
+                        const double* vals, void* rec_out, void* stream);
 
 /* Y^T = (S . T_(n)^T)^T for a COO tensor in the fibre-major layout of mode n
  * (skx_coo_fibre); tab = packed tables of the other modes concatenated,

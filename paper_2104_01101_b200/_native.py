@@ -100,6 +100,7 @@ _SIGS = {
     "skx_allreduce_sum": [c_p, c_p, c_p, c_i64, c_p],
     "skx_reduce_scatter_sum": [c_p, c_p, c_p, c_i64, c_p],
     "skx_allgather": [c_p, c_p, c_p, c_i64, c_p],
+    "skx_coo_pack0_range": [c_i32, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],

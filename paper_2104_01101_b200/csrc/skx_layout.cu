@@ -63,6 +63,25 @@ __global__ void k_pack(int ndim, int mode, int64_t nnz, const int32_t* __restric
   if (keys) keys[e] = (uint32_t)__ldcs(coords + (int64_t)mode * nnz + e);
 }
 
+// Records [lo, hi) of a packing pass whose coordinate rows have stride ld
+// (chunk-wise mode-0 layout of a COO that arrives in pieces)
+template <class Rec>
+__global__ void k_pack_range(int ndim, int mode, int64_t ld, int64_t lo, int64_t hi,
+                             const int32_t* __restrict__ coords, const double* __restrict__ vals,
+                             Rec* __restrict__ rec) {
+  constexpr int NS = (int)(sizeof(Rec::c) / sizeof(int32_t));
+  const int64_t e = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= hi) return;
+  Rec r;
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    const int src = j + (j >= mode ? 1 : 0);
+    r.c[j] = (j < ndim - 1) ? __ldcs(coords + (int64_t)src * ld + e) : 0;
+  }
+  r.v = __ldcs(vals + e);
+  rec[e] = r;
+}
+
 // colptr[c] = first position whose key >= c (keys sorted), c in [0, s]
 __global__ void k_bounds_u32(const uint32_t* __restrict__ keys, int64_t n, int64_t s,
                              int64_t* __restrict__ colptr) {
@@ -151,6 +170,25 @@ extern "C" int skx_coo_fibre(int ndim, const int64_t* shape_h, int mode, int64_t
   if (ndim - 1 <= 2)
     return build<Rec16>(ndim, shape_h, mode, nnz, coords, vals, rec_out, colptr, ws, ws_bytes, s);
   return build<Rec24>(ndim, shape_h, mode, nnz, coords, vals, rec_out, colptr, ws, ws_bytes, s);
+}
+
+// Chunk of the mode-0 fibre layout of a lexsorted COO (records in input
+// order; colptr = the mode-0 slice pointers): the records of nonzeros
+// [lo, hi) from coordinate rows of stride ld.  Built as the chunks of a host
+// upload land, so the layout is complete with the last chunk.
+extern "C" int skx_coo_pack0_range(int ndim, int64_t ld, int64_t lo, int64_t hi,
+                                   const int32_t* coords, const double* vals, void* rec_out,
+                                   void* stream) {
+  SKX_REQUIRE(ndim >= 2 && ndim <= 5, "skx_coo_pack0_range: sparse order 2..5 supported");
+  SKX_REQUIRE(lo >= 0 && lo <= hi && hi <= ld, "skx_coo_pack0_range: bad range");
+  if (hi == lo) return SKX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned g = (unsigned)((hi - lo + 255) / 256);
+  if (ndim - 1 <= 2)
+    k_pack_range<Rec16><<<g, 256, 0, s>>>(ndim, 0, ld, lo, hi, coords, vals, (Rec16*)rec_out);
+  else
+    k_pack_range<Rec24><<<g, 256, 0, s>>>(ndim, 0, ld, lo, hi, coords, vals, (Rec24*)rec_out);
+  return check_launch("skx_coo_pack0_range");
 }
 
 static int bits_for(int64_t n) {  // bits to hold 0..n-1

@@ -254,7 +254,9 @@ def _init_streams():
 
 # host COO inputs of at least this many nonzeros are uploaded in chunks of
 # this many rows (leverage runs; the TensorSketch layouts need the whole tensor)
-UPLOAD_CHUNK = 1 << 26
+# nonzeros per upload chunk (config 5: 30 chunks; 15 measured ~3 ms slower
+# e2e: the last chunk's stage-1 sums are the tail behind the upload)
+UPLOAD_CHUNK = 1 << 25
 
 _UP_STREAMS = {}
 
@@ -496,6 +498,9 @@ class _Run:
             ptr_h = c3["ptr0"]
             s0 = int(ptr_h.numel()) - 1
             packed = torch.empty(nnz, dtype=torch.int32, device="cuda")
+            # the mode-0 fibre layout (the fitness passes' input) is packed
+            # chunk by chunk behind each unpack; its colptr is ptr0
+            rec0 = torch.empty(max(nnz, 1) * 2, dtype=torch.float64, device="cuda")
             with torch.cuda.stream(copy):
                 aux = compact3_aux_to_device(c3)
             s_lo = 0
@@ -517,6 +522,8 @@ class _Run:
                     unpack_compact3(c3, nnz, coords, s_lo, s_hi, packed, aux)
                     cev = torch.cuda.Event()
                     cev.record(conv)
+                    nat.call("skx_coo_pack0_range", 3, nnz, lo, hi, nat.ptr(coords), nat.ptr(vals),
+                             nat.ptr(rec0), nat.stream())
                 conv_ev.append(cev)
                 bounds.append((lo, hi))
                 s_lo = s_hi
@@ -550,6 +557,10 @@ class _Run:
         d = DeviceCoo(self.shape, coords, vals)
         if c3 is not None:
             d._vrange = c3["vrange"]  # from the staging pass: no device scan, no sync
+            rec0.record_stream(conv)
+            aux[0].record_stream(main)
+            d._fibre[0] = (aux[0], rec0)  # colptr = slice pointers (int64, s0 + 1)
+            d._fibre_meta[0] = (0xFFFFFFFF, None)
         st._device = d
         self._host = None
         if c3 is not None:
@@ -611,8 +622,8 @@ class _Run:
                     vptr = ctypes.c_void_p(vals.data_ptr() + lo * 8)
                     nat.call("skx_rrf_stage1_fx_acc", nd, sp_, n, hi - lo, cptr, nnz, vptr, emax,
                              *tabs.args(), tabs.k2, nat.ptr(acc), nat.ptr(flag), bound, nat.stream())
-        # the fitness layout (a packing pass) on the convert stream behind the
-        # last unpack, beside the last chunks' sums
+        # the fitness layout: packed chunk by chunk above (compact staging),
+        # else one packing pass on the convert stream behind the last unpack
         with torch.cuda.stream(conv):
             self.d.fibre(0)
         for sn in side:

@@ -142,3 +142,26 @@ def test_nccl_one_rank(env):
         assert torch.equal(x, y)
     finally:
         assert lib.skx_nccl_destroy(comm) == 0
+
+
+@pytest.mark.parametrize("shape,nnz", [((300, 400, 500), 200_000), ((40, 30, 20, 10), 20_000)])
+def test_pack0_range_matches_mode0_layout(env, shape, nnz):
+    """The mode-0 layout packed chunk by chunk (skx_coo_pack0_range, the e2e
+    upload path) equals the one-pass layout (skx_coo_fibre, mode 0) bit for
+    bit, records and slice pointers."""
+    torch, skx, nat = env
+    from paper_2104_01101_b200.synth import planted_cp_coo_host
+    from paper_2104_01101_b200.tensors import device_of
+    c, v = planted_cp_coo_host(shape, nnz, rank=3, seed=9)
+    d = device_of(skx.SparseTensor(shape, c, v))
+    colptr, rec = d.fibre(0)
+    rw = int(nat.load().skx_coo_rec_words(len(shape)))
+    rec2 = torch.full((d.nnz * rw,), float("nan"), dtype=torch.float64, device="cuda")
+    bounds = np.linspace(0, d.nnz, 8).astype(np.int64)
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        nat.call("skx_coo_pack0_range", len(shape), d.nnz, int(lo), int(hi), nat.ptr(d.coords),
+                 nat.ptr(d.vals), nat.ptr(rec2), nat.stream())
+    torch.cuda.synchronize()
+    assert torch.equal(rec.view(torch.int64)[:d.nnz * rw], rec2.view(torch.int64))
+    ptr0 = np.searchsorted(c[:, 0], np.arange(shape[0] + 1), side="left")
+    assert np.array_equal(colptr.cpu().numpy(), ptr0)
