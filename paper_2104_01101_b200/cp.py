@@ -21,7 +21,8 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import rng as rngmod
-from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, mttkrp_dev, shape_of)
+from .tensors import (CPModel, device_of, fitness_cp_dev, is_sparse_dev, mttkrp_dev, shape_of,
+                      to_host)
 from .tucker import (SweepTrace, TuckerConfig, hooi_dev, hosvd_init_dev,
                      sketched_tucker_run_dev)
 
@@ -200,7 +201,8 @@ def cp_als(t, config, on_core=False):
         raise ValueError("cp_als is the unsketched driver; got a sketch config")
     d = device_of(t)
     factors, weights, trace = cp_als_dev(d, config, on_core=on_core)
-    return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
+    host = to_host(list(factors) + [weights])
+    return CPModel(host[:-1], host[-1]), trace
 
 
 def _lstsq_min_norm_dev(z, y):
@@ -283,7 +285,8 @@ def sketched_cp_als(t, config):
     if config.sketch != "leverage-random":
         raise ValueError("sketched_cp_als needs sketch='leverage-random'")
     factors, weights, trace = sketched_cp_als_dev(device_of(t), config)
-    return CPModel([a.cpu().numpy() for a in factors], weights.cpu().numpy()), trace
+    host = to_host(list(factors) + [weights])
+    return CPModel(host[:-1], host[-1]), trace
 
 
 def cp_via_sketched_tucker_dev(t, config, comm=None):
@@ -357,4 +360,5 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
 def cp_via_sketched_tucker(t, config):
     """CP through sketched Tucker compression (Alg. 6, src/cp.py:177-224)."""
     out, weights, trace = cp_via_sketched_tucker_dev(t, config)
-    return CPModel([a.cpu().numpy() for a in out], weights.cpu().numpy()), trace
+    host = to_host(list(out) + [weights])
+    return CPModel(host[:-1], host[-1]), trace

@@ -31,7 +31,7 @@ from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, filt
                         rrf_table_dev, ts_kron_dev, ts_kron_plan_dev, ts_rhs_dense_dev,
                         ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, compact3_aux_to_device, device_of,
-                      fitness_tucker_dev, is_sparse_dev, unpack_compact3,
+                      fitness_tucker_dev, is_sparse_dev, to_host, unpack_compact3,
                       matricize, shape_of, ttm_dev, ttmc_dev)
 
 SKETCH_KINDS = (None, "tensorsketch", "leverage-random", "leverage-deterministic")
@@ -1022,7 +1022,8 @@ def sketched_tucker_als_dev(t, config, comm=None):
 def sketched_tucker_als(t, config):
     """Sketched rank-constrained Tucker-ALS (src/tucker.py:216-300)."""
     core, factors, trace = sketched_tucker_als_dev(t, config)
-    return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace
+    host = to_host([core] + list(factors))
+    return TuckerModel(host[0], host[1:]), trace
 
 
 def _sparse_gram_dev(d, n, max_side=1 << 15):
@@ -1132,7 +1133,8 @@ def hooi_dev(t, config):
 def hooi(t, config):
     """Exact Tucker-ALS (src/tucker.py:155-193)."""
     core, factors, trace = hooi_dev(t, config)
-    return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace
+    host = to_host([core] + list(factors))
+    return TuckerModel(host[0], host[1:]), trace
 
 
 # ------------------------------------------------------------------ ref-ts
@@ -1236,4 +1238,5 @@ def ref_tucker_ts(t, config):
     """Reference sketched baseline, one variable per sub-problem
     (src/tucker.py:303-364)."""
     core, factors, trace = ref_tucker_ts_dev(t, config)
-    return TuckerModel(core.cpu().numpy(), [a.cpu().numpy() for a in factors]), trace
+    host = to_host([core] + list(factors))
+    return TuckerModel(host[0], host[1:]), trace

@@ -165,3 +165,27 @@ def test_pack0_range_matches_mode0_layout(env, shape, nnz):
     assert torch.equal(rec.view(torch.int64)[:d.nnz * rw], rec2.view(torch.int64))
     ptr0 = np.searchsorted(c[:, 0], np.arange(shape[0] + 1), side="left")
     assert np.array_equal(colptr.cpu().numpy(), ptr0)
+
+
+def test_to_host_matches_cpu(env):
+    """Model download through the pinned staging buffer and parallel host
+    copies equals .cpu() (large, small, non-contiguous and non-float64
+    inputs); the returned arrays are fresh (a second download does not
+    overwrite the first)."""
+    torch, skx, nat = env
+    from paper_2104_01101_b200.tensors import to_host
+    g = torch.Generator(device="cuda").manual_seed(0)
+    big = [torch.randn(200_000, 10, dtype=torch.float64, device="cuda", generator=g) for _ in range(3)]
+    odd = torch.randn(30, 7, dtype=torch.float64, device="cuda", generator=g).t()
+    core = torch.randn(20, 20, 20, dtype=torch.float64, device="cuda", generator=g)
+    ts = big + [odd, core]
+    got = to_host(ts)
+    for a, b in zip(got, ts):
+        assert a.shape == tuple(b.shape) and np.array_equal(a, b.cpu().numpy())
+    again = to_host([t * 2 for t in ts])
+    for a, b in zip(got, ts):
+        assert np.array_equal(a, b.cpu().numpy())  # not aliased to the staging buffer
+    for a, b in zip(again, ts):
+        assert np.array_equal(a, (b * 2).cpu().numpy())
+    ints = to_host([torch.arange(300_000, device="cuda")])
+    assert np.array_equal(ints[0], np.arange(300_000))
