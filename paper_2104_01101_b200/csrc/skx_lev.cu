@@ -87,6 +87,12 @@ __global__ void k_lev_final(int64_t s, const double* __restrict__ part,
 constexpr int kLevFusedThreads = 512;
 constexpr int kLevPer = kLevChunks / kLevFusedThreads;
 
+// Loads of a thread's chunk in batches of kLevB (independent loads in flight:
+// a sequential loop with stores between its loads issued one L2 round trip
+// per element, ~1 ms per 2e5 scores); the arithmetic and its order are those
+// of the element-by-element loop, so the bits are unchanged.
+constexpr int kLevB = 8;
+
 __global__ void __launch_bounds__(kLevFusedThreads) k_lev_prepare1(const double* __restrict__ sc,
                                                                   int64_t s, double* __restrict__ p,
                                                                   double* __restrict__ cdf) {
@@ -98,7 +104,14 @@ __global__ void __launch_bounds__(kLevFusedThreads) k_lev_prepare1(const double*
     int64_t lo, hi;
     lev_chunk(s, t0 + u * kLevFusedThreads, lo, hi);
     double acc = 0.0;
-    for (int64_t i = lo; i < hi; ++i) acc += fmax(sc[i], 0.0);
+    for (int64_t i = lo; i < hi; i += kLevB) {
+      double x[kLevB];
+#pragma unroll
+      for (int b = 0; b < kLevB; ++b) x[b] = i + b < hi ? __ldg(sc + i + b) : 0.0;
+#pragma unroll
+      for (int b = 0; b < kLevB; ++b)
+        if (i + b < hi) acc += fmax(x[b], 0.0);
+    }
     part[t0 + u * kLevFusedThreads] = acc;
   }
   __syncthreads();
@@ -114,11 +127,18 @@ __global__ void __launch_bounds__(kLevFusedThreads) k_lev_prepare1(const double*
     int64_t lo, hi;
     lev_chunk(s, t0 + u * kLevFusedThreads, lo, hi);
     double run = 0.0;
-    for (int64_t i = lo; i < hi; ++i) {
-      const double pi = fmax(sc[i], 0.0) / total;
-      p[i] = pi;
-      run += pi;
-      cdf[i] = run;
+    for (int64_t i = lo; i < hi; i += kLevB) {
+      double x[kLevB];
+#pragma unroll
+      for (int b = 0; b < kLevB; ++b) x[b] = i + b < hi ? __ldg(sc + i + b) : 0.0;
+#pragma unroll
+      for (int b = 0; b < kLevB; ++b) {
+        if (i + b >= hi) break;
+        const double pi = fmax(x[b], 0.0) / total;
+        p[i + b] = pi;
+        run += pi;
+        cdf[i + b] = run;
+      }
     }
     part[t0 + u * kLevFusedThreads] = run;
   }
@@ -142,7 +162,14 @@ __global__ void __launch_bounds__(kLevFusedThreads) k_lev_prepare1(const double*
     int64_t lo, hi;
     lev_chunk(s, t0 + u * kLevFusedThreads, lo, hi);
     const double offs = part[t0 + u * kLevFusedThreads];
-    for (int64_t i = lo; i < hi; ++i) cdf[i] = (cdf[i] + offs) / L;
+    for (int64_t i = lo; i < hi; i += kLevB) {
+      double x[kLevB];
+#pragma unroll
+      for (int b = 0; b < kLevB; ++b) x[b] = i + b < hi ? cdf[i + b] : 0.0;
+#pragma unroll
+      for (int b = 0; b < kLevB; ++b)
+        if (i + b < hi) cdf[i + b] = (x[b] + offs) / L;
+    }
   }
 }
 

@@ -189,3 +189,30 @@ def test_to_host_matches_cpu(env):
         assert np.array_equal(a, (b * 2).cpu().numpy())
     ints = to_host([torch.arange(300_000, device="cuda")])
     assert np.array_equal(ints[0], np.arange(300_000))
+
+
+@pytest.mark.parametrize("s", [1, 7, 1023, 1025, 200_000, 333_333])
+def test_lev_prepare_fused_equals_five_launch_form(env, s, monkeypatch):
+    """The one-CTA leverage cdf (batched loads) and the five-launch form give
+    the same p and cdf bit for bit, zero and negative scores included."""
+    torch, skx, nat = env
+    g = torch.Generator(device="cuda").manual_seed(s)
+    sc = torch.rand(s, dtype=torch.float64, device="cuda", generator=g)
+    if s > 10:
+        sc[::7] = 0.0
+        sc[3::11] = -1e-17
+    outs = []
+    for five in (False, True):
+        if five:
+            monkeypatch.setenv("SKX_LEV_5K", "1")
+        p = torch.empty(s, dtype=torch.float64, device="cuda")
+        cdf = torch.empty(s, dtype=torch.float64, device="cuda")
+        nat.call_ws("skx_lev_prepare", (nat.ptr(sc), s, nat.ptr(p), nat.ptr(cdf)), slot=7)
+        torch.cuda.synchronize()
+        outs.append((p.clone(), cdf.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    ref = np.maximum(sc.cpu().numpy(), 0)
+    ref = ref / ref.sum()
+    c = np.cumsum(ref)
+    # (numpy's sequential cumsum carries ~s eps of its own rounding)
+    assert np.allclose(outs[0][1].cpu().numpy(), c / c[-1], rtol=0, atol=max(1e-14, 4e-16 * s))
