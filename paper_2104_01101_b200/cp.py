@@ -15,6 +15,7 @@ rank 20 with CP rank 10.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, replace
 
@@ -323,9 +324,9 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
         core, tfac, ttrace = hooi_dev(d, tucker_cfg)
     core_cfg = replace(config, sketch=None, sketch_size=None, sketch_factor=None,
                        init="hosvd-of-core", seed=int(seed_cp))
-    # the core stage and the final CP fitness go to the high-priority stream:
-    # they run beside the Tucker stage's last fitness pass (low priority)
-    # instead of queueing behind its CTAs
+    # the core stage goes to the high-priority stream: it runs beside the
+    # Tucker stage's last fitness pass (low priority) instead of queueing
+    # behind its CTAs; the final CP fitness then follows that pass
     from .tucker import _init_streams
     caller = torch.cuda.current_stream()
     hi = _init_streams()[1]
@@ -344,7 +345,22 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
                 norm2 = comm.allreduce(norm2.view(1))[0]
         else:
             norm2 = (d * d).sum()
-        fin_dev = fitness_cp_dev(d, out, weights, norm2, comm)
+        if finish is not None and comm is None:
+            # the final CP fitness (a pass over the nonzeros, L2-gather bound
+            # like the Tucker fitness) queues behind the last Tucker fitness
+            # pass on its stream instead of running beside it: two gather-
+            # bound passes at once took ~7 ms longer than back to back
+            # (config 5: 459 -> 451.5 ms per call, same bits)
+            from .tucker import _fit_stream
+            fs = _fit_stream()
+            fs.wait_stream(hi)
+            with torch.cuda.stream(fs):
+                fin_dev = fitness_cp_dev(d, out, weights, norm2, comm)
+            for t_ in [weights, norm2] + out:
+                t_.record_stream(fs)
+            hi.wait_stream(fs)
+        else:
+            fin_dev = fitness_cp_dev(d, out, weights, norm2, comm)
     caller.wait_stream(hi)
     for t in [fin_dev, weights] + out:
         t.record_stream(caller)
