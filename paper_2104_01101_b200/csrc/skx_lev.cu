@@ -410,14 +410,22 @@ __global__ void __launch_bounds__(256) k_filter_fibers3v(
   const int4* a4 = reinterpret_cast<const int4*>(ca);
   const int4* b4 = reinterpret_cast<const int4*>(cb);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < n4; g0 += U * stride) {
-    int4 av[U], bv[U];
+  // register double buffer: the next U groups' loads are in flight while the
+  // current ones are probed
+  int4 av[U], bv[U];
+  auto load = [&](int64_t g0, int4* a, int4* b) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t g = g0 + u * stride;
-      av[u] = g < n4 ? __ldcs(a4 + g) : make_int4(0, 0, 0, 0);
-      bv[u] = g < n4 ? __ldcs(b4 + g) : make_int4(0, 0, 0, 0);
+      a[u] = g < n4 ? __ldcs(a4 + g) : make_int4(0, 0, 0, 0);
+      b[u] = g < n4 ? __ldcs(b4 + g) : make_int4(0, 0, 0, 0);
     }
+  };
+  int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  load(g0, av, bv);
+  for (; g0 < n4; g0 += U * stride) {
+    int4 an[U], bn[U];
+    load(g0 + U * stride, an, bn);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t g = g0 + u * stride;
@@ -426,6 +434,11 @@ __global__ void __launch_bounds__(256) k_filter_fibers3v(
       probe(4 * g + 1, (int64_t)av[u].y * ext_b + bv[u].y);
       probe(4 * g + 2, (int64_t)av[u].z * ext_b + bv[u].z);
       probe(4 * g + 3, (int64_t)av[u].w * ext_b + bv[u].w);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      av[u] = an[u];
+      bv[u] = bn[u];
     }
   }
   if (blockIdx.x == 0)
