@@ -547,12 +547,16 @@ extern "C" int skx_filter_fibers_coo(int ndim, const int64_t* shape_h, int mode,
     if (al) {
       const size_t smem = (size_t)(1 << (kBloomBits3 - 5)) * 4;
       const int64_t blocks = imax(1, imin((nnz + 2047) / 2048, (int64_t)num_sms() * 2));
-      // four groups of four nonzeros (2 x 16-byte loads each) in flight per
-      // thread (config 5, beside K7: 3.93 ms with two, 3.11 with four, 5.63
-      // with eight per 1e9-nonzero pass)
-      cudaFuncSetAttribute(k_filter_fibers3v<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      k_filter_fibers3v<4><<<(unsigned)blocks, 256, smem, s>>>(
+      // U groups of four nonzeros (2 x 16-byte loads each) per thread, double
+      // buffered (config 5, beside K7: U = 2: filter 2.9 ms per pass, call
+      // 447 ms; U = 4: 2.57 ms but 449 ms -- its registers crowd K7; without
+      // the double buffer U = 2 / 4 / 8 took 3.93 / 3.11 / 5.63 ms)
+#ifndef SKX_FILTER_U
+#define SKX_FILTER_U 2
+#endif
+      cudaFuncSetAttribute(k_filter_fibers3v<SKX_FILTER_U>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_filter_fibers3v<SKX_FILTER_U><<<(unsigned)blocks, 256, smem, s>>>(
           cp.c[o[0]], cp.c[o[1]], shape_h[o[1]], cp.c[mode], shape_h[mode], nnz, vals, sflat, m,
           out_key, out_val, cap, (unsigned long long*)count);
       return check_launch("k_filter_fibers3v");
