@@ -445,6 +445,18 @@ int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_
                          const int64_t* colptr0, const void* rec0, uint32_t c1_mask, double* out,
                          void* ws, size_t* ws_bytes, void* stream);
 
+/* Full TTMc P = X x_0 A0^T x_1 A1^T x_2 A2^T (400 x R0 row-major: P[(b*20+c),
+ * a]) of an order-3 COO at ranks (R0 <= 32, 20, 20) from its mode-0 fibre
+ * layout (colptr0, rec0, c1_mask as skx_tucker_cross_coo): per-slice sums
+ * v a1 a2^T on FP64 tensor cores with both factor rows by TMA gather4, then
+ * one GEMM with A0.  <P, C> is the cross term of any core C on these factors
+ * (src/tensors.py:217-258, 339-353): Algorithm 6's last Tucker fitness and
+ * its final CP fitness (CP model = Tucker model with core [[w; B_0, B_1,
+ * B_2]], src/cp.py:214-224) from one pass over the nonzeros. */
+int skx_tucker_ttmc3_r20(const int64_t* shape_h, int R0, const int64_t* colptr0, const void* rec0,
+                         uint32_t c1_mask, const double* A0, const double* A1, const double* A2,
+                         double* P, void* ws, size_t* ws_bytes, void* stream);
+
 /* CP cross term sum(weights * A_0 .* mttkrp(T, A, 0)) over lexsorted COO.
  * Replaces src/tensors.py:354-357 (+ mttkrp :322-323). */
 int skx_cp_cross_coo(int ndim, const int64_t* shape_h, int64_t R, int64_t nnz,

@@ -101,6 +101,7 @@ _SIGS = {
     "skx_reduce_scatter_sum": [c_p, c_p, c_p, c_i64, c_p],
     "skx_allgather": [c_p, c_p, c_p, c_i64, c_p],
     "skx_coo_pack0_range": [c_i32, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p],
+    "skx_tucker_ttmc3_r20": [c_p, c_i32, c_p, c_p, c_u32, c_p, c_p, c_p, c_p, c_p, c_sz_p, c_p],
     "skx_last_error": [],
     "skx_launch_count": [],
     "skx_version": [],

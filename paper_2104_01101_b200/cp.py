@@ -317,7 +317,7 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
         # the data-independent RRF rejection scans run.  Its last fitness pass
         # keeps running on the fitness stream while the core stage and the
         # final CP fitness below are enqueued (finish() joins it)
-        core, tfac, finish = sketched_tucker_run_dev(t, tucker_cfg, comm)
+        core, tfac, finish = sketched_tucker_run_dev(t, tucker_cfg, comm, ttmc_last=comm is None)
         d = device_of(t)
     else:  # exact HOOI compression stage (src/cp.py:203-204)
         d = device_of(t)
@@ -345,7 +345,19 @@ def cp_via_sketched_tucker_dev(t, config, comm=None):
                 norm2 = comm.allreduce(norm2.view(1))[0]
         else:
             norm2 = (d * d).sum()
-        if finish is not None and comm is None:
+        get_lt = getattr(finish, "last_ttmc", None) if comm is None else None
+        lt = get_lt() if get_lt is not None else None
+        if lt is not None and all(a is b for a, b in zip(lt[1], tfac)):
+            # the last Tucker fitness pass left the full TTMc P of the final
+            # Tucker factors; the CP model is the Tucker model with core
+            # G' = [[w; B_0, B_1, B_2]] on those factors, so its cross term
+            # is <P, G'> -- no second pass over the nonzeros
+            P, _, pev = lt
+            hi.wait_event(pev)
+            gp = torch.einsum("r,ar,br,cr->abc", cw, cfac[0], cfac[1], cfac[2])
+            fin_dev = fitness_cp_dev(None, out, weights, norm2, None, cross=(P * gp).sum())
+            P.record_stream(hi)
+        elif finish is not None and comm is None:
             # the final CP fitness (a pass over the nonzeros, L2-gather bound
             # like the Tucker fitness) queues behind the last Tucker fitness
             # pass on its stream instead of running beside it: two gather-

@@ -1088,6 +1088,127 @@ static bool skx_factor_tmap(CUtensorMap* tm, const double* A, int64_t rows, int 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ---- full TTMc of an order-3 COO at ranks 20 x 20 (modes 1, 2) -------------
+// For Algorithm 6's last Tucker fitness pass: per mode-0 slice i0,
+// M(i0) = sum_e v_e a1_e a2_e^T (20 x 20) on FP64 tensor cores with the
+// nonzeros as the K dimension (m8n8k4: A = a1 rows (b), B = v a2 rows (c),
+// 4 nonzeros per k-step, 3 x 3 tiles of the 24 x 24 padded M), both factor
+// rows gathered by TMA gather4 into shared memory (box 24 over 20 columns:
+// zero padding, conflict-free stride) as k_tucker3_tma2 does for one of them.
+// Then P = sum_i0 A0[i0] (x) M(i0) (skx_gemm_atb) is the whole core-sized
+// TTMc X x_0 A0^T x_1 A1^T x_2 A2^T, and ANY model on these factors has its
+// cross term as one dot with P: the Tucker core's (the fitness) and the CP
+// model's (G' = [[lambda; B_0, B_1, B_2]], Alg. 6's final fitness), so one
+// pass replaces the last Tucker fitness pass plus the CP fitness pass.
+template <int NB, int MB, int D>
+__global__ void __launch_bounds__(256, MB) k_ttmc3_tma(
+    const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2,
+    const int64_t* __restrict__ colptr, int64_t s0, const double* __restrict__ rec,
+    uint32_t c1_mask, double* __restrict__ mout) {
+  constexpr int ST = kT3tST;
+  constexpr int ROWBUF = NB * ST;
+  constexpr int NRB = D + 1, NRC = D + 3;
+  constexpr uint32_t TX = 2 * NB * ST * 8;  // both row sets of a batch
+  extern __shared__ __align__(128) double t3sm[];
+  __shared__ __align__(8) uint64_t bars[8][NRB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  double* rows1 = t3sm + (size_t)wid * (2 * NRB * ROWBUF + NRC * NB * 2);
+  double* rows2 = rows1 + NRB * ROWBUF;
+  double* recs = rows2 + NRB * ROWBUF;
+  if (lane == 0)
+    for (int b = 0; b < NRB; ++b) mbar_init(&bars[wid][b], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t phase = 0;
+  const int64_t nw = blockDim.x >> 5, stride = (int64_t)gridDim.x * nw;
+  for (int64_t i0 = blockIdx.x * nw + wid; i0 < s0; i0 += stride) {
+    const int64_t e0 = colptr[i0], e1 = colptr[i0 + 1];
+    double* mo = mout + i0 * 400;
+    if (e0 == e1) {
+      for (int k = lane; k < 400; k += 32) mo[k] = 0.0;
+      continue;
+    }
+    const int64_t nb = (e1 - e0 + NB - 1) / NB;
+    auto issue_recs = [&](int64_t b) {
+      if (lane < NB) {
+        const int64_t e = e0 + b * NB + lane;
+        cp_async16_cg_zfill(smem_addr(recs + ((b % NRC) * NB + lane) * 2),
+                            rec + 2 * (e < e1 ? e : e0), e < e1 ? 16u : 0u);
+      }
+    };
+    auto issue_rows = [&](int64_t b) {  // records {i1, i2 | bits, v}: both rows by TMA
+      const int slot = (int)(b % NRB);
+      const uint32_t* rb = reinterpret_cast<const uint32_t*>(recs + (b % NRC) * NB * 2);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0) mbar_expect_tx(&bars[wid][slot], TX);
+      __syncwarp();
+      if (lane < NB / 4) {
+        const uint32_t* r4 = rb + 16 * lane;
+        tma_gather4(smem_addr(rows1 + slot * ROWBUF + 4 * lane * ST), &tm1, &bars[wid][slot], 0,
+                    (int32_t)r4[0], (int32_t)r4[4], (int32_t)r4[8], (int32_t)r4[12]);
+        tma_gather4(smem_addr(rows2 + slot * ROWBUF + 4 * lane * ST), &tm2, &bars[wid][slot], 0,
+                    (int32_t)(r4[1] & c1_mask), (int32_t)(r4[5] & c1_mask),
+                    (int32_t)(r4[9] & c1_mask), (int32_t)(r4[13] & c1_mask));
+      }
+    };
+    double d[3][3][2];
+#pragma unroll
+    for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+    for (int64_t b2 = 0; b2 < D + 2 && b2 < nb; ++b2) issue_recs(b2);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    for (int64_t b2 = 0; b2 < D && b2 < nb; ++b2) issue_rows(b2);
+    for (int64_t bi = 0; bi < nb; ++bi) {
+      cp_async_wait<0>();
+      const int slot = (int)(bi % NRB);
+      mbar_wait(&bars[wid][slot], (phase >> slot) & 1u);
+      phase ^= 1u << slot;
+      __syncwarp();
+      if (bi + D < nb) issue_rows(bi + D);
+      if (bi + D + 2 < nb) issue_recs(bi + D + 2);
+      cp_async_commit();
+      const double* r1 = rows1 + slot * ROWBUF;
+      const double* r2 = rows2 + slot * ROWBUF;
+      const double* rv = recs + (bi % NRC) * NB * 2;
+#pragma unroll
+      for (int ks = 0; ks < NB / 4; ++ks) {
+        const int e = 4 * ks + t;
+        const double x = rv[e * 2 + 1];
+        double a[3], bv[3];
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) a[mt] = r1[e * ST + 8 * mt + g];
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) bv[nt] = x * r2[e * ST + 8 * nt + g];
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma884(d[mt][nt][0], d[mt][nt][1], a[mt], bv[nt]);
+      }
+      __syncwarp();  // every lane's reads of this slot before it is refilled
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    // D fragment: lane (g, t) holds M[b = 8 mt + g][c = 8 nt + 2 t, +1]
+#pragma unroll
+    for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int b = 8 * mt + g, c = 8 * nt + 2 * t + j;
+          if (b < 20 && c < 20) mo[b * 20 + c] = d[mt][nt][j];
+        }
+  }
+}
+
+template <int NB, int D>
+constexpr size_t ttmc3_smem_bytes() {
+  return (size_t)8 * (2 * (D + 1) * NB * kT3tST + (D + 3) * NB * 2) * 8;
+}
+
 template <int R, int NB, int D>
 constexpr size_t t3a_smem_bytes() {
   return (size_t)8 * ((D + 1) * 2 * NB * T3A<R>::ST + (D + 3) * NB * 2) * 8;
@@ -1349,6 +1470,43 @@ extern "C" int skx_resid_sq(const double* u, const double* vt, int64_t n_out, in
   }
   k_final_sum<<<1, 1024, 0, st>>>(part, nparts, out);
   return check_launch("skx_resid_sq", 2);
+}
+
+// Full TTMc P = X x_0 A0^T x_1 A1^T x_2 A2^T of an order-3 COO with ranks
+// (R0 <= 32, 20, 20), from its mode-0 fibre layout: per-slice 20 x 20 sums by
+// k_ttmc3_tma into the workspace, then P[(b, c), a] = sum_i0 M(i0)[b][c]
+// A0[i0][a] (skx_gemm_atb).  P is 400 x R0 row-major.  <P, C> is the Tucker
+// cross term of any core C on these factors (src/tensors.py:339-353).
+extern "C" int skx_tucker_ttmc3_r20(const int64_t* shape_h, int R0, const int64_t* colptr0,
+                                    const void* rec0, uint32_t c1_mask, const double* A0,
+                                    const double* A1, const double* A2, double* P, void* ws,
+                                    size_t* ws_bytes, void* stream) {
+  SKX_REQUIRE(ws_bytes != nullptr, "skx_tucker_ttmc3_r20: ws_bytes is NULL");
+  SKX_REQUIRE(R0 >= 1 && R0 <= 32, "skx_tucker_ttmc3_r20: R0 in 1..32");
+  const int64_t s0 = shape_h[0];
+  size_t gws = 0;
+  SKX_TRY(skx_gemm_atb(400, R0, s0, nullptr, 400, nullptr, R0, nullptr, R0, nullptr, &gws, stream));
+  Arena ar(ws, *ws_bytes);
+  double* mslice = ar.take<double>((size_t)s0 * 400);
+  char* gw = ar.take<char>(gws);
+  if (ws == nullptr) {
+    *ws_bytes = ar.used + 256;
+    return SKX_OK;
+  }
+  SKX_REQUIRE(ar.ok(), "skx_tucker_ttmc3_r20: workspace too small");
+  CUtensorMap tm1, tm2;
+  SKX_REQUIRE(skx_factor_tmap(&tm1, A1, shape_h[1], 20, kT3tST) &&
+                  skx_factor_tmap(&tm2, A2, shape_h[2], 20, kT3tST),
+              "skx_tucker_ttmc3_r20: tensor maps unavailable");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = ttmc3_smem_bytes<16, 1>();
+  cudaFuncSetAttribute(k_ttmc3_tma<16, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const unsigned mb = (unsigned)imax(1, (s0 + 7) / 8);
+  k_ttmc3_tma<16, 2, 1><<<mb, 256, sm, s>>>(tm1, tm2, colptr0, s0, (const double*)rec0, c1_mask,
+                                             mslice);
+  SKX_TRY(check_launch("k_ttmc3_tma"));
+  size_t b = gws;
+  return skx_gemm_atb(400, R0, s0, mslice, 400, A0, R0, P, R0, gw, &b, stream);
 }
 
 extern "C" int skx_tucker_cross_coo(int ndim, const int64_t* shape_h, const int64_t* ranks_h,

@@ -817,6 +817,35 @@ def ttmc_all_dense_dev(d, factors, skip=None):
     return cur
 
 
+def ttmc3_r20_eligible(d, factors):
+    """Order-3 COO with ranks (R0 <= 32, 20, 20): skx_tucker_ttmc3_r20 applies."""
+    return (is_sparse_dev(d) and d.ndim == 3 and int(factors[1].shape[1]) == 20
+            and int(factors[2].shape[1]) == 20 and int(factors[0].shape[1]) <= 32)
+
+
+def ttmc3_full_dev(d, factors):
+    """P = X x_0 A0^T x_1 A1^T x_2 A2^T of an order-3 COO at ranks (R0, 20,
+    20) as an (R0, 20, 20) CUDA tensor: one pass over the mode-0 layout
+    (skx_tucker_ttmc3_r20).  <P, C> is the cross term of any core C on these
+    factors."""
+    torch = _torch()
+    R0 = int(factors[0].shape[1])
+    cpt, rec0 = d.fibre(0)
+    shp, sp_ = nat.host_i64(d.shape)
+    p = torch.empty((400, R0), dtype=torch.float64, device="cuda")
+    fa = [f.contiguous() for f in factors]
+    nat.call_ws("skx_tucker_ttmc3_r20",
+                (sp_, R0, nat.ptr(cpt), nat.ptr(rec0), ctypes.c_uint32(d.fibre_mask(0)),
+                 nat.ptr(fa[0]), nat.ptr(fa[1]), nat.ptr(fa[2]), nat.ptr(p)), slot=5)
+    return p.t().reshape(R0, 20, 20)
+
+
+def fitness_from_cross_dev(norm2, cross, mod):
+    torch = _torch()
+    r2 = torch.clamp(norm2 - 2.0 * cross + mod, min=0.0)
+    return 1.0 - torch.sqrt(r2) / torch.sqrt(norm2)
+
+
 def fitness_tucker_dev(d, core, factors, norm2=None, comm=None):
     torch = _torch()
     if norm2 is None:
@@ -862,13 +891,16 @@ def cp_cross_dev(d, factors, weights):
     return ((factors[0] * weights) * m0).sum()
 
 
-def fitness_cp_dev(d, factors, weights, norm2=None, comm=None):
+def fitness_cp_dev(d, factors, weights, norm2=None, comm=None, cross=None):
+    """CP fitness (src/tensors.py:354-368); `cross` = <T, model> when the
+    caller already has it (then d is not read)."""
     torch = _torch()
     if norm2 is None:
         norm2 = d.norm2()[0] if is_sparse_dev(d) else (d * d).sum()
-    cross = cp_cross_dev(d, factors, weights)
-    if comm is not None:
-        cross = comm.allreduce(cross.clone().view(1))[0]
+    if cross is None:
+        cross = cp_cross_dev(d, factors, weights)
+        if comm is not None:
+            cross = comm.allreduce(cross.clone().view(1))[0]
     scaled = factors[0] * weights
     g = torch.ones((factors[0].shape[1],) * 2, dtype=torch.float64, device="cuda")
     for a in factors[1:]:

@@ -31,7 +31,8 @@ from .sketching import (TensorSketchOp, draw_rrf_tables, filter_fibers_dev, filt
                         rrf_table_dev, ts_kron_dev, ts_kron_plan_dev, ts_rhs_dense_dev,
                         ts_rhs_mode_dev)
 from .tensors import (DeviceCoo, SparseTensor, TuckerModel, compact3_aux_to_device, device_of,
-                      fitness_tucker_dev, is_sparse_dev, to_host, unpack_compact3,
+                      fitness_from_cross_dev, fitness_tucker_dev, is_sparse_dev, to_host,
+                      ttmc3_full_dev, ttmc3_r20_eligible, unpack_compact3,
                       matricize, shape_of, ttm_dev, ttmc_dev)
 
 SKETCH_KINDS = (None, "tensorsketch", "leverage-random", "leverage-deterministic")
@@ -363,6 +364,10 @@ class _Run:
         self.use_ts = config.sketch == "tensorsketch"
         # where the sub-problem residuals run (set for the sweeps, see _finish_dense)
         self.res_stream = None
+        # Algorithm 6: take the last sweep's fitness through the full TTMc and
+        # keep it (P, factors, event) for the CP stage's final fitness
+        self.ttmc_last = False
+        self.last_ttmc = None
         self.factors = [None] * self.ndim
         self.ts_ops = [None] * self.ndim
         self.ts_rhs = [None] * self.ndim
@@ -946,7 +951,18 @@ class _Run:
                 # factors that are replaced (not overwritten) by later solves
                 fs.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(fs):
-                    f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, fit_comm)
+                    if (self.ttmc_last and k == nsw - 1 and fit_comm is None
+                            and ttmc3_r20_eligible(self.d, self.factors)):
+                        # Algorithm 6's last Tucker fitness: the full TTMc P
+                        # (one pass, as fast as the cross-term kernel) also
+                        # gives the final CP fitness's cross term (cp.py)
+                        P = ttmc3_full_dev(self.d, self.factors)
+                        f = fitness_from_cross_dev(self.norm2, (P * core).sum(), (core * core).sum())
+                        pev = torch.cuda.Event()
+                        pev.record(fs)
+                        self.last_ttmc = (P, list(self.factors), pev)
+                    else:
+                        f = fitness_tucker_dev(self.d, core, self.factors, self.norm2, fit_comm)
                 for t in [core] + list(self.factors):
                     t.record_stream(fs)
             else:
@@ -996,12 +1012,15 @@ class _Run:
         return k
 
 
-def sketched_tucker_run_dev(t, config, comm=None):
+def sketched_tucker_run_dev(t, config, comm=None, ttmc_last=False):
     """Device-resident run whose trace is completed later: returns (core,
     factors, finish); finish() joins the per-sweep fitness stream and returns
     the SweepTrace.  The model is ready on the caller's stream before the last
-    fitness pass ends, so a caller (Algorithm 6's core stage) can overlap it."""
+    fitness pass ends, so a caller (Algorithm 6's core stage) can overlap it.
+    ttmc_last: the last sweep's fitness pass computes the full TTMc P of the
+    final factors; finish.last_ttmc() returns (P, factors, event) or None."""
     run = _Run(t, config, comm)
+    run.ttmc_last = ttmc_last
     run.initialise_and_prep()
     if run.sparse:
         # modes >= 1 layouts served the RRF stage 1 and the TS right-hand sides;
@@ -1010,6 +1029,7 @@ def sketched_tucker_run_dev(t, config, comm=None):
             run.d.drop_fibre(n)
     trace = SweepTrace()
     core, finish = run.sweeps(trace)
+    finish.last_ttmc = lambda: run.last_ttmc
     return core, list(run.factors), finish
 
 

@@ -206,6 +206,7 @@ def test_config5_alg6_reduced_vs_reference(cg, skx, oracle, monkeypatch, tag):
         def fin():
             seen["trace"] = finish()
             return seen["trace"]
+        fin.last_ttmc = finish.last_ttmc  # the last pass's full TTMc (final CP fitness)
         return core, fac, fin
 
     monkeypatch.setattr(cpmod, "sketched_tucker_run_dev", tucker)

@@ -788,3 +788,43 @@ def test_compact_staging_roundtrip(skx, shape, nnz):
     for a, b in zip(cuts[:-1], cuts[1:]):
         unpack_compact3(c3, nnz, out, a, b, packed, aux)
     assert np.array_equal(out.cpu().numpy().T.astype(np.int64), c)
+
+
+@pytest.mark.parametrize("shape,nnz,R0", [((3000, 4000, 3000), 2_000_000, 20),
+                                          ((2000, 1000, 1500), 1_000_000, 7),
+                                          ((200000, 200000, 200000), 5_000_000, 20),
+                                          ((50, 20000, 20000), 500_000, 20)])
+def test_ttmc3_full_vs_cross_kernels(skx, shape, nnz, R0):
+    """The full TTMc P (skx_tucker_ttmc3_r20) against a chunked einsum, and
+    the cross terms taken from it -- Tucker <P, G>, CP <P, [[w; B_0, B_1,
+    B_2]]> -- against the per-nonzero fitness kernels (K7, CP K7c)."""
+    import torch
+    from paper_2104_01101_b200.synth import planted_cp_coo_device
+    from paper_2104_01101_b200.tensors import (cp_cross_dev, device_of, ttmc3_full_dev,
+                                               tucker_cross_dev)
+    coords, vals = planted_cp_coo_device(shape, nnz, rank=10, noise_sd=0.1, seed=2)
+    d = device_of(skx.SparseTensor.from_device(shape, coords, vals, validate=False))
+    g = torch.Generator(device="cuda").manual_seed(2)
+    ranks = (R0, 20, 20)
+    fac = [torch.linalg.qr(torch.randn(s, r, dtype=torch.float64, device="cuda", generator=g))[0]
+           for s, r in zip(shape, ranks)]
+    core = torch.randn(*ranks, dtype=torch.float64, device="cuda", generator=g)
+    P = ttmc3_full_dev(d, fac)
+    c, v = d.coords.long(), d.vals
+    ref = torch.zeros(ranks, dtype=torch.float64, device="cuda")
+    for lo in range(0, d.nnz, 1 << 20):
+        hi = min(d.nnz, lo + (1 << 20))
+        ref += torch.einsum("e,ea,eb,ec->abc", v[lo:hi], fac[0][c[0, lo:hi]],
+                            fac[1][c[1, lo:hi]], fac[2][c[2, lo:hi]])
+    assert float((P - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+    cross = float((P * core).sum())
+    kref = float(tucker_cross_dev(d, core, fac))
+    assert abs(cross - kref) <= 1e-12 * float(ref.abs().sum() * core.abs().max()), (cross, kref)
+    # CP model on the same factors: factors A_n B_n, weights w
+    B = [torch.randn(r, 10, dtype=torch.float64, device="cuda", generator=g) for r in ranks]
+    w = torch.rand(10, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    gp = torch.einsum("r,ar,br,cr->abc", w, B[0], B[1], B[2])
+    cross_cp = float((P * gp).sum())
+    cf = [(a @ b).contiguous() for a, b in zip(fac, B)]
+    kcp = float(cp_cross_dev(d, cf, w))
+    assert abs(cross_cp - kcp) <= 1e-11 * float(ref.abs().sum() * gp.abs().max()), (cross_cp, kcp)
