@@ -187,6 +187,10 @@ def kernel_work(cfgd, nnz, s0):
         w["skx_tucker_cross_coo"] = dict(bound="tensor", unit="TFLOP/s",
                                          work=nnz * (2 * R * R + 2 * R) + s0 * 2 * R ** 3,
                                          bytes=rec)
+        # full TTMc (Alg. 6's last fitness pass): per nonzero v a1 a2^T (2 R^2
+        # flops), per slice A0[i0] (x) M(i0) (2 R^3)
+        w["skx_tucker_ttmc3_r20"] = dict(bound="tensor", unit="TFLOP/s",
+                                         work=nnz * 2 * R * R + s0 * 2 * R ** 3, bytes=rec)
         w["skx_cp_cross_coo"] = dict(bound="hbm", unit="GB/s", bytes=nnz * 20 + 0)
         # the two other-mode coordinate rows (int32) of every nonzero
         w["skx_filter_fibers_coo"] = dict(bound="hbm", unit="GB/s", bytes=nnz * 8)
@@ -275,7 +279,8 @@ def run_ours(args, cfgd):
     for _ in range(args.warmup):
         step()
     # ---- device-resident timed region
-    hook_names = ["skx_tucker_cross_coo", "skx_cp_cross_coo", "skx_cp_cross_fibre3", "skx_rrf_stage1_coo",
+    hook_names = ["skx_tucker_cross_coo", "skx_tucker_ttmc3_r20", "skx_cp_cross_coo",
+                  "skx_cp_cross_fibre3", "skx_rrf_stage1_coo",
                   "skx_rrf_stage1_fx", "skx_lemire_scan",
                   "skx_filter_fibers_coo", "skx_coo_fibre", "skx_ts_rhs_coo", "skx_resid_sq",
                   "skx_ts_kron_apply", "skx_philox_normal", "skx_tsqr_r", "skx_cp_core_als",
