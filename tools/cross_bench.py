@@ -54,6 +54,17 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
     print(f"cp cross (R={a.cp_rank}): {ms:.3f} ms  value {float(y):.12e}", flush=True)
+    if a.rank == 20:  # full TTMc (Alg. 6's last fitness pass): <P, C> = the Tucker cross term
+        from paper_2104_01101_b200.tensors import ttmc3_full_dev
+        P = ttmc3_full_dev(d, fac)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(a.reps):
+            ttmc3_full_dev(d, fac)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        print(f"full ttmc: {ms:.3f} ms  <P, C> {float((P * core).sum()):.12e}", flush=True)
 
 
 if __name__ == "__main__":
